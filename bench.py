@@ -1,0 +1,403 @@
+"""HB-CSF MTTKRP benchmark (BASELINE.json metric: GFLOP/s on the 3·nnz·R basis,
+R=32, and % of the HBM roofline).
+
+A step = one HB-CSF MTTKRP per mode (all three modes) of the configuration's
+tensor, inputs resident in HBM.  Default workload: BASELINE.json configs[1]
+(nell-2-shaped synthetic, 76.9M nnz, all 3 modes on 1 B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config nell-2|flickr-3d|delicious-3d|nell-1|config1] [--scale S]
+
+N>1 is launched by torchrun: output slices of each mode are sharded across
+ranks by nonzero count (no collective in the timed region); time = max over
+ranks; value = all ranks' flops / that time.
+
+``--impl reference`` times the reference algorithm on the host CPU (the
+oracle port, oracle/tenkit_port.py, with all host threads through its
+scheduled path, as ``tenkit mttkrp --threads N``) on a bounded slice sample of
+the same tensor; rank 0 alone prints it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+RANK = 32
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="nell-2")
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-nnz", type=int, default=300_000)
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or not self.path:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def census_of(h):
+    return {
+        "coo_nnz": h.coo_part.nnz,
+        "csl_slices": h.csl_part.num_slices,
+        "csl_nnz": h.csl_part.nnz,
+        "csf_slices": h.csf_part.num_slices,
+        "csf_fibers": h.csf_part.num_fibers,
+        "csf_nnz": h.csf_part.nnz,
+    }
+
+
+def b_comp(c, dims, mode, r=RANK):
+    """Algorithmic (compulsory) bytes of one mode's MTTKRP, SURVEY §8(d)."""
+    stream = (16 * c["coo_nnz"] + 8 * c["csl_slices"] + 12 * c["csl_nnz"] + 8 * c["csf_slices"]
+              + 8 * c["csf_fibers"] + 8 * c["csf_nnz"])
+    factors = 4 * r * sum(d for i, d in enumerate(dims) if i != mode)
+    out = 4 * r * dims[mode]
+    return stream + factors + out
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_factors(dims, seed):
+    rng = np.random.default_rng(seed)  # cli.py:274-276 convention
+    return [rng.random((d, RANK)) for d in dims]
+
+
+def cpu_sample(t, dims, mode, target_nnz):
+    """Every K-th slice of `mode` (whole slices, so the per-slice structure is
+    the workload's), exported to the host for the CPU oracle."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1904_03329_b200 import _native as N
+
+    idx = torch.empty((t.nnz, t.order), dtype=torch.int32, device="cuda")
+    vals = torch.empty(t.nnz, dtype=torch.float64, device="cuda")
+    N.call("hbk_coo_export_device", t._dev().ptr, C.c_void_p(idx.data_ptr()),
+           C.c_void_p(vals.data_ptr()), None, N.stream_ptr())
+    k = max(1, int(round(t.nnz / max(1, target_nnz))))
+    keep = (idx[:, mode] % k) == 0
+    si = idx[keep].cpu().numpy().view(np.uint32)
+    sv = vals[keep].cpu().numpy()
+    del idx, vals
+    return si, sv, k
+
+
+def time_oracle(si, sv, dims, mode, factors, threads, runs=3):
+    from oracle import tenkit_port as P
+
+    mo = P.allmode_order(dims, mode)
+    h = P.split_hbcsf(P.hbcsf(si, sv, dims, mo), 128)
+    units = None
+    if threads > 1:
+        units, _ = P.block_schedule(h["csf"], 512)
+    P.mttkrp_hbcsf(h, factors, mode, units=units, threads=threads)  # warm-up (cli.py:220-228)
+    ts = []
+    for _ in range(runs):
+        tic = time.perf_counter()
+        P.mttkrp_hbcsf(h, factors, mode, units=units, threads=threads)
+        ts.append(time.perf_counter() - tic)
+    return statistics.median(ts), len(sv)
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference algorithm on the host CPU cores."""
+    import torch
+
+    if rank != 0:
+        return
+    from paper_1904_03329_b200.generate import CONFIGS, config_tensor
+
+    torch.cuda.set_device(0)
+    cfg = CONFIGS[args.config]
+    dims = cfg["dims"]
+    t = config_tensor(args.config, scale=args.scale)
+    factors = make_factors(dims, cfg["seed"])
+    threads = os.cpu_count() or 1
+    samples = [cpu_sample(t, dims, m, args.cpu_sample_nnz) for m in range(len(dims))]
+    steps = []
+    for s in range(args.warmup + args.steps):
+        flops = secs = 0.0
+        for m, (si, sv, _) in enumerate(samples):
+            sec, m_nnz = time_oracle(si, sv, dims, m, factors, threads, runs=1)
+            flops += 3.0 * m_nnz * RANK
+            secs += sec
+        if s >= args.warmup:
+            steps.append(flops / secs / 1e9)
+    value = statistics.median(steps)
+    sample_desc = (f"every K-th output slice per mode (K={[s[2] for s in samples]}, "
+                   f"{[len(s[1]) for s in samples]} nnz), split tau=128, schedule block 512")
+    line = {
+        "impl": "reference", "metric": "MTTKRP GFLOP/s (3*nnz*R, R=32)", "value": value,
+        "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (SURVEY Appendix A power-law generator)",
+        "config": {"workload": f"{args.config} HB-CSF MTTKRP, all modes, R=32", "dims": list(dims),
+                   "nnz": t.nnz, "rank": RANK},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                         "sample": sample_desc},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1904_03329_b200 as hb
+    from paper_1904_03329_b200 import shard
+    from paper_1904_03329_b200.generate import CONFIGS, config_tensor
+    from paper_1904_03329_b200.kernels import _device_factors, plan_for
+
+    cfg = CONFIGS[args.config]
+    dims = cfg["dims"]
+    t0 = time.perf_counter()
+    t = config_tensor(args.config, scale=args.scale)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    nnz_total = t.nnz
+
+    # preprocessing (reported separately, like cli.py preprocessing_seconds)
+    t0 = time.perf_counter()
+    split_cfg = hb.SplitConfig()
+    reps, censuses, plans, ranges = [], [], [], []
+    for mode in range(len(dims)):
+        mo = hb.allmode_order(dims, mode)
+        if world > 1:
+            rr, part = shard.shard_for_rank(t, mode, rank, world)
+        else:
+            rr, part = (0, dims[mode]), t
+        h = hb.split_fibers(hb.build_hbcsf(part, mo), split_cfg)
+        reps.append(h)
+        ranges.append(rr)
+        censuses.append(census_of(h))
+        plans.append(plan_for(h, mode, RANK))
+    torch.cuda.synchronize()
+    prep_s = time.perf_counter() - t0
+
+    f64 = make_factors(dims, cfg["seed"])
+    f_dev = [torch.from_numpy(f).float().cuda() for f in f64]
+    outs = [torch.empty((dims[m], RANK), dtype=torch.float32, device="cuda") for m in range(len(dims))]
+    ptrs = [_device_factors(f_dev, m)[0] for m in range(len(dims))]
+    stream = torch.cuda.current_stream()
+
+    def step():
+        for m in range(len(dims)):
+            plans[m].execute(ptrs[m], outs[m])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    n_modes = len(dims)
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)] for _ in range(n_modes)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        start.record(stream)
+        for s in range(args.steps):
+            for m in range(n_modes):
+                ev[m][s][0].record(stream)
+                plans[m].execute(ptrs[m], outs[m])
+                ev[m][s][1].record(stream)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = start.elapsed_time(stop)
+    per_mode_ms = [statistics.mean(a.elapsed_time(b) for a, b in ev[m]) for m in range(n_modes)]
+    if world > 1:
+        tt = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(tt.item())
+    ms_per_step = elapsed_ms / args.steps
+    flops_step = 3.0 * nnz_total * RANK * n_modes
+    value = flops_step / (ms_per_step * 1e-3) / 1e9
+
+    # roofline over the per-mode launches (each step is one launch per mode)
+    hbm, hbm_src = peaks()
+    bytes_modes = [b_comp(censuses[m], dims, m) for m in range(n_modes)]
+    achieved = sum(bytes_modes) / (sum(per_mode_ms) * 1e-3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        try:
+            d = json.loads(prof.read_text())
+            traffic = d.get(args.config, {}).get("dram_bytes_per_step")
+        except Exception:
+            traffic = None
+
+    # end to end through the public API with host buffers (numpy factors in,
+    # numpy float64 rows out), one mttkrp_hbcsf per mode per step
+    e2e = None
+    if not args.no_e2e and world == 1:
+        for m in range(n_modes):
+            hb.mttkrp_hbcsf(reps[m], f64, m)
+        torch.cuda.synchronize()
+        k = max(3, min(args.steps, 10))
+        tic = time.perf_counter()
+        for _ in range(k):
+            for m in range(n_modes):
+                y, _ = hb.mttkrp_hbcsf(reps[m], f64, m)
+        e2e_s = (time.perf_counter() - tic) / k
+        h2d = sum(4 * RANK * sum(d for i, d in enumerate(dims) if i != m) for m in range(n_modes))
+        d2h = sum(4 * RANK * dims[m] for m in range(n_modes))
+        e2e = {"value": flops_step / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+               "path": "paper_1904_03329_b200.mttkrp_hbcsf(numpy f64 factors) -> numpy f64 rows"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        samples = [cpu_sample(t, dims, m, args.cpu_sample_nnz) for m in range(n_modes)]
+        flops = secs = 0.0
+        for m, (si, sv, _) in enumerate(samples):
+            sec, m_nnz = time_oracle(si, sv, dims, m, f64, threads=1, runs=3)
+            flops += 3.0 * m_nnz * RANK
+            secs += sec
+        cpu = {"value": flops / secs / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "port",
+               "sample": (f"every K-th output slice per mode (K={[s[2] for s in samples]}, "
+                          f"{[len(s[1]) for s in samples]} nnz); oracle mttkrp_hbcsf threads=1, "
+                          "split tau=128, median of 3 after 1 warm-up")}
+
+    if rank == 0:
+        line = {
+            "metric": "MTTKRP GFLOP/s (3*nnz*R, R=32)",
+            "value": value,
+            "unit": "GFLOP/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (SURVEY Appendix A power-law generator, seeded, on device)",
+            "config": {
+                "workload": f"{args.config}-shaped HB-CSF MTTKRP, all {n_modes} modes per step, R=32",
+                "dims": list(dims), "nnz": nnz_total, "rank": RANK, "scale": args.scale,
+                "split": {"fiber_threshold": 128, "block_size": 512},
+                "l2": "inputs larger than L2 (index/value streams 0.75+ GB per mode); factors L2-resident by design",
+                "parallelism": f"slice-sharded dp{world}" if world > 1 else "1 GPU",
+                "census": censuses if world == 1 else None,
+                "preprocessing_s": prep_s, "generate_s": gen_s,
+            },
+            "roofline": {
+                "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
+                "kernel": "k_mttkrp3_r32 (one launch per mode)",
+                "algorithmic_bytes_per_step": sum(bytes_modes),
+                "per_mode_ms": per_mode_ms, "per_mode_bytes": bytes_modes,
+                "per_mode_frac": [b / (ms * 1e-3) / 1e9 / hbm for b, ms in zip(bytes_modes, per_mode_ms)],
+            },
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * n_modes,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

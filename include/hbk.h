@@ -1,0 +1,226 @@
+/*
+ * hbk.h — C ABI of the B200-native HB-CSF / B-CSF sparse MTTKRP library
+ * (libhbk.so, built for sm_100a).
+ *
+ * The reference (`tenkit`, /root/reference/pkg/src/tenkit) is pure Python/NumPy
+ * and has no FFI, so this header is the boundary a maintainer would bind from
+ * the reference's Python API with ctypes.  Each entry
+ * point names the reference function it replaces (file:line, relative to
+ * /root/reference/pkg/src/tenkit/).
+ *
+ * Conventions
+ *  - Every call returns an int status: HBK_OK or one of the HBK_E* codes.  The
+ *    message for the last failure on the calling thread is hbk_last_error().
+ *    The Python shim maps HBK_EINVAL -> ValueError, HBK_ETYPE -> TypeError,
+ *    HBK_ECUDA -> RuntimeError, HBK_ENOMEM -> MemoryError, mirroring the
+ *    reference's exception types (kernels.py:62-88, balance.py:39-48,128-150).
+ *  - Pointers marked [dev] are CUDA device pointers on the current device;
+ *    [host] are host pointers.  `stream` is a cudaStream_t passed as void*
+ *    (NULL = legacy default stream).
+ *  - Handles (hbk_coo, hbk_csl, hbk_csf, hbk_sched, hbk_plan) own their device
+ *    arrays and are immutable after creation (reference: "treat instances as
+ *    immutable", coo.py:58).  They are reference counted: *_retain adds a
+ *    reference, *_release drops one and frees the arrays at zero.
+ *  - Build calls (create/sort/canonicalize/build/split/schedule/plan) may
+ *    synchronise `stream` to learn output sizes.  hbk_plan_execute is fully
+ *    asynchronous on `stream`.
+ *  - Index arrays are uint32 on the device; nnz must be < 2^32 - 1.
+ */
+#ifndef HBK_H
+#define HBK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HBK_ABI_VERSION 1
+#define HBK_MAX_ORDER 8
+
+#define HBK_OK 0
+#define HBK_EINVAL 1 /* ValueError   */
+#define HBK_ETYPE 2  /* TypeError    */
+#define HBK_ECUDA 3  /* RuntimeError */
+#define HBK_ENOMEM 4 /* MemoryError  */
+
+/* SliceKind values, formats.py:41-46 */
+#define HBK_SLICE_COO 0
+#define HBK_SLICE_CSL 1
+#define HBK_SLICE_CSF 2
+
+typedef struct hbk_coo hbk_coo;
+typedef struct hbk_csl hbk_csl;
+typedef struct hbk_csf hbk_csf;
+typedef struct hbk_sched hbk_sched;
+typedef struct hbk_plan hbk_plan;
+
+const char* hbk_last_error(void);
+int hbk_abi_version(void);
+/* Number of SMs of the current device (0 and HBK_ECUDA when no device). */
+int hbk_device_sms(int* sms);
+
+/* ------------------------------------------------------------------ COO --
+ * CooTensor, coo.py:42-114.  Stored as SoA uint32 columns + fp32 values for
+ * the kernels + the caller's fp64 values (kept for exact export).            */
+typedef struct {
+  int order;
+  int64_t dims[HBK_MAX_ORDER];
+  int64_t nnz;
+  int has_sorted;                      /* sorted_under is not None          */
+  int sorted_under[HBK_MAX_ORDER];
+  int unique_mode;                     /* >=0: every slice of that mode holds
+                                          one nonzero (HB-CSF coo_part)      */
+} hbk_coo_info;
+
+/* CooTensor(dims, indices, values, sorted_under): idx [dev] nnz x order
+ * row-major, vals [dev] fp64.  Range checking is the caller's (coo.py:80-84
+ * is done by the Python shim).  sorted_under may be NULL (unknown).        */
+int hbk_coo_create(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx,
+                   const double* vals, const int* sorted_under, void* stream, hbk_coo** out);
+/* Same, from fp32 values (no fp64 copy is kept; export widens fp32). */
+int hbk_coo_create_f32(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx,
+                       const float* vals, const int* sorted_under, void* stream, hbk_coo** out);
+int hbk_coo_info_get(const hbk_coo* t, hbk_coo_info* info);
+/* Copy back: idx [host] nnz x order uint32 row-major, vals [host] fp64. Either may be NULL. */
+int hbk_coo_export(const hbk_coo* t, uint32_t* idx, double* vals, void* stream);
+/* Device views of the SoA columns (col < order) and fp32 values. */
+int hbk_coo_device_arrays(const hbk_coo* t, const uint32_t** cols, const float** vals32);
+/* Device-to-device copy-out: idx [dev] nnz x order row-major, v64/v32 [dev];
+ * any pointer may be NULL. */
+int hbk_coo_export_device(const hbk_coo* t, uint32_t* idx, double* v64, float* v32, void* stream);
+/* sort_by_mode_order, coo.py:208-224: stable lexicographic order, mode_order[0]
+ * major.  Returns a new retained handle (or t itself, retained, when
+ * t->sorted_under == mode_order, coo.py:221-222).                           */
+int hbk_coo_sort(hbk_coo* t, const int* mode_order, void* stream, hbk_coo** out);
+/* canonicalize, coo.py:227-247: identity sort, duplicates merged, exact zeros
+ * dropped.  merge = 0: sum duplicates exactly as np.add.reduceat does
+ * (first + pairwise(rest)), then drop 0.0; merge = 1: keep the first of each
+ * duplicate run (set semantics; used by the synthetic generator).          */
+int hbk_coo_canonicalize(const hbk_coo* t, int merge, void* stream, hbk_coo** out);
+/* Slice view of a COO tensor for mttkrp_coo (kernels.py:109-151): entries
+ * grouped by `mode` (sorted under (mode, *rest) unless already mode-major),
+ * returned as a CSL-shaped handle over ALL slices.                         */
+int hbk_coo_slices(hbk_coo* t, int mode, void* stream, hbk_csl** out);
+void hbk_coo_retain(hbk_coo* t);
+void hbk_coo_release(hbk_coo* t);
+
+/* ------------------------------------------------------------------ CSL --
+ * CslSlices, formats.py:207-233.                                           */
+typedef struct {
+  int order;
+  int64_t dims[HBK_MAX_ORDER];
+  int mode_order[HBK_MAX_ORDER];
+  int64_t num_slices;
+  int64_t nnz;
+} hbk_csl_info;
+
+#define HBK_CSL_SLICE_PTR 0 /* int64  [S+1]           */
+#define HBK_CSL_SLICE_IDX 1 /* uint32 [S]             */
+#define HBK_CSL_REST_IDX 2  /* uint32 [nnz x (N-1)]   */
+#define HBK_CSL_VALUES 3    /* fp64   [nnz]           */
+int hbk_csl_info_get(const hbk_csl* s, hbk_csl_info* info);
+int hbk_csl_export(const hbk_csl* s, int which, void* host_dst, void* stream);
+void hbk_csl_retain(hbk_csl* s);
+void hbk_csl_release(hbk_csl* s);
+
+/* ------------------------------------------------------------------ CSF --
+ * CsfTensor, formats.py:49-117.                                            */
+typedef struct {
+  int order;
+  int64_t dims[HBK_MAX_ORDER];
+  int mode_order[HBK_MAX_ORDER];
+  int64_t nnz;
+  int64_t level_sizes[HBK_MAX_ORDER]; /* len(idxs[d]), d < order-1 */
+  int split;
+} hbk_csf_info;
+
+#define HBK_CSF_PTR 0    /* int64  [level_sizes[level]+1] */
+#define HBK_CSF_IDX 1    /* uint32 [level_sizes[level]]   */
+#define HBK_CSF_LEAF 2   /* uint32 [nnz]                  */
+#define HBK_CSF_VALUES 3 /* fp64   [nnz]                  */
+int hbk_csf_info_get(const hbk_csf* c, hbk_csf_info* info);
+int hbk_csf_export(const hbk_csf* c, int which, int level, void* host_dst, void* stream);
+
+/* build_csf, formats.py:120-168. */
+int hbk_build_csf(hbk_coo* t, const int* mode_order, void* stream, hbk_csf** out);
+/* build_hbcsf, formats.py:260-299: three slice-disjoint parts.  coo_part keeps
+ * unpermuted coordinates sorted under mode_order (formats.py:273-275).     */
+int hbk_build_hbcsf(hbk_coo* t, const int* mode_order, void* stream, hbk_coo** coo_part,
+                    hbk_csl** csl_part, hbk_csf** csf_part);
+/* classify_slices, formats.py:194-204: labels [host] int8 [num_slices]. */
+int hbk_classify_slices(const hbk_csf* c, int8_t* labels, void* stream);
+/* split_fibers, balance.py:65-90.  *out = NULL (status OK) when no fiber
+ * exceeds fiber_threshold (the reference returns the input object).        */
+int hbk_split_fibers(const hbk_csf* c, int64_t fiber_threshold, void* stream, hbk_csf** out);
+void hbk_csf_retain(hbk_csf* c);
+void hbk_csf_release(hbk_csf* c);
+
+/* ------------------------------------------------------------- schedule --
+ * assign_slice_blocks / BlockSchedule, balance.py:100-189.                 */
+typedef struct {
+  int64_t num_units;
+  int64_t num_slices;
+  int64_t num_fibers;
+  int64_t block_size;
+} hbk_sched_info;
+#define HBK_SCHED_UNITS 0 /* int64 [num_units x 4]: block_id, slice_pos, fiber_start, fiber_stop */
+#define HBK_SCHED_MULT 1  /* int64 [num_slices] multiplicities */
+int hbk_assign_slice_blocks(const hbk_csf* c, int64_t block_size, void* stream, hbk_sched** out);
+/* A schedule from host units (BlockSchedule built by the caller):
+ * units [host] int64 num_units x 4 as above, mult [host] int64 [num_slices]. */
+int hbk_sched_from_units(const hbk_csf* c, const int64_t* units, int64_t num_units,
+                         const int64_t* mult, void* stream, hbk_sched** out);
+int hbk_sched_info_get(const hbk_sched* s, hbk_sched_info* info);
+int hbk_sched_export(const hbk_sched* s, int which, int64_t* host_dst, void* stream);
+/* BlockSchedule.validate_for, balance.py:128-150 (HBK_EINVAL on mismatch). */
+int hbk_sched_validate(const hbk_sched* s, const hbk_csf* c, void* stream);
+void hbk_sched_retain(hbk_sched* s);
+void hbk_sched_release(hbk_sched* s);
+
+/* --------------------------------------------------------------- MTTKRP --
+ * mttkrp_hbcsf / mttkrp_csf / mttkrp_csl / mttkrp_coo / mttkrp_scheduled,
+ * kernels.py:109-342.  A plan binds up to three slice-disjoint parts of one
+ * tensor (any may be NULL) for one output mode and rank, precomputes the
+ * work list (B-CSF units), and is then executed any number of times.
+ *   coo  : an HB-CSF coo_part (unique_mode == mode), one nonzero per row
+ *   csl  : a CslSlices (or hbk_coo_slices view) with mode_order[0] == mode
+ *   csf  : a CsfTensor with mode_order[0] == mode (split or not)
+ *   sched: optional BlockSchedule of csf; its units become the CSF work
+ *          units (one 8-lane group per unit) exactly as mttkrp_scheduled.
+ * The output (dims[mode] x rank fp32, row-major, caller-owned) is fully
+ * written: rows owned by no part are zero-filled inside the same launch.  */
+typedef struct {
+  int mode;
+  int rank;
+  int64_t out_rows;
+  int64_t tasks_csf, tasks_csl, tasks_coo, tasks_zero;
+  int64_t split_rows;      /* rows accumulated by more than one task      */
+  int64_t launches;        /* kernel launches per execute                 */
+  int fast_path;           /* 1: order-3 float4 kernel; 0: generic kernel */
+  int64_t op_muls, op_adds; /* OpCount of the reference kernel, R-weighted */
+  int64_t nnz;
+  int64_t stream_bytes;    /* index + value bytes read per execute        */
+} hbk_plan_info;
+
+int hbk_plan_create(hbk_coo* coo, hbk_csl* csl, hbk_csf* csf, hbk_sched* sched, int mode,
+                    int rank, void* stream, hbk_plan** out);
+int hbk_plan_info_get(const hbk_plan* p, hbk_plan_info* info);
+/* factors: [host] array of `order` [dev] pointers, factor d row-major
+ * dims[d] x rank fp32 (factors[mode] is not read, kernels.py:62-66).
+ * out: [dev] dims[mode] x rank fp32.                                       */
+int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out, void* stream);
+void hbk_plan_release(hbk_plan* p);
+
+/* ------------------------------------------------------------ sharding --
+ * Multi-GPU partitioner: slice nnz histogram of `mode`.
+ * hist [dev] int64 [dims[mode]] is overwritten.                            */
+int hbk_coo_slice_histogram(const hbk_coo* t, int mode, int64_t* hist, void* stream);
+/* Keep only entries whose `mode` coordinate lies in [row_begin, row_end). */
+int hbk_coo_select_rows(const hbk_coo* t, int mode, int64_t row_begin, int64_t row_end,
+                        void* stream, hbk_coo** out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HBK_H */

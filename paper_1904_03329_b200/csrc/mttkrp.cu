@@ -1,0 +1,1096 @@
+// HB-CSF / B-CSF MTTKRP on sm_100a.
+//
+// One persistent launch per mode covers all three HB-CSF buckets plus the
+// zero-fill of rows no bucket owns.  The plan cuts each bucket into tasks of
+// ~TASK_NNZ nonzeros (B-CSF: heavy slices are split into chunks, light slices
+// are packed into runs of whole slices); an 8-lane group owns one task, so a
+// warp runs four tasks side by side.  Lanes are vectorised over the rank
+// (float4, 8 lanes = one 128-byte factor row at R=32).
+//
+//   CSF task : per batch of 8 nonzeros, gather the 8 leaf rows C[k] at once,
+//              accumulate v*C[k] into the fiber partial in registers, and at
+//              each fiber end multiply by the fiber row B[j] into the slice
+//              partial (kernels.py:173-184 restated per group).
+//   CSL task : no fiber level: v*B[j]*C[k] straight into the slice partial
+//              (kernels.py:210-214).
+//   COO task : one nonzero = one output row, plain store (kernels.py:137-140
+//              on the HB-CSF coo_part, whose slices hold one nonzero each).
+//   ZERO task: rows owned by no bucket.
+// Output rows of unsplit slices are written with plain stores; chunks of a
+// split slice add into a per-slice fp32 accumulator with vector atomics and
+// the last chunk to finish (arrival counter) stores the row — so every output
+// row is written exactly once and no memset of the output is needed.
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace hbk {
+
+static constexpr uint32_t NOSLOT = 0xFFFFFFFFu;
+static constexpr uint32_t TASK_NNZ_CSF = 128;
+static constexpr uint32_t TASK_NNZ_CSL = 128;
+static constexpr uint32_t TASK_NNZ_COO = 32;
+static constexpr uint32_t TASK_ROWS_ZERO = 64;
+static constexpr uint32_t GEN_TASK_NNZ = 256;
+
+struct Task {
+  uint32_t lo, hi;   // nonzero range (rows range for ZERO tasks)
+  uint32_t s;        // first slice (position in the bucket's slice arrays)
+  uint32_t f;        // first fiber (CSF)
+  uint32_t slot;     // split-slice accumulator slot, NOSLOT for whole slices
+  uint32_t nchunk;   // chunks of that split slice
+  uint32_t pad0, pad1;
+};
+
+struct alignas(16) Work {
+  // task ranges [0,n0) CSF, [n0,n1) CSL, [n1,n2) COO, [n2,n3) ZERO
+  uint32_t n0, n1, n2, n3;
+  const Task* tasks;
+  // CSF bucket
+  const uint32_t* csf_send;   // [S+1] nonzero offset of each slice
+  const uint32_t* csf_sidx;   // [S]   output row of each slice
+  const uint32_t* csf_lptr;   // [F+1]
+  const uint32_t* csf_fidx;   // [F]
+  const uint32_t* csf_leaf;   // [M]
+  const float* csf_val;       // [M]
+  uint32_t csf_F;
+  uint32_t csf_S;
+  // CSL bucket
+  const uint32_t* csl_send;   // slice_ptr [S+1]
+  const uint32_t* csl_sidx;
+  const uint32_t* csl_j;      // rest[0]
+  const uint32_t* csl_k;      // rest[1]
+  const float* csl_val;
+  uint32_t csl_S;
+  // COO bucket (unique rows)
+  const uint32_t* coo_i;
+  const uint32_t* coo_j;
+  const uint32_t* coo_k;
+  const float* coo_val;
+  // ZERO list
+  const uint32_t* zero_rows;
+  // split-slice workspace (self-cleaning)
+  float* ws_acc;
+  uint32_t* ws_cnt;
+  uint32_t* ws_ctr;   // [0] task counter, [1] finished warps
+  uint32_t total_warps;
+};
+
+struct Factors3 {
+  const float4* B;  // factor of mode_order[1] (fiber / rest[0])
+  const float4* C;  // factor of mode_order[2] (leaf / rest[1])
+  float4* out;
+};
+
+__device__ __forceinline__ float4 f4zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ float4 fma4(float a, float4 x, float4 y) {
+  return make_float4(fmaf(a, x.x, y.x), fmaf(a, x.y, y.y), fmaf(a, x.z, y.z), fmaf(a, x.w, y.w));
+}
+__device__ __forceinline__ float4 fmav4(float4 a, float4 x, float4 y) {
+  return make_float4(fmaf(a.x, x.x, y.x), fmaf(a.y, x.y, y.y), fmaf(a.z, x.z, y.z),
+                     fmaf(a.w, x.w, y.w));
+}
+__device__ __forceinline__ float4 mul4(float a, float4 x) {
+  return make_float4(a * x.x, a * x.y, a * x.z, a * x.w);
+}
+__device__ __forceinline__ void red_add4(float4* p, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float4 ld_cg4(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_cg4(float4* p, float4 v) {
+  asm volatile("st.global.cg.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
+// A chunk of a split slice hands its partial to the slice accumulator; the
+// last of the slice's chunks writes the output row (and re-zeroes the slot).
+__device__ __forceinline__ void flush_split(const Work& w, uint32_t slot, uint32_t nchunk,
+                                            uint32_t row, float4 sa, float4* out, int lig,
+                                            unsigned gmask) {
+  float4* acc = reinterpret_cast<float4*>(w.ws_acc) + size_t(slot) * 8 + lig;
+  red_add4(acc, sa);
+  __threadfence();
+  __syncwarp(gmask);
+  uint32_t old = 0;
+  if (lig == 0) old = atomicAdd(w.ws_cnt + slot, 1u);
+  old = __shfl_sync(gmask, old, 0, 8);
+  if (old == nchunk - 1) {
+    __threadfence();
+    float4 r = ld_cg4(acc);
+    out[size_t(row) * 8 + lig] = r;
+    st_cg4(acc, f4zero());
+    if (lig == 0) w.ws_cnt[slot] = 0;
+  }
+}
+
+// ------------------------------------------------------------ CSF task --
+__device__ __forceinline__ void csf_task(const Work& w, const Factors3& fx, const Task& t, int lig,
+                                         unsigned gmask, uint64_t pol_s, uint64_t pol_r) {
+  const uint32_t lo = t.lo, hi = t.hi;
+  if (lo >= hi) return;
+  const bool chunk = t.slot != NOSLOT;
+  uint32_t s = t.s, f = t.f;
+  float4 fa = f4zero(), sa = f4zero();
+  // whole-slice runs flush at slice ends; a chunk flushes once at its end
+  uint32_t send = chunk ? 0xFFFFFFFFu : w.csf_send[s + 1];
+  bool pending = false;  // fiber partial not yet multiplied by its B row
+  for (uint32_t base = lo; base < hi; base += 8) {
+    const uint32_t n = min(8u, hi - base);
+    uint32_t k = 0;
+    float v = 0.f;
+    if (lig < n) {
+      k = ld_stream_u32(w.csf_leaf + base + lig, pol_s);
+      v = ld_stream_f32(w.csf_val + base + lig, pol_s);
+    }
+    // fibers f, f+1, ...: end offsets and coordinates of the next 8
+    uint32_t e = 0xFFFFFFFFu, fi = 0;
+    if (f + lig < w.csf_F) {
+      e = __ldg(w.csf_lptr + f + 1 + lig);
+      fi = __ldg(w.csf_fidx + f + lig);
+    }
+    float4 c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t kj = __shfl_sync(gmask, k, j, 8);
+      c[j] = (uint32_t(j) < n) ? ld_row4(fx.C + size_t(kj) * 8 + lig, pol_r) : f4zero();
+    }
+    // bit p of ebits: a fiber ends after nonzero base+p
+    uint32_t mybit = (e > base && e <= base + n) ? (1u << (e - base - 1)) : 0u;
+    const uint32_t ebits = __reduce_or_sync(gmask, mybit);
+    float4 b[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if ((ebits >> j) & 1u) {
+        uint32_t ord = __popc(ebits & ((1u << j) - 1u));
+        uint32_t fj = __shfl_sync(gmask, fi, ord, 8);
+        b[j] = ld_row4(fx.B + size_t(fj) * 8 + lig, pol_r);
+      } else {
+        b[j] = f4zero();
+      }
+    }
+    // slice ends inside this batch (runs only)
+    uint32_t sbits = 0, se = 0xFFFFFFFFu, si = 0;
+    if (send <= base + n) {
+      if (s + lig < w.csf_S) {
+        se = __ldg(w.csf_send + s + 1 + lig);
+        si = __ldg(w.csf_sidx + s + lig);
+      }
+      uint32_t sb = (se > base && se <= base + n) ? (1u << (se - base - 1)) : 0u;
+      sbits = __reduce_or_sync(gmask, sb);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (uint32_t(j) < n) {
+        float vj = __shfl_sync(gmask, v, j, 8);
+        fa = fma4(vj, c[j], fa);
+        pending = true;
+        if ((ebits >> j) & 1u) {
+          sa = fmav4(fa, b[j], sa);
+          fa = f4zero();
+          pending = false;
+          if ((sbits >> j) & 1u) {
+            uint32_t row = __shfl_sync(gmask, si, __popc(sbits & ((1u << j) - 1u)), 8);
+            fx.out[size_t(row) * 8 + lig] = sa;
+            sa = f4zero();
+          }
+        }
+      }
+    }
+    f += __popc(ebits);
+    if (sbits) {
+      s += __popc(sbits);
+      send = (s < w.csf_S) ? __ldg(w.csf_send + s + 1) : 0xFFFFFFFFu;
+    }
+  }
+  if (chunk) {
+    if (pending) {  // chunk ended inside fiber f
+      uint32_t fj = __ldg(w.csf_fidx + f);
+      sa = fmav4(fa, ld_row4(fx.B + size_t(fj) * 8 + lig, pol_r), sa);
+    }
+    flush_split(w, t.slot, t.nchunk, __ldg(w.csf_sidx + t.s), sa, fx.out, lig, gmask);
+  }
+}
+
+// ------------------------------------------------------------ CSL task --
+__device__ __forceinline__ void csl_task(const Work& w, const Factors3& fx, const Task& t, int lig,
+                                         unsigned gmask, uint64_t pol_s, uint64_t pol_r) {
+  const uint32_t lo = t.lo, hi = t.hi;
+  if (lo >= hi) return;
+  const bool chunk = t.slot != NOSLOT;
+  uint32_t s = t.s;
+  float4 sa = f4zero();
+  uint32_t send = chunk ? 0xFFFFFFFFu : w.csl_send[s + 1];
+  for (uint32_t base = lo; base < hi; base += 8) {
+    const uint32_t n = min(8u, hi - base);
+    uint32_t jx = 0, kx = 0;
+    float v = 0.f;
+    if (lig < n) {
+      jx = ld_stream_u32(w.csl_j + base + lig, pol_s);
+      kx = ld_stream_u32(w.csl_k + base + lig, pol_s);
+      v = ld_stream_f32(w.csl_val + base + lig, pol_s);
+    }
+    float4 b[8], c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t bj = __shfl_sync(gmask, jx, j, 8);
+      uint32_t cj = __shfl_sync(gmask, kx, j, 8);
+      if (uint32_t(j) < n) {
+        b[j] = ld_row4(fx.B + size_t(bj) * 8 + lig, pol_r);
+        c[j] = ld_row4(fx.C + size_t(cj) * 8 + lig, pol_r);
+      } else {
+        b[j] = f4zero();
+        c[j] = f4zero();
+      }
+    }
+    uint32_t sbits = 0, se = 0xFFFFFFFFu, si = 0;
+    if (send <= base + n) {
+      if (s + lig < w.csl_S) {
+        se = __ldg(w.csl_send + s + 1 + lig);
+        si = __ldg(w.csl_sidx + s + lig);
+      }
+      uint32_t sb = (se > base && se <= base + n) ? (1u << (se - base - 1)) : 0u;
+      sbits = __reduce_or_sync(gmask, sb);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (uint32_t(j) < n) {
+        float vj = __shfl_sync(gmask, v, j, 8);
+        sa = fmav4(mul4(vj, b[j]), c[j], sa);
+        if ((sbits >> j) & 1u) {
+          uint32_t row = __shfl_sync(gmask, si, __popc(sbits & ((1u << j) - 1u)), 8);
+          fx.out[size_t(row) * 8 + lig] = sa;
+          sa = f4zero();
+        }
+      }
+    }
+    if (sbits) {
+      s += __popc(sbits);
+      send = (s < w.csl_S) ? __ldg(w.csl_send + s + 1) : 0xFFFFFFFFu;
+    }
+  }
+  if (chunk) flush_split(w, t.slot, t.nchunk, __ldg(w.csl_sidx + t.s), sa, fx.out, lig, gmask);
+}
+
+// ------------------------------------------------------------ COO task --
+__device__ __forceinline__ void coo_task(const Work& w, const Factors3& fx, const Task& t, int lig,
+                                         unsigned gmask, uint64_t pol_s, uint64_t pol_r) {
+  for (uint32_t base = t.lo; base < t.hi; base += 8) {
+    const uint32_t n = min(8u, t.hi - base);
+    uint32_t ix = 0, jx = 0, kx = 0;
+    float v = 0.f;
+    if (lig < n) {
+      ix = ld_stream_u32(w.coo_i + base + lig, pol_s);
+      jx = ld_stream_u32(w.coo_j + base + lig, pol_s);
+      kx = ld_stream_u32(w.coo_k + base + lig, pol_s);
+      v = ld_stream_f32(w.coo_val + base + lig, pol_s);
+    }
+    float4 b[8], c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t bj = __shfl_sync(gmask, jx, j, 8);
+      uint32_t cj = __shfl_sync(gmask, kx, j, 8);
+      if (uint32_t(j) < n) {
+        b[j] = ld_row4(fx.B + size_t(bj) * 8 + lig, pol_r);
+        c[j] = ld_row4(fx.C + size_t(cj) * 8 + lig, pol_r);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t row = __shfl_sync(gmask, ix, j, 8);
+      float vj = __shfl_sync(gmask, v, j, 8);
+      if (uint32_t(j) < n) {
+        float4 r = mul4(vj, b[j]);
+        r.x *= c[j].x;
+        r.y *= c[j].y;
+        r.z *= c[j].z;
+        r.w *= c[j].w;
+        fx.out[size_t(row) * 8 + lig] = r;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void zero_task(const Work& w, const Factors3& fx, const Task& t,
+                                          int lig) {
+  for (uint32_t i = t.lo; i < t.hi; ++i) {
+    uint32_t row = __ldg(w.zero_rows + i);
+    fx.out[size_t(row) * 8 + lig] = f4zero();
+  }
+}
+
+// Persistent kernel: warps pull 4 consecutive tasks at a time (one per group)
+// from a global counter; the last warp out resets the counter.
+__global__ void __launch_bounds__(256) k_mttkrp3_r32(const __grid_constant__ Work w,
+                                                     const __grid_constant__ Factors3 fx) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 3;
+  const int lig = lane & 7;
+  const unsigned gmask = 0xFFu << (8 * g);
+  const uint64_t pol_s = policy_evict_first();
+  const uint64_t pol_r = policy_evict_last();
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(w.ws_ctr, 4u);
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (base >= w.n3) break;
+    const uint32_t ti = base + g;
+    const Task t = w.tasks[ti];
+    if (base < w.n0)
+      csf_task(w, fx, t, lig, gmask, pol_s, pol_r);
+    else if (base < w.n1)
+      csl_task(w, fx, t, lig, gmask, pol_s, pol_r);
+    else if (base < w.n2)
+      coo_task(w, fx, t, lig, gmask, pol_s, pol_r);
+    else
+      zero_task(w, fx, t, lig);
+    __syncwarp();
+  }
+  if (lane == 0) {
+    uint32_t done = atomicAdd(w.ws_ctr + 1, 1u);
+    if (done == w.total_warps - 1) {
+      w.ws_ctr[0] = 0;
+      w.ws_ctr[1] = 0;
+    }
+  }
+}
+
+// --------------------------------------------------------- generic kernel --
+// Any order, any rank: one warp per task, lanes over rank columns, nonzeros
+// walked one at a time.  Used for order > 3 or R != 32 (parity coverage; the
+// benchmark configurations are all order 3, R = 32).
+struct WorkN {
+  int order;
+  int rank;
+  // factors indexed by permuted level (level 0 unused)
+  const float* F[HBK_MAX_ORDER];
+  const float* Fcoo[HBK_MAX_ORDER];  // by original mode
+  int mode;
+  // CSF
+  const uint32_t* csf_anc[HBK_MAX_ORDER];  // level d < order-2 coordinate per fiber (d >= 1)
+  // CSL rest columns
+  const uint32_t* csl_rest[HBK_MAX_ORDER];
+  // COO columns
+  const uint32_t* coo_col[HBK_MAX_ORDER];
+  float* out;
+};
+
+__device__ __forceinline__ void gen_flush_split(const Work& w, const WorkN& wn, uint32_t slot,
+                                                uint32_t nchunk, uint32_t row, int r0, float sa,
+                                                int lane) {
+  const int R = wn.rank;
+  const bool act = r0 + lane < R;
+  float* acc = w.ws_acc + size_t(slot) * R + r0 + lane;
+  if (act) atomicAdd(acc, sa);
+  __threadfence();
+  __syncwarp();
+  uint32_t old = 0;
+  if (lane == 0) old = atomicAdd(w.ws_cnt + slot, 1u);
+  old = __shfl_sync(0xFFFFFFFFu, old, 0);
+  if (old == nchunk - 1) {
+    __threadfence();
+    if (act) {
+      float r = __ldcg(acc);
+      wn.out[size_t(row) * R + r0 + lane] = r;
+      __stcg(acc, 0.f);
+    }
+    __syncwarp();
+    if (lane == 0) w.ws_cnt[slot] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_mttkrp_generic(const __grid_constant__ Work w,
+                                                        const __grid_constant__ WorkN wn) {
+  const int lane = threadIdx.x & 31;
+  const int R = wn.rank;
+  const int N = wn.order;
+  const int nchunks_r = (R + 31) / 32;
+  for (;;) {
+    uint32_t ti = 0;
+    if (lane == 0) ti = atomicAdd(w.ws_ctr, 1u);
+    ti = __shfl_sync(0xFFFFFFFFu, ti, 0);
+    if (ti >= w.n3) break;
+    const Task t = w.tasks[ti];
+    if (t.lo >= t.hi) continue;
+    const bool chunk = t.slot != NOSLOT;
+    for (int rc = 0; rc < nchunks_r; ++rc) {
+      const int r = rc * 32 + lane;
+      const bool act = r < R;
+      if (ti < w.n0) {  // CSF
+        uint32_t s = t.s, f = t.f;
+        uint32_t fend = w.csf_lptr[f + 1];
+        uint32_t send = w.csf_send[s + 1];
+        float fa = 0.f, sa = 0.f;
+        for (uint32_t i = t.lo; i < t.hi; ++i) {
+          uint32_t k = w.csf_leaf[i];
+          float v = w.csf_val[i];
+          if (act) fa = fmaf(v, wn.F[N - 1][size_t(k) * R + r], fa);
+          if (i + 1 == fend) {
+            float m = 1.f;
+            if (act) {
+              m = wn.F[N - 2][size_t(w.csf_fidx[f]) * R + r];
+              for (int d = 1; d < N - 2; ++d) m *= wn.F[d][size_t(wn.csf_anc[d][f]) * R + r];
+            }
+            sa = fmaf(fa, m, sa);
+            fa = 0.f;
+            ++f;
+            if (f < w.csf_F) fend = w.csf_lptr[f + 1];
+            if (!chunk && i + 1 == send) {
+              if (act) wn.out[size_t(w.csf_sidx[s]) * R + r] = sa;
+              sa = 0.f;
+              ++s;
+              if (s < w.csf_S) send = w.csf_send[s + 1];
+            }
+          }
+        }
+        if (chunk) {
+          if (t.hi != w.csf_lptr[f]) {  // ended inside fiber f
+            float m = 1.f;
+            if (act) {
+              m = wn.F[N - 2][size_t(w.csf_fidx[f]) * R + r];
+              for (int d = 1; d < N - 2; ++d) m *= wn.F[d][size_t(wn.csf_anc[d][f]) * R + r];
+            }
+            sa = fmaf(fa, m, sa);
+          }
+          gen_flush_split(w, wn, t.slot, t.nchunk, w.csf_sidx[t.s], rc * 32, sa, lane);
+        }
+      } else if (ti < w.n1) {  // CSL
+        uint32_t s = t.s;
+        uint32_t send = w.csl_send[s + 1];
+        float sa = 0.f;
+        for (uint32_t i = t.lo; i < t.hi; ++i) {
+          if (act) {
+            float p = w.csl_val[i];
+            for (int c = 0; c < N - 1; ++c) p *= wn.F[c + 1][size_t(wn.csl_rest[c][i]) * R + r];
+            sa += p;
+          }
+          if (!chunk && i + 1 == send) {
+            if (act) wn.out[size_t(w.csl_sidx[s]) * R + r] = sa;
+            sa = 0.f;
+            ++s;
+            if (s < w.csl_S) send = w.csl_send[s + 1];
+          }
+        }
+        if (chunk) gen_flush_split(w, wn, t.slot, t.nchunk, w.csl_sidx[t.s], rc * 32, sa, lane);
+      } else if (ti < w.n2) {  // COO (unique rows)
+        for (uint32_t i = t.lo; i < t.hi; ++i) {
+          if (!act) continue;
+          float p = w.coo_val[i];
+          for (int d = 0; d < N; ++d)
+            if (d != wn.mode) p *= wn.Fcoo[d][size_t(wn.coo_col[d][i]) * R + r];
+          wn.out[size_t(wn.coo_col[wn.mode][i]) * R + r] = p;
+        }
+      } else {  // ZERO
+        for (uint32_t i = t.lo; i < t.hi; ++i)
+          if (act) wn.out[size_t(w.zero_rows[i]) * R + r] = 0.f;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    uint32_t done = atomicAdd(w.ws_ctr + 1, 1u);
+    if (done == w.total_warps - 1) {
+      w.ws_ctr[0] = 0;
+      w.ws_ctr[1] = 0;
+    }
+  }
+}
+
+// ------------------------------------------------------- plan building --
+// Slice nonzero offsets of the CSF bucket (leaf_offsets, formats.py:109-111)
+// and the first fiber of every slice (fiber_positions, :102-107).
+struct Chain2 {
+  const uint32_t* ptr[HBK_MAX_ORDER];
+  int nlev;
+};
+__global__ void k_csf_slice_offsets(Chain2 ch, int64_t S, uint32_t* __restrict__ fpos,
+                                    uint32_t* __restrict__ loff) {
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s <= S;
+       s += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t p = uint32_t(s);
+    for (int d = 0; d < ch.nlev - 1; ++d) p = ch.ptr[d][p];
+    fpos[s] = p;
+    loff[s] = ch.ptr[ch.nlev - 1][p];
+  }
+}
+
+// Per slice: number of tasks it opens (chunks of a heavy slice, or 1 if it
+// starts a new run of light slices) and whether it needs an accumulator slot.
+__global__ void k_task_count(const uint32_t* __restrict__ loff, int64_t S, uint32_t T,
+                             uint32_t* __restrict__ cnt, uint32_t* __restrict__ slotf) {
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < S;
+       s += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t a = loff[s], m = loff[s + 1] - a;
+    if (m > T) {
+      cnt[s] = (m + T - 1) / T;
+      slotf[s] = 1;
+    } else {
+      bool start = true;
+      if (s > 0) {
+        uint32_t pa = loff[s - 1], pm = a - pa;
+        start = (pm > T) || (pa / T != a / T);
+      }
+      cnt[s] = start;
+      slotf[s] = 0;
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t fiber_of(const uint32_t* __restrict__ lptr, uint32_t fb,
+                                             uint32_t fe, uint32_t pos) {
+  // last f in [fb, fe) with lptr[f] <= pos
+  uint32_t lo = fb, hi = fe;
+  while (hi - lo > 1) {
+    uint32_t mid = lo + (hi - lo) / 2;
+    if (lptr[mid] <= pos)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_task_fill(const uint32_t* __restrict__ loff, const uint32_t* __restrict__ fpos,
+                            const uint32_t* __restrict__ lptr, int64_t S, uint32_t T,
+                            const uint32_t* __restrict__ toff, const uint32_t* __restrict__ slot,
+                            Task* __restrict__ tasks) {
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < S;
+       s += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t a = loff[s], m = loff[s + 1] - a;
+    uint32_t nt = toff[s + 1] - toff[s];
+    if (nt == 0) continue;
+    if (m > T) {
+      for (uint32_t c = 0; c < nt; ++c) {
+        Task t{};
+        t.lo = a + uint32_t((uint64_t(m) * c) / nt);
+        t.hi = a + uint32_t((uint64_t(m) * (c + 1)) / nt);
+        t.s = uint32_t(s);
+        t.f = fpos ? fiber_of(lptr, fpos[s], fpos[s + 1], t.lo) : 0;
+        t.slot = slot[s];
+        t.nchunk = nt;
+        tasks[toff[s] + c] = t;
+      }
+    } else {
+      Task t{};
+      t.lo = a;
+      t.hi = 0;  // fixed up by k_task_hi
+      t.s = uint32_t(s);
+      t.f = fpos ? fpos[s] : 0;
+      t.slot = NOSLOT;
+      t.nchunk = 1;
+      tasks[toff[s]] = t;
+    }
+  }
+}
+
+__global__ void k_task_hi(Task* __restrict__ tasks, int64_t n, uint32_t M) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    if (tasks[i].slot == NOSLOT) tasks[i].hi = (i + 1 < n) ? tasks[i + 1].lo : M;
+  }
+}
+
+// Schedule-driven CSF tasks (mttkrp_scheduled, kernels.py:256-342): one task
+// per BlockSchedule unit.
+__global__ void k_units_per_slice(const uint32_t* __restrict__ units, int64_t U,
+                                  uint32_t* __restrict__ cnt) {
+  for (int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; u < U;
+       u += int64_t(gridDim.x) * blockDim.x)
+    atomicAdd(cnt + units[3 * u], 1u);
+}
+__global__ void k_slot_flags(const uint32_t* __restrict__ cnt, int64_t S,
+                             uint32_t* __restrict__ f) {
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < S;
+       s += int64_t(gridDim.x) * blockDim.x)
+    f[s] = cnt[s] > 1;
+}
+__global__ void k_units_to_tasks(const uint32_t* __restrict__ units, int64_t U,
+                                 const uint32_t* __restrict__ lptr, const uint32_t* __restrict__ cnt,
+                                 const uint32_t* __restrict__ slot, Task* __restrict__ tasks) {
+  for (int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; u < U;
+       u += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t sp = units[3 * u], fs = units[3 * u + 1], ft = units[3 * u + 2];
+    Task t{};
+    t.lo = lptr[fs];
+    t.hi = lptr[ft];
+    t.s = sp;
+    t.f = fs;
+    t.slot = cnt[sp] > 1 ? slot[sp] : NOSLOT;
+    t.nchunk = cnt[sp];
+    tasks[u] = t;
+  }
+}
+
+__global__ void k_mark_rows(const uint32_t* __restrict__ rows, int64_t n,
+                            uint8_t* __restrict__ mark) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    mark[rows[i]] = 1;
+}
+__global__ void k_unmarked_flags(const uint8_t* __restrict__ mark, int64_t n,
+                                 uint32_t* __restrict__ f) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    f[i] = mark[i] == 0;
+}
+__global__ void k_unmarked_emit(const uint32_t* __restrict__ pos, int64_t n,
+                                uint32_t* __restrict__ rows) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    if (pos[i + 1] != pos[i]) rows[pos[i]] = uint32_t(i);
+}
+__global__ void k_range_tasks(Task* __restrict__ tasks, int64_t ntask, uint32_t total,
+                              uint32_t step) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < ntask;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    Task t{};
+    t.lo = min(total, uint32_t(i) * step);
+    t.hi = min(total, uint32_t(i + 1) * step);
+    t.slot = NOSLOT;
+    t.nchunk = 1;
+    tasks[i] = t;
+  }
+}
+__global__ void k_empty_tasks(Task* __restrict__ tasks, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    Task t{};
+    t.slot = NOSLOT;
+    t.nchunk = 1;
+    tasks[i] = t;
+  }
+}
+
+}  // namespace hbk
+
+struct hbk_plan {
+  int order = 0, mode = 0, rank = 0;
+  int64_t dims[HBK_MAX_ORDER] = {0};
+  int mo[HBK_MAX_ORDER] = {0};
+  hbk_coo* coo = nullptr;
+  hbk_csl* csl = nullptr;
+  hbk_csf* csf = nullptr;
+  hbk_sched* sched = nullptr;
+  hbk::Buf tasks, zero_rows, csf_send, ws;
+  hbk::Work work{};
+  bool fast = false;
+  int grid = 0, block = 256;
+  hbk_plan_info info{};
+  ~hbk_plan() {
+    hbk_coo_release(coo);
+    hbk_csl_release(csl);
+    hbk_csf_release(csf);
+    hbk_sched_release(sched);
+  }
+};
+
+namespace hbk {
+
+static int64_t pad_to(int64_t n, int64_t m) { return (n + m - 1) / m * m; }
+
+// Tasks of one slice-structured bucket (CSF with fpos/lptr, or CSL).
+struct BucketTasks {
+  Scratch tasks;
+  int64_t n = 0;
+  int64_t slots = 0;
+};
+
+static BucketTasks bucket_tasks(const uint32_t* loff, const uint32_t* fpos, const uint32_t* lptr,
+                                int64_t S, uint32_t M, uint32_t T, cudaStream_t st) {
+  BucketTasks bt;
+  if (S == 0) return bt;
+  Scratch cnt((S + 1) * sizeof(uint32_t), st), slot((S + 1) * sizeof(uint32_t), st);
+  k_task_count<<<grid_for(S, 256), 256, 0, st>>>(loff, S, T, cnt.as<uint32_t>(),
+                                                 slot.as<uint32_t>());
+  check_launch("k_task_count");
+  uint32_t n = exclusive_scan_total(cnt.as<uint32_t>(), S, st);
+  uint32_t nslot = exclusive_scan_total(slot.as<uint32_t>(), S, st);
+  bt.tasks = Scratch(size_t(n) * sizeof(Task), st);
+  k_task_fill<<<grid_for(S, 128), 128, 0, st>>>(loff, fpos, lptr, S, T, cnt.as<uint32_t>(),
+                                                slot.as<uint32_t>(), bt.tasks.as<Task>());
+  check_launch("k_task_fill");
+  k_task_hi<<<grid_for(n, 256), 256, 0, st>>>(bt.tasks.as<Task>(), n, M);
+  check_launch("k_task_hi");
+  bt.n = n;
+  bt.slots = nslot;
+  return bt;
+}
+
+__global__ void k_shift_slots(Task* __restrict__ t, int64_t n, uint32_t base) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    if (t[i].slot != NOSLOT) t[i].slot += base;
+}
+
+static void build_plan(hbk_plan* p, cudaStream_t st) {
+  const int N = p->order;
+  const int R = p->rank;
+  // fast path: order 3, R = 32 (8 lanes x float4 per row)
+  p->fast = (N == 3 && R == 32);
+  const int gpw = p->fast ? 4 : 1;
+  const uint32_t Tcsf = p->fast ? TASK_NNZ_CSF : GEN_TASK_NNZ;
+  const uint32_t Tcsl = p->fast ? TASK_NNZ_CSL : GEN_TASK_NNZ;
+  const uint32_t Tcoo = p->fast ? TASK_NNZ_COO : GEN_TASK_NNZ;
+
+  Work& w = p->work;
+  std::memset(&w, 0, sizeof(w));
+  BucketTasks tcsf, tcsl;
+  int64_t n_coo = 0, n_zero = 0;
+  int64_t slots = 0;
+  int64_t stream_bytes = 0;
+  int64_t muls = 0, adds = 0;
+
+  if (p->csf && p->csf->M > 0) {
+    hbk_csf* c = p->csf;
+    const int64_t S = c->n[0];
+    const int L = N - 2;
+    Chain2 ch{};
+    ch.nlev = N - 1;
+    for (int d = 0; d < N - 1; ++d) ch.ptr[d] = c->ptr[d].as<uint32_t>();
+    p->csf_send = dalloc((S + 1) * sizeof(uint32_t), st);
+    Scratch fpos((S + 1) * sizeof(uint32_t), st);
+    k_csf_slice_offsets<<<grid_for(S + 1, 256), 256, 0, st>>>(ch, S, fpos.as<uint32_t>(),
+                                                              p->csf_send.as<uint32_t>());
+    check_launch("k_csf_slice_offsets");
+    if (p->sched) {
+      hbk_sched* sc = p->sched;
+      HBK_REQUIRE(sc->S == S && sc->F == c->n[L], HBK_EINVAL,
+                  "schedule was built for a different tree");
+      Scratch cnt((S + 1) * sizeof(uint32_t), st), slot((S + 1) * sizeof(uint32_t), st);
+      HBK_CUDA(cudaMemsetAsync(cnt.p, 0, (S + 1) * sizeof(uint32_t), st));
+      if (sc->U) {
+        k_units_per_slice<<<grid_for(sc->U, 256), 256, 0, st>>>(sc->units.as<uint32_t>(), sc->U,
+                                                                cnt.as<uint32_t>());
+        check_launch("k_units_per_slice");
+      }
+      k_slot_flags<<<grid_for(S, 256), 256, 0, st>>>(cnt.as<uint32_t>(), S, slot.as<uint32_t>());
+      check_launch("k_slot_flags");
+      uint32_t nslot = exclusive_scan_total(slot.as<uint32_t>(), S, st);
+      tcsf.tasks = Scratch(size_t(sc->U) * sizeof(Task), st);
+      if (sc->U) {
+        k_units_to_tasks<<<grid_for(sc->U, 256), 256, 0, st>>>(
+            sc->units.as<uint32_t>(), sc->U, c->ptr[L].as<uint32_t>(), cnt.as<uint32_t>(),
+            slot.as<uint32_t>(), tcsf.tasks.as<Task>());
+        check_launch("k_units_to_tasks");
+      }
+      tcsf.n = sc->U;
+      tcsf.slots = nslot;
+      // OpCount of mttkrp_scheduled (kernels.py:283-298, 325-330)
+      int64_t mid = 0;
+      if (N > 3) {
+        // mid-level nodes per unit, computed on the host from the exported
+        // pointer arrays (order > 3 only; small parity cases)
+        std::vector<std::vector<uint32_t>> ptr(N - 1);
+        for (int d = 0; d < N - 1; ++d) {
+          ptr[d].resize(c->n[d] + 1);
+          HBK_CUDA(cudaMemcpyAsync(ptr[d].data(), c->ptr[d].p, (c->n[d] + 1) * 4,
+                                   cudaMemcpyDeviceToHost, st));
+        }
+        std::vector<uint32_t> hu(sc->U * 3);
+        if (sc->U)
+          HBK_CUDA(cudaMemcpyAsync(hu.data(), sc->units.p, hu.size() * 4, cudaMemcpyDeviceToHost,
+                                   st));
+        HBK_CUDA(cudaStreamSynchronize(st));
+        for (int64_t u = 0; u < sc->U; ++u) {
+          uint32_t lo = hu[3 * u + 1], hi = hu[3 * u + 2];
+          for (int d = N - 3; d >= 1; --d) {
+            const auto& pd = ptr[d];
+            int64_t a = std::upper_bound(pd.begin(), pd.end(), lo) - pd.begin() - 1;
+            int64_t b = std::lower_bound(pd.begin(), pd.end(), hi) - pd.begin();
+            mid += b - a;
+            lo = uint32_t(a);
+            hi = uint32_t(b);
+          }
+        }
+      }
+      muls += (c->M + c->n[L] + mid) * R;
+      adds += (c->M + mid + sc->U) * R;
+    } else {
+      tcsf = bucket_tasks(p->csf_send.as<uint32_t>(), fpos.as<uint32_t>(),
+                          c->ptr[L].as<uint32_t>(), S, uint32_t(c->M), Tcsf, st);
+      // OpCount of mttkrp_csf (kernels.py:173-185)
+      int64_t m = c->M, a = c->M;
+      for (int d = N - 2; d >= 1; --d) {
+        m += c->n[d];
+        if (d < N - 2) a += c->n[d];
+      }
+      a += c->n[0];
+      muls += m * R;
+      adds += a * R;
+    }
+    slots += tcsf.slots;
+    w.csf_send = p->csf_send.as<uint32_t>();
+    w.csf_sidx = c->idx[0].as<uint32_t>();
+    w.csf_lptr = c->ptr[L].as<uint32_t>();
+    w.csf_fidx = c->idx[L].as<uint32_t>();
+    w.csf_leaf = c->leaf.as<uint32_t>();
+    w.csf_val = c->v32.as<float>();
+    w.csf_F = uint32_t(c->n[L]);
+    w.csf_S = uint32_t(S);
+    stream_bytes += 8 * c->M + 8 * c->n[L] + 8 * S;
+  }
+  if (p->csl && p->csl->M > 0) {
+    hbk_csl* s = p->csl;
+    tcsl = bucket_tasks(s->slice_ptr.as<uint32_t>(), nullptr, nullptr, s->S, uint32_t(s->M), Tcsl,
+                        st);
+    if (tcsl.slots) {
+      k_shift_slots<<<grid_for(tcsl.n, 256), 256, 0, st>>>(tcsl.tasks.as<Task>(), tcsl.n,
+                                                           uint32_t(slots));
+      check_launch("k_shift_slots");
+    }
+    slots += tcsl.slots;
+    w.csl_send = s->slice_ptr.as<uint32_t>();
+    w.csl_sidx = s->slice_idx.as<uint32_t>();
+    w.csl_j = s->rest[0].as<uint32_t>();
+    w.csl_k = N >= 3 ? s->rest[1].as<uint32_t>() : nullptr;
+    w.csl_val = s->v32.as<float>();
+    w.csl_S = uint32_t(s->S);
+    muls += int64_t(N - 1) * s->M * R;
+    adds += s->M * R;
+    stream_bytes += 4 * int64_t(N) * s->M + 8 * s->S;
+  }
+  if (p->coo && p->coo->nnz > 0) {
+    hbk_coo* t = p->coo;
+    n_coo = (t->nnz + Tcoo - 1) / Tcoo;
+    w.coo_i = t->cols[p->mode].as<uint32_t>();
+    w.coo_j = t->cols[p->mo[1]].as<uint32_t>();
+    w.coo_k = t->cols[p->mo[2]].as<uint32_t>();
+    w.coo_val = t->v32.as<float>();
+    muls += int64_t(N - 1) * t->nnz * R;
+    adds += t->nnz * R;
+    stream_bytes += 4 * int64_t(N + 1) * t->nnz;
+  }
+  // rows owned by no bucket
+  const int64_t rows = p->dims[p->mode];
+  {
+    Scratch mark(rows, st);
+    HBK_CUDA(cudaMemsetAsync(mark.p, 0, rows, st));
+    if (p->csf && p->csf->n[0]) {
+      k_mark_rows<<<grid_for(p->csf->n[0], 256), 256, 0, st>>>(p->csf->idx[0].as<uint32_t>(),
+                                                               p->csf->n[0], mark.as<uint8_t>());
+      check_launch("k_mark_rows");
+    }
+    if (p->csl && p->csl->S) {
+      k_mark_rows<<<grid_for(p->csl->S, 256), 256, 0, st>>>(p->csl->slice_idx.as<uint32_t>(),
+                                                            p->csl->S, mark.as<uint8_t>());
+      check_launch("k_mark_rows");
+    }
+    if (p->coo && p->coo->nnz) {
+      k_mark_rows<<<grid_for(p->coo->nnz, 256), 256, 0, st>>>(
+          p->coo->cols[p->mode].as<uint32_t>(), p->coo->nnz, mark.as<uint8_t>());
+      check_launch("k_mark_rows");
+    }
+    Scratch pos((rows + 1) * sizeof(uint32_t), st);
+    k_unmarked_flags<<<grid_for(rows, 256), 256, 0, st>>>(mark.as<uint8_t>(), rows,
+                                                          pos.as<uint32_t>());
+    check_launch("k_unmarked_flags");
+    uint32_t Z = exclusive_scan_total(pos.as<uint32_t>(), rows, st);
+    p->zero_rows = dalloc(size_t(Z) * sizeof(uint32_t), st);
+    if (Z) {
+      k_unmarked_emit<<<grid_for(rows, 256), 256, 0, st>>>(pos.as<uint32_t>(), rows,
+                                                           p->zero_rows.as<uint32_t>());
+      check_launch("k_unmarked_emit");
+    }
+    n_zero = (Z + TASK_ROWS_ZERO - 1) / TASK_ROWS_ZERO;
+    w.zero_rows = p->zero_rows.as<uint32_t>();
+    p->info.tasks_zero = n_zero;
+    // assemble [CSF | CSL | COO | ZERO], each padded to a multiple of gpw
+    const int64_t a0 = pad_to(tcsf.n, gpw), a1 = pad_to(tcsl.n, gpw), a2 = pad_to(n_coo, gpw),
+                  a3 = pad_to(n_zero, gpw);
+    const int64_t total = a0 + a1 + a2 + a3;
+    p->tasks = dalloc(std::max<int64_t>(total, 1) * sizeof(Task), st);
+    Task* T = p->tasks.as<Task>();
+    if (total) {
+      k_empty_tasks<<<grid_for(total, 256), 256, 0, st>>>(T, total);
+      check_launch("k_empty_tasks");
+    }
+    if (tcsf.n)
+      HBK_CUDA(cudaMemcpyAsync(T, tcsf.tasks.p, tcsf.n * sizeof(Task), cudaMemcpyDeviceToDevice,
+                               st));
+    if (tcsl.n)
+      HBK_CUDA(cudaMemcpyAsync(T + a0, tcsl.tasks.p, tcsl.n * sizeof(Task),
+                               cudaMemcpyDeviceToDevice, st));
+    if (n_coo) {
+      k_range_tasks<<<grid_for(n_coo, 256), 256, 0, st>>>(T + a0 + a1, n_coo,
+                                                          uint32_t(p->coo->nnz), Tcoo);
+      check_launch("k_range_tasks");
+    }
+    if (n_zero) {
+      k_range_tasks<<<grid_for(n_zero, 256), 256, 0, st>>>(T + a0 + a1 + a2, n_zero, Z,
+                                                           TASK_ROWS_ZERO);
+      check_launch("k_range_tasks");
+    }
+    w.n0 = uint32_t(a0);
+    w.n1 = uint32_t(a0 + a1);
+    w.n2 = uint32_t(a0 + a1 + a2);
+    w.n3 = uint32_t(total);
+    w.tasks = T;
+    p->info.tasks_csf = tcsf.n;
+    p->info.tasks_csl = tcsl.n;
+    p->info.tasks_coo = n_coo;
+  }
+  // workspace: [ctr(2) pad to 32 words][cnt slots][acc slots x R]
+  const size_t cnt_off = 32 * sizeof(uint32_t);
+  const size_t acc_off = pad_to(cnt_off + slots * sizeof(uint32_t), 256);
+  const size_t ws_bytes = acc_off + size_t(slots) * R * sizeof(float);
+  p->ws = dalloc(ws_bytes, st);
+  HBK_CUDA(cudaMemsetAsync(p->ws.p, 0, ws_bytes, st));
+  w.ws_ctr = reinterpret_cast<uint32_t*>(p->ws.as<char>());
+  w.ws_cnt = reinterpret_cast<uint32_t*>(p->ws.as<char>() + cnt_off);
+  w.ws_acc = reinterpret_cast<float*>(p->ws.as<char>() + acc_off);
+
+  // persistent grid: as many CTAs as fit, a multiple of the SM count
+  int dev = 0, sms = 0, per_sm = 0;
+  HBK_CUDA(cudaGetDevice(&dev));
+  HBK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (p->fast) {
+    HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp3_r32, p->block, 0));
+  } else {
+    HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp_generic, p->block, 0));
+  }
+  per_sm = std::max(per_sm, 1);
+  int64_t want = int64_t(sms) * per_sm;
+  const int64_t warps_needed = (int64_t(w.n3) + gpw - 1) / gpw;
+  const int64_t blocks_needed = std::max<int64_t>(1, (warps_needed + 7) / 8);
+  p->grid = int(std::min(want, blocks_needed));
+  w.total_warps = uint32_t(p->grid) * (p->block / 32);
+
+  p->info.mode = p->mode;
+  p->info.rank = R;
+  p->info.out_rows = rows;
+  p->info.split_rows = slots;
+  p->info.launches = 1;
+  p->info.fast_path = p->fast;
+  int64_t nnz = 0;
+  if (p->csf) nnz += p->csf->M;
+  if (p->csl) nnz += p->csl->M;
+  if (p->coo) nnz += p->coo->nnz;
+  p->info.nnz = nnz;
+  if (nnz == 0) muls = adds = 0;
+  p->info.op_muls = muls;
+  p->info.op_adds = adds;
+  p->info.stream_bytes = stream_bytes;
+  HBK_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace hbk
+
+using namespace hbk;
+
+extern "C" {
+
+int hbk_plan_create(hbk_coo* coo, hbk_csl* csl, hbk_csf* csf, hbk_sched* sched, int mode, int rank,
+                    void* stream, hbk_plan** out) {
+  return guarded([&] {
+    cudaStream_t st = to_stream(stream);
+    HBK_REQUIRE(rank >= 1, HBK_EINVAL, "rank must be at least 1");
+    HBK_REQUIRE(coo || csl || csf, HBK_EINVAL, "plan needs at least one bucket");
+    HBK_REQUIRE(!sched || csf, HBK_EINVAL, "a schedule needs a CSF bucket");
+    int order = 0;
+    const int64_t* dims = nullptr;
+    const int* mo = nullptr;
+    if (csf) {
+      order = csf->order;
+      dims = csf->dims;
+      mo = csf->mode_order;
+    } else if (csl) {
+      order = csl->order;
+      dims = csl->dims;
+      mo = csl->mode_order;
+    } else {
+      order = coo->order;
+      dims = coo->dims;
+      mo = coo->sorted_under;
+    }
+    HBK_REQUIRE(mode >= 0 && mode < order, HBK_EINVAL, "mode out of range");
+    if (csf)
+      HBK_REQUIRE(csf->mode_order[0] == mode, HBK_EINVAL,
+                  "tree was built for mode " + std::to_string(csf->mode_order[0]) +
+                      ", asked for mode " + std::to_string(mode));
+    if (csl)
+      HBK_REQUIRE(csl->mode_order[0] == mode, HBK_EINVAL,
+                  "slices were built for mode " + std::to_string(csl->mode_order[0]) +
+                      ", asked for mode " + std::to_string(mode));
+    if (coo)
+      HBK_REQUIRE(coo->unique_mode == mode && coo->has_sorted, HBK_EINVAL,
+                  "a COO bucket must be an HB-CSF coo_part of this mode");
+    hbk_plan* p = new hbk_plan();
+    std::unique_ptr<hbk_plan> guard(p);
+    p->order = order;
+    p->mode = mode;
+    p->rank = rank;
+    std::copy(dims, dims + order, p->dims);
+    std::copy(mo, mo + order, p->mo);
+    p->coo = coo;
+    p->csl = csl;
+    p->csf = csf;
+    p->sched = sched;
+    hbk_coo_retain(coo);
+    hbk_csl_retain(csl);
+    hbk_csf_retain(csf);
+    hbk_sched_retain(sched);
+    build_plan(p, st);
+    *out = guard.release();
+  });
+}
+
+int hbk_plan_info_get(const hbk_plan* p, hbk_plan_info* info) {
+  return guarded([&] { *info = p->info; });
+}
+
+int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = to_stream(stream);
+    const int N = p->order;
+    for (int d = 0; d < N; ++d)
+      HBK_REQUIRE(d == p->mode || factors[d] != nullptr, HBK_EINVAL, "null factor pointer");
+    HBK_REQUIRE(out != nullptr || p->dims[p->mode] == 0, HBK_EINVAL, "null output pointer");
+    if (p->fast) {
+      Factors3 fx;
+      fx.B = reinterpret_cast<const float4*>(factors[p->mo[1]]);
+      fx.C = reinterpret_cast<const float4*>(factors[p->mo[2]]);
+      fx.out = reinterpret_cast<float4*>(out);
+      HBK_REQUIRE((reinterpret_cast<uintptr_t>(fx.B) | reinterpret_cast<uintptr_t>(fx.C) |
+                   reinterpret_cast<uintptr_t>(out)) %
+                          16 ==
+                      0,
+                  HBK_EINVAL, "factor and output buffers must be 16-byte aligned");
+      k_mttkrp3_r32<<<p->grid, p->block, 0, st>>>(p->work, fx);
+      check_launch("k_mttkrp3_r32");
+    } else {
+      WorkN wn{};
+      wn.order = N;
+      wn.rank = p->rank;
+      wn.mode = p->mode;
+      for (int d = 0; d < N; ++d) {
+        wn.F[d] = factors[p->mo[d]];
+        wn.Fcoo[d] = factors[d];
+      }
+      if (p->csf)
+        for (int d = 1; d < N - 2; ++d) wn.csf_anc[d] = p->csf->anc[d].as<uint32_t>();
+      if (p->csl)
+        for (int c = 0; c < N - 1; ++c) wn.csl_rest[c] = p->csl->rest[c].as<uint32_t>();
+      if (p->coo)
+        for (int d = 0; d < N; ++d) wn.coo_col[d] = p->coo->cols[d].as<uint32_t>();
+      wn.out = out;
+      k_mttkrp_generic<<<p->grid, p->block, 0, st>>>(p->work, wn);
+      check_launch("k_mttkrp_generic");
+    }
+  });
+}
+
+void hbk_plan_release(hbk_plan* p) { delete p; }
+
+}  // extern "C"

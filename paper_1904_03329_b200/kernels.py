@@ -1,0 +1,241 @@
+"""MTTKRP over each storage format, on the GPU.
+
+Mirrors ``tenkit.kernels`` (pkg/src/tenkit/kernels.py): same function names,
+signatures, argument checks, exceptions and ``OpCount`` integers.  Every call
+runs libhbk's sm_100a kernel (one persistent launch per call; see
+csrc/mttkrp.cu).  There is no CPU path: without libhbk.so or a CUDA device
+the calls raise.
+
+Factor matrices may be NumPy arrays (the reference's calling convention:
+uploaded as fp32, result returned as a float64 ``np.ndarray``) or CUDA
+tensors (fp32, row-major; the result is then a CUDA fp32 tensor and nothing
+leaves the device).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as N
+from .coo import CooTensor
+from .formats import CslSlices, CsfTensor, HbCsfTensor
+
+Factors = Sequence
+
+
+@dataclass(frozen=True)
+class OpCount:
+    """Floating-point multiply and add counts (kernels.py:44-59)."""
+
+    muls: int
+    adds: int
+
+    @property
+    def total(self) -> int:
+        return self.muls + self.adds
+
+    def __add__(self, other: "OpCount") -> "OpCount":
+        return OpCount(self.muls + other.muls, self.adds + other.adds)
+
+    def to_dict(self) -> dict:
+        return {"muls": self.muls, "adds": self.adds, "total": self.total}
+
+
+def _is_device(f) -> bool:
+    return type(f).__module__.startswith("torch") and getattr(f, "is_cuda", False)
+
+
+def _check_factors(dims: tuple[int, ...], factors: Factors, mode: int, check_finite: bool = True) -> int:
+    """Validate factor shapes against dims; factors[mode] is not inspected
+    (kernels.py:62-88).  Returns the shared rank R."""
+    if not 0 <= mode < len(dims):
+        raise ValueError(f"mode {mode} out of range for order {len(dims)}")
+    if len(factors) != len(dims):
+        raise ValueError(f"expected {len(dims)} factor matrices, got {len(factors)}")
+    rank = None
+    for d, f in enumerate(factors):
+        if d == mode:
+            continue
+        if _is_device(f):
+            shape = tuple(f.shape)
+            finite = (lambda f=f: bool(f.isfinite().all()))
+        else:
+            f = np.asarray(f)
+            shape = f.shape
+            finite = (lambda f=f: bool(np.isfinite(f).all()))
+        if len(shape) != 2 or shape[0] != dims[d]:
+            raise ValueError(f"factor {d} must have shape ({dims[d]}, R), got {shape}")
+        if rank is None:
+            rank = int(shape[1])
+        elif shape[1] != rank:
+            raise ValueError("factor matrices disagree on rank")
+        if check_finite and not finite():
+            raise ValueError(f"factor {d} has non-finite entries")
+    assert rank is not None
+    return rank
+
+
+def _device_factors(factors: Factors, mode: int):
+    """fp32 contiguous CUDA copies/views of the non-mode factors + pointer array."""
+    torch = N.require_device()
+    keep = []
+    ptrs = (C.c_void_p * len(factors))()
+    on_device = True
+    for d, f in enumerate(factors):
+        if d == mode:
+            ptrs[d] = None
+            continue
+        if _is_device(f):
+            t = f if (f.dtype == torch.float32 and f.is_contiguous()) else f.to(torch.float32).contiguous()
+        else:
+            on_device = False
+            t = torch.from_numpy(np.ascontiguousarray(f, dtype=np.float32)).cuda(non_blocking=False)
+        if t.data_ptr() % 16:
+            t = t.clone()
+        keep.append(t)
+        ptrs[d] = t.data_ptr()
+    return ptrs, keep, on_device
+
+
+class _Plan:
+    """A libhbk plan (work list for one mode/rank/bucket set) plus its info."""
+
+    __slots__ = ("h", "info", "rows", "rank")
+
+    def __init__(self, coo, csl, csf, sched, mode: int, rank: int, rows: int):
+        out = N.new_out()
+        N.call("hbk_plan_create", coo, csl, csf, sched, int(mode), int(rank), N.stream_ptr(),
+               C.byref(out))
+        self.h = N.Handle(out, "hbk_plan_release")
+        info = N.PlanInfo()
+        N.call("hbk_plan_info_get", self.h.ptr, C.byref(info))
+        self.info = info
+        self.rows = rows
+        self.rank = rank
+
+    @property
+    def opcount(self) -> OpCount:
+        return OpCount(int(self.info.op_muls), int(self.info.op_adds))
+
+    def execute(self, factor_ptrs, out=None):
+        torch = N.require_device()
+        if out is None:
+            out = torch.empty((self.rows, self.rank), dtype=torch.float32, device="cuda")
+        N.call("hbk_plan_execute", self.h.ptr, factor_ptrs, C.c_void_p(out.data_ptr()),
+               N.stream_ptr())
+        return out
+
+
+def _get_plan(owner, key, build):
+    plan = owner._plans.get(key)
+    if plan is None:
+        plan = build()
+        owner._plans[key] = plan
+    return plan
+
+
+def _finish(plan: _Plan, factors, mode: int, out=None):
+    ptrs, keep, on_device = _device_factors(factors, mode)
+    y = plan.execute(ptrs, out)
+    if on_device:
+        return y, plan.opcount
+    return y.double().cpu().numpy(), plan.opcount
+
+
+def plan_for(rep, mode: int, rank: int, schedule=None) -> _Plan:
+    """The cached libhbk plan that ``mttkrp(rep, ..., mode)`` executes."""
+    dims = rep.dims
+    if isinstance(rep, HbCsfTensor):
+        sh = schedule._device_for(rep.csf_part) if schedule is not None else None
+        key = (mode, rank, None if sh is None else sh.ptr.value)
+        return _get_plan(rep, key, lambda: _Plan(
+            rep.coo_part._dev().ptr if rep.coo_part.nnz else None,
+            rep.csl_part._h.ptr, rep.csf_part._h.ptr, None if sh is None else sh.ptr,
+            mode, rank, dims[mode]))
+    if isinstance(rep, CsfTensor):
+        sh = schedule._device_for(rep) if schedule is not None else None
+        key = (mode, rank, None if sh is None else sh.ptr.value)
+        return _get_plan(rep, key, lambda: _Plan(None, None, rep._h.ptr,
+                                                 None if sh is None else sh.ptr, mode, rank,
+                                                 dims[mode]))
+    if isinstance(rep, CslSlices):
+        return _get_plan(rep, (mode, rank, None),
+                         lambda: _Plan(None, rep._h.ptr, None, None, mode, rank, dims[mode]))
+    if isinstance(rep, CooTensor):
+        return _get_plan(rep, (mode, rank, None),
+                         lambda: _Plan(None, rep._slices(mode).ptr, None, None, mode, rank, dims[mode]))
+    raise TypeError(f"no MTTKRP kernel for {type(rep).__name__}")
+
+
+def mttkrp_coo(t: CooTensor, factors: Factors, mode: int, threads: int = 1):
+    """MTTKRP over a coordinate list (kernels.py:109-151).
+
+    The entries are grouped by their mode-``mode`` coordinate on the GPU
+    (sorted under (mode, *rest) unless already mode-major) and reduced per
+    output row; ``threads`` is accepted for API compatibility."""
+    r = _check_factors(t.dims, factors, mode)
+    return _finish(plan_for(t, mode, r), factors, mode)
+
+
+def mttkrp_csf(c: CsfTensor, factors: Factors, mode: int):
+    """MTTKRP over a CSF tree built with mode_order[0] == mode (kernels.py:154-186)."""
+    if c.mode_order[0] != mode:
+        raise ValueError(f"tree was built for mode {c.mode_order[0]}, asked for mode {mode}")
+    r = _check_factors(c.dims, factors, mode)
+    return _finish(plan_for(c, mode, r), factors, mode)
+
+
+def mttkrp_csl(s: CslSlices, factors: Factors, mode: int, threads: int = 1):
+    """MTTKRP over compressed slices (kernels.py:189-226)."""
+    if s.mode_order[0] != mode:
+        raise ValueError(f"slices were built for mode {s.mode_order[0]}, asked for mode {mode}")
+    r = _check_factors(s.dims, factors, mode)
+    return _finish(plan_for(s, mode, r), factors, mode)
+
+
+def mttkrp_hbcsf(h: HbCsfTensor, factors: Factors, mode: int, schedule=None, threads: int = 1):
+    """MTTKRP over the hybrid format, all three buckets in one launch
+    (kernels.py:229-253).  A schedule applies to the CSF bucket only."""
+    if h.mode_order[0] != mode:
+        raise ValueError(f"hybrid was built for mode {h.mode_order[0]}, asked for mode {mode}")
+    if schedule is not None:
+        schedule.validate_for(h.csf_part)
+    r = _check_factors(h.dims, factors, mode)
+    return _finish(plan_for(h, mode, r, schedule), factors, mode)
+
+
+def mttkrp_scheduled(c: CsfTensor, schedule, factors: Factors, mode: int, threads: int = 1):
+    """MTTKRP over a CSF tree driven by a block schedule (kernels.py:256-342):
+    one device work unit per schedule unit."""
+    if c.mode_order[0] != mode:
+        raise ValueError(f"tree was built for mode {c.mode_order[0]}, asked for mode {mode}")
+    schedule.validate_for(c)
+    r = _check_factors(c.dims, factors, mode)
+    return _finish(plan_for(c, mode, r, schedule), factors, mode)
+
+
+def mttkrp(rep, factors: Factors, mode: int, **kwargs):
+    """Dispatch MTTKRP by representation type (kernels.py:345-355)."""
+    if isinstance(rep, CooTensor):
+        return mttkrp_coo(rep, factors, mode, **kwargs)
+    if isinstance(rep, CsfTensor):
+        return mttkrp_csf(rep, factors, mode, **kwargs)
+    if isinstance(rep, CslSlices):
+        return mttkrp_csl(rep, factors, mode, **kwargs)
+    if isinstance(rep, HbCsfTensor):
+        return mttkrp_hbcsf(rep, factors, mode, **kwargs)
+    raise TypeError(f"no MTTKRP kernel for {type(rep).__name__}")
+
+
+def mttkrp_device(rep, factors, mode: int, out=None, schedule=None):
+    """Device fast path: CUDA fp32 factors in, CUDA fp32 (dims[mode], R) out,
+    no host synchronisation and no finiteness scan.  Returns (out, OpCount)."""
+    if getattr(rep, "mode_order", None) is not None and rep.mode_order[0] != mode:
+        raise ValueError(f"representation was built for mode {rep.mode_order[0]}, asked for mode {mode}")
+    r = _check_factors(rep.dims, factors, mode, check_finite=False)
+    plan = plan_for(rep, mode, r, schedule)
+    ptrs, keep, _ = _device_factors(factors, mode)
+    return plan.execute(ptrs, out), plan.opcount

@@ -1,0 +1,11 @@
+#!/bin/bash
+# One GPU-box pass: smoke, parity tests, a short bench.  Logs to gpurun_out/.
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 1200 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+if [ -n "$BENCH" ]; then
+  timeout 1200 python bench.py $BENCH > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+fi
+tail -3 gpurun_out/smoke.log gpurun_out/pytest_gpu.log
+tail -c 3000 gpurun_out/bench.log 2>/dev/null
