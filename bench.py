@@ -317,12 +317,14 @@ def main():
     hbm, hbm_src = peaks()
     bytes_modes = [b_comp(censuses[m], dims, m) for m in range(n_modes)]
     achieved = sum(bytes_modes) / (sum(per_mode_ms) * 1e-3) / 1e9
+    # DRAM bytes per launch from the committed ncu capture of this workload
+    # (profiles/ncu_summary.json, written by scripts/make_profile_summary.py)
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
-    if prof.exists():
+    if prof.exists() and args.scale == 1.0:
         try:
-            d = json.loads(prof.read_text())
-            traffic = d.get(args.config, {}).get("dram_bytes_per_step")
+            per = json.loads(prof.read_text()).get(args.config, {}).get("dram_bytes_per_launch")
+            traffic = statistics.mean(per) if per else None
         except Exception:
             traffic = None
 
@@ -384,14 +386,16 @@ def main():
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
-                "kernel": "k_mttkrp3_r32 (one launch per mode)",
+                "kernel": "k_mttkrp3_r32<kind> (one launch per non-empty bucket kind per mode)",
                 "algorithmic_bytes_per_step": sum(bytes_modes),
+                "algorithmic_bytes_per_launch": sum(bytes_modes) / n_modes,
+                "traffic_unit": "DRAM bytes per MTTKRP launch (ncu dram__bytes_read+write, profiles/)",
                 "per_mode_ms": per_mode_ms, "per_mode_bytes": bytes_modes,
                 "per_mode_frac": [b / (ms * 1e-3) / 1e9 / hbm for b, ms in zip(bytes_modes, per_mode_ms)],
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * n_modes,
+            "gpu_launches": args.steps * sum(int(pl.info.launches) for pl in plans),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

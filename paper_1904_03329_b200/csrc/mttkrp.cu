@@ -20,9 +20,11 @@
 // split slice add into a per-slice fp32 accumulator with vector atomics and
 // the last chunk to finish (arrival counter) stores the row — so every output
 // row is written exactly once and no memset of the output is needed.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -49,7 +51,7 @@ struct alignas(16) Work {
   // task ranges [0,n0) CSF, [n0,n1) CSL, [n1,n2) COO, [n2,n3) ZERO
   uint32_t n0, n1, n2, n3;
   const Task* tasks;
-  // CSF bucket
+  // CSF bucket: original tree arrays (generic kernel) ...
   const uint32_t* csf_send;   // [S+1] nonzero offset of each slice
   const uint32_t* csf_sidx;   // [S]   output row of each slice
   const uint32_t* csf_lptr;   // [F+1]
@@ -58,6 +60,8 @@ struct alignas(16) Work {
   const float* csf_val;       // [M]
   uint32_t csf_F;
   uint32_t csf_S;
+  // ... and the kernel-native stream: (leaf | FEND | SEND, value bits)
+  const uint2* csf_pairs;     // [M]
   // CSL bucket
   const uint32_t* csl_send;   // slice_ptr [S+1]
   const uint32_t* csl_sidx;
@@ -65,19 +69,30 @@ struct alignas(16) Work {
   const uint32_t* csl_k;      // rest[1]
   const float* csl_val;
   uint32_t csl_S;
+  const uint2* csl_pairs;     // [M] (rest[1] | SEND, value bits)
   // COO bucket (unique rows)
   const uint32_t* coo_i;
   const uint32_t* coo_j;
   const uint32_t* coo_k;
   const float* coo_val;
+  const uint4* coo_quads;     // [M] (row, j, k, value bits)
+  // hot-row variant: fiber stream with HOT|slot encoding, the hot list
+  const uint32_t* hot_list;   // [nhot]: row | (0x80000000 if the row is a B row)
+  const uint2* csf_stream;    // variant 4: records (row | TRAILER | SEND | HOT, value bits)
+  uint32_t nhot;
   // ZERO list
   const uint32_t* zero_rows;
   // split-slice workspace (self-cleaning)
   float* ws_acc;
   uint32_t* ws_cnt;
-  uint32_t* ws_ctr;   // [0] task counter, [1] finished warps
-  uint32_t total_warps;
+  uint32_t* ws_ctr;   // per kernel kind k: [2k] task counter, [2k+1] finished warps
+  uint32_t total_warps[3];
 };
+
+// flag bits stored in the leaf coordinate of the kernel-native streams
+static constexpr uint32_t FEND = 0x80000000u;  // last nonzero of its fiber
+static constexpr uint32_t SEND = 0x40000000u;  // last nonzero of its slice
+static constexpr uint32_t KMASK = 0x3FFFFFFFu;
 
 struct Factors3 {
   const float4* B;  // factor of mode_order[1] (fiber / rest[0])
@@ -95,6 +110,13 @@ __device__ __forceinline__ float4 fmav4(float4 a, float4 x, float4 y) {
 }
 __device__ __forceinline__ float4 mul4(float a, float4 x) {
   return make_float4(a * x.x, a * x.y, a * x.z, a * x.w);
+}
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 shfl_xor4(float4 v, int m) {
+  return make_float4(__shfl_xor_sync(0xFFFFFFFFu, v.x, m), __shfl_xor_sync(0xFFFFFFFFu, v.y, m),
+                     __shfl_xor_sync(0xFFFFFFFFu, v.z, m), __shfl_xor_sync(0xFFFFFFFFu, v.w, m));
 }
 __device__ __forceinline__ void red_add4(float4* p, float4 v) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
@@ -114,205 +136,260 @@ __device__ __forceinline__ void st_cg4(float4* p, float4 v) {
                "f"(v.w)
                : "memory");
 }
+__device__ __forceinline__ uint2 ld_stream_u2(const uint2* p, uint64_t pol) {
+  uint2 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+      : "=r"(v.x), "=r"(v.y)
+      : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint4 ld_stream_u4(const uint4* p, uint64_t pol) {
+  uint4 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(p), "l"(pol));
+  return v;
+}
+// this group's bits of a warp ballot
+__device__ __forceinline__ uint32_t group_bits(unsigned gmask, bool pred, int g) {
+  return (__ballot_sync(gmask, pred) >> (8 * g)) & 0xFFu;
+}
 
-// A chunk of a split slice hands its partial to the slice accumulator; the
-// last of the slice's chunks writes the output row (and re-zeroes the slot).
-__device__ __forceinline__ void flush_split(const Work& w, uint32_t slot, uint32_t nchunk,
-                                            uint32_t row, float4 sa, float4* out, int lig,
-                                            unsigned gmask) {
-  float4* acc = reinterpret_cast<float4*>(w.ws_acc) + size_t(slot) * 8 + lig;
-  red_add4(acc, sa);
+// ---------------------------------------------------------- fast path --
+// The four 8-lane groups of a warp run their four tasks in lockstep (the
+// warp iterates max(batches) times; a finished group idles with n = 0), so
+// every shuffle is a full-warp, convergent SHFL and group-dependent branches
+// only guard loads and FMAs.
+
+#define FULL 0xFFFFFFFFu
+
+// 16-byte global->shared async copy (L1-allocating: hot fiber rows hit L1).
+// Each lane later reads back only the bytes it copied, so completion needs
+// only this thread's cp.async.wait_all, no barrier.
+__device__ __forceinline__ void cp_async16(float4* smem, const float4* gmem) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// OR of the four groups' bytes of a ballot
+__device__ __forceinline__ uint32_t any_group(uint32_t ballot) {
+  return (ballot | (ballot >> 8) | (ballot >> 16) | (ballot >> 24)) & 0xFFu;
+}
+
+// Split-slice hand-over, warp-convergent: groups with `active` add their
+// partial into the slot accumulator; the group whose add completes the slot
+// count stores the row and re-zeroes the slot for the next launch.
+__device__ __forceinline__ void flush_split(const Work& w, bool active, uint32_t slot,
+                                            uint32_t nchunk, uint32_t inc, uint32_t row,
+                                            float4 sa, float4* out, int lane, int lig) {
+  float4* acc = reinterpret_cast<float4*>(w.ws_acc) + size_t(active ? slot : 0) * 8 + lig;
+  if (active) red_add4(acc, sa);
   __threadfence();
-  __syncwarp(gmask);
+  __syncwarp();
   uint32_t old = 0;
-  if (lig == 0) old = atomicAdd(w.ws_cnt + slot, 1u);
-  old = __shfl_sync(gmask, old, 0, 8);
-  if (old == nchunk - 1) {
+  if (active && lig == 0) old = atomicAdd(w.ws_cnt + slot, inc);
+  old = __shfl_sync(FULL, old, lane & ~7);
+  if (active && old + inc == nchunk) {
     __threadfence();
-    float4 r = ld_cg4(acc);
+    const float4 r = ld_cg4(acc);
     out[size_t(row) * 8 + lig] = r;
     st_cg4(acc, f4zero());
     if (lig == 0) w.ws_cnt[slot] = 0;
   }
 }
 
-// ------------------------------------------------------------ CSF task --
-__device__ __forceinline__ void csf_task(const Work& w, const Factors3& fx, const Task& t, int lig,
-                                         unsigned gmask, uint64_t pol_s, uint64_t pol_r) {
+// ------------------------------------------------------------ CSF tasks --
+// Walks the (leaf|flags, value) stream in batches of 8 nonzeros per group.
+// Fiber and slice boundaries come from the flag bits; fiber coordinates and
+// slice rows are consumed in order from their own streams (no pointer is
+// chased).  The next batch's stream words are loaded before the current
+// batch is reduced.  Returns the partial of a chunk task (zero for runs).
+__device__ __forceinline__ float4 csf_tasks(const Work& w, const Factors3& fx, const Task& t,
+                                            int g, int lig, uint64_t pol_s, uint64_t pol_r,
+                                            float4* __restrict__ slots) {
   const uint32_t lo = t.lo, hi = t.hi;
-  if (lo >= hi) return;
   const bool chunk = t.slot != NOSLOT;
+  const uint32_t my_batches = hi > lo ? (hi - lo + 7) / 8 : 0;
+  const uint32_t nbat = __reduce_max_sync(FULL, my_batches);
+  const float4* Cl = fx.C + lig;
+  const float4* Bl = fx.B + lig;
   uint32_t s = t.s, f = t.f;
   float4 fa = f4zero(), sa = f4zero();
-  // whole-slice runs flush at slice ends; a chunk flushes once at its end
-  uint32_t send = chunk ? 0xFFFFFFFFu : w.csf_send[s + 1];
-  bool pending = false;  // fiber partial not yet multiplied by its B row
-  for (uint32_t base = lo; base < hi; base += 8) {
-    const uint32_t n = min(8u, hi - base);
-    uint32_t k = 0;
-    float v = 0.f;
-    if (lig < n) {
-      k = ld_stream_u32(w.csf_leaf + base + lig, pol_s);
-      v = ld_stream_f32(w.csf_val + base + lig, pol_s);
-    }
-    // fibers f, f+1, ...: end offsets and coordinates of the next 8
-    uint32_t e = 0xFFFFFFFFu, fi = 0;
-    if (f + lig < w.csf_F) {
-      e = __ldg(w.csf_lptr + f + 1 + lig);
-      fi = __ldg(w.csf_fidx + f + lig);
-    }
+  uint2 pr = make_uint2(0u, 0u);
+  if (lo + lig < hi) pr = ld_stream_u2(w.csf_pairs + lo + lig, pol_s);
+  uint32_t fi = (hi > lo && f + lig < w.csf_F) ? __ldg(w.csf_fidx + f + lig) : 0u;
+  uint32_t sr = (hi > lo && !chunk && s + lig < w.csf_S) ? __ldg(w.csf_sidx + s + lig) : 0u;
+  bool pending = false;
+  uint32_t base = lo;
+  for (uint32_t it = 0; it < nbat; ++it, base += 8) {
+    const uint32_t n = base < hi ? min(8u, hi - base) : 0u;
+    const bool live = uint32_t(lig) < n;
+    const uint32_t k = pr.x & KMASK;
+    const float v = __uint_as_float(pr.y);
+    const uint32_t eb_all = __ballot_sync(FULL, live && (pr.x & FEND));
+    const uint32_t sb_all = __ballot_sync(FULL, live && !chunk && (pr.x & SEND));
+    const uint32_t ebits = (eb_all >> (8 * g)) & 0xFFu;
+    const uint32_t sbits = (sb_all >> (8 * g)) & 0xFFu;
+    const uint32_t eany = any_group(eb_all);
+    const uint32_t sany = any_group(sb_all);
     float4 c[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      uint32_t kj = __shfl_sync(gmask, k, j, 8);
-      c[j] = (uint32_t(j) < n) ? ld_row4(fx.C + size_t(kj) * 8 + lig, pol_r) : f4zero();
+      const uint32_t kj = __shfl_sync(FULL, k, j, 8);
+      if (uint32_t(j) < n) c[j] = ld_row4(Cl + size_t(kj) * 8, pol_r);
     }
-    // bit p of ebits: a fiber ends after nonzero base+p
-    uint32_t mybit = (e > base && e <= base + n) ? (1u << (e - base - 1)) : 0u;
-    const uint32_t ebits = __reduce_or_sync(gmask, mybit);
-    float4 b[8];
+    // fiber rows of the fibers ending in this batch -> slot = end position
+    uint32_t tf = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
+      if ((eany >> j) & 1u) {
+        const uint32_t fj = __shfl_sync(FULL, fi, tf, 8);
+        if ((ebits >> j) & 1u) cp_async16(slots + j * 8, Bl + size_t(fj) * 8);
+        tf += (ebits >> j) & 1u;
+      }
+    }
+    // prefetch the next batch's stream words
+    const uint32_t sr_cur = sr;
+    const float vv = v;
+    f += tf;
+    const uint32_t nsl = __popc(sbits);
+    s += nsl;
+    const uint32_t nb = base + 8;
+    if (nb + lig < hi) pr = ld_stream_u2(w.csf_pairs + nb + lig, pol_s);
+    if (tf && nb < hi) fi = (f + lig < w.csf_F) ? __ldg(w.csf_fidx + f + lig) : 0u;
+    if (nsl && nb < hi) sr = (s + lig < w.csf_S) ? __ldg(w.csf_sidx + s + lig) : 0u;
+    cp_async_wait_all();
+    uint32_t ts = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float vj = __shfl_sync(FULL, vv, j, 8);
+      if (uint32_t(j) < n) fa = fma4(vj, c[j], fa);
       if ((ebits >> j) & 1u) {
-        uint32_t ord = __popc(ebits & ((1u << j) - 1u));
-        uint32_t fj = __shfl_sync(gmask, fi, ord, 8);
-        b[j] = ld_row4(fx.B + size_t(fj) * 8 + lig, pol_r);
-      } else {
-        b[j] = f4zero();
+        sa = fmav4(fa, slots[j * 8], sa);
+        fa = f4zero();
       }
-    }
-    // slice ends inside this batch (runs only)
-    uint32_t sbits = 0, se = 0xFFFFFFFFu, si = 0;
-    if (send <= base + n) {
-      if (s + lig < w.csf_S) {
-        se = __ldg(w.csf_send + s + 1 + lig);
-        si = __ldg(w.csf_sidx + s + lig);
-      }
-      uint32_t sb = (se > base && se <= base + n) ? (1u << (se - base - 1)) : 0u;
-      sbits = __reduce_or_sync(gmask, sb);
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (uint32_t(j) < n) {
-        float vj = __shfl_sync(gmask, v, j, 8);
-        fa = fma4(vj, c[j], fa);
-        pending = true;
-        if ((ebits >> j) & 1u) {
-          sa = fmav4(fa, b[j], sa);
-          fa = f4zero();
-          pending = false;
-          if ((sbits >> j) & 1u) {
-            uint32_t row = __shfl_sync(gmask, si, __popc(sbits & ((1u << j) - 1u)), 8);
-            fx.out[size_t(row) * 8 + lig] = sa;
-            sa = f4zero();
-          }
-        }
-      }
-    }
-    f += __popc(ebits);
-    if (sbits) {
-      s += __popc(sbits);
-      send = (s < w.csf_S) ? __ldg(w.csf_send + s + 1) : 0xFFFFFFFFu;
-    }
-  }
-  if (chunk) {
-    if (pending) {  // chunk ended inside fiber f
-      uint32_t fj = __ldg(w.csf_fidx + f);
-      sa = fmav4(fa, ld_row4(fx.B + size_t(fj) * 8 + lig, pol_r), sa);
-    }
-    flush_split(w, t.slot, t.nchunk, __ldg(w.csf_sidx + t.s), sa, fx.out, lig, gmask);
-  }
-}
-
-// ------------------------------------------------------------ CSL task --
-__device__ __forceinline__ void csl_task(const Work& w, const Factors3& fx, const Task& t, int lig,
-                                         unsigned gmask, uint64_t pol_s, uint64_t pol_r) {
-  const uint32_t lo = t.lo, hi = t.hi;
-  if (lo >= hi) return;
-  const bool chunk = t.slot != NOSLOT;
-  uint32_t s = t.s;
-  float4 sa = f4zero();
-  uint32_t send = chunk ? 0xFFFFFFFFu : w.csl_send[s + 1];
-  for (uint32_t base = lo; base < hi; base += 8) {
-    const uint32_t n = min(8u, hi - base);
-    uint32_t jx = 0, kx = 0;
-    float v = 0.f;
-    if (lig < n) {
-      jx = ld_stream_u32(w.csl_j + base + lig, pol_s);
-      kx = ld_stream_u32(w.csl_k + base + lig, pol_s);
-      v = ld_stream_f32(w.csl_val + base + lig, pol_s);
-    }
-    float4 b[8], c[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      uint32_t bj = __shfl_sync(gmask, jx, j, 8);
-      uint32_t cj = __shfl_sync(gmask, kx, j, 8);
-      if (uint32_t(j) < n) {
-        b[j] = ld_row4(fx.B + size_t(bj) * 8 + lig, pol_r);
-        c[j] = ld_row4(fx.C + size_t(cj) * 8 + lig, pol_r);
-      } else {
-        b[j] = f4zero();
-        c[j] = f4zero();
-      }
-    }
-    uint32_t sbits = 0, se = 0xFFFFFFFFu, si = 0;
-    if (send <= base + n) {
-      if (s + lig < w.csl_S) {
-        se = __ldg(w.csl_send + s + 1 + lig);
-        si = __ldg(w.csl_sidx + s + lig);
-      }
-      uint32_t sb = (se > base && se <= base + n) ? (1u << (se - base - 1)) : 0u;
-      sbits = __reduce_or_sync(gmask, sb);
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (uint32_t(j) < n) {
-        float vj = __shfl_sync(gmask, v, j, 8);
-        sa = fmav4(mul4(vj, b[j]), c[j], sa);
+      if ((sany >> j) & 1u) {
+        const uint32_t row = __shfl_sync(FULL, sr_cur, ts, 8);
         if ((sbits >> j) & 1u) {
-          uint32_t row = __shfl_sync(gmask, si, __popc(sbits & ((1u << j) - 1u)), 8);
           fx.out[size_t(row) * 8 + lig] = sa;
           sa = f4zero();
+          ++ts;
         }
       }
     }
-    if (sbits) {
-      s += __popc(sbits);
-      send = (s < w.csl_S) ? __ldg(w.csl_send + s + 1) : 0xFFFFFFFFu;
-    }
+    if (n) pending = !((ebits >> (n - 1)) & 1u);
   }
-  if (chunk) flush_split(w, t.slot, t.nchunk, __ldg(w.csl_sidx + t.s), sa, fx.out, lig, gmask);
+  if (chunk && pending) {  // the chunk ended inside fiber f
+    const uint32_t fj = __ldg(w.csf_fidx + f);
+    sa = fmav4(fa, ld_row4(Bl + size_t(fj) * 8, pol_r), sa);
+  }
+  return sa;
 }
 
-// ------------------------------------------------------------ COO task --
-__device__ __forceinline__ void coo_task(const Work& w, const Factors3& fx, const Task& t, int lig,
-                                         unsigned gmask, uint64_t pol_s, uint64_t pol_r) {
-  for (uint32_t base = t.lo; base < t.hi; base += 8) {
-    const uint32_t n = min(8u, t.hi - base);
-    uint32_t ix = 0, jx = 0, kx = 0;
-    float v = 0.f;
-    if (lig < n) {
-      ix = ld_stream_u32(w.coo_i + base + lig, pol_s);
-      jx = ld_stream_u32(w.coo_j + base + lig, pol_s);
-      kx = ld_stream_u32(w.coo_k + base + lig, pol_s);
-      v = ld_stream_f32(w.coo_val + base + lig, pol_s);
-    }
-    float4 b[8], c[8];
+// ------------------------------------------------------------ CSL tasks --
+__device__ __forceinline__ float4 csl_tasks(const Work& w, const Factors3& fx, const Task& t,
+                                            int g, int lig, uint64_t pol_s, uint64_t pol_r,
+                                            float4* __restrict__ slots) {
+  const uint32_t lo = t.lo, hi = t.hi;
+  const bool chunk = t.slot != NOSLOT;
+  const uint32_t my_batches = hi > lo ? (hi - lo + 7) / 8 : 0;
+  const uint32_t nbat = __reduce_max_sync(FULL, my_batches);
+  const float4* Cl = fx.C + lig;
+  const float4* Bl = fx.B + lig;
+  uint32_t s = t.s;
+  float4 sa = f4zero();
+  uint2 pr = make_uint2(0u, 0u);
+  uint32_t jx = 0;
+  if (lo + lig < hi) {
+    pr = ld_stream_u2(w.csl_pairs + lo + lig, pol_s);
+    jx = ld_stream_u32(w.csl_j + lo + lig, pol_s);
+  }
+  uint32_t sr = (hi > lo && !chunk && s + lig < w.csl_S) ? __ldg(w.csl_sidx + s + lig) : 0u;
+  uint32_t base = lo;
+  for (uint32_t it = 0; it < nbat; ++it, base += 8) {
+    const uint32_t n = base < hi ? min(8u, hi - base) : 0u;
+    const bool live = uint32_t(lig) < n;
+    const uint32_t k = pr.x & KMASK;
+    const float v = __uint_as_float(pr.y);
+    const uint32_t sb_all = __ballot_sync(FULL, live && !chunk && (pr.x & SEND));
+    const uint32_t sbits = (sb_all >> (8 * g)) & 0xFFu;
+    const uint32_t sany = any_group(sb_all);
+    float4 c[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      uint32_t bj = __shfl_sync(gmask, jx, j, 8);
-      uint32_t cj = __shfl_sync(gmask, kx, j, 8);
+      const uint32_t bj = __shfl_sync(FULL, jx, j, 8);
+      const uint32_t cj = __shfl_sync(FULL, k, j, 8);
       if (uint32_t(j) < n) {
-        b[j] = ld_row4(fx.B + size_t(bj) * 8 + lig, pol_r);
-        c[j] = ld_row4(fx.C + size_t(cj) * 8 + lig, pol_r);
+        cp_async16(slots + j * 8, Bl + size_t(bj) * 8);
+        c[j] = ld_row4(Cl + size_t(cj) * 8, pol_r);
       }
     }
+    const uint32_t sr_cur = sr;
+    const float vv = v;
+    const uint32_t nsl = __popc(sbits);
+    s += nsl;
+    const uint32_t nb = base + 8;
+    if (nb + lig < hi) {
+      pr = ld_stream_u2(w.csl_pairs + nb + lig, pol_s);
+      jx = ld_stream_u32(w.csl_j + nb + lig, pol_s);
+    }
+    if (nsl && nb < hi) sr = (s + lig < w.csl_S) ? __ldg(w.csl_sidx + s + lig) : 0u;
+    cp_async_wait_all();
+    uint32_t ts = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      uint32_t row = __shfl_sync(gmask, ix, j, 8);
-      float vj = __shfl_sync(gmask, v, j, 8);
+      const float vj = __shfl_sync(FULL, vv, j, 8);
+      if (uint32_t(j) < n) sa = fmav4(mul4(vj, slots[j * 8]), c[j], sa);
+      if ((sany >> j) & 1u) {
+        const uint32_t row = __shfl_sync(FULL, sr_cur, ts, 8);
+        if ((sbits >> j) & 1u) {
+          fx.out[size_t(row) * 8 + lig] = sa;
+          sa = f4zero();
+          ++ts;
+        }
+      }
+    }
+  }
+  return sa;
+}
+
+// ------------------------------------------------------------ COO tasks --
+__device__ __forceinline__ void coo_tasks(const Work& w, const Factors3& fx, const Task& t,
+                                          int lig, uint64_t pol_s, uint64_t pol_r,
+                                          float4* __restrict__ slots) {
+  const uint32_t lo = t.lo, hi = t.hi;
+  const uint32_t my_batches = hi > lo ? (hi - lo + 7) / 8 : 0;
+  const uint32_t nbat = __reduce_max_sync(FULL, my_batches);
+  const float4* Cl = fx.C + lig;
+  const float4* Bl = fx.B + lig;
+  uint4 q = make_uint4(0u, 0u, 0u, 0u);
+  if (lo + lig < hi) q = ld_stream_u4(w.coo_quads + lo + lig, pol_s);
+  uint32_t base = lo;
+  for (uint32_t it = 0; it < nbat; ++it, base += 8) {
+    const uint32_t n = base < hi ? min(8u, hi - base) : 0u;
+    float4 c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t bj = __shfl_sync(FULL, q.y, j, 8);
+      const uint32_t cj = __shfl_sync(FULL, q.z, j, 8);
       if (uint32_t(j) < n) {
-        float4 r = mul4(vj, b[j]);
+        cp_async16(slots + j * 8, Bl + size_t(bj) * 8);
+        c[j] = ld_row4(Cl + size_t(cj) * 8, pol_r);
+      }
+    }
+    const uint4 cur = q;
+    const uint32_t nb = base + 8;
+    if (nb + lig < hi) q = ld_stream_u4(w.coo_quads + nb + lig, pol_s);
+    cp_async_wait_all();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t row = __shfl_sync(FULL, cur.x, j, 8);
+      const float vj = __uint_as_float(__shfl_sync(FULL, cur.w, j, 8));
+      if (uint32_t(j) < n) {
+        float4 r = mul4(vj, slots[j * 8]);
         r.x *= c[j].x;
         r.y *= c[j].y;
         r.z *= c[j].z;
@@ -326,43 +403,221 @@ __device__ __forceinline__ void coo_task(const Work& w, const Factors3& fx, cons
 __device__ __forceinline__ void zero_task(const Work& w, const Factors3& fx, const Task& t,
                                           int lig) {
   for (uint32_t i = t.lo; i < t.hi; ++i) {
-    uint32_t row = __ldg(w.zero_rows + i);
+    const uint32_t row = __ldg(w.zero_rows + i);
     fx.out[size_t(row) * 8 + lig] = f4zero();
   }
 }
 
-// Persistent kernel: warps pull 4 consecutive tasks at a time (one per group)
-// from a global counter; the last warp out resets the counter.
-__global__ void __launch_bounds__(256) k_mttkrp3_r32(const __grid_constant__ Work w,
-                                                     const __grid_constant__ Factors3 fx) {
+// Persistent kernels, one per bucket kind (separate kernels keep each at 80
+// registers / 24 warps per SM): a warp pulls 4 consecutive tasks at a time
+// (one per 8-lane group) from the kind's counter; the last warp out resets
+// it.  Chunks of one split slice that land in the same warp are summed with
+// shuffles and handed over with a single vector atomic.
+static constexpr int FAST_BLOCK = 256;
+enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2 };
+
+template <int KIND>
+__global__ void __launch_bounds__(FAST_BLOCK, 3)
+    k_mttkrp3_r32(const __grid_constant__ Work w, const __grid_constant__ Factors3 fx) {
+  // per lane: 8 slots of 16 B (one per batch position) for staged B rows
+  __shared__ float4 s_slots[FAST_BLOCK * 8];
   const int lane = threadIdx.x & 31;
   const int g = lane >> 3;
   const int lig = lane & 7;
-  const unsigned gmask = 0xFFu << (8 * g);
+  float4* slots = s_slots + (threadIdx.x >> 3) * 64 + lig;
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_r = policy_evict_last();
+  const uint32_t first = KIND == KIND_CSF ? 0u : (KIND == KIND_CSL ? w.n0 : w.n1);
+  const uint32_t last = KIND == KIND_CSF ? w.n0 : (KIND == KIND_CSL ? w.n1 : w.n3);
+  uint32_t* ctr = w.ws_ctr + 2 * KIND;
   for (;;) {
     uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(w.ws_ctr, 4u);
-    base = __shfl_sync(0xFFFFFFFFu, base, 0);
-    if (base >= w.n3) break;
-    const uint32_t ti = base + g;
-    const Task t = w.tasks[ti];
-    if (base < w.n0)
-      csf_task(w, fx, t, lig, gmask, pol_s, pol_r);
-    else if (base < w.n1)
-      csl_task(w, fx, t, lig, gmask, pol_s, pol_r);
-    else if (base < w.n2)
-      coo_task(w, fx, t, lig, gmask, pol_s, pol_r);
-    else
+    if (lane == 0) base = atomicAdd(ctr, 4u);
+    base = __shfl_sync(FULL, base, 0) + first;
+    if (base >= last) break;
+    const Task t = w.tasks[base + g];
+    if (KIND == KIND_CSF || KIND == KIND_CSL) {
+      const float4 sa = KIND == KIND_CSF ? csf_tasks(w, fx, t, g, lig, pol_s, pol_r, slots)
+                                         : csl_tasks(w, fx, t, g, lig, pol_s, pol_r, slots);
+      const bool mine = t.slot != NOSLOT && t.lo < t.hi;
+      const uint32_t slot0 = __shfl_sync(FULL, t.slot, 0);
+      const bool same = __all_sync(FULL, mine && t.slot == slot0);
+      const uint32_t row =
+          mine ? (KIND == KIND_CSF ? __ldg(w.csf_sidx + t.s) : __ldg(w.csl_sidx + t.s)) : 0u;
+      if (same) {
+        float4 r = add4(sa, shfl_xor4(sa, 8));
+        r = add4(r, shfl_xor4(r, 16));
+        flush_split(w, g == 0, t.slot, t.nchunk, 4u, row, r, fx.out, lane, lig);
+      } else if (__any_sync(FULL, mine)) {
+        flush_split(w, mine, t.slot, t.nchunk, 1u, row, sa, fx.out, lane, lig);
+      }
+    } else if (base < w.n2) {
+      coo_tasks(w, fx, t, lig, pol_s, pol_r, slots);
+    } else {
       zero_task(w, fx, t, lig);
-    __syncwarp();
+    }
   }
   if (lane == 0) {
-    uint32_t done = atomicAdd(w.ws_ctr + 1, 1u);
-    if (done == w.total_warps - 1) {
-      w.ws_ctr[0] = 0;
-      w.ws_ctr[1] = 0;
+    const uint32_t done = atomicAdd(ctr + 1, 1u);
+    if (done == w.total_warps[KIND] - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+  }
+}
+
+// Rows marked HOT in a stream are served from the CTA's shared-memory copy of
+// the most accessed factor rows (ranked at plan time).
+static constexpr uint32_t HOT = 0x20000000u;
+static constexpr uint32_t ROWMASK = 0x1FFFFFFFu;
+
+// --------------------------------------- CSF tasks, trailer-stream variant --
+// The plan turns the CSF bucket into one self-describing stream of 8-byte
+// records in tree order: each fiber segment's nonzeros (leaf row, value)
+// followed by a TRAILER record (fiber row, SEND if it closes the slice).
+// Every record is one factor-row gather (leaf rows from C, trailer rows from
+// B), so a batch of 8 records needs no side streams and the gathers of batch
+// b+1 are issued before batch b is reduced (register double buffering).
+// Rows marked HOT come from the CTA's shared-memory copy.
+static constexpr uint32_t TRAILER = 0x80000000u;
+
+__device__ __forceinline__ void gather8(float4 (&c)[8], uint32_t x, uint32_t n,
+                                        const float4* __restrict__ Cl, const float4* __restrict__ Bl,
+                                        const float4* __restrict__ hot, uint64_t pol) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t xj = __shfl_sync(FULL, x, j, 8);
+    if (uint32_t(j) < n) {
+      if (xj & HOT)
+        c[j] = hot[(xj & ROWMASK) * 8];
+      else
+        c[j] = ld_row4(((xj & TRAILER) ? Bl : Cl) + size_t(xj & ROWMASK) * 8, pol);
+    }
+  }
+}
+
+struct SliceCursor {
+  uint32_t s;   // next slice (run tasks)
+  uint32_t sr;  // lane lig holds the row of slice s + lig
+};
+
+__device__ __forceinline__ void consume8(const float4 (&c)[8], uint2 p, uint32_t n, bool chunk,
+                                         float4& fa, float4& sa, SliceCursor& cur, uint32_t more,
+                                         const Work& w, float4* __restrict__ out, int g, int lig) {
+  const bool live = uint32_t(lig) < n;
+  const uint32_t tb_all = __ballot_sync(FULL, live && (p.x & TRAILER));
+  const uint32_t sb_all = __ballot_sync(FULL, live && !chunk && (p.x & SEND));
+  const uint32_t tbits = (tb_all >> (8 * g)) & 0xFFu;
+  const uint32_t sbits = (sb_all >> (8 * g)) & 0xFFu;
+  const uint32_t sany = any_group(sb_all);
+  const float v = __uint_as_float(p.y);
+  uint32_t ts = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float vj = __shfl_sync(FULL, v, j, 8);
+    if (uint32_t(j) < n) {
+      if ((tbits >> j) & 1u) {
+        sa = fmav4(fa, c[j], sa);
+        fa = f4zero();
+      } else {
+        fa = fma4(vj, c[j], fa);
+      }
+    }
+    if ((sany >> j) & 1u) {
+      const uint32_t row = __shfl_sync(FULL, cur.sr, ts, 8);
+      if ((sbits >> j) & 1u) {
+        out[size_t(row) * 8 + lig] = sa;
+        sa = f4zero();
+        ++ts;
+      }
+    }
+  }
+  if (sany) {
+    cur.s += __popc(sbits);
+    if (sbits && more) cur.sr = (cur.s + lig < w.csf_S) ? __ldg(w.csf_sidx + cur.s + lig) : 0u;
+  }
+}
+
+__device__ __forceinline__ float4 csf_tasks4(const Work& w, const Factors3& fx, const Task& t,
+                                             int g, int lig, uint64_t pol_s, uint64_t pol_r,
+                                             const float4* __restrict__ hot) {
+  const uint32_t lo = t.lo, hi = t.hi;
+  const bool chunk = t.slot != NOSLOT;
+  const uint32_t my_batches = hi > lo ? (hi - lo + 7) / 8 : 0;
+  const uint32_t nbat = __reduce_max_sync(FULL, my_batches);
+  const float4* Cl = fx.C + lig;
+  const float4* Bl = fx.B + lig;
+  const uint2* S = w.csf_stream;
+  auto load = [&](uint32_t it) -> uint2 {
+    const uint32_t e = lo + 8 * it + lig;
+    return e < hi ? ld_stream_u2(S + e, pol_s) : make_uint2(0u, 0u);
+  };
+  auto count = [&](uint32_t it) -> uint32_t {
+    const uint32_t b = lo + 8 * it;
+    return b < hi ? min(8u, hi - b) : 0u;
+  };
+  float4 fa = f4zero(), sa = f4zero();
+  SliceCursor cur{t.s, (hi > lo && !chunk && t.s + lig < w.csf_S) ? __ldg(w.csf_sidx + t.s + lig) : 0u};
+  uint2 pa = load(0), pb = load(1);
+  float4 cA[8], cB[8];
+  gather8(cA, pa.x, count(0), Cl, Bl, hot, pol_r);
+  for (uint32_t it = 0; it < nbat; it += 2) {
+    gather8(cB, pb.x, count(it + 1), Cl, Bl, hot, pol_r);
+    const uint2 ua = pa;
+    pa = load(it + 2);
+    consume8(cA, ua, count(it), chunk, fa, sa, cur, it + 1 < nbat, w, fx.out, g, lig);
+    if (it + 1 >= nbat) break;
+    gather8(cA, pa.x, count(it + 2), Cl, Bl, hot, pol_r);
+    const uint2 ub = pb;
+    pb = load(it + 3);
+    consume8(cB, ub, count(it + 1), chunk, fa, sa, cur, it + 2 < nbat, w, fx.out, g, lig);
+  }
+  return sa;  // chunks end on a trailer, so fa is already folded in
+}
+
+// Variant-4 kernel: 256 threads (2 CTAs/SM) without hot rows, or 512 threads
+// (1 CTA/SM) with up to ~1700 hot rows in dynamic shared memory.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK, 512 / BLOCK)
+    k_mttkrp3_r32_stream(const __grid_constant__ Work w, const __grid_constant__ Factors3 fx) {
+  extern __shared__ float4 s_hot[];
+  for (uint32_t i = threadIdx.x; i < w.nhot * 8; i += blockDim.x) {
+    const uint32_t e = __ldg(w.hot_list + (i >> 3));
+    const float4* src = (e & 0x80000000u) ? fx.B : fx.C;
+    s_hot[i] = __ldg(src + size_t(e & ROWMASK) * 8 + (i & 7));
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 3;
+  const int lig = lane & 7;
+  const float4* hot = s_hot + lig;
+  const uint64_t pol_s = policy_evict_first();
+  const uint64_t pol_r = policy_evict_last();
+  uint32_t* ctr = w.ws_ctr + 2 * KIND_CSF;
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(ctr, 4u);
+    base = __shfl_sync(FULL, base, 0);
+    if (base >= w.n0) break;
+    const Task t = w.tasks[base + g];
+    const float4 sa = csf_tasks4(w, fx, t, g, lig, pol_s, pol_r, hot);
+    const bool mine = t.slot != NOSLOT && t.lo < t.hi;
+    const uint32_t slot0 = __shfl_sync(FULL, t.slot, 0);
+    const bool same = __all_sync(FULL, mine && t.slot == slot0);
+    const uint32_t row = mine ? __ldg(w.csf_sidx + t.s) : 0u;
+    if (same) {
+      float4 r = add4(sa, shfl_xor4(sa, 8));
+      r = add4(r, shfl_xor4(r, 16));
+      flush_split(w, g == 0, t.slot, t.nchunk, 4u, row, r, fx.out, lane, lig);
+    } else if (__any_sync(FULL, mine)) {
+      flush_split(w, mine, t.slot, t.nchunk, 1u, row, sa, fx.out, lane, lig);
+    }
+  }
+  if (lane == 0) {
+    const uint32_t done = atomicAdd(ctr + 1, 1u);
+    if (done == w.total_warps[KIND_CSF] - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
     }
   }
 }
@@ -501,7 +756,7 @@ __global__ void __launch_bounds__(256) k_mttkrp_generic(const __grid_constant__ 
   __syncwarp();
   if (lane == 0) {
     uint32_t done = atomicAdd(w.ws_ctr + 1, 1u);
-    if (done == w.total_warps - 1) {
+    if (done == w.total_warps[0] - 1) {
       w.ws_ctr[0] = 0;
       w.ws_ctr[1] = 0;
     }
@@ -673,6 +928,133 @@ __global__ void k_empty_tasks(Task* __restrict__ tasks, int64_t n) {
   }
 }
 
+// Kernel-native streams (built once per plan).
+__global__ void k_pairs(const uint32_t* __restrict__ k, const float* __restrict__ v, int64_t M,
+                        uint2* __restrict__ out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = make_uint2(k[i], __float_as_uint(v[i]));
+}
+// flag the last nonzero of every segment [ptr[x], ptr[x+1])
+__global__ void k_flag_ends(const uint32_t* __restrict__ ptr, int64_t n, uint32_t flag,
+                            uint2* __restrict__ out) {
+  for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < n;
+       x += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t e = ptr[x + 1];
+    if (e > ptr[x]) out[e - 1].x |= flag;
+  }
+}
+__global__ void k_quads(const uint32_t* __restrict__ i0, const uint32_t* __restrict__ j0,
+                        const uint32_t* __restrict__ k0, const float* __restrict__ v, int64_t M,
+                        uint4* __restrict__ out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = make_uint4(i0[i], j0[i], k0[i], __float_as_uint(v[i]));
+}
+
+__global__ void k_hist_u32(const uint32_t* __restrict__ a, int64_t n, uint32_t* __restrict__ h) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    atomicAdd(h + a[i], 1u);
+}
+__global__ void k_hot_candidates(int64_t DC, int64_t DB, uint32_t* __restrict__ vals) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < DC + DB;
+       i += int64_t(gridDim.x) * blockDim.x)
+    vals[i] = i < DC ? uint32_t(i) : (0x80000000u | uint32_t(i - DC));
+}
+__global__ void k_hot_slots(const uint32_t* __restrict__ list, uint32_t H, uint32_t* __restrict__ slotC,
+                            uint32_t* __restrict__ slotB) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < H;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t e = list[i];
+    if (e & 0x80000000u)
+      slotB[e & ROWMASK] = uint32_t(i);
+    else
+      slotC[e & ROWMASK] = uint32_t(i);
+  }
+}
+
+// Variant-4 stream: segment s (nonzeros [lptr[s], lptr[s+1])) is written at
+// stream positions lptr[s]+s .. lptr[s+1]+s, its trailer last.
+__global__ void k_build_stream(const uint32_t* __restrict__ lptr, const uint32_t* __restrict__ fidx,
+                               const uint8_t* __restrict__ last, int64_t F,
+                               const uint32_t* __restrict__ leaf, const float* __restrict__ v,
+                               const uint32_t* __restrict__ slotC, const uint32_t* __restrict__ slotB,
+                               uint2* __restrict__ out) {
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < F;
+       s += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t a = lptr[s], b = lptr[s + 1];
+    for (uint32_t i = a; i < b; ++i) {
+      const uint32_t k = leaf[i];
+      const uint32_t sl = slotC ? slotC[k] : 0xFFFFFFFFu;
+      out[i + s] = make_uint2(sl != 0xFFFFFFFFu ? (HOT | sl) : k, __float_as_uint(v[i]));
+    }
+    const uint32_t j = fidx[s];
+    const uint32_t sl = slotB ? slotB[j] : 0xFFFFFFFFu;
+    uint32_t x = TRAILER | (sl != 0xFFFFFFFFu ? (HOT | sl) : j);
+    if (last[s]) x |= SEND;
+    out[b + s] = make_uint2(x, 0u);
+  }
+}
+__global__ void k_mark_last_segment(const uint32_t* __restrict__ fpos, int64_t S, uint8_t* __restrict__ last) {
+  for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < S;
+       x += int64_t(gridDim.x) * blockDim.x)
+    if (fpos[x + 1] > fpos[x]) last[fpos[x + 1] - 1] = 1;
+}
+__global__ void k_stream_slice_starts(const uint32_t* __restrict__ loff, const uint32_t* __restrict__ fpos,
+                                      int64_t S, uint32_t* __restrict__ sst) {
+  for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x <= S;
+       x += int64_t(gridDim.x) * blockDim.x)
+    sst[x] = loff[x] + fpos[x];
+}
+// Tasks over the stream: runs of whole light slices, or chunks of a heavy
+// slice cut right after a trailer (so a chunk never ends inside a fiber).
+__global__ void k_task_fill_stream(const uint32_t* __restrict__ sst, const uint32_t* __restrict__ fpos,
+                                   const uint32_t* __restrict__ lptr, int64_t S, uint32_t T,
+                                   const uint32_t* __restrict__ toff, const uint32_t* __restrict__ slot,
+                                   Task* __restrict__ tasks) {
+  for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < S;
+       x += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t a = sst[x], len = sst[x + 1] - a;
+    const uint32_t nt = toff[x + 1] - toff[x];
+    if (nt == 0) continue;
+    if (len > T) {
+      uint32_t prev = a;
+      for (uint32_t c = 0; c < nt; ++c) {
+        uint32_t end;
+        if (c + 1 == nt) {
+          end = sst[x + 1];
+        } else {
+          const uint32_t target = a + uint32_t((uint64_t(len) * (c + 1)) / nt);
+          // first segment of the slice whose trailer sits at or after target-1
+          uint32_t l0 = fpos[x], h0 = fpos[x + 1] - 1;
+          while (l0 < h0) {
+            const uint32_t m = l0 + (h0 - l0) / 2;
+            if (lptr[m + 1] + m + 1 >= target) h0 = m; else l0 = m + 1;
+          }
+          end = lptr[l0 + 1] + l0 + 1;
+          if (end < prev) end = prev;
+        }
+        Task t{};
+        t.lo = prev;
+        t.hi = end;
+        t.s = uint32_t(x);
+        t.slot = slot[x];
+        t.nchunk = nt;
+        tasks[toff[x] + c] = t;
+        prev = end;
+      }
+    } else {
+      Task t{};
+      t.lo = a;
+      t.s = uint32_t(x);
+      t.slot = NOSLOT;
+      t.nchunk = 1;
+      tasks[toff[x]] = t;
+    }
+  }
+}
+
 }  // namespace hbk
 
 struct hbk_plan {
@@ -684,11 +1066,20 @@ struct hbk_plan {
   hbk_csf* csf = nullptr;
   hbk_sched* sched = nullptr;
   hbk::Buf tasks, zero_rows, csf_send, ws;
+  hbk::Buf csf_pairs, csl_pairs, coo_quads, hot_list, csf_stream;
+  hbk_csf* stream_tree = nullptr;  // variant 4: the tree the stream was built from (virtually split)
+  size_t hot_smem = 0;
   hbk::Work work{};
   bool fast = false;
   int grid = 0, block = 256;
+  int grids[3] = {0, 0, 0};
+  int csf_block = 256;
+  int csf_var = 0;  // CSF kernel variant (HBK_CSF_VARIANT): 0 = (leaf|flags,value) pair stream +
+                    // fiber-index stream; 4 = record stream with fiber trailers, double-buffered
+                    // gathers and shared-memory hot rows
   hbk_plan_info info{};
   ~hbk_plan() {
+    hbk_csf_release(stream_tree);
     hbk_coo_release(coo);
     hbk_csl_release(csl);
     hbk_csf_release(csf);
@@ -734,13 +1125,126 @@ __global__ void k_shift_slots(Task* __restrict__ t, int64_t n, uint32_t base) {
     if (t[i].slot != NOSLOT) t[i].slot += base;
 }
 
+// Variant 4: virtually split fibers at tau_p, rank hot rows, emit the
+// record stream and cut it into tasks (runs of light slices / trailer-aligned
+// chunks of heavy slices).
+static BucketTasks build_csf_stream(hbk_plan* p, hbk_csf* c, uint32_t T, cudaStream_t st) {
+  int64_t tau_p = 32;
+  if (const char* e = getenv("HBK_STREAM_TAU")) tau_p = std::max<int64_t>(1, atoll(e));
+  hbk_csf* cs = nullptr;
+  HBK_REQUIRE(hbk_split_fibers(c, tau_p, st, &cs) == HBK_OK, HBK_ECUDA, hbk_last_error());
+  if (!cs) {
+    cs = c;
+    hbk_csf_retain(c);
+  }
+  p->stream_tree = cs;
+  const int L = p->order - 2;
+  const int64_t S = cs->n[0], F = cs->n[L], M = cs->M;
+  Chain2 ch{};
+  ch.nlev = p->order - 1;
+  for (int d = 0; d < p->order - 1; ++d) ch.ptr[d] = cs->ptr[d].as<uint32_t>();
+  Scratch fpos((S + 1) * sizeof(uint32_t), st), loff((S + 1) * sizeof(uint32_t), st);
+  k_csf_slice_offsets<<<grid_for(S + 1, 256), 256, 0, st>>>(ch, S, fpos.as<uint32_t>(), loff.as<uint32_t>());
+  check_launch("k_csf_slice_offsets");
+  // hot rows: leaf rows by nonzero count, fiber rows by segment count
+  const int64_t DC = p->dims[p->mo[2]], DB = p->dims[p->mo[1]];
+  int dev = 0, optin = 0;
+  HBK_CUDA(cudaGetDevice(&dev));
+  HBK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  int64_t hmax = (int64_t(optin) - 2048) / 128;
+  if (const char* e = getenv("HBK_HOT_ROWS")) hmax = std::max<int64_t>(0, atoll(e));
+  hmax = std::min<int64_t>(hmax, DC + DB);
+  Scratch slotC(std::max<int64_t>(DC, 1) * sizeof(uint32_t), st), slotB(std::max<int64_t>(DB, 1) * sizeof(uint32_t), st);
+  int64_t H = 0;
+  if (hmax > 0) {
+    Scratch cnt((DC + DB) * sizeof(uint32_t), st), cnt2((DC + DB) * sizeof(uint32_t), st);
+    Scratch vals((DC + DB) * sizeof(uint32_t), st), vals2((DC + DB) * sizeof(uint32_t), st);
+    HBK_CUDA(cudaMemsetAsync(cnt.p, 0, (DC + DB) * sizeof(uint32_t), st));
+    k_hist_u32<<<grid_for(M, 256), 256, 0, st>>>(cs->leaf.as<uint32_t>(), M, cnt.as<uint32_t>());
+    check_launch("k_hist_u32");
+    k_hist_u32<<<grid_for(F, 256), 256, 0, st>>>(cs->idx[L].as<uint32_t>(), F, cnt.as<uint32_t>() + DC);
+    check_launch("k_hist_u32");
+    k_hot_candidates<<<grid_for(DC + DB, 256), 256, 0, st>>>(DC, DB, vals.as<uint32_t>());
+    check_launch("k_hot_candidates");
+    cub::DoubleBuffer<uint32_t> kb(cnt.as<uint32_t>(), cnt2.as<uint32_t>());
+    cub::DoubleBuffer<uint32_t> vb(vals.as<uint32_t>(), vals2.as<uint32_t>());
+    size_t tmp = 0;
+    HBK_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, kb, vb, int(DC + DB), 0, 32, st));
+    Scratch t(tmp, st);
+    HBK_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.p, tmp, kb, vb, int(DC + DB), 0, 32, st));
+    std::vector<uint32_t> top(hmax);
+    HBK_CUDA(cudaMemcpyAsync(top.data(), kb.Current(), hmax * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    HBK_CUDA(cudaStreamSynchronize(st));
+    while (H < hmax && top[H] >= 2) ++H;
+    if (H) {
+      p->hot_list = dalloc(H * sizeof(uint32_t), st);
+      HBK_CUDA(cudaMemcpyAsync(p->hot_list.p, vb.Current(), H * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+      HBK_CUDA(cudaMemsetAsync(slotC.p, 0xFF, DC * sizeof(uint32_t), st));
+      HBK_CUDA(cudaMemsetAsync(slotB.p, 0xFF, DB * sizeof(uint32_t), st));
+      k_hot_slots<<<grid_for(H, 256), 256, 0, st>>>(p->hot_list.as<uint32_t>(), uint32_t(H),
+                                                    slotC.as<uint32_t>(), slotB.as<uint32_t>());
+      check_launch("k_hot_slots");
+    }
+  }
+  p->work.hot_list = H ? p->hot_list.as<uint32_t>() : nullptr;
+  p->work.nhot = uint32_t(H);
+  p->hot_smem = size_t(H) * 128;
+  // the record stream
+  Scratch last(std::max<int64_t>(F, 1), st);
+  HBK_CUDA(cudaMemsetAsync(last.p, 0, std::max<int64_t>(F, 1), st));
+  k_mark_last_segment<<<grid_for(S, 256), 256, 0, st>>>(fpos.as<uint32_t>(), S, last.as<uint8_t>());
+  check_launch("k_mark_last_segment");
+  p->csf_stream = dalloc((M + F) * sizeof(uint2), st);
+  k_build_stream<<<grid_for(F, 128), 128, 0, st>>>(
+      cs->ptr[L].as<uint32_t>(), cs->idx[L].as<uint32_t>(), last.as<uint8_t>(), F, cs->leaf.as<uint32_t>(),
+      cs->v32.as<float>(), H ? slotC.as<uint32_t>() : nullptr, H ? slotB.as<uint32_t>() : nullptr,
+      p->csf_stream.as<uint2>());
+  check_launch("k_build_stream");
+  p->work.csf_stream = p->csf_stream.as<uint2>();
+  // tasks
+  Scratch sst((S + 1) * sizeof(uint32_t), st);
+  k_stream_slice_starts<<<grid_for(S + 1, 256), 256, 0, st>>>(loff.as<uint32_t>(), fpos.as<uint32_t>(), S,
+                                                              sst.as<uint32_t>());
+  check_launch("k_stream_slice_starts");
+  BucketTasks bt;
+  Scratch cnt((S + 1) * sizeof(uint32_t), st), slot((S + 1) * sizeof(uint32_t), st);
+  k_task_count<<<grid_for(S, 256), 256, 0, st>>>(sst.as<uint32_t>(), S, T, cnt.as<uint32_t>(),
+                                                 slot.as<uint32_t>());
+  check_launch("k_task_count");
+  const uint32_t n = exclusive_scan_total(cnt.as<uint32_t>(), S, st);
+  const uint32_t nslot = exclusive_scan_total(slot.as<uint32_t>(), S, st);
+  bt.tasks = Scratch(size_t(std::max<uint32_t>(n, 1)) * sizeof(Task), st);
+  k_task_fill_stream<<<grid_for(S, 128), 128, 0, st>>>(sst.as<uint32_t>(), fpos.as<uint32_t>(),
+                                                       cs->ptr[L].as<uint32_t>(), S, T, cnt.as<uint32_t>(),
+                                                       slot.as<uint32_t>(), bt.tasks.as<Task>());
+  check_launch("k_task_fill_stream");
+  k_task_hi<<<grid_for(n, 256), 256, 0, st>>>(bt.tasks.as<Task>(), n, uint32_t(M + F));
+  check_launch("k_task_hi");
+  bt.n = n;
+  bt.slots = nslot;
+  HBK_CUDA(cudaStreamSynchronize(st));
+  return bt;
+}
+
+static int max_dyn_smem() {
+  int dev = 0, optin = 0;
+  HBK_CUDA(cudaGetDevice(&dev));
+  HBK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  return optin - 1024;
+}
+
 static void build_plan(hbk_plan* p, cudaStream_t st) {
   const int N = p->order;
   const int R = p->rank;
-  // fast path: order 3, R = 32 (8 lanes x float4 per row)
-  p->fast = (N == 3 && R == 32);
+  // fast path: order 3, R = 32 (8 lanes x float4 per row); the streams keep
+  // two flag bits in the leaf coordinate, so leaf extents must stay < 2^30
+  p->fast = (N == 3 && R == 32 && p->dims[p->mo[2]] < (int64_t(1) << 29) &&
+             p->dims[p->mo[1]] < (int64_t(1) << 29));
   const int gpw = p->fast ? 4 : 1;
-  const uint32_t Tcsf = p->fast ? TASK_NNZ_CSF : GEN_TASK_NNZ;
+  if (const char* e = getenv("HBK_CSF_VARIANT")) p->csf_var = std::max(0, std::min(4, atoi(e)));
+  uint32_t task_nnz = TASK_NNZ_CSF;
+  if (const char* e = getenv("HBK_TASK_NNZ")) task_nnz = std::max(8, atoi(e));
+  const uint32_t Tcsf = p->fast ? task_nnz : GEN_TASK_NNZ;
   const uint32_t Tcsl = p->fast ? TASK_NNZ_CSL : GEN_TASK_NNZ;
   const uint32_t Tcoo = p->fast ? TASK_NNZ_COO : GEN_TASK_NNZ;
 
@@ -764,7 +1268,21 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     k_csf_slice_offsets<<<grid_for(S + 1, 256), 256, 0, st>>>(ch, S, fpos.as<uint32_t>(),
                                                               p->csf_send.as<uint32_t>());
     check_launch("k_csf_slice_offsets");
-    if (p->sched) {
+    // schedule-driven plans execute the schedule's units on the pair-stream kernel
+    if (p->sched && p->csf_var == 4) p->csf_var = 0;
+    if (!p->fast) p->csf_var = 0;
+    const bool stream4 = p->csf_var == 4;
+    if (stream4) {
+      tcsf = build_csf_stream(p, c, Tcsf, st);
+      int64_t m = c->M, a = c->M;
+      for (int d = N - 2; d >= 1; --d) {
+        m += c->n[d];
+        if (d < N - 2) a += c->n[d];
+      }
+      a += c->n[0];
+      muls += m * R;
+      adds += a * R;
+    } else if (p->sched) {
       hbk_sched* sc = p->sched;
       HBK_REQUIRE(sc->S == S && sc->F == c->n[L], HBK_EINVAL,
                   "schedule was built for a different tree");
@@ -839,7 +1357,23 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     w.csf_val = c->v32.as<float>();
     w.csf_F = uint32_t(c->n[L]);
     w.csf_S = uint32_t(S);
-    stream_bytes += 8 * c->M + 8 * c->n[L] + 8 * S;
+    if (p->fast && !stream4) {
+      p->csf_pairs = dalloc(c->M * sizeof(uint2), st);
+      uint2* pp = p->csf_pairs.as<uint2>();
+      k_pairs<<<grid_for(c->M, 256), 256, 0, st>>>(c->leaf.as<uint32_t>(), c->v32.as<float>(),
+                                                   c->M, pp);
+      check_launch("k_pairs");
+      k_flag_ends<<<grid_for(c->n[L], 256), 256, 0, st>>>(c->ptr[L].as<uint32_t>(), c->n[L], FEND,
+                                                          pp);
+      check_launch("k_flag_ends");
+      k_flag_ends<<<grid_for(S, 256), 256, 0, st>>>(p->csf_send.as<uint32_t>(), S, SEND, pp);
+      check_launch("k_flag_ends");
+      w.csf_pairs = pp;
+    }
+    if (stream4)
+      stream_bytes += 8 * (c->M + p->stream_tree->n[L]) + 4 * S;
+    else
+      stream_bytes += p->fast ? 8 * c->M + 4 * c->n[L] + 4 * S : 8 * c->M + 8 * c->n[L] + 8 * S;
   }
   if (p->csl && p->csl->M > 0) {
     hbk_csl* s = p->csl;
@@ -857,9 +1391,19 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     w.csl_k = N >= 3 ? s->rest[1].as<uint32_t>() : nullptr;
     w.csl_val = s->v32.as<float>();
     w.csl_S = uint32_t(s->S);
+    if (p->fast) {
+      p->csl_pairs = dalloc(s->M * sizeof(uint2), st);
+      uint2* pp = p->csl_pairs.as<uint2>();
+      k_pairs<<<grid_for(s->M, 256), 256, 0, st>>>(s->rest[1].as<uint32_t>(), s->v32.as<float>(),
+                                                   s->M, pp);
+      check_launch("k_pairs");
+      k_flag_ends<<<grid_for(s->S, 256), 256, 0, st>>>(s->slice_ptr.as<uint32_t>(), s->S, SEND, pp);
+      check_launch("k_flag_ends");
+      w.csl_pairs = pp;
+    }
     muls += int64_t(N - 1) * s->M * R;
     adds += s->M * R;
-    stream_bytes += 4 * int64_t(N) * s->M + 8 * s->S;
+    stream_bytes += 4 * int64_t(N) * s->M + (p->fast ? 4 : 8) * s->S;
   }
   if (p->coo && p->coo->nnz > 0) {
     hbk_coo* t = p->coo;
@@ -868,6 +1412,13 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     w.coo_j = t->cols[p->mo[1]].as<uint32_t>();
     w.coo_k = t->cols[p->mo[2]].as<uint32_t>();
     w.coo_val = t->v32.as<float>();
+    if (p->fast) {
+      p->coo_quads = dalloc(t->nnz * sizeof(uint4), st);
+      k_quads<<<grid_for(t->nnz, 256), 256, 0, st>>>(w.coo_i, w.coo_j, w.coo_k, w.coo_val, t->nnz,
+                                                     p->coo_quads.as<uint4>());
+      check_launch("k_quads");
+      w.coo_quads = p->coo_quads.as<uint4>();
+    }
     muls += int64_t(N - 1) * t->nnz * R;
     adds += t->nnz * R;
     stream_bytes += 4 * int64_t(N + 1) * t->nnz;
@@ -955,23 +1506,67 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   int dev = 0, sms = 0, per_sm = 0;
   HBK_CUDA(cudaGetDevice(&dev));
   HBK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  auto grid_for_tasks = [&](int64_t ntask, int per) {
+    per = std::max(per, 1);
+    const int64_t want = int64_t(sms) * per;
+    const int64_t warps_needed = (ntask + gpw - 1) / gpw;
+    const int64_t blocks_needed = std::max<int64_t>(1, (warps_needed + 7) / 8);
+    return int(std::min(want, blocks_needed));
+  };
+  int launches = 0;
   if (p->fast) {
-    HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp3_r32, p->block, 0));
+    p->block = FAST_BLOCK;
+    const int64_t ntk[3] = {int64_t(w.n0), int64_t(w.n1) - w.n0, int64_t(w.n3) - w.n1};
+    for (int k = 0; k < 3; ++k) {
+      if (k == 0 && p->csf_var == 4) {
+        const bool hotb = p->work.nhot > 0;
+        const int blk = hotb ? 512 : 256;
+        const void* fn = hotb ? (const void*)k_mttkrp3_r32_stream<512> : (const void*)k_mttkrp3_r32_stream<256>;
+        // the attribute is process-global: raise it to the device maximum once
+        // so plans with different hot-row counts never lower it under each other
+        HBK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn_smem()));
+        HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, blk, p->hot_smem));
+        per_sm = std::max(per_sm, 1);
+        const int64_t warps_needed = (ntk[0] + gpw - 1) / gpw;
+        const int64_t blocks_needed = std::max<int64_t>(1, (warps_needed + blk / 32 - 1) / (blk / 32));
+        p->grids[0] = ntk[0] > 0 ? int(std::min<int64_t>(int64_t(sms) * per_sm, blocks_needed)) : 0;
+        p->csf_block = blk;
+        w.total_warps[0] = uint32_t(p->grids[0]) * (blk / 32);
+        launches += ntk[0] > 0;
+        continue;
+      }
+      if (k == 0)
+        HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp3_r32<KIND_CSF>,
+                                                               p->block, 0));
+      if (k == 1)
+        HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp3_r32<KIND_CSL>,
+                                                               p->block, 0));
+      if (k == 2)
+        HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp3_r32<KIND_COO>,
+                                                               p->block, 0));
+      p->grids[k] = ntk[k] > 0 ? grid_for_tasks(ntk[k], per_sm) : 0;
+      w.total_warps[k] = uint32_t(p->grids[k]) * (p->block / 32);
+      launches += ntk[k] > 0;
+    }
+    // a plan with no task at all still launches once (nothing to write, but
+    // keeps launch accounting uniform)
+    if (launches == 0) {
+      p->grids[2] = 1;
+      w.total_warps[2] = p->block / 32;
+      launches = 1;
+    }
   } else {
     HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp_generic, p->block, 0));
+    p->grid = grid_for_tasks(w.n3, per_sm);
+    w.total_warps[0] = uint32_t(p->grid) * (p->block / 32);
+    launches = 1;
   }
-  per_sm = std::max(per_sm, 1);
-  int64_t want = int64_t(sms) * per_sm;
-  const int64_t warps_needed = (int64_t(w.n3) + gpw - 1) / gpw;
-  const int64_t blocks_needed = std::max<int64_t>(1, (warps_needed + 7) / 8);
-  p->grid = int(std::min(want, blocks_needed));
-  w.total_warps = uint32_t(p->grid) * (p->block / 32);
 
   p->info.mode = p->mode;
   p->info.rank = R;
   p->info.out_rows = rows;
   p->info.split_rows = slots;
-  p->info.launches = 1;
+  p->info.launches = launches;
   p->info.fast_path = p->fast;
   int64_t nnz = 0;
   if (p->csf) nnz += p->csf->M;
@@ -1067,7 +1662,16 @@ int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out,
                           16 ==
                       0,
                   HBK_EINVAL, "factor and output buffers must be 16-byte aligned");
-      k_mttkrp3_r32<<<p->grid, p->block, 0, st>>>(p->work, fx);
+      if (p->grids[0]) {
+        if (p->csf_var == 4 && p->csf_block == 512)
+          k_mttkrp3_r32_stream<512><<<p->grids[0], 512, p->hot_smem, st>>>(p->work, fx);
+        else if (p->csf_var == 4)
+          k_mttkrp3_r32_stream<256><<<p->grids[0], 256, p->hot_smem, st>>>(p->work, fx);
+        else
+          k_mttkrp3_r32<KIND_CSF><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
+      }
+      if (p->grids[1]) k_mttkrp3_r32<KIND_CSL><<<p->grids[1], p->block, 0, st>>>(p->work, fx);
+      if (p->grids[2]) k_mttkrp3_r32<KIND_COO><<<p->grids[2], p->block, 0, st>>>(p->work, fx);
       check_launch("k_mttkrp3_r32");
     } else {
       WorkN wn{};

@@ -56,21 +56,27 @@ def powerlaw_tensor(dims, nnz: int, alpha, seed: int, scale: float = 1.0) -> Coo
     gen.manual_seed(int(seed))
     have = torch.empty((0, len(dims)), dtype=torch.int32, device="cuda")
     need = nnz
-    for _ in range(64):
+    import os, time
+    verbose = bool(os.environ.get("HBK_GEN_VERBOSE"))
+    for it in range(64):
+        tic = time.perf_counter()
         draw = int(math.ceil(1.15 * need)) + 16
         new = torch.stack([_draw_mode(torch, gen, draw, d, a) for d, a in zip(dims, alpha)], dim=1)
         cand = torch.cat([have, new], dim=0)
         zero = torch.zeros(cand.shape[0], dtype=torch.float32, device="cuda")
         uniq = unique_coordinates(CooTensor(dims, cand, zero))
         have = _coords_of(torch, uniq)
+        if verbose:
+            torch.cuda.synchronize()
+            print(f"[gen] iter {it}: drew {draw}, unique {have.shape[0]}/{nnz} "
+                  f"({time.perf_counter() - tic:.2f}s)", flush=True)
         if have.shape[0] >= nnz:
             break
         need = nnz - have.shape[0]
     else:
         raise RuntimeError("could not draw enough distinct coordinates")
     if have.shape[0] > nnz:
-        keys = torch.rand(have.shape[0], generator=gen, device="cuda", dtype=torch.float64)
-        keep = torch.topk(keys, nnz, largest=False).indices
+        keep = torch.randperm(have.shape[0], generator=gen, device="cuda")[:nnz]
         have = have[keep]
     vals = 1.0 - torch.rand(nnz, generator=gen, device="cuda", dtype=torch.float64)
     return canonicalize(CooTensor(dims, have, vals))

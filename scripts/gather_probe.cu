@@ -1,0 +1,275 @@
+// Gather-throughput probe: how fast can B200 gather 128-byte factor rows by
+// index (the MTTKRP inner operation)?  Standalone; build & run on the box:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/gp scripts/gather_probe.cu && /tmp/gp
+// Variants:
+//   ldg<U,W>   : 8 lanes x LDG.128 per row, U rows in flight per 8-lane group,
+//                W warps per block (occupancy).
+//   tma<S>     : each lane issues cp.async.bulk (TMA) of its own row into a
+//                per-warp S-stage smem ring (mbarrier complete_tx), consumer
+//                reads LDS.128.
+// Index streams: Zipf(1) over 28818 rows (nell-2 leaf mode, L2-resident
+// factor) and uniform / Zipf over 25.5M rows (nell-1 leaf mode, 3.2 GB).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <cmath>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e = (x);                                                             \
+    if (e != cudaSuccess) {                                                          \
+      printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+      exit(1);                                                                       \
+    }                                                                                \
+  } while (0)
+
+__device__ __forceinline__ float4 ldrow(const float4* p) {
+  float4 v;
+  asm("ld.global.nc.L1::evict_last.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p));
+  return v;
+}
+
+template <int U>
+__global__ void k_ldg(const float4* __restrict__ F, const uint32_t* __restrict__ idx, int64_t n,
+                      float4* __restrict__ out) {
+  const int lane = threadIdx.x & 31, g = lane >> 3, lig = lane & 7;
+  const int64_t gid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 3;
+  const int64_t ngroups = (int64_t(gridDim.x) * blockDim.x) >> 3;
+  float4 acc = make_float4(0, 0, 0, 0);
+  for (int64_t base = gid * U; base < n; base += ngroups * U) {
+    uint32_t k = (base + lig < n && lig < U) ? idx[base + lig] : 0;
+    float4 r[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      uint32_t kj = __shfl_sync(0xffffffffu, k, j % 8, 8);
+      r[j] = ldrow(F + size_t(kj) * 8 + lig);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      acc.x += r[j].x;
+      acc.y += r[j].y;
+      acc.z += r[j].z;
+      acc.w += r[j].w;
+    }
+  }
+  (void)g;
+  out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = acc;
+}
+
+// 4 lanes x LDG.256 per row (8 rows per warp instruction)
+struct f8 {
+  float v[8];
+};
+__device__ __forceinline__ f8 ldrow8(const float* p) {
+  f8 r;
+  asm("ld.global.nc.L1::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+        "=f"(r.v[6]), "=f"(r.v[7])
+      : "l"(p));
+  return r;
+}
+template <int U>
+__global__ void k_ldg256(const float* __restrict__ F, const uint32_t* __restrict__ idx, int64_t n,
+                         float* __restrict__ out) {
+  const int lane = threadIdx.x & 31, lig = lane & 3;
+  const int64_t gid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 2;
+  const int64_t ngroups = (int64_t(gridDim.x) * blockDim.x) >> 2;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t base = gid * U; base < n; base += ngroups * U) {
+    uint32_t k[U / 4 > 0 ? U / 4 : 1];
+#pragma unroll
+    for (int q = 0; q < (U + 3) / 4; ++q) k[q] = (base + 4 * q + lig < n) ? idx[base + 4 * q + lig] : 0;
+    f8 r[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      uint32_t kj = __shfl_sync(0xffffffffu, k[j / 4], j % 4, 4);
+      r[j] = ldrow8(F + size_t(kj) * 32 + lig * 8);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += r[j].v[i];
+  }
+  float s = 0;
+  for (int i = 0; i < 8; ++i) s += acc[i];
+  out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = s;
+}
+
+// ---- TMA (cp.async.bulk) gather -------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n }\n" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_row(void* smem, const void* g, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 128, [%2];" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(g), "r"((uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+
+template <int S>
+__global__ void k_tma(const float4* __restrict__ F, const uint32_t* __restrict__ idx, int64_t n,
+                      float4* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lig = lane & 7, g = lane >> 3;
+  const int nw = blockDim.x >> 5;
+  float4* ring = reinterpret_cast<float4*>(smem) + size_t(warp) * S * 32 * 8;  // S stages x 32 rows x 8 float4
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(nw) * S * 32 * 128) + warp * S;
+  if (lane == 0)
+    for (int s = 0; s < S; ++s) mbar_init(bars + s, 1);
+  __syncwarp();
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const int64_t wid = blockIdx.x * int64_t(nw) + warp;
+  const int64_t nwarps = int64_t(gridDim.x) * nw;
+  // warp batch = 32 rows (lane l fetches row idx[base + l])
+  const int64_t nbatch = (n + 31) / 32;
+  float4 acc = make_float4(0, 0, 0, 0);
+  int64_t mine = wid < nbatch ? (nbatch - 1 - wid) / nwarps + 1 : 0;
+  auto issue = [&](int64_t b, int s) {
+    const int64_t e = (wid + b * nwarps) * 32 + lane;
+    const int64_t rem = n - (wid + b * nwarps) * 32; const int cnt = rem < 32 ? (int)rem : 32;
+    if (lane == 0) mbar_expect(bars + s, cnt * 128);
+    __syncwarp();
+    if (lane < cnt) bulk_row(ring + (s * 32 + lane) * 8, F + size_t(idx[e]) * 8, bars + s);
+  };
+  for (int s = 0; s < S - 1 && s < mine; ++s) issue(s, s);
+  for (int64_t b = 0; b < mine; ++b) {
+    const int s = b % S;
+    if (b + S - 1 < mine) issue(b + S - 1, (b + S - 1) % S);
+    mbar_wait(bars + s, (b / S) & 1);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4 r = ring[(s * 32 + g * 8 + j) * 8 + lig];
+      acc.x += r.x;
+      acc.y += r.y;
+      acc.z += r.z;
+      acc.w += r.w;
+    }
+    __syncwarp();
+  }
+  out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = acc;
+}
+
+static std::vector<uint32_t> zipf_stream(int64_t n, uint32_t rows, double alpha, uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> U(0.0, 1.0);
+  std::vector<uint32_t> v(n);
+  const double top = double(rows) + 1.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double u = U(rng), x;
+    if (alpha == 1.0)
+      x = std::exp(u * std::log(top));
+    else if (alpha == 0.0)
+      x = 1.0 + u * (top - 1.0);
+    else
+      x = std::pow((std::pow(top, 1 - alpha) - 1) * u + 1, 1 / (1 - alpha));
+    int64_t k = int64_t(std::floor(x)) - 1;
+    if (k < 0) k = 0;
+    if (k >= rows) k = rows - 1;
+    v[i] = uint32_t(k);
+  }
+  return v;
+}
+
+template <class Fn>
+static float time_ms(Fn fn, int reps = 10) {
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  fn();
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(a));
+  for (int i = 0; i < reps; ++i) fn();
+  CK(cudaEventRecord(b));
+  CK(cudaEventSynchronize(b));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  return ms / reps;
+}
+
+int main() {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int64_t n = 40'000'000;
+  struct Case {
+    const char* name;
+    uint32_t rows;
+    double alpha;
+  } cases[] = {{"zipf1 28818 rows (L2)", 28818, 1.0},
+               {"zipf1 25.5M rows (HBM)", 25495389, 1.0},
+               {"uniform 25.5M rows (HBM)", 25495389, 0.0}};
+  float4* out;
+  CK(cudaMalloc(&out, size_t(sms) * 64 * 256 * sizeof(float4)));
+  for (auto& c : cases) {
+    std::vector<uint32_t> h = zipf_stream(n, c.rows, c.alpha, 7);
+    uint32_t* idx;
+    float4* F;
+    CK(cudaMalloc(&idx, n * 4));
+    CK(cudaMemcpy(idx, h.data(), n * 4, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&F, size_t(c.rows) * 128));
+    {
+      std::vector<float> hf(size_t(c.rows) * 32);
+      for (size_t i = 0; i < hf.size(); ++i) hf[i] = float((i * 2654435761u) % 1000) * 1e-3f;
+      CK(cudaMemcpy(F, hf.data(), hf.size() * 4, cudaMemcpyHostToDevice));
+    }
+    const double gb = double(n) * 128 / 1e9;
+    printf("== %s: %lld gathers of 128 B (%.2f GB)\n", c.name, (long long)n, gb);
+#define RUN_LDG(U, THREADS, BLOCKS_PER_SM)                                                        \
+  {                                                                                               \
+    int g = sms * BLOCKS_PER_SM;                                                                  \
+    float ms = time_ms([&] { k_ldg<U><<<g, THREADS>>>(F, idx, n, out); });                        \
+    printf("  ldg U=%2d thr=%d blk/sm=%d : %.3f ms  %.2f Grows/s  %.1f GB/s\n", U, THREADS,       \
+           BLOCKS_PER_SM, ms, n / ms / 1e6, gb / ms * 1e3);                                       \
+  }
+    RUN_LDG(8, 256, 2);
+    RUN_LDG(8, 256, 4);
+    RUN_LDG(8, 256, 8);
+    RUN_LDG(16, 256, 2);
+    RUN_LDG(16, 256, 4);
+    RUN_LDG(32, 256, 2);
+#define RUN_TMA(S, THREADS, BLOCKS_PER_SM)                                                          \
+  {                                                                                                 \
+    size_t sm = size_t(THREADS / 32) * S * (32 * 128 + 8);                                          \
+    CK(cudaFuncSetAttribute(k_tma<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));       \
+    int g = sms * BLOCKS_PER_SM;                                                                    \
+    float ms = time_ms([&] { k_tma<S><<<g, THREADS, sm>>>(F, idx, n, out); });                      \
+    CK(cudaGetLastError());                                                                         \
+    printf("  tma S=%d thr=%d blk/sm=%d smem=%zuKB: %.3f ms  %.2f Grows/s  %.1f GB/s\n", S, THREADS, \
+           BLOCKS_PER_SM, sm / 1024, ms, n / ms / 1e6, gb / ms * 1e3);                              \
+  }
+#define RUN_LDG8(U, THREADS, BLOCKS_PER_SM)                                                       \
+  {                                                                                               \
+    int g = sms * BLOCKS_PER_SM;                                                                  \
+    float ms = time_ms([&] { k_ldg256<U><<<g, THREADS>>>((const float*)F, idx, n, (float*)out); }); \
+    printf("  ldg256 U=%2d thr=%d blk/sm=%d : %.3f ms  %.2f Grows/s  %.1f GB/s\n", U, THREADS,   \
+           BLOCKS_PER_SM, ms, n / ms / 1e6, gb / ms * 1e3);                                       \
+  }
+    RUN_LDG8(4, 256, 2);
+    RUN_LDG8(4, 256, 4);
+    RUN_LDG8(8, 256, 2);
+    RUN_LDG8(8, 256, 3);
+    RUN_LDG8(16, 256, 2);
+    if (getenv("TMA")) RUN_TMA(2, 256, 2);
+
+    CK(cudaFree(idx));
+    CK(cudaFree(F));
+  }
+  return 0;
+}

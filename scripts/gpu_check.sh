@@ -7,5 +7,5 @@ timeout 1200 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS} > gpurun_out/pyt
 if [ -n "$BENCH" ]; then
   timeout 1200 python bench.py $BENCH > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 fi
-tail -3 gpurun_out/smoke.log gpurun_out/pytest_gpu.log
+tail -n 3 gpurun_out/smoke.log gpurun_out/pytest_gpu.log
 tail -c 3000 gpurun_out/bench.log 2>/dev/null
