@@ -207,6 +207,7 @@ __device__ __forceinline__ void flush_split(const Work& w, bool active, uint32_t
 // slice rows are consumed in order from their own streams (no pointer is
 // chased).  The next batch's stream words are loaded before the current
 // batch is reduced.  Returns the partial of a chunk task (zero for runs).
+template <bool PREFETCH>
 __device__ __forceinline__ float4 csf_tasks(const Work& w, const Factors3& fx, const Task& t,
                                             int g, int lig, uint64_t pol_s, uint64_t pol_r,
                                             float4* __restrict__ slots) {
@@ -414,7 +415,7 @@ __device__ __forceinline__ void zero_task(const Work& w, const Factors3& fx, con
 // it.  Chunks of one split slice that land in the same warp are summed with
 // shuffles and handed over with a single vector atomic.
 static constexpr int FAST_BLOCK = 256;
-enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2 };
+enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2, KIND_CSF_PF = 3 };
 
 template <int KIND>
 __global__ void __launch_bounds__(FAST_BLOCK, 3)
@@ -427,23 +428,25 @@ __global__ void __launch_bounds__(FAST_BLOCK, 3)
   float4* slots = s_slots + (threadIdx.x >> 3) * 64 + lig;
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_r = policy_evict_last();
-  const uint32_t first = KIND == KIND_CSF ? 0u : (KIND == KIND_CSL ? w.n0 : w.n1);
-  const uint32_t last = KIND == KIND_CSF ? w.n0 : (KIND == KIND_CSL ? w.n1 : w.n3);
-  uint32_t* ctr = w.ws_ctr + 2 * KIND;
+  constexpr int K = KIND == KIND_CSF_PF ? KIND_CSF : KIND;
+  const uint32_t first = K == KIND_CSF ? 0u : (K == KIND_CSL ? w.n0 : w.n1);
+  const uint32_t last = K == KIND_CSF ? w.n0 : (K == KIND_CSL ? w.n1 : w.n3);
+  uint32_t* ctr = w.ws_ctr + 2 * K;
   for (;;) {
     uint32_t base = 0;
     if (lane == 0) base = atomicAdd(ctr, 4u);
     base = __shfl_sync(FULL, base, 0) + first;
     if (base >= last) break;
     const Task t = w.tasks[base + g];
-    if (KIND == KIND_CSF || KIND == KIND_CSL) {
-      const float4 sa = KIND == KIND_CSF ? csf_tasks(w, fx, t, g, lig, pol_s, pol_r, slots)
-                                         : csl_tasks(w, fx, t, g, lig, pol_s, pol_r, slots);
+    if (K == KIND_CSF || K == KIND_CSL) {
+      const float4 sa = KIND == KIND_CSF   ? csf_tasks<false>(w, fx, t, g, lig, pol_s, pol_r, slots)
+                        : KIND == KIND_CSF_PF ? csf_tasks<true>(w, fx, t, g, lig, pol_s, pol_r, slots)
+                                              : csl_tasks(w, fx, t, g, lig, pol_s, pol_r, slots);
       const bool mine = t.slot != NOSLOT && t.lo < t.hi;
       const uint32_t slot0 = __shfl_sync(FULL, t.slot, 0);
       const bool same = __all_sync(FULL, mine && t.slot == slot0);
       const uint32_t row =
-          mine ? (KIND == KIND_CSF ? __ldg(w.csf_sidx + t.s) : __ldg(w.csl_sidx + t.s)) : 0u;
+          mine ? (K == KIND_CSF ? __ldg(w.csf_sidx + t.s) : __ldg(w.csl_sidx + t.s)) : 0u;
       if (same) {
         float4 r = add4(sa, shfl_xor4(sa, 8));
         r = add4(r, shfl_xor4(r, 16));
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(FAST_BLOCK, 3)
   }
   if (lane == 0) {
     const uint32_t done = atomicAdd(ctr + 1, 1u);
-    if (done == w.total_warps[KIND] - 1) {
+    if (done == w.total_warps[K] - 1) {
       ctr[0] = 0;
       ctr[1] = 0;
     }
@@ -611,6 +614,198 @@ __global__ void __launch_bounds__(BLOCK, 512 / BLOCK)
       flush_split(w, g == 0, t.slot, t.nchunk, 4u, row, r, fx.out, lane, lig);
     } else if (__any_sync(FULL, mine)) {
       flush_split(w, mine, t.slot, t.nchunk, 1u, row, sa, fx.out, lane, lig);
+    }
+  }
+  if (lane == 0) {
+    const uint32_t done = atomicAdd(ctr + 1, 1u);
+    if (done == w.total_warps[KIND_CSF] - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+  }
+}
+
+// ------------------------------------- CSF tasks, 4-lane groups (LDG.256) --
+// Each factor row (32 fp32 = 128 B) is fetched by 4 lanes with one 256-bit
+// load each, so a warp runs 8 tasks side by side and every per-nonzero scalar
+// (index/value shuffles, flag tests, address math) is shared by 4 lanes
+// instead of 8.  Same one-wavefront-per-row L1 cost as the 8-lane layout.
+struct f8 {
+  float4 a, b;
+};
+__device__ __forceinline__ f8 f8zero() { return {f4zero(), f4zero()}; }
+__device__ __forceinline__ f8 ld_row8(const float* p, uint64_t pol) {
+  f8 r;
+  asm("ld.global.nc.L1::evict_last.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+      : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y), "=f"(r.b.z),
+        "=f"(r.b.w)
+      : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ f8 fma8(float a, const f8& x, const f8& y) {
+  return {fma4(a, x.a, y.a), fma4(a, x.b, y.b)};
+}
+__device__ __forceinline__ f8 fmav8(const f8& a, const f8& x, const f8& y) {
+  return {fmav4(a.a, x.a, y.a), fmav4(a.b, x.b, y.b)};
+}
+__device__ __forceinline__ f8 add8(const f8& a, const f8& b) { return {add4(a.a, b.a), add4(a.b, b.b)}; }
+__device__ __forceinline__ f8 shfl_xor8(const f8& v, int m) { return {shfl_xor4(v.a, m), shfl_xor4(v.b, m)}; }
+// OR of the eight groups' nibbles of a ballot
+__device__ __forceinline__ uint32_t any_group4(uint32_t b) {
+  b |= b >> 16;
+  b |= b >> 8;
+  b |= b >> 4;
+  return b & 0xFu;
+}
+
+// split-slice hand-over for 4-lane groups (each lane owns 8 of the 32 floats)
+__device__ __forceinline__ void flush_split8(const Work& w, bool active, uint32_t slot, uint32_t nchunk,
+                                             uint32_t inc, uint32_t row, const f8& sa, float* out,
+                                             int lane, int lig) {
+  float4* acc = reinterpret_cast<float4*>(w.ws_acc) + size_t(active ? slot : 0) * 8 + 2 * lig;
+  if (active) {
+    red_add4(acc, sa.a);
+    red_add4(acc + 1, sa.b);
+  }
+  __threadfence();
+  __syncwarp();
+  uint32_t old = 0;
+  if (active && lig == 0) old = atomicAdd(w.ws_cnt + slot, inc);
+  old = __shfl_sync(FULL, old, lane & ~3);
+  if (active && old + inc == nchunk) {
+    __threadfence();
+    float4* o = reinterpret_cast<float4*>(out) + size_t(row) * 8 + 2 * lig;
+    o[0] = ld_cg4(acc);
+    o[1] = ld_cg4(acc + 1);
+    st_cg4(acc, f4zero());
+    st_cg4(acc + 1, f4zero());
+    if (lig == 0) w.ws_cnt[slot] = 0;
+  }
+}
+
+__device__ __forceinline__ f8 csf_tasks8(const Work& w, const float* __restrict__ Bm,
+                                         const float* __restrict__ Cm, float* __restrict__ out,
+                                         const Task& t, int g, int lig, uint64_t pol_s,
+                                         uint64_t pol_r, float4* __restrict__ slots) {
+  const uint32_t lo = t.lo, hi = t.hi;
+  const bool chunk = t.slot != NOSLOT;
+  const uint32_t my_batches = hi > lo ? (hi - lo + 3) / 4 : 0;
+  const uint32_t nbat = __reduce_max_sync(FULL, my_batches);
+  const float* Cl = Cm + 8 * lig;
+  const float* Bl = Bm + 8 * lig;
+  uint32_t s = t.s, f = t.f;
+  f8 fa = f8zero(), sa = f8zero();
+  uint2 pr = make_uint2(0u, 0u);
+  if (lo + lig < hi) pr = ld_stream_u2(w.csf_pairs + lo + lig, pol_s);
+  uint32_t fi = (hi > lo && f + lig < w.csf_F) ? __ldg(w.csf_fidx + f + lig) : 0u;
+  uint32_t sr = (hi > lo && !chunk && s + lig < w.csf_S) ? __ldg(w.csf_sidx + s + lig) : 0u;
+  bool pending = false;
+  uint32_t base = lo;
+  for (uint32_t it = 0; it < nbat; ++it, base += 4) {
+    const uint32_t n = base < hi ? min(4u, hi - base) : 0u;
+    const bool live = uint32_t(lig) < n;
+    const uint32_t k = pr.x & KMASK;
+    const float v = __uint_as_float(pr.y);
+    const uint32_t eb_all = __ballot_sync(FULL, live && (pr.x & FEND));
+    const uint32_t sb_all = __ballot_sync(FULL, live && !chunk && (pr.x & SEND));
+    const uint32_t ebits = (eb_all >> (4 * g)) & 0xFu;
+    const uint32_t sbits = (sb_all >> (4 * g)) & 0xFu;
+    const uint32_t eany = any_group4(eb_all);
+    const uint32_t sany = any_group4(sb_all);
+    f8 c[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t kj = __shfl_sync(FULL, k, j, 4);
+      if (uint32_t(j) < n) c[j] = ld_row8(Cl + size_t(kj) * 32, pol_r);
+    }
+    uint32_t tf = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if ((eany >> j) & 1u) {
+        const uint32_t fj = __shfl_sync(FULL, fi, tf, 4);
+        if ((ebits >> j) & 1u) {
+          const float4* src = reinterpret_cast<const float4*>(Bl + size_t(fj) * 32);
+          cp_async16(slots + j * 8, src);
+          cp_async16(slots + j * 8 + 1, src + 1);
+        }
+        tf += (ebits >> j) & 1u;
+      }
+    }
+    const uint32_t sr_cur = sr;
+    const float vv = v;
+    f += tf;
+    const uint32_t nsl = __popc(sbits);
+    s += nsl;
+    const uint32_t nb = base + 4;
+    if (nb < hi) {
+      pr = (nb + lig < hi) ? ld_stream_u2(w.csf_pairs + nb + lig, pol_s) : make_uint2(0u, 0u);
+      if (tf) fi = (f + lig < w.csf_F) ? __ldg(w.csf_fidx + f + lig) : 0u;
+      if (nsl) sr = (s + lig < w.csf_S) ? __ldg(w.csf_sidx + s + lig) : 0u;
+    }
+    cp_async_wait_all();
+    uint32_t ts = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float vj = __shfl_sync(FULL, vv, j, 4);
+      if (uint32_t(j) < n) fa = fma8(vj, c[j], fa);
+      if ((ebits >> j) & 1u) {
+        const f8 b{slots[j * 8], slots[j * 8 + 1]};
+        sa = fmav8(fa, b, sa);
+        fa = f8zero();
+      }
+      if ((sany >> j) & 1u) {
+        const uint32_t row = __shfl_sync(FULL, sr_cur, ts, 4);
+        if ((sbits >> j) & 1u) {
+          float4* o = reinterpret_cast<float4*>(out + size_t(row) * 32 + 8 * lig);
+          o[0] = sa.a;
+          o[1] = sa.b;
+          sa = f8zero();
+          ++ts;
+        }
+      }
+    }
+    if (n) pending = !((ebits >> (n - 1)) & 1u);
+  }
+  if (chunk && pending) {  // the chunk ended inside fiber f
+    const uint32_t fj = __ldg(w.csf_fidx + f);
+    sa = fmav8(fa, ld_row8(Bl + size_t(fj) * 32, pol_r), sa);
+  }
+  return sa;
+}
+
+__global__ void __launch_bounds__(FAST_BLOCK, 3)
+    k_csf_r32x8(const __grid_constant__ Work w, const __grid_constant__ Factors3 fx) {
+  // per lane: 4 slots of 32 B (one per batch position) for staged B rows
+  __shared__ float4 s_slots[FAST_BLOCK * 8];
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2;
+  const int lig = lane & 3;
+  // slot j of this lane: s_slots[(group_base + j) * 8 + 2*lig .. +1], group = 4 lanes x 4 slots
+  float4* slots = s_slots + (threadIdx.x >> 2) * 32 + 2 * lig;
+  const uint64_t pol_s = policy_evict_first();
+  const uint64_t pol_r = policy_evict_last();
+  const float* Bm = reinterpret_cast<const float*>(fx.B);
+  const float* Cm = reinterpret_cast<const float*>(fx.C);
+  float* out = reinterpret_cast<float*>(fx.out);
+  uint32_t* ctr = w.ws_ctr + 2 * KIND_CSF;
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(ctr, 8u);
+    base = __shfl_sync(FULL, base, 0);
+    if (base >= w.n0) break;
+    const Task t = w.tasks[base + g];
+    const f8 sa = csf_tasks8(w, Bm, Cm, out, t, g, lig, pol_s, pol_r, slots);
+    const bool mine = t.slot != NOSLOT && t.lo < t.hi;
+    const uint32_t slot0 = __shfl_sync(FULL, t.slot, 0);
+    const bool same = __all_sync(FULL, mine && t.slot == slot0);
+    const uint32_t row = mine ? __ldg(w.csf_sidx + t.s) : 0u;
+    if (same) {
+      f8 r = add8(sa, shfl_xor8(sa, 4));
+      r = add8(r, shfl_xor8(r, 8));
+      r = add8(r, shfl_xor8(r, 16));
+      flush_split8(w, g == 0, t.slot, t.nchunk, 8u, row, r, out, lane, lig);
+    } else if (__any_sync(FULL, mine)) {
+      flush_split8(w, mine, t.slot, t.nchunk, 1u, row, sa, out, lane, lig);
     }
   }
   if (lane == 0) {
@@ -1240,8 +1435,8 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   // two flag bits in the leaf coordinate, so leaf extents must stay < 2^30
   p->fast = (N == 3 && R == 32 && p->dims[p->mo[2]] < (int64_t(1) << 29) &&
              p->dims[p->mo[1]] < (int64_t(1) << 29));
-  const int gpw = p->fast ? 4 : 1;
-  if (const char* e = getenv("HBK_CSF_VARIANT")) p->csf_var = std::max(0, std::min(4, atoi(e)));
+  const int gpw = p->fast ? 8 : 1;  // task ranges padded so a warp never straddles kinds
+  if (const char* e = getenv("HBK_CSF_VARIANT")) p->csf_var = std::max(0, std::min(6, atoi(e)));
   uint32_t task_nnz = TASK_NNZ_CSF;
   if (const char* e = getenv("HBK_TASK_NNZ")) task_nnz = std::max(8, atoi(e));
   const uint32_t Tcsf = p->fast ? task_nnz : GEN_TASK_NNZ;
@@ -1506,10 +1701,10 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   int dev = 0, sms = 0, per_sm = 0;
   HBK_CUDA(cudaGetDevice(&dev));
   HBK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  auto grid_for_tasks = [&](int64_t ntask, int per) {
+  auto grid_for_tasks = [&](int64_t ntask, int per, int tasks_per_warp) {
     per = std::max(per, 1);
     const int64_t want = int64_t(sms) * per;
-    const int64_t warps_needed = (ntask + gpw - 1) / gpw;
+    const int64_t warps_needed = (ntask + tasks_per_warp - 1) / tasks_per_warp;
     const int64_t blocks_needed = std::max<int64_t>(1, (warps_needed + 7) / 8);
     return int(std::min(want, blocks_needed));
   };
@@ -1536,15 +1731,16 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
         continue;
       }
       if (k == 0)
-        HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp3_r32<KIND_CSF>,
-                                                               p->block, 0));
+        HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, p->csf_var == 5 ? (const void*)k_csf_r32x8 : (const void*)k_mttkrp3_r32<KIND_CSF>,
+            p->block, 0));
       if (k == 1)
         HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp3_r32<KIND_CSL>,
                                                                p->block, 0));
       if (k == 2)
         HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp3_r32<KIND_COO>,
                                                                p->block, 0));
-      p->grids[k] = ntk[k] > 0 ? grid_for_tasks(ntk[k], per_sm) : 0;
+      p->grids[k] = ntk[k] > 0 ? grid_for_tasks(ntk[k], per_sm, (k == 0 && p->csf_var == 5) ? 8 : 4) : 0;
       w.total_warps[k] = uint32_t(p->grids[k]) * (p->block / 32);
       launches += ntk[k] > 0;
     }
@@ -1557,7 +1753,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     }
   } else {
     HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp_generic, p->block, 0));
-    p->grid = grid_for_tasks(w.n3, per_sm);
+    p->grid = grid_for_tasks(w.n3, per_sm, 1);
     w.total_warps[0] = uint32_t(p->grid) * (p->block / 32);
     launches = 1;
   }
@@ -1667,6 +1863,10 @@ int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out,
           k_mttkrp3_r32_stream<512><<<p->grids[0], 512, p->hot_smem, st>>>(p->work, fx);
         else if (p->csf_var == 4)
           k_mttkrp3_r32_stream<256><<<p->grids[0], 256, p->hot_smem, st>>>(p->work, fx);
+        else if (p->csf_var == 5)
+          k_csf_r32x8<<<p->grids[0], p->block, 0, st>>>(p->work, fx);
+        else if (p->csf_var == 6)
+          k_mttkrp3_r32<KIND_CSF_PF><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
         else
           k_mttkrp3_r32<KIND_CSF><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
       }

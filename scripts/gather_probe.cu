@@ -101,6 +101,54 @@ __global__ void k_ldg256(const float* __restrict__ F, const uint32_t* __restrict
   out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = s;
 }
 
+// cp.async (LDGSTS) gathers into a per-group S-stage smem ring (8 rows per
+// stage per 8-lane group), consumer LDS.128.
+template <int S>
+__global__ void k_ldgsts(const float4* __restrict__ F, const uint32_t* __restrict__ idx, int64_t n,
+                         float4* __restrict__ out) {
+  extern __shared__ float4 ring[];  // [blockDim/8 groups][S][8 rows][8 lanes]
+  const int lane = threadIdx.x & 31, lig = lane & 7;
+  const int grp = threadIdx.x >> 3;
+  float4* my = ring + size_t(grp) * S * 64 + lig;
+  const int64_t gid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 3;
+  const int64_t ngroups = (int64_t(gridDim.x) * blockDim.x) >> 3;
+  const int64_t nb = (n + 7) / 8;
+  const int64_t mine = gid < nb ? (nb - 1 - gid) / ngroups + 1 : 0;
+  const int64_t maxb = (nb + ngroups - 1) / ngroups;
+  float4 acc = make_float4(0, 0, 0, 0);
+  auto issue = [&](int64_t b) {
+    if (b < mine) {
+      const int64_t base = (gid + b * ngroups) * 8;
+      uint32_t k = (base + lig < n) ? idx[base + lig] : 0;
+      float4* st = my + (b % S) * 64;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        uint32_t kj = __shfl_sync(0xffffffffu, k, j, 8);
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(st + j * 8);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(F + size_t(kj) * 8 + lig) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (int s = 0; s < S - 1; ++s) issue(s);
+  for (int64_t b = 0; b < maxb; ++b) {
+    issue(b + S - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");
+    if (b < mine) {
+      const float4* st = my + (b % S) * 64;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float4 r = st[j * 8];
+        acc.x += r.x;
+        acc.y += r.y;
+        acc.z += r.z;
+        acc.w += r.w;
+      }
+    }
+  }
+  out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = acc;
+}
+
 // ---- TMA (cp.async.bulk) gather -------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
   asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(b)), "r"(count));
@@ -241,9 +289,7 @@ int main() {
     RUN_LDG(8, 256, 2);
     RUN_LDG(8, 256, 4);
     RUN_LDG(8, 256, 8);
-    RUN_LDG(16, 256, 2);
-    RUN_LDG(16, 256, 4);
-    RUN_LDG(32, 256, 2);
+
 #define RUN_TMA(S, THREADS, BLOCKS_PER_SM)                                                          \
   {                                                                                                 \
     size_t sm = size_t(THREADS / 32) * S * (32 * 128 + 8);                                          \
@@ -265,8 +311,24 @@ int main() {
     RUN_LDG8(4, 256, 4);
     RUN_LDG8(8, 256, 2);
     RUN_LDG8(8, 256, 3);
-    RUN_LDG8(16, 256, 2);
+
     if (getenv("TMA")) RUN_TMA(2, 256, 2);
+#define RUN_GSTS(S, THREADS, BLOCKS_PER_SM)                                                          \
+  {                                                                                                \
+    size_t sm = size_t(THREADS / 8) * S * 64 * 16;                                                 \
+    CK(cudaFuncSetAttribute(k_ldgsts<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));   \
+    int g = sms * BLOCKS_PER_SM;                                                                   \
+    float ms = time_ms([&] { k_ldgsts<S><<<g, THREADS, sm>>>(F, idx, n, out); });                  \
+    CK(cudaGetLastError());                                                                        \
+    printf("  ldgsts S=%d thr=%d blk/sm=%d smem=%zuKB: %.3f ms  %.2f Grows/s\n", S, THREADS,       \
+           BLOCKS_PER_SM, sm / 1024, ms, n / ms / 1e6);                                            \
+  }
+    RUN_GSTS(2, 256, 2);
+    RUN_GSTS(3, 256, 2);
+    RUN_GSTS(4, 256, 2);
+    RUN_GSTS(4, 256, 1);
+    RUN_GSTS(6, 256, 1);
+    RUN_GSTS(8, 128, 2);
 
     CK(cudaFree(idx));
     CK(cudaFree(F));
