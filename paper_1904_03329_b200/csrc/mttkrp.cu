@@ -76,10 +76,6 @@ struct alignas(16) Work {
   const uint32_t* coo_k;
   const float* coo_val;
   const uint4* coo_quads;     // [M] (row, j, k, value bits)
-  // hot-row variant: fiber stream with HOT|slot encoding, the hot list
-  const uint32_t* hot_list;   // [nhot]: row | (0x80000000 if the row is a B row)
-  const uint2* csf_stream;    // variant 4: records (row | TRAILER | SEND | HOT, value bits)
-  uint32_t nhot;
   // ZERO list
   const uint32_t* zero_rows;
   // split-slice workspace (self-cleaning)
@@ -150,10 +146,6 @@ __device__ __forceinline__ uint4 ld_stream_u4(const uint4* p, uint64_t pol) {
       : "l"(p), "l"(pol));
   return v;
 }
-// this group's bits of a warp ballot
-__device__ __forceinline__ uint32_t group_bits(unsigned gmask, bool pred, int g) {
-  return (__ballot_sync(gmask, pred) >> (8 * g)) & 0xFFu;
-}
 
 // ---------------------------------------------------------- fast path --
 // The four 8-lane groups of a warp run their four tasks in lockstep (the
@@ -207,7 +199,6 @@ __device__ __forceinline__ void flush_split(const Work& w, bool active, uint32_t
 // slice rows are consumed in order from their own streams (no pointer is
 // chased).  The next batch's stream words are loaded before the current
 // batch is reduced.  Returns the partial of a chunk task (zero for runs).
-template <bool PREFETCH>
 __device__ __forceinline__ float4 csf_tasks(const Work& w, const Factors3& fx, const Task& t,
                                             int g, int lig, uint64_t pol_s, uint64_t pol_r,
                                             float4* __restrict__ slots) {
@@ -415,7 +406,7 @@ __device__ __forceinline__ void zero_task(const Work& w, const Factors3& fx, con
 // it.  Chunks of one split slice that land in the same warp are summed with
 // shuffles and handed over with a single vector atomic.
 static constexpr int FAST_BLOCK = 256;
-enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2, KIND_CSF_PF = 3 };
+enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2 };
 
 template <int KIND>
 __global__ void __launch_bounds__(FAST_BLOCK, 3)
@@ -428,7 +419,7 @@ __global__ void __launch_bounds__(FAST_BLOCK, 3)
   float4* slots = s_slots + (threadIdx.x >> 3) * 64 + lig;
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_r = policy_evict_last();
-  constexpr int K = KIND == KIND_CSF_PF ? KIND_CSF : KIND;
+  constexpr int K = KIND;
   const uint32_t first = K == KIND_CSF ? 0u : (K == KIND_CSL ? w.n0 : w.n1);
   const uint32_t last = K == KIND_CSF ? w.n0 : (K == KIND_CSL ? w.n1 : w.n3);
   uint32_t* ctr = w.ws_ctr + 2 * K;
@@ -439,9 +430,8 @@ __global__ void __launch_bounds__(FAST_BLOCK, 3)
     if (base >= last) break;
     const Task t = w.tasks[base + g];
     if (K == KIND_CSF || K == KIND_CSL) {
-      const float4 sa = KIND == KIND_CSF   ? csf_tasks<false>(w, fx, t, g, lig, pol_s, pol_r, slots)
-                        : KIND == KIND_CSF_PF ? csf_tasks<true>(w, fx, t, g, lig, pol_s, pol_r, slots)
-                                              : csl_tasks(w, fx, t, g, lig, pol_s, pol_r, slots);
+      const float4 sa = K == KIND_CSF ? csf_tasks(w, fx, t, g, lig, pol_s, pol_r, slots)
+                                      : csl_tasks(w, fx, t, g, lig, pol_s, pol_r, slots);
       const bool mine = t.slot != NOSLOT && t.lo < t.hi;
       const uint32_t slot0 = __shfl_sync(FULL, t.slot, 0);
       const bool same = __all_sync(FULL, mine && t.slot == slot0);
@@ -469,353 +459,6 @@ __global__ void __launch_bounds__(FAST_BLOCK, 3)
   }
 }
 
-// Rows marked HOT in a stream are served from the CTA's shared-memory copy of
-// the most accessed factor rows (ranked at plan time).
-static constexpr uint32_t HOT = 0x20000000u;
-static constexpr uint32_t ROWMASK = 0x1FFFFFFFu;
-
-// --------------------------------------- CSF tasks, trailer-stream variant --
-// The plan turns the CSF bucket into one self-describing stream of 8-byte
-// records in tree order: each fiber segment's nonzeros (leaf row, value)
-// followed by a TRAILER record (fiber row, SEND if it closes the slice).
-// Every record is one factor-row gather (leaf rows from C, trailer rows from
-// B), so a batch of 8 records needs no side streams and the gathers of batch
-// b+1 are issued before batch b is reduced (register double buffering).
-// Rows marked HOT come from the CTA's shared-memory copy.
-static constexpr uint32_t TRAILER = 0x80000000u;
-
-__device__ __forceinline__ void gather8(float4 (&c)[8], uint32_t x, uint32_t n,
-                                        const float4* __restrict__ Cl, const float4* __restrict__ Bl,
-                                        const float4* __restrict__ hot, uint64_t pol) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t xj = __shfl_sync(FULL, x, j, 8);
-    if (uint32_t(j) < n) {
-      if (xj & HOT)
-        c[j] = hot[(xj & ROWMASK) * 8];
-      else
-        c[j] = ld_row4(((xj & TRAILER) ? Bl : Cl) + size_t(xj & ROWMASK) * 8, pol);
-    }
-  }
-}
-
-struct SliceCursor {
-  uint32_t s;   // next slice (run tasks)
-  uint32_t sr;  // lane lig holds the row of slice s + lig
-};
-
-__device__ __forceinline__ void consume8(const float4 (&c)[8], uint2 p, uint32_t n, bool chunk,
-                                         float4& fa, float4& sa, SliceCursor& cur, uint32_t more,
-                                         const Work& w, float4* __restrict__ out, int g, int lig) {
-  const bool live = uint32_t(lig) < n;
-  const uint32_t tb_all = __ballot_sync(FULL, live && (p.x & TRAILER));
-  const uint32_t sb_all = __ballot_sync(FULL, live && !chunk && (p.x & SEND));
-  const uint32_t tbits = (tb_all >> (8 * g)) & 0xFFu;
-  const uint32_t sbits = (sb_all >> (8 * g)) & 0xFFu;
-  const uint32_t sany = any_group(sb_all);
-  const float v = __uint_as_float(p.y);
-  uint32_t ts = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float vj = __shfl_sync(FULL, v, j, 8);
-    if (uint32_t(j) < n) {
-      if ((tbits >> j) & 1u) {
-        sa = fmav4(fa, c[j], sa);
-        fa = f4zero();
-      } else {
-        fa = fma4(vj, c[j], fa);
-      }
-    }
-    if ((sany >> j) & 1u) {
-      const uint32_t row = __shfl_sync(FULL, cur.sr, ts, 8);
-      if ((sbits >> j) & 1u) {
-        out[size_t(row) * 8 + lig] = sa;
-        sa = f4zero();
-        ++ts;
-      }
-    }
-  }
-  if (sany) {
-    cur.s += __popc(sbits);
-    if (sbits && more) cur.sr = (cur.s + lig < w.csf_S) ? __ldg(w.csf_sidx + cur.s + lig) : 0u;
-  }
-}
-
-__device__ __forceinline__ float4 csf_tasks4(const Work& w, const Factors3& fx, const Task& t,
-                                             int g, int lig, uint64_t pol_s, uint64_t pol_r,
-                                             const float4* __restrict__ hot) {
-  const uint32_t lo = t.lo, hi = t.hi;
-  const bool chunk = t.slot != NOSLOT;
-  const uint32_t my_batches = hi > lo ? (hi - lo + 7) / 8 : 0;
-  const uint32_t nbat = __reduce_max_sync(FULL, my_batches);
-  const float4* Cl = fx.C + lig;
-  const float4* Bl = fx.B + lig;
-  const uint2* S = w.csf_stream;
-  auto load = [&](uint32_t it) -> uint2 {
-    const uint32_t e = lo + 8 * it + lig;
-    return e < hi ? ld_stream_u2(S + e, pol_s) : make_uint2(0u, 0u);
-  };
-  auto count = [&](uint32_t it) -> uint32_t {
-    const uint32_t b = lo + 8 * it;
-    return b < hi ? min(8u, hi - b) : 0u;
-  };
-  float4 fa = f4zero(), sa = f4zero();
-  SliceCursor cur{t.s, (hi > lo && !chunk && t.s + lig < w.csf_S) ? __ldg(w.csf_sidx + t.s + lig) : 0u};
-  uint2 pa = load(0), pb = load(1);
-  float4 cA[8], cB[8];
-  gather8(cA, pa.x, count(0), Cl, Bl, hot, pol_r);
-  for (uint32_t it = 0; it < nbat; it += 2) {
-    gather8(cB, pb.x, count(it + 1), Cl, Bl, hot, pol_r);
-    const uint2 ua = pa;
-    pa = load(it + 2);
-    consume8(cA, ua, count(it), chunk, fa, sa, cur, it + 1 < nbat, w, fx.out, g, lig);
-    if (it + 1 >= nbat) break;
-    gather8(cA, pa.x, count(it + 2), Cl, Bl, hot, pol_r);
-    const uint2 ub = pb;
-    pb = load(it + 3);
-    consume8(cB, ub, count(it + 1), chunk, fa, sa, cur, it + 2 < nbat, w, fx.out, g, lig);
-  }
-  return sa;  // chunks end on a trailer, so fa is already folded in
-}
-
-// Variant-4 kernel: 256 threads (2 CTAs/SM) without hot rows, or 512 threads
-// (1 CTA/SM) with up to ~1700 hot rows in dynamic shared memory.
-template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK, 512 / BLOCK)
-    k_mttkrp3_r32_stream(const __grid_constant__ Work w, const __grid_constant__ Factors3 fx) {
-  extern __shared__ float4 s_hot[];
-  for (uint32_t i = threadIdx.x; i < w.nhot * 8; i += blockDim.x) {
-    const uint32_t e = __ldg(w.hot_list + (i >> 3));
-    const float4* src = (e & 0x80000000u) ? fx.B : fx.C;
-    s_hot[i] = __ldg(src + size_t(e & ROWMASK) * 8 + (i & 7));
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int g = lane >> 3;
-  const int lig = lane & 7;
-  const float4* hot = s_hot + lig;
-  const uint64_t pol_s = policy_evict_first();
-  const uint64_t pol_r = policy_evict_last();
-  uint32_t* ctr = w.ws_ctr + 2 * KIND_CSF;
-  for (;;) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(ctr, 4u);
-    base = __shfl_sync(FULL, base, 0);
-    if (base >= w.n0) break;
-    const Task t = w.tasks[base + g];
-    const float4 sa = csf_tasks4(w, fx, t, g, lig, pol_s, pol_r, hot);
-    const bool mine = t.slot != NOSLOT && t.lo < t.hi;
-    const uint32_t slot0 = __shfl_sync(FULL, t.slot, 0);
-    const bool same = __all_sync(FULL, mine && t.slot == slot0);
-    const uint32_t row = mine ? __ldg(w.csf_sidx + t.s) : 0u;
-    if (same) {
-      float4 r = add4(sa, shfl_xor4(sa, 8));
-      r = add4(r, shfl_xor4(r, 16));
-      flush_split(w, g == 0, t.slot, t.nchunk, 4u, row, r, fx.out, lane, lig);
-    } else if (__any_sync(FULL, mine)) {
-      flush_split(w, mine, t.slot, t.nchunk, 1u, row, sa, fx.out, lane, lig);
-    }
-  }
-  if (lane == 0) {
-    const uint32_t done = atomicAdd(ctr + 1, 1u);
-    if (done == w.total_warps[KIND_CSF] - 1) {
-      ctr[0] = 0;
-      ctr[1] = 0;
-    }
-  }
-}
-
-// ------------------------------------- CSF tasks, 4-lane groups (LDG.256) --
-// Each factor row (32 fp32 = 128 B) is fetched by 4 lanes with one 256-bit
-// load each, so a warp runs 8 tasks side by side and every per-nonzero scalar
-// (index/value shuffles, flag tests, address math) is shared by 4 lanes
-// instead of 8.  Same one-wavefront-per-row L1 cost as the 8-lane layout.
-struct f8 {
-  float4 a, b;
-};
-__device__ __forceinline__ f8 f8zero() { return {f4zero(), f4zero()}; }
-__device__ __forceinline__ f8 ld_row8(const float* p, uint64_t pol) {
-  f8 r;
-  asm("ld.global.nc.L1::evict_last.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
-      : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y), "=f"(r.b.z),
-        "=f"(r.b.w)
-      : "l"(p), "l"(pol));
-  return r;
-}
-__device__ __forceinline__ f8 fma8(float a, const f8& x, const f8& y) {
-  return {fma4(a, x.a, y.a), fma4(a, x.b, y.b)};
-}
-__device__ __forceinline__ f8 fmav8(const f8& a, const f8& x, const f8& y) {
-  return {fmav4(a.a, x.a, y.a), fmav4(a.b, x.b, y.b)};
-}
-__device__ __forceinline__ f8 add8(const f8& a, const f8& b) { return {add4(a.a, b.a), add4(a.b, b.b)}; }
-__device__ __forceinline__ f8 shfl_xor8(const f8& v, int m) { return {shfl_xor4(v.a, m), shfl_xor4(v.b, m)}; }
-// OR of the eight groups' nibbles of a ballot
-__device__ __forceinline__ uint32_t any_group4(uint32_t b) {
-  b |= b >> 16;
-  b |= b >> 8;
-  b |= b >> 4;
-  return b & 0xFu;
-}
-
-// split-slice hand-over for 4-lane groups (each lane owns 8 of the 32 floats)
-__device__ __forceinline__ void flush_split8(const Work& w, bool active, uint32_t slot, uint32_t nchunk,
-                                             uint32_t inc, uint32_t row, const f8& sa, float* out,
-                                             int lane, int lig) {
-  float4* acc = reinterpret_cast<float4*>(w.ws_acc) + size_t(active ? slot : 0) * 8 + 2 * lig;
-  if (active) {
-    red_add4(acc, sa.a);
-    red_add4(acc + 1, sa.b);
-  }
-  __threadfence();
-  __syncwarp();
-  uint32_t old = 0;
-  if (active && lig == 0) old = atomicAdd(w.ws_cnt + slot, inc);
-  old = __shfl_sync(FULL, old, lane & ~3);
-  if (active && old + inc == nchunk) {
-    __threadfence();
-    float4* o = reinterpret_cast<float4*>(out) + size_t(row) * 8 + 2 * lig;
-    o[0] = ld_cg4(acc);
-    o[1] = ld_cg4(acc + 1);
-    st_cg4(acc, f4zero());
-    st_cg4(acc + 1, f4zero());
-    if (lig == 0) w.ws_cnt[slot] = 0;
-  }
-}
-
-__device__ __forceinline__ f8 csf_tasks8(const Work& w, const float* __restrict__ Bm,
-                                         const float* __restrict__ Cm, float* __restrict__ out,
-                                         const Task& t, int g, int lig, uint64_t pol_s,
-                                         uint64_t pol_r, float4* __restrict__ slots) {
-  const uint32_t lo = t.lo, hi = t.hi;
-  const bool chunk = t.slot != NOSLOT;
-  const uint32_t my_batches = hi > lo ? (hi - lo + 3) / 4 : 0;
-  const uint32_t nbat = __reduce_max_sync(FULL, my_batches);
-  const float* Cl = Cm + 8 * lig;
-  const float* Bl = Bm + 8 * lig;
-  uint32_t s = t.s, f = t.f;
-  f8 fa = f8zero(), sa = f8zero();
-  uint2 pr = make_uint2(0u, 0u);
-  if (lo + lig < hi) pr = ld_stream_u2(w.csf_pairs + lo + lig, pol_s);
-  uint32_t fi = (hi > lo && f + lig < w.csf_F) ? __ldg(w.csf_fidx + f + lig) : 0u;
-  uint32_t sr = (hi > lo && !chunk && s + lig < w.csf_S) ? __ldg(w.csf_sidx + s + lig) : 0u;
-  bool pending = false;
-  uint32_t base = lo;
-  for (uint32_t it = 0; it < nbat; ++it, base += 4) {
-    const uint32_t n = base < hi ? min(4u, hi - base) : 0u;
-    const bool live = uint32_t(lig) < n;
-    const uint32_t k = pr.x & KMASK;
-    const float v = __uint_as_float(pr.y);
-    const uint32_t eb_all = __ballot_sync(FULL, live && (pr.x & FEND));
-    const uint32_t sb_all = __ballot_sync(FULL, live && !chunk && (pr.x & SEND));
-    const uint32_t ebits = (eb_all >> (4 * g)) & 0xFu;
-    const uint32_t sbits = (sb_all >> (4 * g)) & 0xFu;
-    const uint32_t eany = any_group4(eb_all);
-    const uint32_t sany = any_group4(sb_all);
-    f8 c[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t kj = __shfl_sync(FULL, k, j, 4);
-      if (uint32_t(j) < n) c[j] = ld_row8(Cl + size_t(kj) * 32, pol_r);
-    }
-    uint32_t tf = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if ((eany >> j) & 1u) {
-        const uint32_t fj = __shfl_sync(FULL, fi, tf, 4);
-        if ((ebits >> j) & 1u) {
-          const float4* src = reinterpret_cast<const float4*>(Bl + size_t(fj) * 32);
-          cp_async16(slots + j * 8, src);
-          cp_async16(slots + j * 8 + 1, src + 1);
-        }
-        tf += (ebits >> j) & 1u;
-      }
-    }
-    const uint32_t sr_cur = sr;
-    const float vv = v;
-    f += tf;
-    const uint32_t nsl = __popc(sbits);
-    s += nsl;
-    const uint32_t nb = base + 4;
-    if (nb < hi) {
-      pr = (nb + lig < hi) ? ld_stream_u2(w.csf_pairs + nb + lig, pol_s) : make_uint2(0u, 0u);
-      if (tf) fi = (f + lig < w.csf_F) ? __ldg(w.csf_fidx + f + lig) : 0u;
-      if (nsl) sr = (s + lig < w.csf_S) ? __ldg(w.csf_sidx + s + lig) : 0u;
-    }
-    cp_async_wait_all();
-    uint32_t ts = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float vj = __shfl_sync(FULL, vv, j, 4);
-      if (uint32_t(j) < n) fa = fma8(vj, c[j], fa);
-      if ((ebits >> j) & 1u) {
-        const f8 b{slots[j * 8], slots[j * 8 + 1]};
-        sa = fmav8(fa, b, sa);
-        fa = f8zero();
-      }
-      if ((sany >> j) & 1u) {
-        const uint32_t row = __shfl_sync(FULL, sr_cur, ts, 4);
-        if ((sbits >> j) & 1u) {
-          float4* o = reinterpret_cast<float4*>(out + size_t(row) * 32 + 8 * lig);
-          o[0] = sa.a;
-          o[1] = sa.b;
-          sa = f8zero();
-          ++ts;
-        }
-      }
-    }
-    if (n) pending = !((ebits >> (n - 1)) & 1u);
-  }
-  if (chunk && pending) {  // the chunk ended inside fiber f
-    const uint32_t fj = __ldg(w.csf_fidx + f);
-    sa = fmav8(fa, ld_row8(Bl + size_t(fj) * 32, pol_r), sa);
-  }
-  return sa;
-}
-
-__global__ void __launch_bounds__(FAST_BLOCK, 3)
-    k_csf_r32x8(const __grid_constant__ Work w, const __grid_constant__ Factors3 fx) {
-  // per lane: 4 slots of 32 B (one per batch position) for staged B rows
-  __shared__ float4 s_slots[FAST_BLOCK * 8];
-  const int lane = threadIdx.x & 31;
-  const int g = lane >> 2;
-  const int lig = lane & 3;
-  // slot j of this lane: s_slots[(group_base + j) * 8 + 2*lig .. +1], group = 4 lanes x 4 slots
-  float4* slots = s_slots + (threadIdx.x >> 2) * 32 + 2 * lig;
-  const uint64_t pol_s = policy_evict_first();
-  const uint64_t pol_r = policy_evict_last();
-  const float* Bm = reinterpret_cast<const float*>(fx.B);
-  const float* Cm = reinterpret_cast<const float*>(fx.C);
-  float* out = reinterpret_cast<float*>(fx.out);
-  uint32_t* ctr = w.ws_ctr + 2 * KIND_CSF;
-  for (;;) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(ctr, 8u);
-    base = __shfl_sync(FULL, base, 0);
-    if (base >= w.n0) break;
-    const Task t = w.tasks[base + g];
-    const f8 sa = csf_tasks8(w, Bm, Cm, out, t, g, lig, pol_s, pol_r, slots);
-    const bool mine = t.slot != NOSLOT && t.lo < t.hi;
-    const uint32_t slot0 = __shfl_sync(FULL, t.slot, 0);
-    const bool same = __all_sync(FULL, mine && t.slot == slot0);
-    const uint32_t row = mine ? __ldg(w.csf_sidx + t.s) : 0u;
-    if (same) {
-      f8 r = add8(sa, shfl_xor8(sa, 4));
-      r = add8(r, shfl_xor8(r, 8));
-      r = add8(r, shfl_xor8(r, 16));
-      flush_split8(w, g == 0, t.slot, t.nchunk, 8u, row, r, out, lane, lig);
-    } else if (__any_sync(FULL, mine)) {
-      flush_split8(w, mine, t.slot, t.nchunk, 1u, row, sa, out, lane, lig);
-    }
-  }
-  if (lane == 0) {
-    const uint32_t done = atomicAdd(ctr + 1, 1u);
-    if (done == w.total_warps[KIND_CSF] - 1) {
-      ctr[0] = 0;
-      ctr[1] = 0;
-    }
-  }
-}
 
 // --------------------------------------------------------- generic kernel --
 // Any order, any rank: one warp per task, lanes over rank columns, nonzeros
@@ -1147,109 +790,6 @@ __global__ void k_quads(const uint32_t* __restrict__ i0, const uint32_t* __restr
     out[i] = make_uint4(i0[i], j0[i], k0[i], __float_as_uint(v[i]));
 }
 
-__global__ void k_hist_u32(const uint32_t* __restrict__ a, int64_t n, uint32_t* __restrict__ h) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x)
-    atomicAdd(h + a[i], 1u);
-}
-__global__ void k_hot_candidates(int64_t DC, int64_t DB, uint32_t* __restrict__ vals) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < DC + DB;
-       i += int64_t(gridDim.x) * blockDim.x)
-    vals[i] = i < DC ? uint32_t(i) : (0x80000000u | uint32_t(i - DC));
-}
-__global__ void k_hot_slots(const uint32_t* __restrict__ list, uint32_t H, uint32_t* __restrict__ slotC,
-                            uint32_t* __restrict__ slotB) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < H;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const uint32_t e = list[i];
-    if (e & 0x80000000u)
-      slotB[e & ROWMASK] = uint32_t(i);
-    else
-      slotC[e & ROWMASK] = uint32_t(i);
-  }
-}
-
-// Variant-4 stream: segment s (nonzeros [lptr[s], lptr[s+1])) is written at
-// stream positions lptr[s]+s .. lptr[s+1]+s, its trailer last.
-__global__ void k_build_stream(const uint32_t* __restrict__ lptr, const uint32_t* __restrict__ fidx,
-                               const uint8_t* __restrict__ last, int64_t F,
-                               const uint32_t* __restrict__ leaf, const float* __restrict__ v,
-                               const uint32_t* __restrict__ slotC, const uint32_t* __restrict__ slotB,
-                               uint2* __restrict__ out) {
-  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < F;
-       s += int64_t(gridDim.x) * blockDim.x) {
-    const uint32_t a = lptr[s], b = lptr[s + 1];
-    for (uint32_t i = a; i < b; ++i) {
-      const uint32_t k = leaf[i];
-      const uint32_t sl = slotC ? slotC[k] : 0xFFFFFFFFu;
-      out[i + s] = make_uint2(sl != 0xFFFFFFFFu ? (HOT | sl) : k, __float_as_uint(v[i]));
-    }
-    const uint32_t j = fidx[s];
-    const uint32_t sl = slotB ? slotB[j] : 0xFFFFFFFFu;
-    uint32_t x = TRAILER | (sl != 0xFFFFFFFFu ? (HOT | sl) : j);
-    if (last[s]) x |= SEND;
-    out[b + s] = make_uint2(x, 0u);
-  }
-}
-__global__ void k_mark_last_segment(const uint32_t* __restrict__ fpos, int64_t S, uint8_t* __restrict__ last) {
-  for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < S;
-       x += int64_t(gridDim.x) * blockDim.x)
-    if (fpos[x + 1] > fpos[x]) last[fpos[x + 1] - 1] = 1;
-}
-__global__ void k_stream_slice_starts(const uint32_t* __restrict__ loff, const uint32_t* __restrict__ fpos,
-                                      int64_t S, uint32_t* __restrict__ sst) {
-  for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x <= S;
-       x += int64_t(gridDim.x) * blockDim.x)
-    sst[x] = loff[x] + fpos[x];
-}
-// Tasks over the stream: runs of whole light slices, or chunks of a heavy
-// slice cut right after a trailer (so a chunk never ends inside a fiber).
-__global__ void k_task_fill_stream(const uint32_t* __restrict__ sst, const uint32_t* __restrict__ fpos,
-                                   const uint32_t* __restrict__ lptr, int64_t S, uint32_t T,
-                                   const uint32_t* __restrict__ toff, const uint32_t* __restrict__ slot,
-                                   Task* __restrict__ tasks) {
-  for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < S;
-       x += int64_t(gridDim.x) * blockDim.x) {
-    const uint32_t a = sst[x], len = sst[x + 1] - a;
-    const uint32_t nt = toff[x + 1] - toff[x];
-    if (nt == 0) continue;
-    if (len > T) {
-      uint32_t prev = a;
-      for (uint32_t c = 0; c < nt; ++c) {
-        uint32_t end;
-        if (c + 1 == nt) {
-          end = sst[x + 1];
-        } else {
-          const uint32_t target = a + uint32_t((uint64_t(len) * (c + 1)) / nt);
-          // first segment of the slice whose trailer sits at or after target-1
-          uint32_t l0 = fpos[x], h0 = fpos[x + 1] - 1;
-          while (l0 < h0) {
-            const uint32_t m = l0 + (h0 - l0) / 2;
-            if (lptr[m + 1] + m + 1 >= target) h0 = m; else l0 = m + 1;
-          }
-          end = lptr[l0 + 1] + l0 + 1;
-          if (end < prev) end = prev;
-        }
-        Task t{};
-        t.lo = prev;
-        t.hi = end;
-        t.s = uint32_t(x);
-        t.slot = slot[x];
-        t.nchunk = nt;
-        tasks[toff[x] + c] = t;
-        prev = end;
-      }
-    } else {
-      Task t{};
-      t.lo = a;
-      t.s = uint32_t(x);
-      t.slot = NOSLOT;
-      t.nchunk = 1;
-      tasks[toff[x]] = t;
-    }
-  }
-}
-
 }  // namespace hbk
 
 struct hbk_plan {
@@ -1261,20 +801,13 @@ struct hbk_plan {
   hbk_csf* csf = nullptr;
   hbk_sched* sched = nullptr;
   hbk::Buf tasks, zero_rows, csf_send, ws;
-  hbk::Buf csf_pairs, csl_pairs, coo_quads, hot_list, csf_stream;
-  hbk_csf* stream_tree = nullptr;  // variant 4: the tree the stream was built from (virtually split)
-  size_t hot_smem = 0;
+  hbk::Buf csf_pairs, csl_pairs, coo_quads;
   hbk::Work work{};
   bool fast = false;
   int grid = 0, block = 256;
   int grids[3] = {0, 0, 0};
-  int csf_block = 256;
-  int csf_var = 0;  // CSF kernel variant (HBK_CSF_VARIANT): 0 = (leaf|flags,value) pair stream +
-                    // fiber-index stream; 4 = record stream with fiber trailers, double-buffered
-                    // gathers and shared-memory hot rows
   hbk_plan_info info{};
   ~hbk_plan() {
-    hbk_csf_release(stream_tree);
     hbk_coo_release(coo);
     hbk_csl_release(csl);
     hbk_csf_release(csf);
@@ -1320,114 +853,6 @@ __global__ void k_shift_slots(Task* __restrict__ t, int64_t n, uint32_t base) {
     if (t[i].slot != NOSLOT) t[i].slot += base;
 }
 
-// Variant 4: virtually split fibers at tau_p, rank hot rows, emit the
-// record stream and cut it into tasks (runs of light slices / trailer-aligned
-// chunks of heavy slices).
-static BucketTasks build_csf_stream(hbk_plan* p, hbk_csf* c, uint32_t T, cudaStream_t st) {
-  int64_t tau_p = 32;
-  if (const char* e = getenv("HBK_STREAM_TAU")) tau_p = std::max<int64_t>(1, atoll(e));
-  hbk_csf* cs = nullptr;
-  HBK_REQUIRE(hbk_split_fibers(c, tau_p, st, &cs) == HBK_OK, HBK_ECUDA, hbk_last_error());
-  if (!cs) {
-    cs = c;
-    hbk_csf_retain(c);
-  }
-  p->stream_tree = cs;
-  const int L = p->order - 2;
-  const int64_t S = cs->n[0], F = cs->n[L], M = cs->M;
-  Chain2 ch{};
-  ch.nlev = p->order - 1;
-  for (int d = 0; d < p->order - 1; ++d) ch.ptr[d] = cs->ptr[d].as<uint32_t>();
-  Scratch fpos((S + 1) * sizeof(uint32_t), st), loff((S + 1) * sizeof(uint32_t), st);
-  k_csf_slice_offsets<<<grid_for(S + 1, 256), 256, 0, st>>>(ch, S, fpos.as<uint32_t>(), loff.as<uint32_t>());
-  check_launch("k_csf_slice_offsets");
-  // hot rows: leaf rows by nonzero count, fiber rows by segment count
-  const int64_t DC = p->dims[p->mo[2]], DB = p->dims[p->mo[1]];
-  int dev = 0, optin = 0;
-  HBK_CUDA(cudaGetDevice(&dev));
-  HBK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  int64_t hmax = (int64_t(optin) - 2048) / 128;
-  if (const char* e = getenv("HBK_HOT_ROWS")) hmax = std::max<int64_t>(0, atoll(e));
-  hmax = std::min<int64_t>(hmax, DC + DB);
-  Scratch slotC(std::max<int64_t>(DC, 1) * sizeof(uint32_t), st), slotB(std::max<int64_t>(DB, 1) * sizeof(uint32_t), st);
-  int64_t H = 0;
-  if (hmax > 0) {
-    Scratch cnt((DC + DB) * sizeof(uint32_t), st), cnt2((DC + DB) * sizeof(uint32_t), st);
-    Scratch vals((DC + DB) * sizeof(uint32_t), st), vals2((DC + DB) * sizeof(uint32_t), st);
-    HBK_CUDA(cudaMemsetAsync(cnt.p, 0, (DC + DB) * sizeof(uint32_t), st));
-    k_hist_u32<<<grid_for(M, 256), 256, 0, st>>>(cs->leaf.as<uint32_t>(), M, cnt.as<uint32_t>());
-    check_launch("k_hist_u32");
-    k_hist_u32<<<grid_for(F, 256), 256, 0, st>>>(cs->idx[L].as<uint32_t>(), F, cnt.as<uint32_t>() + DC);
-    check_launch("k_hist_u32");
-    k_hot_candidates<<<grid_for(DC + DB, 256), 256, 0, st>>>(DC, DB, vals.as<uint32_t>());
-    check_launch("k_hot_candidates");
-    cub::DoubleBuffer<uint32_t> kb(cnt.as<uint32_t>(), cnt2.as<uint32_t>());
-    cub::DoubleBuffer<uint32_t> vb(vals.as<uint32_t>(), vals2.as<uint32_t>());
-    size_t tmp = 0;
-    HBK_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, kb, vb, int(DC + DB), 0, 32, st));
-    Scratch t(tmp, st);
-    HBK_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.p, tmp, kb, vb, int(DC + DB), 0, 32, st));
-    std::vector<uint32_t> top(hmax);
-    HBK_CUDA(cudaMemcpyAsync(top.data(), kb.Current(), hmax * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    HBK_CUDA(cudaStreamSynchronize(st));
-    while (H < hmax && top[H] >= 2) ++H;
-    if (H) {
-      p->hot_list = dalloc(H * sizeof(uint32_t), st);
-      HBK_CUDA(cudaMemcpyAsync(p->hot_list.p, vb.Current(), H * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
-      HBK_CUDA(cudaMemsetAsync(slotC.p, 0xFF, DC * sizeof(uint32_t), st));
-      HBK_CUDA(cudaMemsetAsync(slotB.p, 0xFF, DB * sizeof(uint32_t), st));
-      k_hot_slots<<<grid_for(H, 256), 256, 0, st>>>(p->hot_list.as<uint32_t>(), uint32_t(H),
-                                                    slotC.as<uint32_t>(), slotB.as<uint32_t>());
-      check_launch("k_hot_slots");
-    }
-  }
-  p->work.hot_list = H ? p->hot_list.as<uint32_t>() : nullptr;
-  p->work.nhot = uint32_t(H);
-  p->hot_smem = size_t(H) * 128;
-  // the record stream
-  Scratch last(std::max<int64_t>(F, 1), st);
-  HBK_CUDA(cudaMemsetAsync(last.p, 0, std::max<int64_t>(F, 1), st));
-  k_mark_last_segment<<<grid_for(S, 256), 256, 0, st>>>(fpos.as<uint32_t>(), S, last.as<uint8_t>());
-  check_launch("k_mark_last_segment");
-  p->csf_stream = dalloc((M + F) * sizeof(uint2), st);
-  k_build_stream<<<grid_for(F, 128), 128, 0, st>>>(
-      cs->ptr[L].as<uint32_t>(), cs->idx[L].as<uint32_t>(), last.as<uint8_t>(), F, cs->leaf.as<uint32_t>(),
-      cs->v32.as<float>(), H ? slotC.as<uint32_t>() : nullptr, H ? slotB.as<uint32_t>() : nullptr,
-      p->csf_stream.as<uint2>());
-  check_launch("k_build_stream");
-  p->work.csf_stream = p->csf_stream.as<uint2>();
-  // tasks
-  Scratch sst((S + 1) * sizeof(uint32_t), st);
-  k_stream_slice_starts<<<grid_for(S + 1, 256), 256, 0, st>>>(loff.as<uint32_t>(), fpos.as<uint32_t>(), S,
-                                                              sst.as<uint32_t>());
-  check_launch("k_stream_slice_starts");
-  BucketTasks bt;
-  Scratch cnt((S + 1) * sizeof(uint32_t), st), slot((S + 1) * sizeof(uint32_t), st);
-  k_task_count<<<grid_for(S, 256), 256, 0, st>>>(sst.as<uint32_t>(), S, T, cnt.as<uint32_t>(),
-                                                 slot.as<uint32_t>());
-  check_launch("k_task_count");
-  const uint32_t n = exclusive_scan_total(cnt.as<uint32_t>(), S, st);
-  const uint32_t nslot = exclusive_scan_total(slot.as<uint32_t>(), S, st);
-  bt.tasks = Scratch(size_t(std::max<uint32_t>(n, 1)) * sizeof(Task), st);
-  k_task_fill_stream<<<grid_for(S, 128), 128, 0, st>>>(sst.as<uint32_t>(), fpos.as<uint32_t>(),
-                                                       cs->ptr[L].as<uint32_t>(), S, T, cnt.as<uint32_t>(),
-                                                       slot.as<uint32_t>(), bt.tasks.as<Task>());
-  check_launch("k_task_fill_stream");
-  k_task_hi<<<grid_for(n, 256), 256, 0, st>>>(bt.tasks.as<Task>(), n, uint32_t(M + F));
-  check_launch("k_task_hi");
-  bt.n = n;
-  bt.slots = nslot;
-  HBK_CUDA(cudaStreamSynchronize(st));
-  return bt;
-}
-
-static int max_dyn_smem() {
-  int dev = 0, optin = 0;
-  HBK_CUDA(cudaGetDevice(&dev));
-  HBK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  return optin - 1024;
-}
-
 static void build_plan(hbk_plan* p, cudaStream_t st) {
   const int N = p->order;
   const int R = p->rank;
@@ -1435,8 +860,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   // two flag bits in the leaf coordinate, so leaf extents must stay < 2^30
   p->fast = (N == 3 && R == 32 && p->dims[p->mo[2]] < (int64_t(1) << 29) &&
              p->dims[p->mo[1]] < (int64_t(1) << 29));
-  const int gpw = p->fast ? 8 : 1;  // task ranges padded so a warp never straddles kinds
-  if (const char* e = getenv("HBK_CSF_VARIANT")) p->csf_var = std::max(0, std::min(6, atoi(e)));
+  const int gpw = p->fast ? 4 : 1;  // task ranges padded so a warp never straddles kinds
   uint32_t task_nnz = TASK_NNZ_CSF;
   if (const char* e = getenv("HBK_TASK_NNZ")) task_nnz = std::max(8, atoi(e));
   const uint32_t Tcsf = p->fast ? task_nnz : GEN_TASK_NNZ;
@@ -1463,21 +887,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     k_csf_slice_offsets<<<grid_for(S + 1, 256), 256, 0, st>>>(ch, S, fpos.as<uint32_t>(),
                                                               p->csf_send.as<uint32_t>());
     check_launch("k_csf_slice_offsets");
-    // schedule-driven plans execute the schedule's units on the pair-stream kernel
-    if (p->sched && p->csf_var == 4) p->csf_var = 0;
-    if (!p->fast) p->csf_var = 0;
-    const bool stream4 = p->csf_var == 4;
-    if (stream4) {
-      tcsf = build_csf_stream(p, c, Tcsf, st);
-      int64_t m = c->M, a = c->M;
-      for (int d = N - 2; d >= 1; --d) {
-        m += c->n[d];
-        if (d < N - 2) a += c->n[d];
-      }
-      a += c->n[0];
-      muls += m * R;
-      adds += a * R;
-    } else if (p->sched) {
+    if (p->sched) {
       hbk_sched* sc = p->sched;
       HBK_REQUIRE(sc->S == S && sc->F == c->n[L], HBK_EINVAL,
                   "schedule was built for a different tree");
@@ -1552,7 +962,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     w.csf_val = c->v32.as<float>();
     w.csf_F = uint32_t(c->n[L]);
     w.csf_S = uint32_t(S);
-    if (p->fast && !stream4) {
+    if (p->fast) {
       p->csf_pairs = dalloc(c->M * sizeof(uint2), st);
       uint2* pp = p->csf_pairs.as<uint2>();
       k_pairs<<<grid_for(c->M, 256), 256, 0, st>>>(c->leaf.as<uint32_t>(), c->v32.as<float>(),
@@ -1565,10 +975,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       check_launch("k_flag_ends");
       w.csf_pairs = pp;
     }
-    if (stream4)
-      stream_bytes += 8 * (c->M + p->stream_tree->n[L]) + 4 * S;
-    else
-      stream_bytes += p->fast ? 8 * c->M + 4 * c->n[L] + 4 * S : 8 * c->M + 8 * c->n[L] + 8 * S;
+    stream_bytes += p->fast ? 8 * c->M + 4 * c->n[L] + 4 * S : 8 * c->M + 8 * c->n[L] + 8 * S;
   }
   if (p->csl && p->csl->M > 0) {
     hbk_csl* s = p->csl;
@@ -1713,34 +1120,16 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     p->block = FAST_BLOCK;
     const int64_t ntk[3] = {int64_t(w.n0), int64_t(w.n1) - w.n0, int64_t(w.n3) - w.n1};
     for (int k = 0; k < 3; ++k) {
-      if (k == 0 && p->csf_var == 4) {
-        const bool hotb = p->work.nhot > 0;
-        const int blk = hotb ? 512 : 256;
-        const void* fn = hotb ? (const void*)k_mttkrp3_r32_stream<512> : (const void*)k_mttkrp3_r32_stream<256>;
-        // the attribute is process-global: raise it to the device maximum once
-        // so plans with different hot-row counts never lower it under each other
-        HBK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn_smem()));
-        HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, blk, p->hot_smem));
-        per_sm = std::max(per_sm, 1);
-        const int64_t warps_needed = (ntk[0] + gpw - 1) / gpw;
-        const int64_t blocks_needed = std::max<int64_t>(1, (warps_needed + blk / 32 - 1) / (blk / 32));
-        p->grids[0] = ntk[0] > 0 ? int(std::min<int64_t>(int64_t(sms) * per_sm, blocks_needed)) : 0;
-        p->csf_block = blk;
-        w.total_warps[0] = uint32_t(p->grids[0]) * (blk / 32);
-        launches += ntk[0] > 0;
-        continue;
-      }
       if (k == 0)
-        HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, p->csf_var == 5 ? (const void*)k_csf_r32x8 : (const void*)k_mttkrp3_r32<KIND_CSF>,
-            p->block, 0));
+        HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp3_r32<KIND_CSF>,
+                                                               p->block, 0));
       if (k == 1)
         HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp3_r32<KIND_CSL>,
                                                                p->block, 0));
       if (k == 2)
         HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp3_r32<KIND_COO>,
                                                                p->block, 0));
-      p->grids[k] = ntk[k] > 0 ? grid_for_tasks(ntk[k], per_sm, (k == 0 && p->csf_var == 5) ? 8 : 4) : 0;
+      p->grids[k] = ntk[k] > 0 ? grid_for_tasks(ntk[k], per_sm, 4) : 0;
       w.total_warps[k] = uint32_t(p->grids[k]) * (p->block / 32);
       launches += ntk[k] > 0;
     }
@@ -1858,18 +1247,7 @@ int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out,
                           16 ==
                       0,
                   HBK_EINVAL, "factor and output buffers must be 16-byte aligned");
-      if (p->grids[0]) {
-        if (p->csf_var == 4 && p->csf_block == 512)
-          k_mttkrp3_r32_stream<512><<<p->grids[0], 512, p->hot_smem, st>>>(p->work, fx);
-        else if (p->csf_var == 4)
-          k_mttkrp3_r32_stream<256><<<p->grids[0], 256, p->hot_smem, st>>>(p->work, fx);
-        else if (p->csf_var == 5)
-          k_csf_r32x8<<<p->grids[0], p->block, 0, st>>>(p->work, fx);
-        else if (p->csf_var == 6)
-          k_mttkrp3_r32<KIND_CSF_PF><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
-        else
-          k_mttkrp3_r32<KIND_CSF><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
-      }
+      if (p->grids[0]) k_mttkrp3_r32<KIND_CSF><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
       if (p->grids[1]) k_mttkrp3_r32<KIND_CSL><<<p->grids[1], p->block, 0, st>>>(p->work, fx);
       if (p->grids[2]) k_mttkrp3_r32<KIND_COO><<<p->grids[2], p->block, 0, st>>>(p->work, fx);
       check_launch("k_mttkrp3_r32");
