@@ -210,6 +210,11 @@ int hbk_plan_info_get(const hbk_plan* p, hbk_plan_info* info);
  * dims[d] x rank fp32 (factors[mode] is not read, kernels.py:62-66).
  * out: [dev] dims[mode] x rank fp32.                                       */
 int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out, void* stream);
+/* fp64 mode: factors/out fp64, the buckets' original fp64 values, fp64
+ * accumulation (generic kernel).  For accuracy-sensitive callers, e.g. the
+ * CP-ALS fit, whose algebraic form amplifies fp32 rounding near convergence. */
+int hbk_plan_execute_f64(const hbk_plan* p, const double* const* factors, double* out,
+                         void* stream);
 void hbk_plan_release(hbk_plan* p);
 
 /* ------------------------------------------------------------ sharding --

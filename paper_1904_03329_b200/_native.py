@@ -123,6 +123,7 @@ _SIGS = {
     "hbk_plan_create": ([vp, vp, vp, vp, C.c_int, C.c_int, vp, C.POINTER(vp)], C.c_int),
     "hbk_plan_info_get": ([vp, C.POINTER(PlanInfo)], C.c_int),
     "hbk_plan_execute": ([vp, vp, vp, vp], C.c_int),
+    "hbk_plan_execute_f64": ([vp, vp, vp, vp], C.c_int),
     "hbk_plan_release": ([vp], None),
     "hbk_coo_slice_histogram": ([vp, C.c_int, vp, vp], C.c_int),
     "hbk_coo_select_rows": ([vp, C.c_int, i64, i64, vp, C.POINTER(vp)], C.c_int),

@@ -464,12 +464,18 @@ __global__ void __launch_bounds__(FAST_BLOCK, 3)
 // Any order, any rank: one warp per task, lanes over rank columns, nonzeros
 // walked one at a time.  Used for order > 3 or R != 32 (parity coverage; the
 // benchmark configurations are all order 3, R = 32).
+template <class T>
 struct WorkN {
   int order;
   int rank;
   // factors indexed by permuted level (level 0 unused)
-  const float* F[HBK_MAX_ORDER];
-  const float* Fcoo[HBK_MAX_ORDER];  // by original mode
+  const T* F[HBK_MAX_ORDER];
+  const T* Fcoo[HBK_MAX_ORDER];  // by original mode
+  // nonzero values of each bucket in T (fp32 copies or the fp64 originals)
+  const T* csf_val;
+  const T* csl_val;
+  const T* coo_val;
+  T* acc;  // split-slice accumulators [slots x rank]
   int mode;
   // CSF
   const uint32_t* csf_anc[HBK_MAX_ORDER];  // level d < order-2 coordinate per fiber (d >= 1)
@@ -477,15 +483,16 @@ struct WorkN {
   const uint32_t* csl_rest[HBK_MAX_ORDER];
   // COO columns
   const uint32_t* coo_col[HBK_MAX_ORDER];
-  float* out;
+  T* out;
 };
 
-__device__ __forceinline__ void gen_flush_split(const Work& w, const WorkN& wn, uint32_t slot,
-                                                uint32_t nchunk, uint32_t row, int r0, float sa,
+template <class T>
+__device__ __forceinline__ void gen_flush_split(const Work& w, const WorkN<T>& wn, uint32_t slot,
+                                                uint32_t nchunk, uint32_t row, int r0, T sa,
                                                 int lane) {
   const int R = wn.rank;
   const bool act = r0 + lane < R;
-  float* acc = w.ws_acc + size_t(slot) * R + r0 + lane;
+  T* acc = wn.acc + size_t(slot) * R + r0 + lane;
   if (act) atomicAdd(acc, sa);
   __threadfence();
   __syncwarp();
@@ -495,17 +502,18 @@ __device__ __forceinline__ void gen_flush_split(const Work& w, const WorkN& wn, 
   if (old == nchunk - 1) {
     __threadfence();
     if (act) {
-      float r = __ldcg(acc);
+      const T r = __ldcg(acc);
       wn.out[size_t(row) * R + r0 + lane] = r;
-      __stcg(acc, 0.f);
+      __stcg(acc, T(0));
     }
     __syncwarp();
     if (lane == 0) w.ws_cnt[slot] = 0;
   }
 }
 
+template <class T>
 __global__ void __launch_bounds__(256) k_mttkrp_generic(const __grid_constant__ Work w,
-                                                        const __grid_constant__ WorkN wn) {
+                                                        const __grid_constant__ WorkN<T> wn) {
   const int lane = threadIdx.x & 31;
   const int R = wn.rank;
   const int N = wn.order;
@@ -525,24 +533,24 @@ __global__ void __launch_bounds__(256) k_mttkrp_generic(const __grid_constant__ 
         uint32_t s = t.s, f = t.f;
         uint32_t fend = w.csf_lptr[f + 1];
         uint32_t send = w.csf_send[s + 1];
-        float fa = 0.f, sa = 0.f;
+        T fa = 0, sa = 0;
         for (uint32_t i = t.lo; i < t.hi; ++i) {
           uint32_t k = w.csf_leaf[i];
-          float v = w.csf_val[i];
-          if (act) fa = fmaf(v, wn.F[N - 1][size_t(k) * R + r], fa);
+          const T v = wn.csf_val[i];
+          if (act) fa = v * wn.F[N - 1][size_t(k) * R + r] + fa;
           if (i + 1 == fend) {
-            float m = 1.f;
+            T m = 1;
             if (act) {
               m = wn.F[N - 2][size_t(w.csf_fidx[f]) * R + r];
               for (int d = 1; d < N - 2; ++d) m *= wn.F[d][size_t(wn.csf_anc[d][f]) * R + r];
             }
-            sa = fmaf(fa, m, sa);
-            fa = 0.f;
+            sa = fa * m + sa;
+            fa = 0;
             ++f;
             if (f < w.csf_F) fend = w.csf_lptr[f + 1];
             if (!chunk && i + 1 == send) {
               if (act) wn.out[size_t(w.csf_sidx[s]) * R + r] = sa;
-              sa = 0.f;
+              sa = 0;
               ++s;
               if (s < w.csf_S) send = w.csf_send[s + 1];
             }
@@ -550,28 +558,28 @@ __global__ void __launch_bounds__(256) k_mttkrp_generic(const __grid_constant__ 
         }
         if (chunk) {
           if (t.hi != w.csf_lptr[f]) {  // ended inside fiber f
-            float m = 1.f;
+            T m = 1;
             if (act) {
               m = wn.F[N - 2][size_t(w.csf_fidx[f]) * R + r];
               for (int d = 1; d < N - 2; ++d) m *= wn.F[d][size_t(wn.csf_anc[d][f]) * R + r];
             }
-            sa = fmaf(fa, m, sa);
+            sa = fa * m + sa;
           }
           gen_flush_split(w, wn, t.slot, t.nchunk, w.csf_sidx[t.s], rc * 32, sa, lane);
         }
       } else if (ti < w.n1) {  // CSL
         uint32_t s = t.s;
         uint32_t send = w.csl_send[s + 1];
-        float sa = 0.f;
+        T sa = 0;
         for (uint32_t i = t.lo; i < t.hi; ++i) {
           if (act) {
-            float p = w.csl_val[i];
+            T p = wn.csl_val[i];
             for (int c = 0; c < N - 1; ++c) p *= wn.F[c + 1][size_t(wn.csl_rest[c][i]) * R + r];
             sa += p;
           }
           if (!chunk && i + 1 == send) {
             if (act) wn.out[size_t(w.csl_sidx[s]) * R + r] = sa;
-            sa = 0.f;
+            sa = 0;
             ++s;
             if (s < w.csl_S) send = w.csl_send[s + 1];
           }
@@ -580,14 +588,14 @@ __global__ void __launch_bounds__(256) k_mttkrp_generic(const __grid_constant__ 
       } else if (ti < w.n2) {  // COO (unique rows)
         for (uint32_t i = t.lo; i < t.hi; ++i) {
           if (!act) continue;
-          float p = w.coo_val[i];
+          T p = wn.coo_val[i];
           for (int d = 0; d < N; ++d)
             if (d != wn.mode) p *= wn.Fcoo[d][size_t(wn.coo_col[d][i]) * R + r];
           wn.out[size_t(wn.coo_col[wn.mode][i]) * R + r] = p;
         }
       } else {  // ZERO
         for (uint32_t i = t.lo; i < t.hi; ++i)
-          if (act) wn.out[size_t(w.zero_rows[i]) * R + r] = 0.f;
+          if (act) wn.out[size_t(w.zero_rows[i]) * R + r] = T(0);
       }
     }
   }
@@ -805,6 +813,7 @@ struct hbk_plan {
   hbk::Work work{};
   bool fast = false;
   int grid = 0, block = 256;
+  int gen_grid = 0;
   int grids[3] = {0, 0, 0};
   hbk_plan_info info{};
   ~hbk_plan() {
@@ -1097,7 +1106,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   // workspace: [ctr(2) pad to 32 words][cnt slots][acc slots x R]
   const size_t cnt_off = 32 * sizeof(uint32_t);
   const size_t acc_off = pad_to(cnt_off + slots * sizeof(uint32_t), 256);
-  const size_t ws_bytes = acc_off + size_t(slots) * R * sizeof(float);
+  const size_t ws_bytes = acc_off + size_t(slots) * R * sizeof(double);  // fp64 mode shares it
   p->ws = dalloc(ws_bytes, st);
   HBK_CUDA(cudaMemsetAsync(p->ws.p, 0, ws_bytes, st));
   w.ws_ctr = reinterpret_cast<uint32_t*>(p->ws.as<char>());
@@ -1141,10 +1150,14 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       launches = 1;
     }
   } else {
-    HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp_generic, p->block, 0));
-    p->grid = grid_for_tasks(w.n3, per_sm, 1);
-    w.total_warps[0] = uint32_t(p->grid) * (p->block / 32);
     launches = 1;
+  }
+  // generic (any order / rank, fp32 or fp64) launch configuration, available
+  // on every plan: one warp per task
+  {
+    int per_gen = 0;
+    HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_gen, k_mttkrp_generic<double>, 256, 0));
+    p->gen_grid = grid_for_tasks(w.n3, per_gen, 1);
   }
 
   p->info.mode = p->mode;
@@ -1165,6 +1178,51 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   HBK_CUDA(cudaStreamSynchronize(st));
 }
 
+}  // namespace hbk
+
+namespace hbk {
+// Generic (any order, any rank) launch in fp32 or fp64.  The fp64 variant
+// reads the buckets' original fp64 values and accumulates in fp64.
+template <class T>
+static void launch_generic(const hbk_plan* p, const T* const* factors, T* out, cudaStream_t st) {
+  const int N = p->order;
+  WorkN<T> wn{};
+  wn.order = N;
+  wn.rank = p->rank;
+  wn.mode = p->mode;
+  for (int d = 0; d < N; ++d) {
+    wn.F[d] = factors[p->mo[d]];
+    wn.Fcoo[d] = factors[d];
+  }
+  auto vals = [](const Buf& v32, const Buf& v64) -> const T* {
+    if constexpr (sizeof(T) == 8) {
+      HBK_REQUIRE(bool(v64), HBK_EINVAL, "fp64 MTTKRP needs a tensor created with fp64 values");
+      return v64.as<T>();
+    } else {
+      (void)v64;
+      return v32.as<T>();
+    }
+  };
+  if (p->csf) {
+    for (int d = 1; d < N - 2; ++d) wn.csf_anc[d] = p->csf->anc[d].as<uint32_t>();
+    if (p->csf->M) wn.csf_val = vals(p->csf->v32, p->csf->v64);
+  }
+  if (p->csl) {
+    for (int c = 0; c < N - 1; ++c) wn.csl_rest[c] = p->csl->rest[c].as<uint32_t>();
+    if (p->csl->M) wn.csl_val = vals(p->csl->v32, p->csl->v64);
+  }
+  if (p->coo) {
+    for (int d = 0; d < N; ++d) wn.coo_col[d] = p->coo->cols[d].as<uint32_t>();
+    if (p->coo->nnz) wn.coo_val = vals(p->coo->v32, p->coo->v64);
+  }
+  wn.acc = reinterpret_cast<T*>(p->work.ws_acc);
+  wn.out = out;
+  Work w = p->work;
+  w.total_warps[0] = uint32_t(p->gen_grid) * (p->block / 32);
+  // the generic kernel pulls single tasks; reuse the fp32 generic counter slot
+  k_mttkrp_generic<T><<<p->gen_grid, 256, 0, st>>>(w, wn);
+  check_launch("k_mttkrp_generic");
+}
 }  // namespace hbk
 
 using namespace hbk;
@@ -1252,24 +1310,19 @@ int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out,
       if (p->grids[2]) k_mttkrp3_r32<KIND_COO><<<p->grids[2], p->block, 0, st>>>(p->work, fx);
       check_launch("k_mttkrp3_r32");
     } else {
-      WorkN wn{};
-      wn.order = N;
-      wn.rank = p->rank;
-      wn.mode = p->mode;
-      for (int d = 0; d < N; ++d) {
-        wn.F[d] = factors[p->mo[d]];
-        wn.Fcoo[d] = factors[d];
-      }
-      if (p->csf)
-        for (int d = 1; d < N - 2; ++d) wn.csf_anc[d] = p->csf->anc[d].as<uint32_t>();
-      if (p->csl)
-        for (int c = 0; c < N - 1; ++c) wn.csl_rest[c] = p->csl->rest[c].as<uint32_t>();
-      if (p->coo)
-        for (int d = 0; d < N; ++d) wn.coo_col[d] = p->coo->cols[d].as<uint32_t>();
-      wn.out = out;
-      k_mttkrp_generic<<<p->grid, p->block, 0, st>>>(p->work, wn);
-      check_launch("k_mttkrp_generic");
+      launch_generic<float>(p, factors, out, st);
     }
+  });
+}
+
+int hbk_plan_execute_f64(const hbk_plan* p, const double* const* factors, double* out,
+                         void* stream) {
+  return guarded([&] {
+    for (int d = 0; d < p->order; ++d)
+      HBK_REQUIRE(d == p->mode || factors[d] != nullptr, HBK_EINVAL, "null factor pointer");
+    HBK_REQUIRE(out != nullptr, HBK_EINVAL, "null output pointer");
+    HBK_REQUIRE(p->gen_grid > 0, HBK_EINVAL, "plan has no fp64 launch configuration");
+    launch_generic<double>(p, factors, out, to_stream(stream));
   });
 }
 

@@ -78,9 +78,12 @@ def _check_factors(dims: tuple[int, ...], factors: Factors, mode: int, check_fin
     return rank
 
 
-def _device_factors(factors: Factors, mode: int):
-    """fp32 contiguous CUDA copies/views of the non-mode factors + pointer array."""
+def _device_factors(factors: Factors, mode: int, precision: str = "fp32"):
+    """Contiguous CUDA copies/views (fp32, or fp64 for precision="fp64") of the
+    non-mode factors + the pointer array."""
     torch = N.require_device()
+    dt = torch.float64 if precision == "fp64" else torch.float32
+    npdt = np.float64 if precision == "fp64" else np.float32
     keep = []
     ptrs = (C.c_void_p * len(factors))()
     on_device = True
@@ -89,10 +92,10 @@ def _device_factors(factors: Factors, mode: int):
             ptrs[d] = None
             continue
         if _is_device(f):
-            t = f if (f.dtype == torch.float32 and f.is_contiguous()) else f.to(torch.float32).contiguous()
+            t = f if (f.dtype == dt and f.is_contiguous()) else f.to(dt).contiguous()
         else:
             on_device = False
-            t = torch.from_numpy(np.ascontiguousarray(f, dtype=np.float32)).cuda(non_blocking=False)
+            t = torch.from_numpy(np.ascontiguousarray(f, dtype=npdt)).cuda(non_blocking=False)
         if t.data_ptr() % 16:
             t = t.clone()
         keep.append(t)
@@ -120,12 +123,13 @@ class _Plan:
     def opcount(self) -> OpCount:
         return OpCount(int(self.info.op_muls), int(self.info.op_adds))
 
-    def execute(self, factor_ptrs, out=None):
+    def execute(self, factor_ptrs, out=None, precision: str = "fp32"):
         torch = N.require_device()
+        dt = torch.float64 if precision == "fp64" else torch.float32
         if out is None:
-            out = torch.empty((self.rows, self.rank), dtype=torch.float32, device="cuda")
-        N.call("hbk_plan_execute", self.h.ptr, factor_ptrs, C.c_void_p(out.data_ptr()),
-               N.stream_ptr())
+            out = torch.empty((self.rows, self.rank), dtype=dt, device="cuda")
+        fn = "hbk_plan_execute_f64" if precision == "fp64" else "hbk_plan_execute"
+        N.call(fn, self.h.ptr, factor_ptrs, C.c_void_p(out.data_ptr()), N.stream_ptr())
         return out
 
 
@@ -137,9 +141,15 @@ def _get_plan(owner, key, build):
     return plan
 
 
-def _finish(plan: _Plan, factors, mode: int, out=None):
-    ptrs, keep, on_device = _device_factors(factors, mode)
-    y = plan.execute(ptrs, out)
+def _check_precision(precision: str) -> str:
+    if precision not in ("fp32", "fp64"):
+        raise ValueError(f"precision must be 'fp32' or 'fp64', got {precision!r}")
+    return precision
+
+
+def _finish(plan: _Plan, factors, mode: int, out=None, precision: str = "fp32"):
+    ptrs, keep, on_device = _device_factors(factors, mode, _check_precision(precision))
+    y = plan.execute(ptrs, out, precision)
     if on_device:
         return y, plan.opcount
     return y.double().cpu().numpy(), plan.opcount
@@ -170,33 +180,35 @@ def plan_for(rep, mode: int, rank: int, schedule=None) -> _Plan:
     raise TypeError(f"no MTTKRP kernel for {type(rep).__name__}")
 
 
-def mttkrp_coo(t: CooTensor, factors: Factors, mode: int, threads: int = 1):
+def mttkrp_coo(t: CooTensor, factors: Factors, mode: int, threads: int = 1, *, precision: str = "fp32"):
     """MTTKRP over a coordinate list (kernels.py:109-151).
 
     The entries are grouped by their mode-``mode`` coordinate on the GPU
     (sorted under (mode, *rest) unless already mode-major) and reduced per
     output row; ``threads`` is accepted for API compatibility."""
     r = _check_factors(t.dims, factors, mode)
-    return _finish(plan_for(t, mode, r), factors, mode)
+    return _finish(plan_for(t, mode, r), factors, mode, precision=precision)
 
 
-def mttkrp_csf(c: CsfTensor, factors: Factors, mode: int):
+def mttkrp_csf(c: CsfTensor, factors: Factors, mode: int, *, precision: str = "fp32"):
     """MTTKRP over a CSF tree built with mode_order[0] == mode (kernels.py:154-186)."""
     if c.mode_order[0] != mode:
         raise ValueError(f"tree was built for mode {c.mode_order[0]}, asked for mode {mode}")
     r = _check_factors(c.dims, factors, mode)
-    return _finish(plan_for(c, mode, r), factors, mode)
+    return _finish(plan_for(c, mode, r), factors, mode, precision=precision)
 
 
-def mttkrp_csl(s: CslSlices, factors: Factors, mode: int, threads: int = 1):
+def mttkrp_csl(s: CslSlices, factors: Factors, mode: int, threads: int = 1, *,
+               precision: str = "fp32"):
     """MTTKRP over compressed slices (kernels.py:189-226)."""
     if s.mode_order[0] != mode:
         raise ValueError(f"slices were built for mode {s.mode_order[0]}, asked for mode {mode}")
     r = _check_factors(s.dims, factors, mode)
-    return _finish(plan_for(s, mode, r), factors, mode)
+    return _finish(plan_for(s, mode, r), factors, mode, precision=precision)
 
 
-def mttkrp_hbcsf(h: HbCsfTensor, factors: Factors, mode: int, schedule=None, threads: int = 1):
+def mttkrp_hbcsf(h: HbCsfTensor, factors: Factors, mode: int, schedule=None, threads: int = 1, *,
+                 precision: str = "fp32"):
     """MTTKRP over the hybrid format, all three buckets in one launch
     (kernels.py:229-253).  A schedule applies to the CSF bucket only."""
     if h.mode_order[0] != mode:
@@ -204,17 +216,18 @@ def mttkrp_hbcsf(h: HbCsfTensor, factors: Factors, mode: int, schedule=None, thr
     if schedule is not None:
         schedule.validate_for(h.csf_part)
     r = _check_factors(h.dims, factors, mode)
-    return _finish(plan_for(h, mode, r, schedule), factors, mode)
+    return _finish(plan_for(h, mode, r, schedule), factors, mode, precision=precision)
 
 
-def mttkrp_scheduled(c: CsfTensor, schedule, factors: Factors, mode: int, threads: int = 1):
+def mttkrp_scheduled(c: CsfTensor, schedule, factors: Factors, mode: int, threads: int = 1, *,
+                     precision: str = "fp32"):
     """MTTKRP over a CSF tree driven by a block schedule (kernels.py:256-342):
     one device work unit per schedule unit."""
     if c.mode_order[0] != mode:
         raise ValueError(f"tree was built for mode {c.mode_order[0]}, asked for mode {mode}")
     schedule.validate_for(c)
     r = _check_factors(c.dims, factors, mode)
-    return _finish(plan_for(c, mode, r, schedule), factors, mode)
+    return _finish(plan_for(c, mode, r, schedule), factors, mode, precision=precision)
 
 
 def mttkrp(rep, factors: Factors, mode: int, **kwargs):
@@ -230,12 +243,16 @@ def mttkrp(rep, factors: Factors, mode: int, **kwargs):
     raise TypeError(f"no MTTKRP kernel for {type(rep).__name__}")
 
 
-def mttkrp_device(rep, factors, mode: int, out=None, schedule=None):
-    """Device fast path: CUDA fp32 factors in, CUDA fp32 (dims[mode], R) out,
-    no host synchronisation and no finiteness scan.  Returns (out, OpCount)."""
+def mttkrp_device(rep, factors, mode: int, out=None, schedule=None, precision: str | None = None):
+    """Device fast path: CUDA factors in, CUDA (dims[mode], R) out, no host
+    synchronisation and no finiteness scan.  The kernel precision follows the
+    factors' dtype (float64 -> fp64 kernel) unless given.  Returns (out, OpCount)."""
     if getattr(rep, "mode_order", None) is not None and rep.mode_order[0] != mode:
         raise ValueError(f"representation was built for mode {rep.mode_order[0]}, asked for mode {mode}")
     r = _check_factors(rep.dims, factors, mode, check_finite=False)
+    if precision is None:
+        ref = next(f for d, f in enumerate(factors) if d != mode)
+        precision = "fp64" if str(getattr(ref, "dtype", "")) == "torch.float64" else "fp32"
     plan = plan_for(rep, mode, r, schedule)
-    ptrs, keep, _ = _device_factors(factors, mode)
-    return plan.execute(ptrs, out), plan.opcount
+    ptrs, keep, _ = _device_factors(factors, mode, _check_precision(precision))
+    return plan.execute(ptrs, out, precision), plan.opcount

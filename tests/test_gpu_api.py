@@ -1,0 +1,286 @@
+"""GPU tests of the drop-in API beyond the golden fixtures: the reference's
+hand examples and argument guards (test_kernels.py:38-56, 274-308), edge
+cases (empty, single nonzero, order 4, ranks the fast path does not take),
+device-tensor inputs, and parity against the CPU oracle on power-law tensors
+large enough to exercise heavy-slice chunking and all three buckets."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from helpers import row_dev
+from oracle import loops
+from oracle import tenkit_port as P
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def hb():
+    import paper_1904_03329_b200 as hb
+
+    return hb
+
+
+def _rand(rng, dims, nnz):
+    cap = int(np.prod(dims))
+    flats = rng.choice(cap, size=nnz, replace=False)
+    idx = np.empty((nnz, len(dims)), dtype=np.int64)
+    rem = flats
+    for d in range(len(dims) - 1, -1, -1):
+        idx[:, d] = rem % dims[d]
+        rem //= dims[d]
+    return idx.astype(np.uint32), rng.uniform(0.1, 1.0, nnz)
+
+
+def _powerlaw(rng, dims, nnz, alpha=1.0):
+    cols = []
+    for d in dims:
+        u = rng.random(nnz)
+        x = np.exp(u * np.log(d + 1.0)) if alpha == 1.0 else 1.0 + u * d
+        cols.append(np.minimum(np.floor(x).astype(np.int64) - 1, d - 1))
+    idx = np.stack(cols, 1).astype(np.uint32)
+    return P.canonical(idx, rng.uniform(0.1, 1.0, nnz))
+
+
+# reference hand examples -------------------------------------------------
+def test_coo_single_nonzero_hand_example(hb):
+    t = hb.CooTensor((1, 1, 1), np.zeros((1, 3), dtype=np.int64), [5.0])
+    f = [np.array([[0.0]]), np.array([[3.0]]), np.array([[7.0]])]
+    out, ops = hb.mttkrp_coo(hb.canonicalize(t), f, 0)
+    assert out[0, 0] == 105.0 and ops.total == 3
+
+
+def test_csl_two_entry_hand_example(hb):
+    t = hb.canonicalize(hb.CooTensor((1, 2, 2), np.array([[0, 0, 0], [0, 1, 1]]), [2.0, 3.0]))
+    h = hb.build_hbcsf(t, (0, 1, 2))
+    assert h.coo_part.nnz == 0 and h.csf_part.num_slices == 0
+    assert len(h.csl_part.slice_idx) == 1
+    f = [np.zeros((1, 1)), np.array([[1.0], [10.0]]), np.array([[1.0], [100.0]])]
+    out, ops = hb.mttkrp_csl(h.csl_part, f, 0)
+    assert out[0, 0] == 3002.0 and ops.total == 6
+
+
+# edge cases --------------------------------------------------------------
+def test_empty_tensor(hb):
+    t = hb.canonicalize(hb.CooTensor((2, 3, 4), np.empty((0, 3), dtype=np.int64), np.empty(0)))
+    assert t.nnz == 0 and t.sorted_under == (0, 1, 2)
+    c = hb.build_csf(t, (0, 1, 2))
+    assert all(p.tolist() == [0] for p in c.ptrs) and c.num_slices == 0
+    h = hb.build_hbcsf(t, (0, 1, 2))
+    assert h.nnz == 0
+    f = [np.ones((d, 3)) for d in (2, 3, 4)]
+    for rep in (t, c, h):
+        y, ops = hb.mttkrp(rep, f, 0)
+        assert y.shape == (2, 3) and not y.any() and ops.total == 0
+    assert hb.split_fibers(c, hb.SplitConfig()) is c
+    s = hb.assign_slice_blocks(c, hb.SplitConfig())
+    assert s.num_blocks == 0 and len(s.multiplicities) == 0
+
+
+def test_rows_without_nonzeros_are_zero(hb):
+    idx = np.array([[3, 0, 1], [3, 1, 1], [7, 2, 0]], dtype=np.uint32)
+    t = hb.CooTensor((10, 3, 2), idx, [1.0, 2.0, 3.0])
+    f = [np.ones((10, 32)), np.ones((3, 32)), np.ones((2, 32))]
+    y, _ = hb.mttkrp_hbcsf(hb.build_hbcsf(t, (0, 1, 2)), f, 0)
+    assert np.allclose(y[3], 3.0) and np.allclose(y[7], 3.0)
+    assert not np.delete(y, [3, 7], axis=0).any()
+
+
+@pytest.mark.parametrize("rank", [1, 2, 7, 16, 32, 33, 64])
+def test_ranks_match_loop_oracle(hb, rng, rank):
+    idx, vals = _rand(rng, (9, 8, 7), 150)
+    t = hb.CooTensor((9, 8, 7), idx, vals)
+    f = [rng.standard_normal((d, rank)) for d in (9, 8, 7)]
+    f = [x.astype(np.float32).astype(np.float64) for x in f]
+    for mode in range(3):
+        ref = loops.mttkrp_entries(idx, vals, (9, 8, 7), f, mode)
+        h = hb.build_hbcsf(t, hb.allmode_order(t.dims, mode))
+        for rep in (h, hb.split_fibers(h, hb.SplitConfig(2, 4, 2)), t):
+            y, _ = hb.mttkrp(rep, f, mode)
+            assert row_dev(y, ref) <= TOL
+
+
+def test_fp64_mode_matches_loop_oracle(hb, rng):
+    idx, vals = _rand(rng, (20, 15, 12), 900)
+    t = hb.CooTensor((20, 15, 12), idx, vals)
+    f = [rng.standard_normal((d, 32)) for d in (20, 15, 12)]
+    for mode in range(3):
+        ref = loops.mttkrp_entries(idx, vals, (20, 15, 12), f, mode)
+        mo = hb.allmode_order(t.dims, mode)
+        h = hb.split_fibers(hb.build_hbcsf(t, mo), hb.SplitConfig(3, 8, 2))
+        for y, _ in (hb.mttkrp(h, f, mode, precision="fp64"), hb.mttkrp(t, f, mode, precision="fp64"),
+                     hb.mttkrp(hb.build_csf(t, mo), f, mode, precision="fp64")):
+            assert row_dev(y, ref) <= 1e-12
+    with pytest.raises(ValueError):
+        hb.mttkrp(h, f, 0, precision="fp16")
+
+
+def test_order4_and_order5(hb, rng):
+    for dims, nnz in (((6, 5, 4, 3), 200), ((4, 3, 5, 3, 2), 150)):
+        idx, vals = _rand(rng, dims, nnz)
+        t = hb.CooTensor(dims, idx, vals)
+        f = [rng.random((d, 32)).astype(np.float32).astype(np.float64) for d in dims]
+        for mode in range(len(dims)):
+            ref = loops.mttkrp_entries(idx, vals, dims, f, mode)
+            mo = hb.allmode_order(dims, mode)
+            h = hb.build_hbcsf(t, mo)
+            cfg = hb.SplitConfig(2, 4, 2)
+            hs = hb.split_fibers(h, cfg)
+            sched = hb.assign_slice_blocks(hs.csf_part, cfg)
+            for y, ops in (hb.mttkrp(h, f, mode), hb.mttkrp_hbcsf(hs, f, mode, schedule=sched),
+                           hb.mttkrp(hb.build_csf(t, mo), f, mode)):
+                assert row_dev(y, ref) <= TOL
+            # OpCount of the scheduled CSF path matches the oracle's executed-site count
+            ref_h = P.split_hbcsf(P.hbcsf(idx, vals, dims, mo), 2)
+            units, _ = P.block_schedule(ref_h["csf"], 4)
+            _, k = P.mttkrp_hbcsf(ref_h, f, mode, units=units)
+            _, ops = hb.mttkrp_hbcsf(hs, f, mode, schedule=sched)
+            assert (ops.muls, ops.adds) == k
+
+
+# argument guards (same exception types as the reference) -----------------
+def test_argument_guards(hb, rng):
+    idx, vals = _rand(rng, (5, 4, 3), 20)
+    t = hb.CooTensor((5, 4, 3), idx, vals)
+    h = hb.build_hbcsf(t, (0, 2, 1))
+    f = [np.ones((5, 2)), np.ones((4, 2)), np.ones((3, 2))]
+    with pytest.raises(ValueError):
+        hb.mttkrp_hbcsf(h, f, 1)  # built for mode 0
+    with pytest.raises(ValueError):
+        hb.mttkrp_csf(h.csf_part, f, 2)
+    with pytest.raises(ValueError):
+        hb.mttkrp(h, f[:2], 0)
+    with pytest.raises(ValueError):
+        hb.mttkrp(h, [f[0], np.ones((4, 3)), f[2]], 0)
+    with pytest.raises(ValueError):
+        hb.mttkrp(h, [f[0], np.ones((5, 2)), f[2]], 0)
+    with pytest.raises(ValueError):
+        hb.mttkrp(h, [f[0], np.full((4, 2), np.inf), f[2]], 0)
+    with pytest.raises(TypeError):
+        hb.mttkrp(h.csf_part, f, 0, threads=2)  # mttkrp_csf takes no threads
+    with pytest.raises(TypeError):
+        hb.mttkrp([1, 2], f, 0)
+    with pytest.raises(ValueError):
+        hb.build_hbcsf(t, (0, 0, 1))
+    # factors[mode] is never read
+    y, _ = hb.mttkrp(h, [None, f[1], f[2]], 0)
+    assert y.shape == (5, 2)
+
+
+def test_foreign_schedule_rejected(hb, rng):
+    i1, v1 = _rand(rng, (10, 8, 8), 200)
+    i2, v2 = _rand(rng, (10, 8, 8), 100)
+    cfg = hb.SplitConfig()
+    c1 = hb.build_csf(hb.CooTensor((10, 8, 8), i1, v1), (0, 1, 2))
+    c2 = hb.build_csf(hb.CooTensor((10, 8, 8), i2, v2), (0, 1, 2))
+    sched = hb.assign_slice_blocks(c1, cfg)
+    with pytest.raises(ValueError):
+        sched.validate_for(c2)
+    f = [np.ones((d, 4)) for d in (10, 8, 8)]
+    with pytest.raises(ValueError):
+        hb.mttkrp_scheduled(c2, sched, f, 0)
+
+
+def test_host_built_schedule_and_units(hb, rng):
+    idx, vals = _rand(rng, (6, 20, 30), 500)
+    t = hb.CooTensor((6, 20, 30), idx, vals)
+    cfg = hb.SplitConfig(4, 32, 32)
+    c = hb.split_fibers(hb.build_csf(t, (0, 1, 2)), cfg)
+    s = hb.assign_slice_blocks(c, cfg)
+    host = hb.BlockSchedule(units=s.units, multiplicities=s.multiplicities,
+                            num_slices=s.num_slices, num_fibers=s.num_fibers)
+    host.validate_for(c)
+    f = [rng.random((d, 32)) for d in (6, 20, 30)]
+    a, ka = hb.mttkrp_scheduled(c, s, f, 0)
+    b, kb = hb.mttkrp_scheduled(c, host, f, 0)
+    assert np.allclose(a, b, rtol=1e-6) and ka == kb
+    assert all(isinstance(u, hb.ScheduleUnit) for u in s.units)
+    bad = hb.BlockSchedule(units=s.units[1:], multiplicities=s.multiplicities,
+                           num_slices=s.num_slices, num_fibers=s.num_fibers)
+    with pytest.raises(ValueError):
+        bad.validate_for(c)
+
+
+# device tensors ------------------------------------------------------------
+def test_device_tensor_inputs(hb, rng):
+    import torch
+
+    idx, vals = _rand(rng, (30, 20, 10), 800)
+    t_host = hb.CooTensor((30, 20, 10), idx, vals)
+    t_dev = hb.CooTensor((30, 20, 10), torch.from_numpy(idx.astype(np.int64)).cuda(),
+                         torch.from_numpy(vals).cuda())
+    assert t_dev == t_host
+    f = [torch.rand((d, 32), device="cuda") for d in (30, 20, 10)]
+    fh = [x.double().cpu().numpy() for x in f]
+    for mode in range(3):
+        h = hb.build_hbcsf(t_dev, hb.allmode_order(t_dev.dims, mode))
+        y, _ = hb.mttkrp(h, f, mode)
+        assert y.is_cuda and y.dtype == torch.float32
+        yd, _ = hb.mttkrp_device(h, f, mode)
+        yh, _ = hb.mttkrp(h, fh, mode)
+        assert row_dev(y.double().cpu().numpy(), yh) <= 1e-6
+        assert row_dev(yd.double().cpu().numpy(), yh) <= 1e-6
+
+
+def test_canonicalize_merges_duplicates_on_device(hb, rng):
+    idx = rng.integers(0, 4, size=(3000, 3)).astype(np.uint32)
+    vals = rng.standard_normal(3000)
+    idx = np.vstack([idx, [[5, 5, 5], [5, 5, 5]]]).astype(np.uint32)
+    vals = np.concatenate([vals, [0.25, -0.25]])  # cancels exactly -> dropped
+    ref_i, ref_v = P.canonical(idx, vals)
+    c = hb.canonicalize(hb.CooTensor((6, 6, 6), idx, vals))
+    assert np.array_equal(c.indices, ref_i) and c.values.tobytes() == ref_v.tobytes()
+    assert not ((c.indices == 5).all(axis=1)).any()
+
+
+# power-law tensors: heavy-slice chunking, all buckets, wide keys ---------
+@pytest.mark.parametrize("shape,nnz", [((300, 5000, 2000), 400_000), ((2000, 300000, 30000), 300_000)])
+def test_powerlaw_parity_with_oracle(hb, shape, nnz):
+    rng = np.random.default_rng(4)
+    idx, vals = _powerlaw(rng, shape, nnz)
+    t = hb.CooTensor(shape, idx, vals, sorted_under=(0, 1, 2))
+    f = [rng.random((d, 32)).astype(np.float32).astype(np.float64) for d in shape]
+    for mode in range(3):
+        mo = hb.allmode_order(shape, mode)
+        h = hb.build_hbcsf(t, mo)
+        ref = P.hbcsf(idx, vals, shape, mo)
+        assert np.array_equal(h.coo_part.indices, ref["coo"][0])
+        assert np.array_equal(h.csl_part.slice_ptr, ref["csl"]["slice_ptr"])
+        assert np.array_equal(h.csl_part.rest_idx, ref["csl"]["rest_idx"])
+        for d in range(2):
+            assert np.array_equal(h.csf_part.ptrs[d], ref["csf"]["ptrs"][d])
+            assert np.array_equal(h.csf_part.idxs[d], ref["csf"]["idxs"][d])
+        hs = hb.split_fibers(h, hb.SplitConfig())
+        refs = P.split_hbcsf(ref, 128)
+        assert np.array_equal(hs.csf_part.ptrs[1], refs["csf"]["ptrs"][1])
+        sched = hb.assign_slice_blocks(hs.csf_part, hb.SplitConfig())
+        units, mult = P.block_schedule(refs["csf"], 512)
+        assert np.array_equal(sched.units_array(), units)
+        assert np.array_equal(sched.multiplicities, mult)
+        yr, kr = P.mttkrp_hbcsf(ref, f, mode)
+        y, ops = hb.mttkrp_hbcsf(h, f, mode)
+        assert row_dev(y, yr) <= TOL and (ops.muls, ops.adds) == kr
+        y2, _ = hb.mttkrp_hbcsf(hs, f, mode)
+        assert row_dev(y2, yr) <= TOL
+        y3, _ = hb.mttkrp_hbcsf(hs, f, mode, schedule=sched)
+        assert row_dev(y3, yr) <= TOL
+
+
+def test_linearity_and_repeatability(hb):
+    rng = np.random.default_rng(9)
+    shape = (500, 4000, 3000)
+    idx, vals = _powerlaw(rng, shape, 200_000)
+    f = [rng.random((d, 32)) for d in shape]
+    t1 = hb.CooTensor(shape, idx, vals, sorted_under=(0, 1, 2))
+    t2 = hb.CooTensor(shape, idx, 2.0 * vals, sorted_under=(0, 1, 2))
+    for mode in range(3):
+        mo = hb.allmode_order(shape, mode)
+        h1, h2 = hb.build_hbcsf(t1, mo), hb.build_hbcsf(t2, mo)
+        a, _ = hb.mttkrp(h1, f, mode)
+        b, _ = hb.mttkrp(h2, f, mode)
+        assert row_dev(b, 2.0 * a) <= 1e-6
+        a2, _ = hb.mttkrp(h1, f, mode)  # the plan is reused; the workspace self-cleans
+        assert row_dev(a2, a) <= 1e-6
