@@ -221,9 +221,16 @@ void hbk_plan_release(hbk_plan* p);
  * Multi-GPU partitioner: slice nnz histogram of `mode`.
  * hist [dev] int64 [dims[mode]] is overwritten.                            */
 int hbk_coo_slice_histogram(const hbk_coo* t, int mode, int64_t* hist, void* stream);
-/* Keep only entries whose `mode` coordinate lies in [row_begin, row_end). */
+/* Keep only entries whose `mode` coordinate lies in [row_begin, row_end)
+ * (coordinates and dims unchanged). */
 int hbk_coo_select_rows(const hbk_coo* t, int mode, int64_t row_begin, int64_t row_end,
                         void* stream, hbk_coo** out);
+/* The same selection, rebased: the shard's `mode` coordinates are shifted by
+ * -row_begin and dims[mode] = row_end - row_begin (> 0), so an MTTKRP of the
+ * shard writes exactly the rank's own output rows (no zero-fill of the other
+ * ranks' rows).  Used by the row-sharded multi-GPU CP-ALS.                 */
+int hbk_coo_shard_rows(const hbk_coo* t, int mode, int64_t row_begin, int64_t row_end,
+                       void* stream, hbk_coo** out);
 
 #ifdef __cplusplus
 }

@@ -1487,12 +1487,13 @@ __global__ void k_row_flags(const uint32_t* __restrict__ col, int64_t M, uint32_
 }
 __global__ void k_row_compact(const uint32_t* __restrict__ pos, Cols in, MCols out, int order,
                               const float* __restrict__ v32, const double* __restrict__ v64,
-                              int64_t M, float* __restrict__ o32, double* __restrict__ o64) {
+                              int64_t M, float* __restrict__ o32, double* __restrict__ o64,
+                              int shift_mode, uint32_t shift) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
        i += int64_t(gridDim.x) * blockDim.x) {
     if (pos[i + 1] != pos[i]) {
       uint32_t d = pos[i];
-      for (int m = 0; m < order; ++m) out.c[m][d] = in.c[m][i];
+      for (int m = 0; m < order; ++m) out.c[m][d] = in.c[m][i] - (m == shift_mode ? shift : 0u);
       o32[d] = v32[i];
       if (o64) o64[d] = v64[i];
     }
@@ -1513,12 +1514,11 @@ extern "C" int hbk_coo_slice_histogram(const hbk_coo* t, int mode, int64_t* hist
   });
 }
 
-extern "C" int hbk_coo_select_rows(const hbk_coo* t, int mode, int64_t lo, int64_t hi,
-                                   void* stream, hbk_coo** out) {
-  return guarded([&] {
+static hbk_coo* coo_rows(const hbk_coo* t, int mode, int64_t lo, int64_t hi, bool rebase,
+                         cudaStream_t st) {
     HBK_REQUIRE(mode >= 0 && mode < t->order, HBK_EINVAL, "mode out of range");
     HBK_REQUIRE(0 <= lo && lo <= hi && hi <= t->dims[mode], HBK_EINVAL, "row range out of bounds");
-    cudaStream_t st = to_stream(stream);
+    HBK_REQUIRE(!rebase || hi > lo, HBK_EINVAL, "a rebased shard needs at least one row");
     const int64_t M = t->nnz;
     Scratch pos((M + 1) * sizeof(uint32_t), st);
     uint32_t K = 0;
@@ -1528,17 +1528,29 @@ extern "C" int hbk_coo_select_rows(const hbk_coo* t, int mode, int64_t lo, int64
       check_launch("k_row_flags");
       K = exclusive_scan_total(pos.as<uint32_t>(), M, st);
     }
-    hbk_coo* o = new_coo_like(t, K, bool(t->v64), st);
+    std::unique_ptr<hbk_coo, void (*)(hbk_coo*)> o(new_coo_like(t, K, bool(t->v64), st),
+                                                [](hbk_coo* p) { hbk_coo_release(p); });
     if (K) {
-      k_row_compact<<<grid_for(M, 256), 256, 0, st>>>(pos.as<uint32_t>(), cols_of(t), mcols_of(o),
+      k_row_compact<<<grid_for(M, 256), 256, 0, st>>>(pos.as<uint32_t>(), cols_of(t), mcols_of(o.get()),
                                                       t->order, t->v32.as<float>(),
                                                       t->v64.as<double>(), M, o->v32.as<float>(),
-                                                      o->v64.as<double>());
+                                                      o->v64.as<double>(), rebase ? mode : -1,
+                                                      uint32_t(lo));
       check_launch("k_row_compact");
     }
+    if (rebase) o->dims[mode] = hi - lo;
     o->has_sorted = t->has_sorted;
     std::copy(t->sorted_under, t->sorted_under + t->order, o->sorted_under);
     HBK_CUDA(cudaStreamSynchronize(st));
-    *out = o;
-  });
+    return o.release();
+}
+
+extern "C" int hbk_coo_shard_rows(const hbk_coo* t, int mode, int64_t lo, int64_t hi,
+                                  void* stream, hbk_coo** out) {
+  return guarded([&] { *out = coo_rows(t, mode, lo, hi, true, to_stream(stream)); });
+}
+
+extern "C" int hbk_coo_select_rows(const hbk_coo* t, int mode, int64_t lo, int64_t hi,
+                                   void* stream, hbk_coo** out) {
+  return guarded([&] { *out = coo_rows(t, mode, lo, hi, false, to_stream(stream)); });
 }

@@ -56,6 +56,16 @@ def select_rows(t: CooTensor, mode: int, lo: int, hi: int) -> CooTensor:
     return CooTensor._from_handle(N.Handle(out, "hbk_coo_release"))
 
 
+def shard_rows(t: CooTensor, mode: int, lo: int, hi: int) -> CooTensor:
+    """Entries whose mode-``mode`` coordinate lies in [lo, hi), rebased: the
+    shard has dims[mode] = hi - lo and coordinates shifted by -lo, so its
+    MTTKRP produces exactly rows [lo, hi) of the full output."""
+    out = N.new_out()
+    N.call("hbk_coo_shard_rows", t._dev().ptr, int(mode), int(lo), int(hi), N.stream_ptr(),
+           C.byref(out))
+    return CooTensor._from_handle(N.Handle(out, "hbk_coo_release"))
+
+
 def shard_for_rank(t: CooTensor, mode: int, rank: int, world: int):
     """(row range, shard tensor) owned by `rank` for `mode`."""
     ranges = plan_row_ranges(slice_histogram(t, mode).cpu().numpy(), world)

@@ -62,6 +62,66 @@ __global__ void k_ldg(const float4* __restrict__ F, const uint32_t* __restrict__
   out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = acc;
 }
 
+
+// 32 lanes x LDG.32 per row: one 128-byte line per warp instruction.
+__device__ __forceinline__ float ldf(const float* p) {
+  float v;
+  asm("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+template <int U>
+__global__ void k_ldg32(const float* __restrict__ F, const uint32_t* __restrict__ idx, int64_t n,
+                        float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  float acc = 0.f;
+  for (int64_t base = wid * 32; base < n; base += nw * 32) {
+    uint32_t k = (base + lane < n) ? idx[base + lane] : 0;
+#pragma unroll
+    for (int j0 = 0; j0 < 32; j0 += U) {
+      float r[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        uint32_t kj = __shfl_sync(0xffffffffu, k, j0 + j);
+        r[j] = ldf(F + size_t(kj) * 32 + lane);
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) acc += r[j];
+    }
+  }
+  out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = acc;
+}
+// 16 lanes x LDG.64 per row: two lines per warp instruction.
+__device__ __forceinline__ float2 ldf2(const float2* p) {
+  float2 v;
+  asm("ld.global.nc.L1::evict_last.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+template <int U>
+__global__ void k_ldg64(const float2* __restrict__ F, const uint32_t* __restrict__ idx, int64_t n,
+                        float2* __restrict__ out) {
+  const int lane = threadIdx.x & 31, h = lane >> 4, l16 = lane & 15;
+  const int64_t wid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  float2 acc = make_float2(0.f, 0.f);
+  for (int64_t base = wid * 32; base < n; base += nw * 32) {
+    uint32_t k = (base + lane < n) ? idx[base + lane] : 0;
+#pragma unroll
+    for (int j0 = 0; j0 < 16; j0 += U) {
+      float2 r[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        uint32_t kj = __shfl_sync(0xffffffffu, k, 2 * (j0 + j) + h);
+        r[j] = ldf2(F + size_t(kj) * 16 + l16);
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) { acc.x += r[j].x; acc.y += r[j].y; }
+    }
+  }
+  out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = acc;
+}
+
 // 4 lanes x LDG.256 per row (8 rows per warp instruction)
 struct f8 {
   float v[8];
@@ -286,6 +346,27 @@ int main() {
     printf("  ldg U=%2d thr=%d blk/sm=%d : %.3f ms  %.2f Grows/s  %.1f GB/s\n", U, THREADS,       \
            BLOCKS_PER_SM, ms, n / ms / 1e6, gb / ms * 1e3);                                       \
   }
+#define RUN_L32(U, THREADS, BLOCKS_PER_SM)                                                        \
+  {                                                                                               \
+    int g = sms * BLOCKS_PER_SM;                                                                  \
+    float ms = time_ms([&] { k_ldg32<U><<<g, THREADS>>>((const float*)F, idx, n, (float*)out); }); \
+    printf("  ldg32 U=%2d thr=%d blk/sm=%d : %.3f ms  %.2f Grows/s  %.1f GB/s\n", U, THREADS,    \
+           BLOCKS_PER_SM, ms, n / ms / 1e6, gb / ms * 1e3);                                       \
+  }
+#define RUN_L64(U, THREADS, BLOCKS_PER_SM)                                                        \
+  {                                                                                               \
+    int g = sms * BLOCKS_PER_SM;                                                                  \
+    float ms = time_ms([&] { k_ldg64<U><<<g, THREADS>>>((const float2*)F, idx, n, (float2*)out); }); \
+    printf("  ldg64 U=%2d thr=%d blk/sm=%d : %.3f ms  %.2f Grows/s  %.1f GB/s\n", U, THREADS,    \
+           BLOCKS_PER_SM, ms, n / ms / 1e6, gb / ms * 1e3);                                       \
+  }
+    RUN_L32(8, 256, 4);
+    RUN_L32(16, 256, 4);
+    RUN_L32(16, 256, 8);
+    RUN_L32(32, 256, 4);
+    RUN_L64(8, 256, 4);
+    RUN_L64(8, 256, 8);
+    RUN_L64(16, 256, 4);
     RUN_LDG(8, 256, 2);
     RUN_LDG(8, 256, 4);
     RUN_LDG(8, 256, 8);

@@ -1,0 +1,87 @@
+"""GPU checks of the row-sharded path: rebased shards reproduce the full
+MTTKRP row for row, and cp_als_distributed on a one-rank NCCL group matches
+the single-GPU cp_als (the multi-rank collectives are covered on CPU with
+gloo in test_distributed_cpu.py)."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import tenkit_port as P
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hb():
+    import paper_1904_03329_b200 as hb
+
+    return hb
+
+
+def _powerlaw(rng, dims, nnz):
+    cols = [np.minimum(np.floor(np.exp(rng.random(nnz) * np.log(d + 1))) - 1, d - 1) for d in dims]
+    idx = np.stack(cols, 1).astype(np.uint32)
+    return P.canonical(idx, rng.random(nnz) + 0.01)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_shards_concatenate_to_full_mttkrp(hb, world):
+    from paper_1904_03329_b200 import shard
+
+    rng = np.random.default_rng(11 + world)
+    dims = (120, 90, 300)
+    idx, vals = _powerlaw(rng, dims, 20000)
+    t = hb.CooTensor(dims, idx, vals, sorted_under=(0, 1, 2))
+    fs = [rng.random((d, 32)).astype(np.float32).astype(np.float64) for d in dims]
+    for mode in range(3):
+        mo = hb.allmode_order(dims, mode)
+        ref, _ = P.mttkrp_hbcsf(P.hbcsf(idx, vals, dims, mo), fs, mode)
+        hist = shard.slice_histogram(t, mode).cpu().numpy()
+        assert np.array_equal(hist, np.bincount(idx[:, mode], minlength=dims[mode]))
+        ranges = shard.plan_row_ranges(hist, world)
+        parts = []
+        for lo, hi in ranges:
+            if hi == lo:
+                continue
+            part = shard.shard_rows(t, mode, lo, hi)
+            assert part.dims[mode] == hi - lo
+            h = hb.split_fibers(hb.build_hbcsf(part, mo), hb.SplitConfig())
+            f = list(fs)
+            f[mode] = np.zeros((hi - lo, 32))
+            y, _ = hb.mttkrp_hbcsf(h, f, mode)
+            parts.append(y)
+        y = np.concatenate(parts)
+        assert y.shape == ref.shape
+        assert P.row_deviation(y, ref) <= 1e-4
+
+
+def test_cp_als_distributed_single_rank_matches_cp_als(hb):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1904_03329_b200.distributed import cp_als_distributed
+
+    rng = np.random.default_rng(5)
+    dims = (40, 30, 50)
+    idx, vals = _powerlaw(rng, dims, 6000)
+    t = hb.CooTensor(dims, idx, vals, sorted_under=(0, 1, 2))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        m1, h1 = cp_als_distributed(t, rank=8, max_iters=5, fit_tol=1e-14, seed=3)
+    finally:
+        dist.destroy_process_group()
+    m0, h0 = hb.cp_als(t, rank=8, max_iters=5, fit_tol=1e-14, seed=3)
+    assert len(h0) == len(h1)
+    assert np.allclose([h.fit for h in h1], [h.fit for h in h0], atol=1e-5, rtol=0)
+    assert np.allclose(m1.lam, m0.lam, rtol=1e-3)
+    fits_ref, _, _ = P.cp_als(idx, vals, dims, rank=8, max_iters=5, fit_tol=1e-14, seed=3)
+    assert np.allclose([h.fit for h in h1], fits_ref, atol=1e-5, rtol=0)
