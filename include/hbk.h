@@ -201,6 +201,7 @@ typedef struct {
   int64_t op_muls, op_adds; /* OpCount of the reference kernel, R-weighted */
   int64_t nnz;
   int64_t stream_bytes;    /* index + value bytes read per execute        */
+  int64_t tasks_heavy;     /* group tasks of the heavy-slice CSF layout   */
 } hbk_plan_info;
 
 int hbk_plan_create(hbk_coo* coo, hbk_csl* csl, hbk_csf* csf, hbk_sched* sched, int mode,

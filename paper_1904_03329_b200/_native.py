@@ -82,6 +82,7 @@ class PlanInfo(C.Structure):
         ("op_adds", i64),
         ("nnz", i64),
         ("stream_bytes", i64),
+        ("tasks_heavy", i64),
     ]
 
 

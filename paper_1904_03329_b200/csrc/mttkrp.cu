@@ -89,6 +89,7 @@ struct alignas(16) Work {
 static constexpr uint32_t FEND = 0x80000000u;  // last nonzero of its fiber
 static constexpr uint32_t SEND = 0x40000000u;  // last nonzero of its slice
 static constexpr uint32_t KMASK = 0x3FFFFFFFu;
+static constexpr uint32_t FB = 0x80000000u;    // B-row position (B-position streams)
 
 struct Factors3 {
   const float4* B;  // factor of mode_order[1] (fiber / rest[0])
@@ -281,6 +282,70 @@ __device__ __forceinline__ float4 csf_tasks(const Work& w, const Factors3& fx, c
   return sa;
 }
 
+// CSF tasks over a "B-position" stream: each fiber's (leaf, value) pairs
+// are followed by one extra position (j | FB, 0) naming the fiber's B row, so
+// B rows are gathered by the same LDG batch as the leaf rows (no shared-memory
+// staging: the L1 data pipe carries each row once).  At a B position the
+// fiber partial is multiplied into the slice partial; slice ends (SEND) sit
+// on B positions.  Dead lanes carry (0, 0): leaf row 0 times v = 0.
+__device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const Factors3& fx, const Task& t,
+                                                 int g, int lig, uint64_t pol_s, uint64_t pol_r) {
+  const uint32_t lo = t.lo, hi = t.hi;
+  const bool chunk = t.slot != NOSLOT;
+  const uint32_t nbat = __reduce_max_sync(FULL, hi > lo ? (hi - lo + 7) / 8 : 0u);
+  const float4* Cl = fx.C + lig;
+  const float4* Bl = fx.B + lig;
+  const uint2* pairs = w.csf_pairs;
+  const uint32_t Sm1 = w.csf_S ? w.csf_S - 1 : 0;
+  uint32_t s = t.s;
+  float4 fa = f4zero(), sa = f4zero();
+  uint2 pr = make_uint2(0u, 0u);
+  if (lo + lig < hi) pr = ld_stream_u2(pairs + lo + lig, pol_s);
+  uint32_t sr = chunk ? 0u : __ldg(w.csf_sidx + min(s + lig, Sm1));
+  uint32_t base = lo;
+  for (uint32_t it = 0; it < nbat; ++it, base += 8) {
+    const uint32_t bb_all = __ballot_sync(FULL, pr.x & FB);
+    const uint32_t sb_all = __ballot_sync(FULL, !chunk && (pr.x & SEND));
+    const uint32_t bbits = (bb_all >> (8 * g)) & 0xFFu;
+    const uint32_t sbits = (sb_all >> (8 * g)) & 0xFFu;
+    const uint32_t sany = any_group(sb_all);
+    float4 r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t xj = __shfl_sync(FULL, pr.x, j, 8);
+      const float4* rowp = ((xj & FB) ? Bl : Cl) + size_t(xj & KMASK) * 8;
+      r[j] = ld_row4(rowp, pol_r);
+    }
+    const float vv = __uint_as_float(pr.y);
+    const uint32_t sr_cur = sr;
+    const uint32_t nsl = __popc(sbits);
+    s += nsl;
+    const uint32_t nb = base + 8;
+    pr = make_uint2(0u, 0u);
+    if (nb + lig < hi) pr = ld_stream_u2(pairs + nb + lig, pol_s);
+    if (__any_sync(FULL, nsl != 0)) sr = __ldg(w.csf_sidx + min(s + lig, Sm1));
+    uint32_t ts = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float vj = __shfl_sync(FULL, vv, j, 8);
+      fa = fma4(vj, r[j], fa);
+      if ((bbits >> j) & 1u) {
+        sa = fmav4(fa, r[j], sa);
+        fa = f4zero();
+      }
+      if ((sany >> j) & 1u) {
+        const uint32_t row = __shfl_sync(FULL, sr_cur, ts, 8);
+        if ((sbits >> j) & 1u) {
+          fx.out[size_t(row) * 8 + lig] = sa;
+          sa = f4zero();
+          ++ts;
+        }
+      }
+    }
+  }
+  return sa;
+}
+
 // ------------------------------------------------------------ CSL tasks --
 __device__ __forceinline__ float4 csl_tasks(const Work& w, const Factors3& fx, const Task& t,
                                             int g, int lig, uint64_t pol_s, uint64_t pol_r,
@@ -406,10 +471,10 @@ __device__ __forceinline__ void zero_task(const Work& w, const Factors3& fx, con
 // it.  Chunks of one split slice that land in the same warp are summed with
 // shuffles and handed over with a single vector atomic.
 static constexpr int FAST_BLOCK = 256;
-enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2 };
+enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2, KIND_CSF_BPOS = 3, KIND_CSF_BPOS4 = 4 };
 
 template <int KIND>
-__global__ void __launch_bounds__(FAST_BLOCK, 3)
+__global__ void __launch_bounds__(FAST_BLOCK, KIND == KIND_CSF_BPOS4 ? 4 : 3)
     k_mttkrp3_r32(const __grid_constant__ Work w, const __grid_constant__ Factors3 fx) {
   // per lane: 8 slots of 16 B (one per batch position) for staged B rows
   __shared__ float4 s_slots[FAST_BLOCK * 8];
@@ -419,7 +484,7 @@ __global__ void __launch_bounds__(FAST_BLOCK, 3)
   float4* slots = s_slots + (threadIdx.x >> 3) * 64 + lig;
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_r = policy_evict_last();
-  constexpr int K = KIND;
+  constexpr int K = (KIND == KIND_CSF_BPOS || KIND == KIND_CSF_BPOS4) ? KIND_CSF : KIND;
   const uint32_t first = K == KIND_CSF ? 0u : (K == KIND_CSL ? w.n0 : w.n1);
   const uint32_t last = K == KIND_CSF ? w.n0 : (K == KIND_CSL ? w.n1 : w.n3);
   uint32_t* ctr = w.ws_ctr + 2 * K;
@@ -430,8 +495,10 @@ __global__ void __launch_bounds__(FAST_BLOCK, 3)
     if (base >= last) break;
     const Task t = w.tasks[base + g];
     if (K == KIND_CSF || K == KIND_CSL) {
-      const float4 sa = K == KIND_CSF ? csf_tasks(w, fx, t, g, lig, pol_s, pol_r, slots)
-                                      : csl_tasks(w, fx, t, g, lig, pol_s, pol_r, slots);
+      const float4 sa =
+          (KIND == KIND_CSF_BPOS || KIND == KIND_CSF_BPOS4) ? csf_bpos_tasks(w, fx, t, g, lig, pol_s, pol_r)
+          : K == KIND_CSF       ? csf_tasks(w, fx, t, g, lig, pol_s, pol_r, slots)
+                                : csl_tasks(w, fx, t, g, lig, pol_s, pol_r, slots);
       const bool mine = t.slot != NOSLOT && t.lo < t.hi;
       const uint32_t slot0 = __shfl_sync(FULL, t.slot, 0);
       const bool same = __all_sync(FULL, mine && t.slot == slot0);
@@ -629,12 +696,16 @@ __global__ void k_csf_slice_offsets(Chain2 ch, int64_t S, uint32_t* __restrict__
 
 // Per slice: number of tasks it opens (chunks of a heavy slice, or 1 if it
 // starts a new run of light slices) and whether it needs an accumulator slot.
-__global__ void k_task_count(const uint32_t* __restrict__ loff, int64_t S, uint32_t T,
+// Slices with more than H nonzeros belong to the heavy layout and open none.
+__global__ void k_task_count(const uint32_t* __restrict__ loff, int64_t S, uint32_t T, uint32_t H,
                              uint32_t* __restrict__ cnt, uint32_t* __restrict__ slotf) {
   for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < S;
        s += int64_t(gridDim.x) * blockDim.x) {
     uint32_t a = loff[s], m = loff[s + 1] - a;
-    if (m > T) {
+    if (m > H) {
+      cnt[s] = 0;
+      slotf[s] = 0;
+    } else if (m > T) {
       cnt[s] = (m + T - 1) / T;
       slotf[s] = 1;
     } else {
@@ -664,14 +735,14 @@ __device__ __forceinline__ uint32_t fiber_of(const uint32_t* __restrict__ lptr, 
 }
 
 __global__ void k_task_fill(const uint32_t* __restrict__ loff, const uint32_t* __restrict__ fpos,
-                            const uint32_t* __restrict__ lptr, int64_t S, uint32_t T,
+                            const uint32_t* __restrict__ lptr, int64_t S, uint32_t T, uint32_t H,
                             const uint32_t* __restrict__ toff, const uint32_t* __restrict__ slot,
-                            Task* __restrict__ tasks) {
+                            const uint32_t* __restrict__ posoff, Task* __restrict__ tasks) {
   for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < S;
        s += int64_t(gridDim.x) * blockDim.x) {
     uint32_t a = loff[s], m = loff[s + 1] - a;
+    if (m > H) continue;
     uint32_t nt = toff[s + 1] - toff[s];
-    if (nt == 0) continue;
     if (m > T) {
       for (uint32_t c = 0; c < nt; ++c) {
         Task t{};
@@ -683,10 +754,11 @@ __global__ void k_task_fill(const uint32_t* __restrict__ loff, const uint32_t* _
         t.nchunk = nt;
         tasks[toff[s] + c] = t;
       }
-    } else {
+      continue;
+    }
+    if (nt) {
       Task t{};
-      t.lo = a;
-      t.hi = 0;  // fixed up by k_task_hi
+      t.lo = a + (posoff ? posoff[s] : 0u);
       t.s = uint32_t(s);
       t.f = fpos ? fpos[s] : 0;
       t.slot = NOSLOT;
@@ -696,10 +768,17 @@ __global__ void k_task_fill(const uint32_t* __restrict__ loff, const uint32_t* _
   }
 }
 
-__global__ void k_task_hi(Task* __restrict__ tasks, int64_t n, uint32_t M) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    if (tasks[i].slot == NOSLOT) tasks[i].hi = (i + 1 < n) ? tasks[i + 1].lo : M;
+// A run of light slices ends at its last slice (the next slice opens a task
+// or belongs to the heavy layout); that slice sets the run's end.
+__global__ void k_run_hi(const uint32_t* __restrict__ loff, int64_t S, uint32_t T, uint32_t H,
+                         const uint32_t* __restrict__ toff, const uint32_t* __restrict__ posoff,
+                         Task* __restrict__ tasks) {
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < S;
+       s += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t m = loff[s + 1] - loff[s];
+    if (m > T) continue;
+    const bool last = s + 1 == S || toff[s + 2] != toff[s + 1] || loff[s + 2] - loff[s + 1] > H;
+    if (last) tasks[toff[s + 1] - 1].hi = loff[s + 1] + (posoff ? posoff[s + 1] : 0u);
   }
 }
 
@@ -774,6 +853,29 @@ __global__ void k_empty_tasks(Task* __restrict__ tasks, int64_t n) {
   }
 }
 
+// B-position stream of a CSF bucket in tree order: fiber f's pairs start at
+// position lptr[f] + f and are followed by (fidx[f] | FB, 0).
+__global__ void k_bpos_stream(const uint32_t* __restrict__ lptr, const uint32_t* __restrict__ fidx,
+                              const uint32_t* __restrict__ leaf, const float* __restrict__ val,
+                              int64_t F, uint2* __restrict__ out) {
+  for (int64_t f = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; f < F;
+       f += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t a = lptr[f], b = lptr[f + 1];
+    uint2* o = out + a + f;
+    for (uint32_t i = a; i < b; ++i) *o++ = make_uint2(leaf[i], __float_as_uint(val[i]));
+    *o = make_uint2(fidx[f] | FB, 0u);
+  }
+}
+// SEND on the B position of each slice's last fiber
+__global__ void k_bpos_send(const uint32_t* __restrict__ fpos, const uint32_t* __restrict__ lptr,
+                            int64_t S, uint2* __restrict__ out) {
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < S;
+       s += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t f0 = fpos[s], f1 = fpos[s + 1];
+    if (f1 > f0) out[lptr[f1] + f1 - 1].x |= SEND;
+  }
+}
+
 // Kernel-native streams (built once per plan).
 __global__ void k_pairs(const uint32_t* __restrict__ k, const float* __restrict__ v, int64_t M,
                         uint2* __restrict__ out) {
@@ -810,8 +912,14 @@ struct hbk_plan {
   hbk_sched* sched = nullptr;
   hbk::Buf tasks, zero_rows, csf_send, ws;
   hbk::Buf csf_pairs, csl_pairs, coo_quads;
-  hbk::Work work{};
+  hbk::Work work{};      // fast kernels (light CSF tasks when the heavy layout is on)
+  hbk::Work work_gen{};  // generic kernel (every CSF slice in tree order)
+  hbk::Work work_heavy{};
+  hbk::Buf heavy_pairs, heavy_fj, heavy_tasks, gen_tasks;
+  int grid_heavy = 0;
   bool fast = false;
+  int csf_variant = 2;  // 0: smem-slot kernel, 1|2: B-position streams at 3|4 CTAs per SM (HBK_CSF_VARIANT)
+  bool bpos = false;
   int grid = 0, block = 256;
   int gen_grid = 0;
   int grids[3] = {0, 0, 0};
@@ -835,25 +943,321 @@ struct BucketTasks {
   int64_t slots = 0;
 };
 
+// posoff (optional): per-slice offset added to nonzero offsets to obtain
+// stream positions (B-position streams: the fibers before the slice).
 static BucketTasks bucket_tasks(const uint32_t* loff, const uint32_t* fpos, const uint32_t* lptr,
-                                int64_t S, uint32_t M, uint32_t T, cudaStream_t st) {
+                                int64_t S, uint32_t M, uint32_t T, cudaStream_t st,
+                                uint32_t H = 0xFFFFFFFFu, const uint32_t* posoff = nullptr) {
   BucketTasks bt;
+  (void)M;
   if (S == 0) return bt;
   Scratch cnt((S + 1) * sizeof(uint32_t), st), slot((S + 1) * sizeof(uint32_t), st);
-  k_task_count<<<grid_for(S, 256), 256, 0, st>>>(loff, S, T, cnt.as<uint32_t>(),
+  k_task_count<<<grid_for(S, 256), 256, 0, st>>>(loff, S, T, H, cnt.as<uint32_t>(),
                                                  slot.as<uint32_t>());
   check_launch("k_task_count");
   uint32_t n = exclusive_scan_total(cnt.as<uint32_t>(), S, st);
   uint32_t nslot = exclusive_scan_total(slot.as<uint32_t>(), S, st);
-  bt.tasks = Scratch(size_t(n) * sizeof(Task), st);
-  k_task_fill<<<grid_for(S, 128), 128, 0, st>>>(loff, fpos, lptr, S, T, cnt.as<uint32_t>(),
-                                                slot.as<uint32_t>(), bt.tasks.as<Task>());
-  check_launch("k_task_fill");
-  k_task_hi<<<grid_for(n, 256), 256, 0, st>>>(bt.tasks.as<Task>(), n, M);
-  check_launch("k_task_hi");
+  bt.tasks = Scratch(size_t(std::max<uint32_t>(n, 1)) * sizeof(Task), st);
+  if (n) {
+    k_task_fill<<<grid_for(S, 128), 128, 0, st>>>(loff, fpos, lptr, S, T, H, cnt.as<uint32_t>(),
+                                                  slot.as<uint32_t>(), posoff, bt.tasks.as<Task>());
+    check_launch("k_task_fill");
+    k_run_hi<<<grid_for(S, 256), 256, 0, st>>>(loff, S, T, H, cnt.as<uint32_t>(), posoff,
+                                               bt.tasks.as<Task>());
+    check_launch("k_run_hi");
+  }
   bt.n = n;
   bt.slots = nslot;
   return bt;
+}
+
+// ------------------------------------------------- heavy CSF slices --
+// Heavy slices (nnz > H) get a kernel-native layout in which the four 8-lane
+// groups of a warp walk fibers of equal length side by side.  Each fiber is
+// cut into segments of <= tau nonzeros; a slice's segments are sorted by
+// length (longest first, stable) and cut into warp tasks of ~W nonzeros; the
+// segments of a warp task are dealt round-robin to its four groups, and each
+// group's segments are laid out contiguously as a (leaf | FEND, value)
+// stream with its own list of fiber coordinates.  Lockstep groups then end
+// their fibers at the same batch positions, so the per-fiber work of the
+// kernel (B-row fetch, fiber-partial x B-row, reset) is shared by four
+// fibers instead of being paid once per fiber.  The four groups of a warp
+// task belong to one slice, so their partials are combined with shuffles
+// and handed over with a single vector atomic.  Reordering fibers within a
+// slice does not change any output row (a row is the sum over its slice's
+// fibers, kernels.py:173-184); only fp32 summation order differs.
+
+__global__ void k_fiber_slice(const uint32_t* __restrict__ fpos, int64_t S, int64_t F,
+                              uint32_t* __restrict__ fslice) {
+  for (int64_t f = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; f < F;
+       f += int64_t(gridDim.x) * blockDim.x) {
+    // last s with fpos[s] <= f
+    int64_t lo = 0, hi = S;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (fpos[mid] <= uint32_t(f)) lo = mid; else hi = mid;
+    }
+    fslice[f] = uint32_t(lo);
+  }
+}
+
+__global__ void k_seg_count(const uint32_t* __restrict__ fslice, const uint32_t* __restrict__ loff,
+                            const uint32_t* __restrict__ lptr, int64_t F, uint32_t H, uint32_t tau,
+                            uint32_t* __restrict__ nseg) {
+  for (int64_t f = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; f < F;
+       f += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t s = fslice[f];
+    const uint32_t m = loff[s + 1] - loff[s];
+    const uint32_t len = lptr[f + 1] - lptr[f];
+    nseg[f] = m > H ? (len + tau - 1) / tau : 0u;
+  }
+}
+
+__global__ void k_seg_emit(const uint32_t* __restrict__ fslice, const uint32_t* __restrict__ lptr,
+                           const uint32_t* __restrict__ fidx, const uint32_t* __restrict__ segoff,
+                           int64_t F, uint32_t tau, unsigned long long* __restrict__ key,
+                           uint32_t* __restrict__ val, uint32_t* __restrict__ soff,
+                           uint32_t* __restrict__ slen, uint32_t* __restrict__ sj,
+                           uint32_t* __restrict__ ss) {
+  for (int64_t f = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; f < F;
+       f += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t a = segoff[f], b = segoff[f + 1];
+    if (a == b) continue;
+    const uint32_t s = fslice[f], j = fidx[f];
+    uint32_t off = lptr[f];
+    const uint32_t end = lptr[f + 1];
+    for (uint32_t q = a; q < b; ++q, off += tau) {
+      const uint32_t len = min(tau, end - off);
+      key[q] = (static_cast<unsigned long long>(s) << 16) | (0xFFFFu - len);
+      val[q] = q;
+      soff[q] = off;
+      slen[q] = len;
+      sj[q] = j;
+      ss[q] = s;
+    }
+  }
+}
+
+// per sorted segment i: local warp-task index within its slice; the last
+// segment of a slice records the slice's task count
+__global__ void k_seg_task(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ slen,
+                           const uint32_t* __restrict__ ss, const uint32_t* __restrict__ P,
+                           const uint32_t* __restrict__ hoff, int64_t G, uint32_t W,
+                           uint32_t* __restrict__ tloc, uint32_t* __restrict__ ntask) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < G;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t s = ss[perm[i]];
+    const uint32_t t = (P[i] - hoff[s]) / W;
+    tloc[i] = t;
+    if (i + 1 == G || ss[perm[i + 1]] != s) ntask[s] = t + 1;
+  }
+}
+
+__global__ void k_seg_task_first(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ ss,
+                                 const uint32_t* __restrict__ tloc, const uint32_t* __restrict__ tbase,
+                                 int64_t G, uint32_t* __restrict__ tfirst,
+                                 uint32_t* __restrict__ tslice) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < G;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t s = ss[perm[i]];
+    const bool first = i == 0 || ss[perm[i - 1]] != s || tloc[i - 1] != tloc[i];
+    if (first) {
+      const uint32_t w = tbase[s] + tloc[i];
+      tfirst[w] = uint32_t(i);
+      tslice[w] = s;
+    }
+  }
+}
+
+// per group task (w, g): segment count and nonzero count
+__global__ void k_group_sizes(const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ perm,
+                              const uint32_t* __restrict__ slen, int64_t NW, uint32_t G,
+                              uint32_t extra, uint32_t* __restrict__ gnnz,
+                              uint32_t* __restrict__ gseg) {
+  for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < NW * 4;
+       x += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t w = x >> 2;
+    const uint32_t g = uint32_t(x & 3);
+    const uint32_t a = tfirst[w], b = (w + 1 < NW) ? tfirst[w + 1] : G;
+    uint32_t n = 0, c = 0;
+    for (uint32_t i = a + g; i < b; i += 4) {
+      n += slen[perm[i]] + extra;
+      ++c;
+    }
+    gnnz[x] = n;
+    gseg[x] = c;
+  }
+}
+
+// copy each group's segments into its contiguous stream, FEND on segment ends
+__global__ void k_group_fill(const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ perm,
+                             const uint32_t* __restrict__ soff, const uint32_t* __restrict__ slen,
+                             const uint32_t* __restrict__ sj, const uint32_t* __restrict__ gofs,
+                             const uint32_t* __restrict__ fofs, int64_t NW, uint32_t G,
+                             const uint32_t* __restrict__ leaf, const float* __restrict__ val,
+                             bool bpos, uint2* __restrict__ pairs, uint32_t* __restrict__ fj) {
+  for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < NW * 4;
+       x += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t w = x >> 2;
+    const uint32_t g = uint32_t(x & 3);
+    const uint32_t a = tfirst[w], b = (w + 1 < NW) ? tfirst[w + 1] : G;
+    uint32_t dst = gofs[x], fpos = fofs[x];
+    for (uint32_t i = a + g; i < b; i += 4) {
+      const uint32_t q = perm[i];
+      const uint32_t off = soff[q], len = slen[q];
+      for (uint32_t t = 0; t < len; ++t)
+        pairs[dst + t] = make_uint2(leaf[off + t] | (!bpos && t + 1 == len ? FEND : 0u),
+                                    __float_as_uint(val[off + t]));
+      dst += len;
+      if (bpos) pairs[dst++] = make_uint2(sj[q] | FB, 0u);
+      fj[fpos++] = sj[q];
+    }
+  }
+}
+
+__global__ void k_group_tasks(const uint32_t* __restrict__ tslice, const uint32_t* __restrict__ gofs,
+                              const uint32_t* __restrict__ gnnz, const uint32_t* __restrict__ fofs,
+                              const uint32_t* __restrict__ hrank, const uint32_t* __restrict__ nchunk,
+                              int64_t NW, uint32_t slot_base, Task* __restrict__ tasks) {
+  for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < NW * 4;
+       x += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t s = tslice[x >> 2];
+    Task t{};
+    t.lo = gofs[x];
+    t.hi = gofs[x] + gnnz[x];
+    t.s = s;
+    t.f = fofs[x];
+    t.slot = slot_base + hrank[s];
+    t.nchunk = nchunk[s];
+    tasks[x] = t;
+  }
+}
+
+__global__ void k_slice_nchunk(const uint32_t* __restrict__ tslice, const uint32_t* __restrict__ gseg,
+                               int64_t NW, uint32_t* __restrict__ nchunk) {
+  for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < NW;
+       w += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t n = 0;
+    for (int g = 0; g < 4; ++g) n += gseg[4 * w + g] != 0;
+    atomicAdd(nchunk + tslice[w], n);
+  }
+}
+
+__global__ void k_heavy_flags(const uint32_t* __restrict__ loff, int64_t S, uint32_t H,
+                              uint32_t* __restrict__ hflag, uint32_t* __restrict__ hnnz) {
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < S;
+       s += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t m = loff[s + 1] - loff[s];
+    hflag[s] = m > H;
+    hnnz[s] = m > H ? m : 0u;
+  }
+}
+
+__global__ void k_gather_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ perm,
+                             int64_t n, uint32_t* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = src[perm[i]];
+}
+
+struct HeavyLayout {
+  Buf pairs, fj, tasks;
+  int64_t ntasks = 0;  // group tasks (4 per warp task)
+  int64_t slots = 0;   // heavy slices (one accumulator slot each)
+  int64_t segments = 0;
+};
+
+// Builds the heavy-slice layout of a 3rd-order CSF bucket (see above).
+static HeavyLayout heavy_layout(const hbk_csf* c, const uint32_t* loff, const uint32_t* fpos,
+                                uint32_t H, uint32_t tau, uint32_t W, uint32_t slot_base, bool bpos,
+                                cudaStream_t st) {
+  HeavyLayout hl;
+  const int64_t S = c->n[0], F = c->n[1];
+  const uint32_t* lptr = c->ptr[1].as<uint32_t>();
+  const uint32_t* fidx = c->idx[1].as<uint32_t>();
+  Scratch hflag((S + 1) * 4, st), hoff((S + 1) * 4, st);
+  k_heavy_flags<<<grid_for(S, 256), 256, 0, st>>>(loff, S, H, hflag.as<uint32_t>(), hoff.as<uint32_t>());
+  check_launch("k_heavy_flags");
+  const uint32_t nheavy = exclusive_scan_total(hflag.as<uint32_t>(), S, st);  // -> heavy rank
+  if (nheavy == 0) return hl;
+  exclusive_scan_total(hoff.as<uint32_t>(), S, st);
+  Scratch fslice((F + 1) * 4, st), segoff((F + 1) * 4, st);
+  k_fiber_slice<<<grid_for(F, 256), 256, 0, st>>>(fpos, S, F, fslice.as<uint32_t>());
+  check_launch("k_fiber_slice");
+  k_seg_count<<<grid_for(F, 256), 256, 0, st>>>(fslice.as<uint32_t>(), loff, lptr, F, H, tau,
+                                                segoff.as<uint32_t>());
+  check_launch("k_seg_count");
+  const uint32_t G = exclusive_scan_total(segoff.as<uint32_t>(), F, st);
+  hl.segments = G;
+  Scratch key_a(size_t(G) * 8, st), key_b(size_t(G) * 8, st), val_a(size_t(G) * 4, st),
+      val_b(size_t(G) * 4, st);
+  Scratch soff(size_t(G) * 4, st), slen(size_t(G) * 4, st), sj(size_t(G) * 4, st),
+      ss(size_t(G) * 4, st);
+  k_seg_emit<<<grid_for(F, 256), 256, 0, st>>>(
+      fslice.as<uint32_t>(), lptr, fidx, segoff.as<uint32_t>(), F, tau,
+      key_a.as<unsigned long long>(), val_a.as<uint32_t>(), soff.as<uint32_t>(),
+      slen.as<uint32_t>(), sj.as<uint32_t>(), ss.as<uint32_t>());
+  check_launch("k_seg_emit");
+  int sbits = 1;
+  while ((int64_t(1) << sbits) < S) ++sbits;
+  cub::DoubleBuffer<unsigned long long> kb(key_a.as<unsigned long long>(),
+                                           key_b.as<unsigned long long>());
+  cub::DoubleBuffer<uint32_t> vb(val_a.as<uint32_t>(), val_b.as<uint32_t>());
+  size_t tmp = 0;
+  HBK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, int(G), 0, 16 + sbits, st));
+  {
+    Scratch t(tmp, st);
+    HBK_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, kb, vb, int(G), 0, 16 + sbits, st));
+  }
+  const uint32_t* perm = vb.Current();
+  // nonzero prefix of the sorted segments -> local warp task of each segment
+  Scratch P((size_t(G) + 1) * 4, st), tloc(size_t(G) * 4, st), ntask((S + 1) * 4, st);
+  k_gather_u32<<<grid_for(G, 256), 256, 0, st>>>(slen.as<uint32_t>(), perm, G, P.as<uint32_t>());
+  check_launch("k_gather_u32");
+  exclusive_scan_total(P.as<uint32_t>(), G, st);
+  HBK_CUDA(cudaMemsetAsync(ntask.p, 0, (S + 1) * 4, st));
+  k_seg_task<<<grid_for(G, 256), 256, 0, st>>>(perm, slen.as<uint32_t>(), ss.as<uint32_t>(),
+                                               P.as<uint32_t>(), hoff.as<uint32_t>(), G, W,
+                                               tloc.as<uint32_t>(), ntask.as<uint32_t>());
+  check_launch("k_seg_task");
+  const uint32_t NW = exclusive_scan_total(ntask.as<uint32_t>(), S, st);  // -> task base
+  Scratch tfirst(size_t(NW) * 4, st), tslice(size_t(NW) * 4, st);
+  k_seg_task_first<<<grid_for(G, 256), 256, 0, st>>>(perm, ss.as<uint32_t>(), tloc.as<uint32_t>(),
+                                                     ntask.as<uint32_t>(), G,
+                                                     tfirst.as<uint32_t>(), tslice.as<uint32_t>());
+  check_launch("k_seg_task_first");
+  const int64_t NG = int64_t(NW) * 4;
+  Scratch gofs((NG + 1) * 4, st), gnnz(NG * 4, st), fofs((NG + 1) * 4, st);
+  k_group_sizes<<<grid_for(NG, 256), 256, 0, st>>>(tfirst.as<uint32_t>(), perm,
+                                                   slen.as<uint32_t>(), NW, G, bpos ? 1u : 0u,
+                                                   gofs.as<uint32_t>(), fofs.as<uint32_t>());
+  check_launch("k_group_sizes");
+  HBK_CUDA(cudaMemcpyAsync(gnnz.p, gofs.p, NG * 4, cudaMemcpyDeviceToDevice, st));
+  Scratch gseg(NG * 4, st), nchunk((S + 1) * 4, st);
+  HBK_CUDA(cudaMemcpyAsync(gseg.p, fofs.p, NG * 4, cudaMemcpyDeviceToDevice, st));
+  const uint32_t Mh = exclusive_scan_total(gofs.as<uint32_t>(), NG, st);
+  exclusive_scan_total(fofs.as<uint32_t>(), NG, st);
+  HBK_CUDA(cudaMemsetAsync(nchunk.p, 0, (S + 1) * 4, st));
+  k_slice_nchunk<<<grid_for(NW, 256), 256, 0, st>>>(tslice.as<uint32_t>(), gseg.as<uint32_t>(), NW,
+                                                    nchunk.as<uint32_t>());
+  check_launch("k_slice_nchunk");
+  hl.pairs = dalloc(size_t(std::max<uint32_t>(Mh, 1)) * sizeof(uint2), st);
+  hl.fj = dalloc(size_t(std::max<uint32_t>(G, 1)) * 4, st);
+  hl.tasks = dalloc(size_t(NG) * sizeof(Task), st);
+  k_group_fill<<<grid_for(NG, 128), 128, 0, st>>>(
+      tfirst.as<uint32_t>(), perm, soff.as<uint32_t>(), slen.as<uint32_t>(), sj.as<uint32_t>(),
+      gofs.as<uint32_t>(), fofs.as<uint32_t>(), NW, G, c->leaf.as<uint32_t>(), c->v32.as<float>(),
+      bpos, hl.pairs.as<uint2>(), hl.fj.as<uint32_t>());
+  check_launch("k_group_fill");
+  k_group_tasks<<<grid_for(NG, 256), 256, 0, st>>>(tslice.as<uint32_t>(), gofs.as<uint32_t>(),
+                                                   gnnz.as<uint32_t>(), fofs.as<uint32_t>(),
+                                                   hflag.as<uint32_t>(), nchunk.as<uint32_t>(), NW,
+                                                   slot_base, hl.tasks.as<Task>());
+  check_launch("k_group_tasks");
+  hl.ntasks = NG;
+  hl.slots = nheavy;
+  HBK_CUDA(cudaStreamSynchronize(st));
+  return hl;
 }
 
 __global__ void k_shift_slots(Task* __restrict__ t, int64_t n, uint32_t base) {
@@ -872,13 +1276,26 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   const int gpw = p->fast ? 4 : 1;  // task ranges padded so a warp never straddles kinds
   uint32_t task_nnz = TASK_NNZ_CSF;
   if (const char* e = getenv("HBK_TASK_NNZ")) task_nnz = std::max(8, atoi(e));
+  if (const char* e = getenv("HBK_CSF_VARIANT")) p->csf_variant = atoi(e);
   const uint32_t Tcsf = p->fast ? task_nnz : GEN_TASK_NNZ;
   const uint32_t Tcsl = p->fast ? TASK_NNZ_CSL : GEN_TASK_NNZ;
   const uint32_t Tcoo = p->fast ? TASK_NNZ_COO : GEN_TASK_NNZ;
 
   Work& w = p->work;
   std::memset(&w, 0, sizeof(w));
-  BucketTasks tcsf, tcsl;
+  BucketTasks tcsf, tcsl, tcsf_light;
+  // heavy-slice layout (fast path): slices with more than H nonzeros
+  // B-position streams (default fast CSF path): every slice with more than
+  // Tcsf nonzeros goes to the heavy layout, lighter slices form runs
+  p->bpos = p->fast && !p->sched && p->csf_variant >= 1;
+  uint32_t heavy_H = p->bpos ? Tcsf : 4 * Tcsf, heavy_tau = 32, heavy_W = 2048;
+  if (const char* e = getenv("HBK_HEAVY_H")) heavy_H = uint32_t(std::max(0, atoi(e)));
+  if (const char* e = getenv("HBK_HEAVY_TAU")) heavy_tau = uint32_t(std::min(65535, std::max(1, atoi(e))));
+  if (const char* e = getenv("HBK_HEAVY_W")) heavy_W = uint32_t(std::max(1, atoi(e)));
+  heavy_W = std::max(heavy_W, heavy_tau);
+  if (p->bpos) heavy_H = Tcsf;
+  const bool heavy_on = p->fast && !p->sched && heavy_H > 0 && heavy_H >= Tcsf;
+  int64_t heavy_ntasks = 0, heavy_segments = 0;
   int64_t n_coo = 0, n_zero = 0;
   int64_t slots = 0;
   int64_t stream_bytes = 0;
@@ -952,6 +1369,21 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     } else {
       tcsf = bucket_tasks(p->csf_send.as<uint32_t>(), fpos.as<uint32_t>(),
                           c->ptr[L].as<uint32_t>(), S, uint32_t(c->M), Tcsf, st);
+      if (heavy_on) {
+        tcsf_light = bucket_tasks(p->csf_send.as<uint32_t>(), fpos.as<uint32_t>(),
+                                  c->ptr[L].as<uint32_t>(), S, uint32_t(c->M), Tcsf, st, heavy_H,
+                                  p->bpos ? fpos.as<uint32_t>() : nullptr);
+        HeavyLayout hl = heavy_layout(c, p->csf_send.as<uint32_t>(), fpos.as<uint32_t>(), heavy_H,
+                                      heavy_tau, heavy_W, uint32_t(tcsf_light.slots), p->bpos, st);
+        HBK_REQUIRE(tcsf_light.slots + hl.slots == tcsf.slots, HBK_ECUDA,
+                    "heavy layout slot accounting mismatch");
+        p->heavy_pairs = hl.pairs;
+        p->heavy_fj = hl.fj;
+        p->heavy_tasks = hl.tasks;
+        heavy_ntasks = hl.ntasks;
+        heavy_segments = hl.segments;
+        p->info.tasks_heavy = hl.ntasks;
+      }
       // OpCount of mttkrp_csf (kernels.py:173-185)
       int64_t m = c->M, a = c->M;
       for (int d = N - 2; d >= 1; --d) {
@@ -971,7 +1403,19 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     w.csf_val = c->v32.as<float>();
     w.csf_F = uint32_t(c->n[L]);
     w.csf_S = uint32_t(S);
-    if (p->fast) {
+    if (p->bpos) {
+      const int64_t P = c->M + c->n[L];
+      p->csf_pairs = dalloc(P * sizeof(uint2), st);
+      uint2* pp = p->csf_pairs.as<uint2>();
+      k_bpos_stream<<<grid_for(c->n[L], 128), 128, 0, st>>>(
+          c->ptr[L].as<uint32_t>(), c->idx[L].as<uint32_t>(), c->leaf.as<uint32_t>(),
+          c->v32.as<float>(), c->n[L], pp);
+      check_launch("k_bpos_stream");
+      k_bpos_send<<<grid_for(S, 256), 256, 0, st>>>(fpos.as<uint32_t>(), c->ptr[L].as<uint32_t>(),
+                                                    S, pp);
+      check_launch("k_bpos_send");
+      w.csf_pairs = pp;
+    } else if (p->fast) {
       p->csf_pairs = dalloc(c->M * sizeof(uint2), st);
       uint2* pp = p->csf_pairs.as<uint2>();
       k_pairs<<<grid_for(c->M, 256), 256, 0, st>>>(c->leaf.as<uint32_t>(), c->v32.as<float>(),
@@ -1069,37 +1513,44 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     w.zero_rows = p->zero_rows.as<uint32_t>();
     p->info.tasks_zero = n_zero;
     // assemble [CSF | CSL | COO | ZERO], each padded to a multiple of gpw
-    const int64_t a0 = pad_to(tcsf.n, gpw), a1 = pad_to(tcsl.n, gpw), a2 = pad_to(n_coo, gpw),
-                  a3 = pad_to(n_zero, gpw);
-    const int64_t total = a0 + a1 + a2 + a3;
-    p->tasks = dalloc(std::max<int64_t>(total, 1) * sizeof(Task), st);
-    Task* T = p->tasks.as<Task>();
-    if (total) {
-      k_empty_tasks<<<grid_for(total, 256), 256, 0, st>>>(T, total);
-      check_launch("k_empty_tasks");
+    auto assemble = [&](const BucketTasks& tc, Buf& store, Work& wo) {
+      const int64_t a0 = pad_to(tc.n, gpw), a1 = pad_to(tcsl.n, gpw), a2 = pad_to(n_coo, gpw),
+                    a3 = pad_to(n_zero, gpw);
+      const int64_t total = a0 + a1 + a2 + a3;
+      store = dalloc(std::max<int64_t>(total, 1) * sizeof(Task), st);
+      Task* T = store.as<Task>();
+      if (total) {
+        k_empty_tasks<<<grid_for(total, 256), 256, 0, st>>>(T, total);
+        check_launch("k_empty_tasks");
+      }
+      if (tc.n)
+        HBK_CUDA(cudaMemcpyAsync(T, tc.tasks.p, tc.n * sizeof(Task), cudaMemcpyDeviceToDevice, st));
+      if (tcsl.n)
+        HBK_CUDA(cudaMemcpyAsync(T + a0, tcsl.tasks.p, tcsl.n * sizeof(Task),
+                                 cudaMemcpyDeviceToDevice, st));
+      if (n_coo) {
+        k_range_tasks<<<grid_for(n_coo, 256), 256, 0, st>>>(T + a0 + a1, n_coo,
+                                                            uint32_t(p->coo->nnz), Tcoo);
+        check_launch("k_range_tasks");
+      }
+      if (n_zero) {
+        k_range_tasks<<<grid_for(n_zero, 256), 256, 0, st>>>(T + a0 + a1 + a2, n_zero, Z,
+                                                             TASK_ROWS_ZERO);
+        check_launch("k_range_tasks");
+      }
+      wo.n0 = uint32_t(a0);
+      wo.n1 = uint32_t(a0 + a1);
+      wo.n2 = uint32_t(a0 + a1 + a2);
+      wo.n3 = uint32_t(total);
+      wo.tasks = T;
+    };
+    if (heavy_on) {
+      assemble(tcsf_light, p->tasks, w);
+      assemble(tcsf, p->gen_tasks, p->work_gen);
+    } else {
+      assemble(tcsf, p->tasks, w);
     }
-    if (tcsf.n)
-      HBK_CUDA(cudaMemcpyAsync(T, tcsf.tasks.p, tcsf.n * sizeof(Task), cudaMemcpyDeviceToDevice,
-                               st));
-    if (tcsl.n)
-      HBK_CUDA(cudaMemcpyAsync(T + a0, tcsl.tasks.p, tcsl.n * sizeof(Task),
-                               cudaMemcpyDeviceToDevice, st));
-    if (n_coo) {
-      k_range_tasks<<<grid_for(n_coo, 256), 256, 0, st>>>(T + a0 + a1, n_coo,
-                                                          uint32_t(p->coo->nnz), Tcoo);
-      check_launch("k_range_tasks");
-    }
-    if (n_zero) {
-      k_range_tasks<<<grid_for(n_zero, 256), 256, 0, st>>>(T + a0 + a1 + a2, n_zero, Z,
-                                                           TASK_ROWS_ZERO);
-      check_launch("k_range_tasks");
-    }
-    w.n0 = uint32_t(a0);
-    w.n1 = uint32_t(a0 + a1);
-    w.n2 = uint32_t(a0 + a1 + a2);
-    w.n3 = uint32_t(total);
-    w.tasks = T;
-    p->info.tasks_csf = tcsf.n;
+    p->info.tasks_csf = heavy_on ? tcsf_light.n : tcsf.n;
     p->info.tasks_csl = tcsl.n;
     p->info.tasks_coo = n_coo;
   }
@@ -1112,6 +1563,18 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   w.ws_ctr = reinterpret_cast<uint32_t*>(p->ws.as<char>());
   w.ws_cnt = reinterpret_cast<uint32_t*>(p->ws.as<char>() + cnt_off);
   w.ws_acc = reinterpret_cast<float*>(p->ws.as<char>() + acc_off);
+  if (!heavy_on) {
+    p->work_gen = w;
+  } else {
+    Work& wg = p->work_gen;
+    const Work keep = wg;
+    wg = w;
+    wg.n0 = keep.n0;
+    wg.n1 = keep.n1;
+    wg.n2 = keep.n2;
+    wg.n3 = keep.n3;
+    wg.tasks = keep.tasks;
+  }
 
   // persistent grid: as many CTAs as fit, a multiple of the SM count
   int dev = 0, sms = 0, per_sm = 0;
@@ -1130,8 +1593,11 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     const int64_t ntk[3] = {int64_t(w.n0), int64_t(w.n1) - w.n0, int64_t(w.n3) - w.n1};
     for (int k = 0; k < 3; ++k) {
       if (k == 0)
-        HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp3_r32<KIND_CSF>,
-                                                               p->block, 0));
+        HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm,
+            p->bpos ? (p->csf_variant == 2 ? k_mttkrp3_r32<KIND_CSF_BPOS4> : k_mttkrp3_r32<KIND_CSF_BPOS>)
+                  : k_mttkrp3_r32<KIND_CSF>,
+            p->block, 0));
       if (k == 1)
         HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp3_r32<KIND_CSL>,
                                                                p->block, 0));
@@ -1141,6 +1607,24 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       p->grids[k] = ntk[k] > 0 ? grid_for_tasks(ntk[k], per_sm, 4) : 0;
       w.total_warps[k] = uint32_t(p->grids[k]) * (p->block / 32);
       launches += ntk[k] > 0;
+    }
+    if (heavy_ntasks) {
+      Work& wh = p->work_heavy;
+      wh = w;
+      wh.n0 = uint32_t(heavy_ntasks);
+      wh.n1 = wh.n2 = wh.n3 = wh.n0;
+      wh.tasks = p->heavy_tasks.as<Task>();
+      wh.csf_pairs = p->heavy_pairs.as<uint2>();
+      wh.csf_fidx = p->heavy_fj.as<uint32_t>();
+      wh.csf_F = uint32_t(heavy_segments);
+      HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm,
+          p->bpos ? (p->csf_variant == 2 ? k_mttkrp3_r32<KIND_CSF_BPOS4> : k_mttkrp3_r32<KIND_CSF_BPOS>)
+                  : k_mttkrp3_r32<KIND_CSF>,
+          p->block, 0));
+      p->grid_heavy = grid_for_tasks(heavy_ntasks, per_sm, 4);
+      wh.total_warps[0] = uint32_t(p->grid_heavy) * (p->block / 32);
+      launches += 1;
     }
     // a plan with no task at all still launches once (nothing to write, but
     // keeps launch accounting uniform)
@@ -1157,7 +1641,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   {
     int per_gen = 0;
     HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_gen, k_mttkrp_generic<double>, 256, 0));
-    p->gen_grid = grid_for_tasks(w.n3, per_gen, 1);
+    p->gen_grid = grid_for_tasks(p->work_gen.n3, per_gen, 1);
   }
 
   p->info.mode = p->mode;
@@ -1217,7 +1701,7 @@ static void launch_generic(const hbk_plan* p, const T* const* factors, T* out, c
   }
   wn.acc = reinterpret_cast<T*>(p->work.ws_acc);
   wn.out = out;
-  Work w = p->work;
+  Work w = p->work_gen;
   w.total_warps[0] = uint32_t(p->gen_grid) * (p->block / 32);
   // the generic kernel pulls single tasks; reuse the fp32 generic counter slot
   k_mttkrp_generic<T><<<p->gen_grid, 256, 0, st>>>(w, wn);
@@ -1305,7 +1789,22 @@ int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out,
                           16 ==
                       0,
                   HBK_EINVAL, "factor and output buffers must be 16-byte aligned");
-      if (p->grids[0]) k_mttkrp3_r32<KIND_CSF><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
+      if (p->grids[0]) {
+        if (p->bpos && p->csf_variant == 2)
+          k_mttkrp3_r32<KIND_CSF_BPOS4><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
+        else if (p->bpos)
+          k_mttkrp3_r32<KIND_CSF_BPOS><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
+        else
+          k_mttkrp3_r32<KIND_CSF><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
+      }
+      if (p->grid_heavy) {
+        if (p->bpos && p->csf_variant == 2)
+          k_mttkrp3_r32<KIND_CSF_BPOS4><<<p->grid_heavy, p->block, 0, st>>>(p->work_heavy, fx);
+        else if (p->bpos)
+          k_mttkrp3_r32<KIND_CSF_BPOS><<<p->grid_heavy, p->block, 0, st>>>(p->work_heavy, fx);
+        else
+          k_mttkrp3_r32<KIND_CSF><<<p->grid_heavy, p->block, 0, st>>>(p->work_heavy, fx);
+      }
       if (p->grids[1]) k_mttkrp3_r32<KIND_CSL><<<p->grids[1], p->block, 0, st>>>(p->work, fx);
       if (p->grids[2]) k_mttkrp3_r32<KIND_COO><<<p->grids[2], p->block, 0, st>>>(p->work, fx);
       check_launch("k_mttkrp3_r32");

@@ -72,30 +72,155 @@ def _check_factors(dims: tuple[int, ...], factors: Factors, mode: int, check_fin
             rank = int(shape[1])
         elif shape[1] != rank:
             raise ValueError("factor matrices disagree on rank")
-        if check_finite and not finite():
+        # host arrays under "staged": checked while they are converted into
+        # the pinned upload buffers (_HostStage.upload), before any kernel runs
+        if check_finite and not (check_finite == "staged" and not _is_device(f)) and not finite():
             raise ValueError(f"factor {d} has non-finite entries")
     assert rank is not None
     return rank
 
 
+class _HostStage:
+    """Upload/download path of the host-array calling convention (the
+    reference's: NumPy float64 factors in, NumPy float64 rows out).
+
+    Each factor is converted to the kernel's dtype *while* being copied into a
+    page-locked staging buffer; the factors of one call (and chunks of large
+    factors) are converted concurrently on a host thread pool (NumPy releases
+    the GIL in these loops), and each factor's host-to-device copy is issued
+    asynchronously as soon as it is staged.  The finiteness check of
+    kernels.py:82-86 runs on the converted data (half the bytes) and falls
+    back to the exact check of the source only when that fails.  The result
+    comes back through one async device-to-host copy into a pinned buffer,
+    widened to float64 on the host."""
+
+    CHUNK_BYTES = 8 << 20  # conversion work unit (bytes of the source factor)
+
+    def __init__(self):
+        import os
+        import threading
+        from concurrent.futures import ThreadPoolExecutor
+
+        self.lock = threading.Lock()
+        self.workers = max(1, min(8, (os.cpu_count() or 1)))
+        self.pool = ThreadPoolExecutor(self.workers, thread_name_prefix="hbk-stage")
+        self.bufs = {}
+
+    def _pinned(self, torch, key, n, dtype):
+        buf, ev = self.bufs.get(key, (None, None))
+        if buf is None or buf.numel() < n or buf.dtype != dtype:
+            buf, ev = torch.empty(max(n, 1), dtype=dtype, pin_memory=True), None
+        if ev is not None:
+            ev.synchronize()  # the previous copy out of this buffer is done
+        return buf
+
+    def _spans(self, rows, width, itemsize):
+        step = max(1, self.CHUNK_BYTES // max(1, width * itemsize))
+        return [(a, min(rows, a + step)) for a in range(0, rows, step)]
+
+    def _map(self, fn, spans):
+        if len(spans) == 1:
+            return [fn(*spans[0])]
+        return [fu.result() for fu in [self.pool.submit(fn, a, b) for a, b in spans]]
+
+    def upload_all(self, torch, items, dt):
+        """items: [(d, host array)] -> {d: CUDA tensor}.  The factors are
+        converted concurrently (one pool task per factor, or per chunk of a
+        large one); the host-to-device copies are issued by the calling
+        thread, on its current stream, as soon as each factor is staged."""
+        srcs = {}
+        for d, f in items:
+            src = np.ascontiguousarray(f)
+            if src.ndim != 2:
+                raise ValueError(f"factor {d} must be a 2-D array")
+            srcs[d] = src
+        out = {}
+        with self.lock:
+            stages, jobs = {}, []
+            for d, src in srcs.items():
+                rows, width = src.shape
+                buf = self._pinned(torch, ("in", d), rows * width, dt)
+                stages[d] = (buf, buf.numpy()[: rows * width].reshape(rows, width))
+                for a, b in self._spans(rows, width, src.itemsize):
+                    jobs.append((d, a, b))
+
+            def convert(d, a, b):
+                src, stage = srcs[d], stages[d][1]
+                np.copyto(stage[a:b], src[a:b], casting="unsafe")
+                return bool(np.isfinite(stage[a:b]).all()) or bool(np.isfinite(src[a:b]).all())
+
+            if len(jobs) == 1:
+                futs = [None]
+                results = [convert(*jobs[0])]
+            else:
+                futs = [self.pool.submit(convert, *j) for j in jobs]
+                results = None
+            left = {d: sum(1 for j in jobs if j[0] == d) for d in srcs}
+            bad = None
+            for i, (d, a, b) in enumerate(jobs):
+                ok = results[i] if results is not None else futs[i].result()
+                if not ok and bad is None:
+                    bad = d
+                left[d] -= 1
+                if left[d] == 0 and bad is None:
+                    rows, width = srcs[d].shape
+                    dev = torch.empty((rows, width), dtype=dt, device="cuda")
+                    if rows * width:
+                        dev.copy_(stages[d][0][: rows * width].view(rows, width), non_blocking=True)
+                    out[d] = dev
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream())
+            for d in srcs:
+                self.bufs[("in", d)] = (stages[d][0], ev)
+            if bad is not None:
+                raise ValueError(f"factor {bad} has non-finite entries")
+        return out
+
+    def download(self, torch, y):
+        out = np.empty(tuple(y.shape), dtype=np.float64)
+        if y.numel() == 0:
+            return out
+        rows = int(y.shape[0])
+        width = y.numel() // max(1, rows)
+        with self.lock:
+            buf = self._pinned(torch, ("out",), y.numel(), y.dtype)
+            buf[: y.numel()].view(y.shape).copy_(y, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            src = buf.numpy()[: y.numel()].reshape(rows, width)
+            dst = out.reshape(rows, width)
+            self._map(lambda a, b: np.copyto(dst[a:b], src[a:b]), self._spans(rows, width, 8))
+            self.bufs[("out",)] = (buf, None)
+        return out
+
+
+_stage = None
+
+
+def _host_stage() -> _HostStage:
+    global _stage
+    if _stage is None:
+        _stage = _HostStage()
+    return _stage
+
+
 def _device_factors(factors: Factors, mode: int, precision: str = "fp32"):
     """Contiguous CUDA copies/views (fp32, or fp64 for precision="fp64") of the
-    non-mode factors + the pointer array."""
+    non-mode factors + the pointer array.  Host arrays go through the pinned
+    staging path (and are checked for non-finite entries there)."""
     torch = N.require_device()
     dt = torch.float64 if precision == "fp64" else torch.float32
-    npdt = np.float64 if precision == "fp64" else np.float32
     keep = []
     ptrs = (C.c_void_p * len(factors))()
-    on_device = True
+    host = [(d, f) for d, f in enumerate(factors) if d != mode and not _is_device(f)]
+    staged = _host_stage().upload_all(torch, host, dt) if host else {}
+    on_device = not host
     for d, f in enumerate(factors):
         if d == mode:
             ptrs[d] = None
             continue
-        if _is_device(f):
+        t = staged.get(d)
+        if t is None:
             t = f if (f.dtype == dt and f.is_contiguous()) else f.to(dt).contiguous()
-        else:
-            on_device = False
-            t = torch.from_numpy(np.ascontiguousarray(f, dtype=npdt)).cuda(non_blocking=False)
         if t.data_ptr() % 16:
             t = t.clone()
         keep.append(t)
@@ -152,7 +277,7 @@ def _finish(plan: _Plan, factors, mode: int, out=None, precision: str = "fp32"):
     y = plan.execute(ptrs, out, precision)
     if on_device:
         return y, plan.opcount
-    return y.double().cpu().numpy(), plan.opcount
+    return _host_stage().download(N.require_device(), y), plan.opcount
 
 
 def plan_for(rep, mode: int, rank: int, schedule=None) -> _Plan:
@@ -186,7 +311,7 @@ def mttkrp_coo(t: CooTensor, factors: Factors, mode: int, threads: int = 1, *, p
     The entries are grouped by their mode-``mode`` coordinate on the GPU
     (sorted under (mode, *rest) unless already mode-major) and reduced per
     output row; ``threads`` is accepted for API compatibility."""
-    r = _check_factors(t.dims, factors, mode)
+    r = _check_factors(t.dims, factors, mode, check_finite="staged")
     return _finish(plan_for(t, mode, r), factors, mode, precision=precision)
 
 
@@ -194,7 +319,7 @@ def mttkrp_csf(c: CsfTensor, factors: Factors, mode: int, *, precision: str = "f
     """MTTKRP over a CSF tree built with mode_order[0] == mode (kernels.py:154-186)."""
     if c.mode_order[0] != mode:
         raise ValueError(f"tree was built for mode {c.mode_order[0]}, asked for mode {mode}")
-    r = _check_factors(c.dims, factors, mode)
+    r = _check_factors(c.dims, factors, mode, check_finite="staged")
     return _finish(plan_for(c, mode, r), factors, mode, precision=precision)
 
 
@@ -203,7 +328,7 @@ def mttkrp_csl(s: CslSlices, factors: Factors, mode: int, threads: int = 1, *,
     """MTTKRP over compressed slices (kernels.py:189-226)."""
     if s.mode_order[0] != mode:
         raise ValueError(f"slices were built for mode {s.mode_order[0]}, asked for mode {mode}")
-    r = _check_factors(s.dims, factors, mode)
+    r = _check_factors(s.dims, factors, mode, check_finite="staged")
     return _finish(plan_for(s, mode, r), factors, mode, precision=precision)
 
 
@@ -215,7 +340,7 @@ def mttkrp_hbcsf(h: HbCsfTensor, factors: Factors, mode: int, schedule=None, thr
         raise ValueError(f"hybrid was built for mode {h.mode_order[0]}, asked for mode {mode}")
     if schedule is not None:
         schedule.validate_for(h.csf_part)
-    r = _check_factors(h.dims, factors, mode)
+    r = _check_factors(h.dims, factors, mode, check_finite="staged")
     return _finish(plan_for(h, mode, r, schedule), factors, mode, precision=precision)
 
 
@@ -226,7 +351,7 @@ def mttkrp_scheduled(c: CsfTensor, schedule, factors: Factors, mode: int, thread
     if c.mode_order[0] != mode:
         raise ValueError(f"tree was built for mode {c.mode_order[0]}, asked for mode {mode}")
     schedule.validate_for(c)
-    r = _check_factors(c.dims, factors, mode)
+    r = _check_factors(c.dims, factors, mode, check_finite="staged")
     return _finish(plan_for(c, mode, r, schedule), factors, mode, precision=precision)
 
 

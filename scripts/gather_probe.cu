@@ -15,6 +15,7 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <algorithm>
 #include <random>
 #include <vector>
 
@@ -117,6 +118,42 @@ __global__ void k_ldg64(const float2* __restrict__ F, const uint32_t* __restrict
       }
 #pragma unroll
       for (int j = 0; j < U; ++j) { acc.x += r[j].x; acc.y += r[j].y; }
+    }
+  }
+  out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = acc;
+}
+
+// hot-row cache: rows [0, H) of F staged in shared memory once per CTA
+// (the synthetic power-law streams are hottest at low indices); a row is read
+// with LDS.128 when k < H, else LDG.128.  8 lanes x float4 per row.
+template <int U, bool ALL>
+__global__ void k_hot(const float4* __restrict__ F, const uint32_t* __restrict__ idx, int64_t n,
+                      int H, float4* __restrict__ out) {
+  extern __shared__ float4 cache[];
+  for (int i = threadIdx.x; i < H * 8; i += blockDim.x) cache[i] = F[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, lig = lane & 7;
+  const int64_t gid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 3;
+  const int64_t ngroups = (int64_t(gridDim.x) * blockDim.x) >> 3;
+  float4 acc = make_float4(0, 0, 0, 0);
+  for (int64_t base = gid * U; base < n; base += ngroups * U) {
+    uint32_t k = (base + lig < n && lig < U) ? idx[base + lig] : 0;
+    if (ALL) k %= H;
+    float4 r[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      uint32_t kj = __shfl_sync(0xffffffffu, k, j % 8, 8);
+      if (kj < (uint32_t)H)
+        r[j] = cache[kj * 8 + lig];
+      else
+        r[j] = ldrow(F + size_t(kj) * 8 + lig);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      acc.x += r[j].x;
+      acc.y += r[j].y;
+      acc.z += r[j].z;
+      acc.w += r[j].w;
     }
   }
   out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = acc;
@@ -360,6 +397,24 @@ int main() {
     printf("  ldg64 U=%2d thr=%d blk/sm=%d : %.3f ms  %.2f Grows/s  %.1f GB/s\n", U, THREADS,    \
            BLOCKS_PER_SM, ms, n / ms / 1e6, gb / ms * 1e3);                                       \
   }
+#define RUN_HOT(ALL, H, THREADS, BLOCKS_PER_SM)                                                 \
+  {                                                                                               \
+    int hh = (ALL) ? (H) : std::min<int>((H), (int)c.rows);                                        \
+    size_t sm = size_t(hh) * 128;                                                                 \
+    CK(cudaFuncSetAttribute(k_hot<8, ALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm))); \
+    int g = sms * BLOCKS_PER_SM;                                                                  \
+    float ms = time_ms([&] { k_hot<8, ALL><<<g, THREADS, sm>>>(F, idx, n, hh, out); });          \
+    CK(cudaGetLastError());                                                                       \
+    printf("  hot all=%d H=%d thr=%d blk/sm=%d : %.3f ms  %.2f Grows/s\n", (int)(ALL), hh,       \
+           THREADS, BLOCKS_PER_SM, ms, n / ms / 1e6);                                             \
+  }
+    RUN_HOT(true, 512, 1024, 1);
+    RUN_HOT(true, 1536, 1024, 1);
+    RUN_HOT(false, 512, 512, 2);
+    RUN_HOT(false, 768, 512, 2);
+    RUN_HOT(false, 1024, 1024, 1);
+    RUN_HOT(false, 1536, 1024, 1);
+    RUN_HOT(false, 1536, 768, 1);
     RUN_L32(8, 256, 4);
     RUN_L32(16, 256, 4);
     RUN_L32(16, 256, 8);

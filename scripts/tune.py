@@ -24,6 +24,7 @@ ap.add_argument("--var", type=int, nargs="+", default=[0, 1, 2])
 ap.add_argument("--task", type=int, nargs="+", default=[128])
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--check", action="store_true")
+ap.add_argument("--heavy", nargs="+", default=["512:64:512"], help="H:tau:W of the heavy-slice layout (H=0 off)")
 args = ap.parse_args()
 
 cfg = CONFIGS[args.config]
@@ -33,8 +34,10 @@ reps = [hb.split_fibers(hb.build_hbcsf(t, hb.allmode_order(dims, m)), hb.SplitCo
 rng = np.random.default_rng(cfg["seed"])
 f = [torch.from_numpy(rng.random((d, 32))).float().cuda() for d in dims]
 ref = None
-for var in args.var:
-    for task in args.task:
+import itertools
+for var, task, hv in itertools.product(args.var, args.task, args.heavy):
+        H, tau, W = hv.split(":")
+        os.environ["HBK_HEAVY_H"], os.environ["HBK_HEAVY_TAU"], os.environ["HBK_HEAVY_W"] = H, tau, W
         os.environ["HBK_CSF_VARIANT"] = str(var)
         os.environ["HBK_TASK_NNZ"] = str(task)
         ms = []
@@ -61,4 +64,4 @@ for var in args.var:
         else:
             dev = max(float(((o - r).norm(dim=1) / (1 + r.norm(dim=1))).max()) for o, r in zip(outs, ref))
             dev = f" maxdev_vs_first={dev:.2e}"
-        print(f"var={var} task={task}: per-mode ms {[round(x, 4) for x in ms]} sum {sum(ms):.4f}{dev}", flush=True)
+        print(f"var={var} task={task} heavy={hv}: per-mode ms {[round(x, 4) for x in ms]} sum {sum(ms):.4f}{dev}", flush=True)
