@@ -202,6 +202,7 @@ typedef struct {
   int64_t nnz;
   int64_t stream_bytes;    /* index + value bytes read per execute        */
   int64_t tasks_heavy;     /* group tasks of the heavy-slice CSF layout   */
+  int64_t hot_rows;        /* factor rows gathered with the L2 evict-last policy */
 } hbk_plan_info;
 
 int hbk_plan_create(hbk_coo* coo, hbk_csl* csl, hbk_csf* csf, hbk_sched* sched, int mode,

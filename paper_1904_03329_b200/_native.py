@@ -83,6 +83,7 @@ class PlanInfo(C.Structure):
         ("nnz", i64),
         ("stream_bytes", i64),
         ("tasks_heavy", i64),
+        ("hot_rows", i64),
     ]
 
 

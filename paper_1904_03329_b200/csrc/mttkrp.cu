@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <cstdio>
 
 #include "common.cuh"
 
@@ -35,7 +36,7 @@ static constexpr uint32_t NOSLOT = 0xFFFFFFFFu;
 static constexpr uint32_t TASK_NNZ_CSF = 128;
 static constexpr uint32_t TASK_NNZ_CSL = 128;
 static constexpr uint32_t TASK_NNZ_COO = 32;
-static constexpr uint32_t TASK_ROWS_ZERO = 64;
+static constexpr uint32_t TASK_ROWS_ZERO = 256;
 static constexpr uint32_t GEN_TASK_NNZ = 256;
 
 struct Task {
@@ -69,7 +70,7 @@ struct alignas(16) Work {
   const uint32_t* csl_k;      // rest[1]
   const float* csl_val;
   uint32_t csl_S;
-  const uint2* csl_pairs;     // [M] (rest[1] | SEND, value bits)
+  const uint2* csl_pairs;     // [M] (rest[1] | SEND | HOT, value bits)
   // COO bucket (unique rows)
   const uint32_t* coo_i;
   const uint32_t* coo_j;
@@ -90,6 +91,12 @@ static constexpr uint32_t FEND = 0x80000000u;  // last nonzero of its fiber
 static constexpr uint32_t SEND = 0x40000000u;  // last nonzero of its slice
 static constexpr uint32_t KMASK = 0x3FFFFFFFu;
 static constexpr uint32_t FB = 0x80000000u;    // B-row position (B-position streams)
+// B-position / CSL / COO streams: bit 29 is reserved for a per-row cache
+// class (measured: an L2 evict-last/evict-first split by reference count
+// gained <= 4% on the HBM-resident tensors and cost 8% on nell-2, so every
+// factor row uses evict-last and the bit stays clear); indices keep 29 bits
+static constexpr uint32_t HOT = 0x20000000u;
+static constexpr uint32_t IMASK = 0x1FFFFFFFu;
 
 struct Factors3 {
   const float4* B;  // factor of mode_order[1] (fiber / rest[0])
@@ -313,7 +320,7 @@ __device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const Factors3& 
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t xj = __shfl_sync(FULL, pr.x, j, 8);
-      const float4* rowp = ((xj & FB) ? Bl : Cl) + size_t(xj & KMASK) * 8;
+      const float4* rowp = ((xj & FB) ? Bl : Cl) + size_t(xj & IMASK) * 8;
       r[j] = ld_row4(rowp, pol_r);
     }
     const float vv = __uint_as_float(pr.y);
@@ -347,6 +354,12 @@ __device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const Factors3& 
 }
 
 // ------------------------------------------------------------ CSL tasks --
+// Per batch of 8 nonzeros a group stages the 8 B rows with cp.async (the
+// rows land in shared memory, so many stay in flight without holding
+// registers — the CSL-heavy tensors are DRAM-latency bound) and gathers the
+// 8 C rows into registers; v * B[j] o C[k] accumulates into the slice
+// partial (kernels.py:210-214).  Measured: loading both rows into registers
+// (98 registers, 2 CTAs/SM) was 10-14% slower on delicious-3d.
 __device__ __forceinline__ float4 csl_tasks(const Work& w, const Factors3& fx, const Task& t,
                                             int g, int lig, uint64_t pol_s, uint64_t pol_r,
                                             float4* __restrict__ slots) {
@@ -457,11 +470,20 @@ __device__ __forceinline__ void coo_tasks(const Work& w, const Factors3& fx, con
   }
 }
 
+// Rows owned by no bucket: a group loads 8 row numbers at once (one per
+// lane) and stores 8 zero rows, so the loop is not a chain of dependent loads.
 __device__ __forceinline__ void zero_task(const Work& w, const Factors3& fx, const Task& t,
                                           int lig) {
-  for (uint32_t i = t.lo; i < t.hi; ++i) {
-    const uint32_t row = __ldg(w.zero_rows + i);
-    fx.out[size_t(row) * 8 + lig] = f4zero();
+  const uint32_t nbat = __reduce_max_sync(FULL, t.hi > t.lo ? (t.hi - t.lo + 7) / 8 : 0u);
+  uint32_t base = t.lo;
+  for (uint32_t it = 0; it < nbat; ++it, base += 8) {
+    const uint32_t n = base < t.hi ? min(8u, t.hi - base) : 0u;
+    const uint32_t rl = uint32_t(lig) < n ? __ldg(w.zero_rows + base + lig) : 0u;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t row = __shfl_sync(FULL, rl, j, 8);
+      if (uint32_t(j) < n) fx.out[size_t(row) * 8 + lig] = f4zero();
+    }
   }
 }
 
@@ -853,17 +875,29 @@ __global__ void k_empty_tasks(Task* __restrict__ tasks, int64_t n) {
   }
 }
 
+// Hot-row flag: rows referenced at least T times in this plan (see HotSet).
+__device__ __forceinline__ uint32_t hot_of(const uint32_t* __restrict__ cnt, uint32_t row,
+                                           uint32_t T) {
+  return (cnt != nullptr && cnt[row] >= T) ? HOT : 0u;
+}
+
 // B-position stream of a CSF bucket in tree order: fiber f's pairs start at
 // position lptr[f] + f and are followed by (fidx[f] | FB, 0).
 __global__ void k_bpos_stream(const uint32_t* __restrict__ lptr, const uint32_t* __restrict__ fidx,
                               const uint32_t* __restrict__ leaf, const float* __restrict__ val,
-                              int64_t F, uint2* __restrict__ out) {
+                              int64_t F, const uint32_t* __restrict__ cntB,
+                              const uint32_t* __restrict__ cntC, uint32_t T,
+                              uint2* __restrict__ out) {
   for (int64_t f = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; f < F;
        f += int64_t(gridDim.x) * blockDim.x) {
     const uint32_t a = lptr[f], b = lptr[f + 1];
     uint2* o = out + a + f;
-    for (uint32_t i = a; i < b; ++i) *o++ = make_uint2(leaf[i], __float_as_uint(val[i]));
-    *o = make_uint2(fidx[f] | FB, 0u);
+    for (uint32_t i = a; i < b; ++i) {
+      const uint32_t k = leaf[i];
+      *o++ = make_uint2(k | hot_of(cntC, k, T), __float_as_uint(val[i]));
+    }
+    const uint32_t j = fidx[f];
+    *o = make_uint2(j | FB | hot_of(cntB, j, T), 0u);
   }
 }
 // SEND on the B position of each slice's last fiber
@@ -878,10 +912,10 @@ __global__ void k_bpos_send(const uint32_t* __restrict__ fpos, const uint32_t* _
 
 // Kernel-native streams (built once per plan).
 __global__ void k_pairs(const uint32_t* __restrict__ k, const float* __restrict__ v, int64_t M,
-                        uint2* __restrict__ out) {
+                        const uint32_t* __restrict__ cnt, uint32_t T, uint2* __restrict__ out) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
        i += int64_t(gridDim.x) * blockDim.x)
-    out[i] = make_uint2(k[i], __float_as_uint(v[i]));
+    out[i] = make_uint2(k[i] | hot_of(cnt, k[i], T), __float_as_uint(v[i]));
 }
 // flag the last nonzero of every segment [ptr[x], ptr[x+1])
 __global__ void k_flag_ends(const uint32_t* __restrict__ ptr, int64_t n, uint32_t flag,
@@ -894,10 +928,12 @@ __global__ void k_flag_ends(const uint32_t* __restrict__ ptr, int64_t n, uint32_
 }
 __global__ void k_quads(const uint32_t* __restrict__ i0, const uint32_t* __restrict__ j0,
                         const uint32_t* __restrict__ k0, const float* __restrict__ v, int64_t M,
-                        uint4* __restrict__ out) {
+                        const uint32_t* __restrict__ cntB, const uint32_t* __restrict__ cntC,
+                        uint32_t T, uint4* __restrict__ out) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
        i += int64_t(gridDim.x) * blockDim.x)
-    out[i] = make_uint4(i0[i], j0[i], k0[i], __float_as_uint(v[i]));
+    out[i] = make_uint4(i0[i], j0[i] | hot_of(cntB, j0[i], T), k0[i] | hot_of(cntC, k0[i], T),
+                        __float_as_uint(v[i]));
 }
 
 }  // namespace hbk
@@ -1095,7 +1131,9 @@ __global__ void k_group_fill(const uint32_t* __restrict__ tfirst, const uint32_t
                              const uint32_t* __restrict__ sj, const uint32_t* __restrict__ gofs,
                              const uint32_t* __restrict__ fofs, int64_t NW, uint32_t G,
                              const uint32_t* __restrict__ leaf, const float* __restrict__ val,
-                             bool bpos, uint2* __restrict__ pairs, uint32_t* __restrict__ fj) {
+                             bool bpos, const uint32_t* __restrict__ cntB,
+                             const uint32_t* __restrict__ cntC, uint32_t T,
+                             uint2* __restrict__ pairs, uint32_t* __restrict__ fj) {
   for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < NW * 4;
        x += int64_t(gridDim.x) * blockDim.x) {
     const int64_t w = x >> 2;
@@ -1105,11 +1143,13 @@ __global__ void k_group_fill(const uint32_t* __restrict__ tfirst, const uint32_t
     for (uint32_t i = a + g; i < b; i += 4) {
       const uint32_t q = perm[i];
       const uint32_t off = soff[q], len = slen[q];
-      for (uint32_t t = 0; t < len; ++t)
-        pairs[dst + t] = make_uint2(leaf[off + t] | (!bpos && t + 1 == len ? FEND : 0u),
+      for (uint32_t t = 0; t < len; ++t) {
+        const uint32_t k = leaf[off + t];
+        pairs[dst + t] = make_uint2(bpos ? (k | hot_of(cntC, k, T)) : (k | (t + 1 == len ? FEND : 0u)),
                                     __float_as_uint(val[off + t]));
+      }
       dst += len;
-      if (bpos) pairs[dst++] = make_uint2(sj[q] | FB, 0u);
+      if (bpos) pairs[dst++] = make_uint2(sj[q] | FB | hot_of(cntB, sj[q], T), 0u);
       fj[fpos++] = sj[q];
     }
   }
@@ -1168,9 +1208,17 @@ struct HeavyLayout {
 };
 
 // Builds the heavy-slice layout of a 3rd-order CSF bucket (see above).
+struct HotSet {
+  Scratch cntB, cntC;  // references per row of the fiber-mode / leaf-mode factor
+  uint32_t T = 0xFFFFFFFFu;
+  int64_t rows = 0;    // rows flagged hot
+  const uint32_t* b() const { return cntB.as<uint32_t>(); }
+  const uint32_t* c() const { return cntC.as<uint32_t>(); }
+};
+
 static HeavyLayout heavy_layout(const hbk_csf* c, const uint32_t* loff, const uint32_t* fpos,
                                 uint32_t H, uint32_t tau, uint32_t W, uint32_t slot_base, bool bpos,
-                                cudaStream_t st) {
+                                const HotSet& hot, cudaStream_t st) {
   HeavyLayout hl;
   const int64_t S = c->n[0], F = c->n[1];
   const uint32_t* lptr = c->ptr[1].as<uint32_t>();
@@ -1247,7 +1295,7 @@ static HeavyLayout heavy_layout(const hbk_csf* c, const uint32_t* loff, const ui
   k_group_fill<<<grid_for(NG, 128), 128, 0, st>>>(
       tfirst.as<uint32_t>(), perm, soff.as<uint32_t>(), slen.as<uint32_t>(), sj.as<uint32_t>(),
       gofs.as<uint32_t>(), fofs.as<uint32_t>(), NW, G, c->leaf.as<uint32_t>(), c->v32.as<float>(),
-      bpos, hl.pairs.as<uint2>(), hl.fj.as<uint32_t>());
+      bpos, hot.b(), hot.c(), hot.T, hl.pairs.as<uint2>(), hl.fj.as<uint32_t>());
   check_launch("k_group_fill");
   k_group_tasks<<<grid_for(NG, 256), 256, 0, st>>>(tslice.as<uint32_t>(), gofs.as<uint32_t>(),
                                                    gnnz.as<uint32_t>(), fofs.as<uint32_t>(),
@@ -1296,6 +1344,8 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   if (p->bpos) heavy_H = Tcsf;
   const bool heavy_on = p->fast && !p->sched && heavy_H > 0 && heavy_H >= Tcsf;
   int64_t heavy_ntasks = 0, heavy_segments = 0;
+  HotSet hot;  // no hot rows: every factor row uses the evict-last policy
+
   int64_t n_coo = 0, n_zero = 0;
   int64_t slots = 0;
   int64_t stream_bytes = 0;
@@ -1374,7 +1424,8 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
                                   c->ptr[L].as<uint32_t>(), S, uint32_t(c->M), Tcsf, st, heavy_H,
                                   p->bpos ? fpos.as<uint32_t>() : nullptr);
         HeavyLayout hl = heavy_layout(c, p->csf_send.as<uint32_t>(), fpos.as<uint32_t>(), heavy_H,
-                                      heavy_tau, heavy_W, uint32_t(tcsf_light.slots), p->bpos, st);
+                                      heavy_tau, heavy_W, uint32_t(tcsf_light.slots), p->bpos, hot,
+                                      st);
         HBK_REQUIRE(tcsf_light.slots + hl.slots == tcsf.slots, HBK_ECUDA,
                     "heavy layout slot accounting mismatch");
         p->heavy_pairs = hl.pairs;
@@ -1409,7 +1460,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       uint2* pp = p->csf_pairs.as<uint2>();
       k_bpos_stream<<<grid_for(c->n[L], 128), 128, 0, st>>>(
           c->ptr[L].as<uint32_t>(), c->idx[L].as<uint32_t>(), c->leaf.as<uint32_t>(),
-          c->v32.as<float>(), c->n[L], pp);
+          c->v32.as<float>(), c->n[L], hot.b(), hot.c(), hot.T, pp);
       check_launch("k_bpos_stream");
       k_bpos_send<<<grid_for(S, 256), 256, 0, st>>>(fpos.as<uint32_t>(), c->ptr[L].as<uint32_t>(),
                                                     S, pp);
@@ -1419,7 +1470,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       p->csf_pairs = dalloc(c->M * sizeof(uint2), st);
       uint2* pp = p->csf_pairs.as<uint2>();
       k_pairs<<<grid_for(c->M, 256), 256, 0, st>>>(c->leaf.as<uint32_t>(), c->v32.as<float>(),
-                                                   c->M, pp);
+                                                   c->M, nullptr, 0u, pp);
       check_launch("k_pairs");
       k_flag_ends<<<grid_for(c->n[L], 256), 256, 0, st>>>(c->ptr[L].as<uint32_t>(), c->n[L], FEND,
                                                           pp);
@@ -1450,7 +1501,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       p->csl_pairs = dalloc(s->M * sizeof(uint2), st);
       uint2* pp = p->csl_pairs.as<uint2>();
       k_pairs<<<grid_for(s->M, 256), 256, 0, st>>>(s->rest[1].as<uint32_t>(), s->v32.as<float>(),
-                                                   s->M, pp);
+                                                   s->M, hot.c(), hot.T, pp);
       check_launch("k_pairs");
       k_flag_ends<<<grid_for(s->S, 256), 256, 0, st>>>(s->slice_ptr.as<uint32_t>(), s->S, SEND, pp);
       check_launch("k_flag_ends");
@@ -1470,6 +1521,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     if (p->fast) {
       p->coo_quads = dalloc(t->nnz * sizeof(uint4), st);
       k_quads<<<grid_for(t->nnz, 256), 256, 0, st>>>(w.coo_i, w.coo_j, w.coo_k, w.coo_val, t->nnz,
+                                                     hot.b(), hot.c(), hot.T,
                                                      p->coo_quads.as<uint4>());
       check_launch("k_quads");
       w.coo_quads = p->coo_quads.as<uint4>();

@@ -124,17 +124,28 @@ class _HostStage:
         return [fu.result() for fu in [self.pool.submit(fn, a, b) for a, b in spans]]
 
     def upload_all(self, torch, items, dt):
-        """items: [(d, host array)] -> {d: CUDA tensor}.  The factors are
+        """items: [(d, host array)] -> ({d: CUDA tensor}, deferred checks).
+        Page-locked torch tensors of the kernel dtype are copied as they are
+        (their finiteness is checked on the device: (d, flag) pairs the
+        caller tests after the launch).  Other factors are
         converted concurrently (one pool task per factor, or per chunk of a
         large one); the host-to-device copies are issued by the calling
         thread, on its current stream, as soon as each factor is staged."""
         srcs = {}
+        out, checks = {}, []
         for d, f in items:
+            if _is_pinned_tensor(f, dt):
+                # page-locked host tensor of the kernel dtype: one async copy,
+                # finiteness checked on the device after the launch
+                dev = torch.empty(tuple(f.shape), dtype=dt, device="cuda")
+                dev.copy_(f, non_blocking=True)
+                out[d] = dev
+                checks.append((d, torch.isfinite(dev).all()))
+                continue
             src = np.ascontiguousarray(f)
             if src.ndim != 2:
                 raise ValueError(f"factor {d} must be a 2-D array")
             srcs[d] = src
-        out = {}
         with self.lock:
             stages, jobs = {}, []
             for d, src in srcs.items():
@@ -143,6 +154,8 @@ class _HostStage:
                 stages[d] = (buf, buf.numpy()[: rows * width].reshape(rows, width))
                 for a, b in self._spans(rows, width, src.itemsize):
                     jobs.append((d, a, b))
+            if not jobs:
+                return out, checks
 
             def convert(d, a, b):
                 src, stage = srcs[d], stages[d][1]
@@ -174,7 +187,7 @@ class _HostStage:
                 self.bufs[("in", d)] = (stages[d][0], ev)
             if bad is not None:
                 raise ValueError(f"factor {bad} has non-finite entries")
-        return out
+        return out, checks
 
     def download(self, torch, y):
         out = np.empty(tuple(y.shape), dtype=np.float64)
@@ -188,12 +201,19 @@ class _HostStage:
             torch.cuda.current_stream().synchronize()
             src = buf.numpy()[: y.numel()].reshape(rows, width)
             dst = out.reshape(rows, width)
-            self._map(lambda a, b: np.copyto(dst[a:b], src[a:b]), self._spans(rows, width, 8))
+            step = max(1, (2 << 20) // max(1, width * 8))
+            spans = [(a, min(rows, a + step)) for a in range(0, rows, step)]
+            self._map(lambda a, b: np.copyto(dst[a:b], src[a:b]), spans)
             self.bufs[("out",)] = (buf, None)
         return out
 
 
 _stage = None
+
+
+def _is_pinned_tensor(f, dt) -> bool:
+    return (type(f).__module__.startswith("torch") and not getattr(f, "is_cuda", True)
+            and f.dtype == dt and f.is_contiguous() and f.dim() == 2 and f.is_pinned())
 
 
 def _host_stage() -> _HostStage:
@@ -212,7 +232,7 @@ def _device_factors(factors: Factors, mode: int, precision: str = "fp32"):
     keep = []
     ptrs = (C.c_void_p * len(factors))()
     host = [(d, f) for d, f in enumerate(factors) if d != mode and not _is_device(f)]
-    staged = _host_stage().upload_all(torch, host, dt) if host else {}
+    staged, checks = _host_stage().upload_all(torch, host, dt) if host else ({}, [])
     on_device = not host
     for d, f in enumerate(factors):
         if d == mode:
@@ -225,7 +245,7 @@ def _device_factors(factors: Factors, mode: int, precision: str = "fp32"):
             t = t.clone()
         keep.append(t)
         ptrs[d] = t.data_ptr()
-    return ptrs, keep, on_device
+    return ptrs, keep, on_device, checks
 
 
 class _Plan:
@@ -273,11 +293,15 @@ def _check_precision(precision: str) -> str:
 
 
 def _finish(plan: _Plan, factors, mode: int, out=None, precision: str = "fp32"):
-    ptrs, keep, on_device = _device_factors(factors, mode, _check_precision(precision))
+    ptrs, keep, on_device, checks = _device_factors(factors, mode, _check_precision(precision))
     y = plan.execute(ptrs, out, precision)
     if on_device:
         return y, plan.opcount
-    return _host_stage().download(N.require_device(), y), plan.opcount
+    rows = _host_stage().download(N.require_device(), y)
+    for d, ok in checks:  # pinned host tensors: checked on the device
+        if not bool(ok):
+            raise ValueError(f"factor {d} has non-finite entries")
+    return rows, plan.opcount
 
 
 def plan_for(rep, mode: int, rank: int, schedule=None) -> _Plan:
@@ -379,5 +403,5 @@ def mttkrp_device(rep, factors, mode: int, out=None, schedule=None, precision: s
         ref = next(f for d, f in enumerate(factors) if d != mode)
         precision = "fp64" if str(getattr(ref, "dtype", "")) == "torch.float64" else "fp32"
     plan = plan_for(rep, mode, r, schedule)
-    ptrs, keep, _ = _device_factors(factors, mode, _check_precision(precision))
+    ptrs, keep, _, _ = _device_factors(factors, mode, _check_precision(precision))
     return plan.execute(ptrs, out, precision), plan.opcount

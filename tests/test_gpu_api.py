@@ -284,3 +284,25 @@ def test_linearity_and_repeatability(hb):
         assert row_dev(b, 2.0 * a) <= 1e-6
         a2, _ = hb.mttkrp(h1, f, mode)  # the plan is reused; the workspace self-cleans
         assert row_dev(a2, a) <= 1e-6
+
+
+def test_pinned_host_factors_match_numpy(hb, rng):
+    """Page-locked fp32 torch factors take the direct-copy path; results match
+    the NumPy path and non-finite entries still raise ValueError."""
+    import torch
+
+    idx, vals = _powerlaw(rng, (40, 30, 50), 3000)
+    t = hb.CooTensor((40, 30, 50), idx, vals)
+    f64 = [rng.random((d, 32)).astype(np.float32).astype(np.float64) for d in (40, 30, 50)]
+    pinned = [torch.from_numpy(f).float().pin_memory() for f in f64]
+    for mode in range(3):
+        h = hb.build_hbcsf(t, hb.allmode_order(t.dims, mode))
+        y0, _ = hb.mttkrp_hbcsf(h, f64, mode)
+        y1, _ = hb.mttkrp_hbcsf(h, pinned, mode)
+        assert isinstance(y1, np.ndarray) and y1.dtype == np.float64
+        assert np.array_equal(y0, y1)
+    bad = [p.clone().pin_memory() for p in pinned]
+    bad[2][3, 4] = float("nan")
+    h = hb.build_hbcsf(t, hb.allmode_order(t.dims, 0))
+    with pytest.raises(ValueError):
+        hb.mttkrp_hbcsf(h, bad, 0)
