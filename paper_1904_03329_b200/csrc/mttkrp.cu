@@ -70,7 +70,7 @@ struct alignas(16) Work {
   const uint32_t* csl_k;      // rest[1]
   const float* csl_val;
   uint32_t csl_S;
-  const uint2* csl_pairs;     // [M] (rest[1] | SEND | HOT, value bits)
+  const uint2* csl_pairs;     // [M] (rest[1] | SEND, value bits)
   // COO bucket (unique rows)
   const uint32_t* coo_i;
   const uint32_t* coo_j;
@@ -91,12 +91,12 @@ static constexpr uint32_t FEND = 0x80000000u;  // last nonzero of its fiber
 static constexpr uint32_t SEND = 0x40000000u;  // last nonzero of its slice
 static constexpr uint32_t KMASK = 0x3FFFFFFFu;
 static constexpr uint32_t FB = 0x80000000u;    // B-row position (B-position streams)
-// B-position / CSL / COO streams: bit 29 is reserved for a per-row cache
-// class (measured: an L2 evict-last/evict-first split by reference count
-// gained <= 4% on the HBM-resident tensors and cost 8% on nell-2, so every
-// factor row uses evict-last and the bit stays clear); indices keep 29 bits
-static constexpr uint32_t HOT = 0x20000000u;
-static constexpr uint32_t IMASK = 0x1FFFFFFFu;
+// B-position streams keep the row index pre-scaled to float4 units (x8) in
+// bits 0..29 (rows < 2^27); bit 31 = FB, bit 30 = SEND.  (Measured and
+// dropped: a per-row L2 evict-last/evict-first class by reference count —
+// <= 4% on the HBM-resident tensors, -8% on nell-2 — and a persisting L2
+// set-aside, which was slower.)
+static constexpr uint32_t XMASK = 0x3FFFFFFFu;
 
 struct Factors3 {
   const float4* B;  // factor of mode_order[1] (fiber / rest[0])
@@ -295,10 +295,14 @@ __device__ __forceinline__ float4 csf_tasks(const Work& w, const Factors3& fx, c
 // staging: the L1 data pipe carries each row once).  At a B position the
 // fiber partial is multiplied into the slice partial; slice ends (SEND) sit
 // on B positions.  Dead lanes carry (0, 0): leaf row 0 times v = 0.
+// UNIFORM (padded heavy layout): the four groups' streams have identical
+// structure, so B positions are warp-uniform and take a uniform branch
+// instead of predicated FMAs; heavy tasks are slice chunks (no SEND).
+template <bool UNIFORM>
 __device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const Factors3& fx, const Task& t,
                                                  int g, int lig, uint64_t pol_s, uint64_t pol_r) {
   const uint32_t lo = t.lo, hi = t.hi;
-  const bool chunk = t.slot != NOSLOT;
+  const bool chunk = UNIFORM || t.slot != NOSLOT;
   const uint32_t nbat = __reduce_max_sync(FULL, hi > lo ? (hi - lo + 7) / 8 : 0u);
   const float4* Cl = fx.C + lig;
   const float4* Bl = fx.B + lig;
@@ -312,29 +316,43 @@ __device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const Factors3& 
   uint32_t base = lo;
   for (uint32_t it = 0; it < nbat; ++it, base += 8) {
     const uint32_t bb_all = __ballot_sync(FULL, pr.x & FB);
-    const uint32_t sb_all = __ballot_sync(FULL, !chunk && (pr.x & SEND));
-    const uint32_t bbits = (bb_all >> (8 * g)) & 0xFFu;
-    const uint32_t sbits = (sb_all >> (8 * g)) & 0xFFu;
-    const uint32_t sany = any_group(sb_all);
+    const uint32_t bbits = UNIFORM ? (bb_all & 0xFFu) : ((bb_all >> (8 * g)) & 0xFFu);
+    uint32_t sbits = 0, sany = 0;
+    if (!UNIFORM) {
+      const uint32_t sb_all = __ballot_sync(FULL, !chunk && (pr.x & SEND));
+      sbits = (sb_all >> (8 * g)) & 0xFFu;
+      sany = any_group(sb_all);
+    }
     float4 r[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t xj = __shfl_sync(FULL, pr.x, j, 8);
-      const float4* rowp = ((xj & FB) ? Bl : Cl) + size_t(xj & IMASK) * 8;
-      r[j] = ld_row4(rowp, pol_r);
+      const float4* bp = (UNIFORM ? ((bbits >> j) & 1u) : (xj & FB)) ? Bl : Cl;
+      r[j] = ld_row4(bp + (xj & XMASK), pol_r);
     }
     const float vv = __uint_as_float(pr.y);
     const uint32_t sr_cur = sr;
-    const uint32_t nsl = __popc(sbits);
-    s += nsl;
     const uint32_t nb = base + 8;
     pr = make_uint2(0u, 0u);
     if (nb + lig < hi) pr = ld_stream_u2(pairs + nb + lig, pol_s);
-    if (__any_sync(FULL, nsl != 0)) sr = __ldg(w.csf_sidx + min(s + lig, Sm1));
+    if (!UNIFORM) {
+      const uint32_t nsl = __popc(sbits);
+      s += nsl;
+      if (__any_sync(FULL, nsl != 0)) sr = __ldg(w.csf_sidx + min(s + lig, Sm1));
+    }
     uint32_t ts = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float vj = __shfl_sync(FULL, vv, j, 8);
+      if (UNIFORM) {
+        if ((bbits >> j) & 1u) {
+          sa = fmav4(fa, r[j], sa);
+          fa = f4zero();
+        } else {
+          fa = fma4(vj, r[j], fa);
+        }
+        continue;
+      }
       fa = fma4(vj, r[j], fa);
       if ((bbits >> j) & 1u) {
         sa = fmav4(fa, r[j], sa);
@@ -493,10 +511,10 @@ __device__ __forceinline__ void zero_task(const Work& w, const Factors3& fx, con
 // it.  Chunks of one split slice that land in the same warp are summed with
 // shuffles and handed over with a single vector atomic.
 static constexpr int FAST_BLOCK = 256;
-enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2, KIND_CSF_BPOS = 3, KIND_CSF_BPOS4 = 4 };
+enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2, KIND_CSF_BPOS = 3, KIND_CSF_BPOS4 = 4, KIND_CSF_UNI = 5 };
 
 template <int KIND>
-__global__ void __launch_bounds__(FAST_BLOCK, KIND == KIND_CSF_BPOS4 ? 4 : 3)
+__global__ void __launch_bounds__(FAST_BLOCK, (KIND == KIND_CSF_BPOS4 || KIND == KIND_CSF_UNI) ? 4 : 3)
     k_mttkrp3_r32(const __grid_constant__ Work w, const __grid_constant__ Factors3 fx) {
   // per lane: 8 slots of 16 B (one per batch position) for staged B rows
   __shared__ float4 s_slots[FAST_BLOCK * 8];
@@ -506,7 +524,7 @@ __global__ void __launch_bounds__(FAST_BLOCK, KIND == KIND_CSF_BPOS4 ? 4 : 3)
   float4* slots = s_slots + (threadIdx.x >> 3) * 64 + lig;
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_r = policy_evict_last();
-  constexpr int K = (KIND == KIND_CSF_BPOS || KIND == KIND_CSF_BPOS4) ? KIND_CSF : KIND;
+  constexpr int K = (KIND == KIND_CSF_BPOS || KIND == KIND_CSF_BPOS4 || KIND == KIND_CSF_UNI) ? KIND_CSF : KIND;
   const uint32_t first = K == KIND_CSF ? 0u : (K == KIND_CSL ? w.n0 : w.n1);
   const uint32_t last = K == KIND_CSF ? w.n0 : (K == KIND_CSL ? w.n1 : w.n3);
   uint32_t* ctr = w.ws_ctr + 2 * K;
@@ -518,7 +536,8 @@ __global__ void __launch_bounds__(FAST_BLOCK, KIND == KIND_CSF_BPOS4 ? 4 : 3)
     const Task t = w.tasks[base + g];
     if (K == KIND_CSF || K == KIND_CSL) {
       const float4 sa =
-          (KIND == KIND_CSF_BPOS || KIND == KIND_CSF_BPOS4) ? csf_bpos_tasks(w, fx, t, g, lig, pol_s, pol_r)
+          KIND == KIND_CSF_UNI ? csf_bpos_tasks<true>(w, fx, t, g, lig, pol_s, pol_r)
+          : (KIND == KIND_CSF_BPOS || KIND == KIND_CSF_BPOS4) ? csf_bpos_tasks<false>(w, fx, t, g, lig, pol_s, pol_r)
           : K == KIND_CSF       ? csf_tasks(w, fx, t, g, lig, pol_s, pol_r, slots)
                                 : csl_tasks(w, fx, t, g, lig, pol_s, pol_r, slots);
       const bool mine = t.slot != NOSLOT && t.lo < t.hi;
@@ -875,29 +894,19 @@ __global__ void k_empty_tasks(Task* __restrict__ tasks, int64_t n) {
   }
 }
 
-// Hot-row flag: rows referenced at least T times in this plan (see HotSet).
-__device__ __forceinline__ uint32_t hot_of(const uint32_t* __restrict__ cnt, uint32_t row,
-                                           uint32_t T) {
-  return (cnt != nullptr && cnt[row] >= T) ? HOT : 0u;
-}
-
 // B-position stream of a CSF bucket in tree order: fiber f's pairs start at
-// position lptr[f] + f and are followed by (fidx[f] | FB, 0).
+// position lptr[f] + f and are followed by (fidx[f] | FB, 0).  Row indices
+// are stored pre-scaled to float4 units (x8) so the kernel's address is one
+// IMAD.WIDE off the lane's base pointer.
 __global__ void k_bpos_stream(const uint32_t* __restrict__ lptr, const uint32_t* __restrict__ fidx,
                               const uint32_t* __restrict__ leaf, const float* __restrict__ val,
-                              int64_t F, const uint32_t* __restrict__ cntB,
-                              const uint32_t* __restrict__ cntC, uint32_t T,
-                              uint2* __restrict__ out) {
+                              int64_t F, uint2* __restrict__ out) {
   for (int64_t f = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; f < F;
        f += int64_t(gridDim.x) * blockDim.x) {
     const uint32_t a = lptr[f], b = lptr[f + 1];
     uint2* o = out + a + f;
-    for (uint32_t i = a; i < b; ++i) {
-      const uint32_t k = leaf[i];
-      *o++ = make_uint2(k | hot_of(cntC, k, T), __float_as_uint(val[i]));
-    }
-    const uint32_t j = fidx[f];
-    *o = make_uint2(j | FB | hot_of(cntB, j, T), 0u);
+    for (uint32_t i = a; i < b; ++i) *o++ = make_uint2(leaf[i] << 3, __float_as_uint(val[i]));
+    *o = make_uint2((fidx[f] << 3) | FB, 0u);
   }
 }
 // SEND on the B position of each slice's last fiber
@@ -912,10 +921,10 @@ __global__ void k_bpos_send(const uint32_t* __restrict__ fpos, const uint32_t* _
 
 // Kernel-native streams (built once per plan).
 __global__ void k_pairs(const uint32_t* __restrict__ k, const float* __restrict__ v, int64_t M,
-                        const uint32_t* __restrict__ cnt, uint32_t T, uint2* __restrict__ out) {
+                        uint2* __restrict__ out) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
        i += int64_t(gridDim.x) * blockDim.x)
-    out[i] = make_uint2(k[i] | hot_of(cnt, k[i], T), __float_as_uint(v[i]));
+    out[i] = make_uint2(k[i], __float_as_uint(v[i]));
 }
 // flag the last nonzero of every segment [ptr[x], ptr[x+1])
 __global__ void k_flag_ends(const uint32_t* __restrict__ ptr, int64_t n, uint32_t flag,
@@ -928,12 +937,10 @@ __global__ void k_flag_ends(const uint32_t* __restrict__ ptr, int64_t n, uint32_
 }
 __global__ void k_quads(const uint32_t* __restrict__ i0, const uint32_t* __restrict__ j0,
                         const uint32_t* __restrict__ k0, const float* __restrict__ v, int64_t M,
-                        const uint32_t* __restrict__ cntB, const uint32_t* __restrict__ cntC,
-                        uint32_t T, uint4* __restrict__ out) {
+                        uint4* __restrict__ out) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
        i += int64_t(gridDim.x) * blockDim.x)
-    out[i] = make_uint4(i0[i], j0[i] | hot_of(cntB, j0[i], T), k0[i] | hot_of(cntC, k0[i], T),
-                        __float_as_uint(v[i]));
+    out[i] = make_uint4(i0[i], j0[i], k0[i], __float_as_uint(v[i]));
 }
 
 }  // namespace hbk
@@ -1105,10 +1112,14 @@ __global__ void k_seg_task_first(const uint32_t* __restrict__ perm, const uint32
   }
 }
 
-// per group task (w, g): segment count and nonzero count
+// per group task (w, g): segment count and stream length.  B-position
+// layout (pad): the four groups of a warp task get identical structure —
+// quad q (segments 4q..4q+3, longest first) is padded to the length of its
+// first segment, plus one B position — so every group stream has length
+// sum_q (L_q + 1) and the kernel's fiber ends are warp-uniform.
 __global__ void k_group_sizes(const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ perm,
                               const uint32_t* __restrict__ slen, int64_t NW, uint32_t G,
-                              uint32_t extra, uint32_t* __restrict__ gnnz,
+                              bool pad, uint32_t* __restrict__ gnnz,
                               uint32_t* __restrict__ gseg) {
   for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < NW * 4;
        x += int64_t(gridDim.x) * blockDim.x) {
@@ -1116,40 +1127,61 @@ __global__ void k_group_sizes(const uint32_t* __restrict__ tfirst, const uint32_
     const uint32_t g = uint32_t(x & 3);
     const uint32_t a = tfirst[w], b = (w + 1 < NW) ? tfirst[w + 1] : G;
     uint32_t n = 0, c = 0;
-    for (uint32_t i = a + g; i < b; i += 4) {
-      n += slen[perm[i]] + extra;
-      ++c;
+    if (pad) {
+      for (uint32_t i = a; i < b; i += 4) n += slen[perm[i]] + 1;
+      c = (b - a + 3) / 4;
+    } else {
+      for (uint32_t i = a + g; i < b; i += 4) {
+        n += slen[perm[i]];
+        ++c;
+      }
     }
     gnnz[x] = n;
     gseg[x] = c;
   }
 }
 
-// copy each group's segments into its contiguous stream, FEND on segment ends
+// copy each group's segments into its contiguous stream: FEND on segment
+// ends (smem-slot kernel), or the padded B-position layout (pad)
 __global__ void k_group_fill(const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ perm,
                              const uint32_t* __restrict__ soff, const uint32_t* __restrict__ slen,
                              const uint32_t* __restrict__ sj, const uint32_t* __restrict__ gofs,
                              const uint32_t* __restrict__ fofs, int64_t NW, uint32_t G,
                              const uint32_t* __restrict__ leaf, const float* __restrict__ val,
-                             bool bpos, const uint32_t* __restrict__ cntB,
-                             const uint32_t* __restrict__ cntC, uint32_t T,
-                             uint2* __restrict__ pairs, uint32_t* __restrict__ fj) {
+                             bool pad, uint2* __restrict__ pairs, uint32_t* __restrict__ fj) {
   for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < NW * 4;
        x += int64_t(gridDim.x) * blockDim.x) {
     const int64_t w = x >> 2;
     const uint32_t g = uint32_t(x & 3);
     const uint32_t a = tfirst[w], b = (w + 1 < NW) ? tfirst[w + 1] : G;
     uint32_t dst = gofs[x], fpos = fofs[x];
+    if (pad) {
+      for (uint32_t i0 = a; i0 < b; i0 += 4) {
+        const uint32_t Lq = slen[perm[i0]];
+        const uint32_t i = i0 + g;
+        uint32_t len = 0, off = 0, j = 0;
+        if (i < b) {
+          const uint32_t q = perm[i];
+          len = slen[q];
+          off = soff[q];
+          j = sj[q];
+        }
+        for (uint32_t t = 0; t < len; ++t)
+          pairs[dst + t] = make_uint2(leaf[off + t] << 3, __float_as_uint(val[off + t]));
+        for (uint32_t t = len; t < Lq; ++t) pairs[dst + t] = make_uint2(0u, 0u);
+        dst += Lq;
+        pairs[dst++] = make_uint2((j << 3) | FB, 0u);
+        fj[fpos++] = j;
+      }
+      continue;
+    }
     for (uint32_t i = a + g; i < b; i += 4) {
       const uint32_t q = perm[i];
       const uint32_t off = soff[q], len = slen[q];
-      for (uint32_t t = 0; t < len; ++t) {
-        const uint32_t k = leaf[off + t];
-        pairs[dst + t] = make_uint2(bpos ? (k | hot_of(cntC, k, T)) : (k | (t + 1 == len ? FEND : 0u)),
+      for (uint32_t t = 0; t < len; ++t)
+        pairs[dst + t] = make_uint2(leaf[off + t] | (t + 1 == len ? FEND : 0u),
                                     __float_as_uint(val[off + t]));
-      }
       dst += len;
-      if (bpos) pairs[dst++] = make_uint2(sj[q] | FB | hot_of(cntB, sj[q], T), 0u);
       fj[fpos++] = sj[q];
     }
   }
@@ -1208,17 +1240,9 @@ struct HeavyLayout {
 };
 
 // Builds the heavy-slice layout of a 3rd-order CSF bucket (see above).
-struct HotSet {
-  Scratch cntB, cntC;  // references per row of the fiber-mode / leaf-mode factor
-  uint32_t T = 0xFFFFFFFFu;
-  int64_t rows = 0;    // rows flagged hot
-  const uint32_t* b() const { return cntB.as<uint32_t>(); }
-  const uint32_t* c() const { return cntC.as<uint32_t>(); }
-};
-
 static HeavyLayout heavy_layout(const hbk_csf* c, const uint32_t* loff, const uint32_t* fpos,
                                 uint32_t H, uint32_t tau, uint32_t W, uint32_t slot_base, bool bpos,
-                                const HotSet& hot, cudaStream_t st) {
+                                cudaStream_t st) {
   HeavyLayout hl;
   const int64_t S = c->n[0], F = c->n[1];
   const uint32_t* lptr = c->ptr[1].as<uint32_t>();
@@ -1277,25 +1301,25 @@ static HeavyLayout heavy_layout(const hbk_csf* c, const uint32_t* loff, const ui
   const int64_t NG = int64_t(NW) * 4;
   Scratch gofs((NG + 1) * 4, st), gnnz(NG * 4, st), fofs((NG + 1) * 4, st);
   k_group_sizes<<<grid_for(NG, 256), 256, 0, st>>>(tfirst.as<uint32_t>(), perm,
-                                                   slen.as<uint32_t>(), NW, G, bpos ? 1u : 0u,
+                                                   slen.as<uint32_t>(), NW, G, bpos,
                                                    gofs.as<uint32_t>(), fofs.as<uint32_t>());
   check_launch("k_group_sizes");
   HBK_CUDA(cudaMemcpyAsync(gnnz.p, gofs.p, NG * 4, cudaMemcpyDeviceToDevice, st));
   Scratch gseg(NG * 4, st), nchunk((S + 1) * 4, st);
   HBK_CUDA(cudaMemcpyAsync(gseg.p, fofs.p, NG * 4, cudaMemcpyDeviceToDevice, st));
   const uint32_t Mh = exclusive_scan_total(gofs.as<uint32_t>(), NG, st);
-  exclusive_scan_total(fofs.as<uint32_t>(), NG, st);
+  const uint32_t Fh = exclusive_scan_total(fofs.as<uint32_t>(), NG, st);
   HBK_CUDA(cudaMemsetAsync(nchunk.p, 0, (S + 1) * 4, st));
   k_slice_nchunk<<<grid_for(NW, 256), 256, 0, st>>>(tslice.as<uint32_t>(), gseg.as<uint32_t>(), NW,
                                                     nchunk.as<uint32_t>());
   check_launch("k_slice_nchunk");
   hl.pairs = dalloc(size_t(std::max<uint32_t>(Mh, 1)) * sizeof(uint2), st);
-  hl.fj = dalloc(size_t(std::max<uint32_t>(G, 1)) * 4, st);
+  hl.fj = dalloc(size_t(std::max<uint32_t>(Fh, 1)) * 4, st);
   hl.tasks = dalloc(size_t(NG) * sizeof(Task), st);
   k_group_fill<<<grid_for(NG, 128), 128, 0, st>>>(
       tfirst.as<uint32_t>(), perm, soff.as<uint32_t>(), slen.as<uint32_t>(), sj.as<uint32_t>(),
       gofs.as<uint32_t>(), fofs.as<uint32_t>(), NW, G, c->leaf.as<uint32_t>(), c->v32.as<float>(),
-      bpos, hot.b(), hot.c(), hot.T, hl.pairs.as<uint2>(), hl.fj.as<uint32_t>());
+      bpos, hl.pairs.as<uint2>(), hl.fj.as<uint32_t>());
   check_launch("k_group_fill");
   k_group_tasks<<<grid_for(NG, 256), 256, 0, st>>>(tslice.as<uint32_t>(), gofs.as<uint32_t>(),
                                                    gnnz.as<uint32_t>(), fofs.as<uint32_t>(),
@@ -1304,6 +1328,7 @@ static HeavyLayout heavy_layout(const hbk_csf* c, const uint32_t* loff, const ui
   check_launch("k_group_tasks");
   hl.ntasks = NG;
   hl.slots = nheavy;
+  hl.segments = Fh;
   HBK_CUDA(cudaStreamSynchronize(st));
   return hl;
 }
@@ -1335,7 +1360,8 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   // heavy-slice layout (fast path): slices with more than H nonzeros
   // B-position streams (default fast CSF path): every slice with more than
   // Tcsf nonzeros goes to the heavy layout, lighter slices form runs
-  p->bpos = p->fast && !p->sched && p->csf_variant >= 1;
+  p->bpos = p->fast && !p->sched && p->csf_variant >= 1 && p->dims[p->mo[1]] < (int64_t(1) << 27) &&
+            p->dims[p->mo[2]] < (int64_t(1) << 27);
   uint32_t heavy_H = p->bpos ? Tcsf : 4 * Tcsf, heavy_tau = 32, heavy_W = 2048;
   if (const char* e = getenv("HBK_HEAVY_H")) heavy_H = uint32_t(std::max(0, atoi(e)));
   if (const char* e = getenv("HBK_HEAVY_TAU")) heavy_tau = uint32_t(std::min(65535, std::max(1, atoi(e))));
@@ -1344,7 +1370,6 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   if (p->bpos) heavy_H = Tcsf;
   const bool heavy_on = p->fast && !p->sched && heavy_H > 0 && heavy_H >= Tcsf;
   int64_t heavy_ntasks = 0, heavy_segments = 0;
-  HotSet hot;  // no hot rows: every factor row uses the evict-last policy
 
   int64_t n_coo = 0, n_zero = 0;
   int64_t slots = 0;
@@ -1424,8 +1449,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
                                   c->ptr[L].as<uint32_t>(), S, uint32_t(c->M), Tcsf, st, heavy_H,
                                   p->bpos ? fpos.as<uint32_t>() : nullptr);
         HeavyLayout hl = heavy_layout(c, p->csf_send.as<uint32_t>(), fpos.as<uint32_t>(), heavy_H,
-                                      heavy_tau, heavy_W, uint32_t(tcsf_light.slots), p->bpos, hot,
-                                      st);
+                                      heavy_tau, heavy_W, uint32_t(tcsf_light.slots), p->bpos, st);
         HBK_REQUIRE(tcsf_light.slots + hl.slots == tcsf.slots, HBK_ECUDA,
                     "heavy layout slot accounting mismatch");
         p->heavy_pairs = hl.pairs;
@@ -1460,7 +1484,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       uint2* pp = p->csf_pairs.as<uint2>();
       k_bpos_stream<<<grid_for(c->n[L], 128), 128, 0, st>>>(
           c->ptr[L].as<uint32_t>(), c->idx[L].as<uint32_t>(), c->leaf.as<uint32_t>(),
-          c->v32.as<float>(), c->n[L], hot.b(), hot.c(), hot.T, pp);
+          c->v32.as<float>(), c->n[L], pp);
       check_launch("k_bpos_stream");
       k_bpos_send<<<grid_for(S, 256), 256, 0, st>>>(fpos.as<uint32_t>(), c->ptr[L].as<uint32_t>(),
                                                     S, pp);
@@ -1470,7 +1494,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       p->csf_pairs = dalloc(c->M * sizeof(uint2), st);
       uint2* pp = p->csf_pairs.as<uint2>();
       k_pairs<<<grid_for(c->M, 256), 256, 0, st>>>(c->leaf.as<uint32_t>(), c->v32.as<float>(),
-                                                   c->M, nullptr, 0u, pp);
+                                                   c->M, pp);
       check_launch("k_pairs");
       k_flag_ends<<<grid_for(c->n[L], 256), 256, 0, st>>>(c->ptr[L].as<uint32_t>(), c->n[L], FEND,
                                                           pp);
@@ -1501,7 +1525,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       p->csl_pairs = dalloc(s->M * sizeof(uint2), st);
       uint2* pp = p->csl_pairs.as<uint2>();
       k_pairs<<<grid_for(s->M, 256), 256, 0, st>>>(s->rest[1].as<uint32_t>(), s->v32.as<float>(),
-                                                   s->M, hot.c(), hot.T, pp);
+                                                   s->M, pp);
       check_launch("k_pairs");
       k_flag_ends<<<grid_for(s->S, 256), 256, 0, st>>>(s->slice_ptr.as<uint32_t>(), s->S, SEND, pp);
       check_launch("k_flag_ends");
@@ -1521,7 +1545,6 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     if (p->fast) {
       p->coo_quads = dalloc(t->nnz * sizeof(uint4), st);
       k_quads<<<grid_for(t->nnz, 256), 256, 0, st>>>(w.coo_i, w.coo_j, w.coo_k, w.coo_val, t->nnz,
-                                                     hot.b(), hot.c(), hot.T,
                                                      p->coo_quads.as<uint4>());
       check_launch("k_quads");
       w.coo_quads = p->coo_quads.as<uint4>();
@@ -1670,10 +1693,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       wh.csf_fidx = p->heavy_fj.as<uint32_t>();
       wh.csf_F = uint32_t(heavy_segments);
       HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &per_sm,
-          p->bpos ? (p->csf_variant == 2 ? k_mttkrp3_r32<KIND_CSF_BPOS4> : k_mttkrp3_r32<KIND_CSF_BPOS>)
-                  : k_mttkrp3_r32<KIND_CSF>,
-          p->block, 0));
+          &per_sm, p->bpos ? k_mttkrp3_r32<KIND_CSF_UNI> : k_mttkrp3_r32<KIND_CSF>, p->block, 0));
       p->grid_heavy = grid_for_tasks(heavy_ntasks, per_sm, 4);
       wh.total_warps[0] = uint32_t(p->grid_heavy) * (p->block / 32);
       launches += 1;
@@ -1850,10 +1870,8 @@ int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out,
           k_mttkrp3_r32<KIND_CSF><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
       }
       if (p->grid_heavy) {
-        if (p->bpos && p->csf_variant == 2)
-          k_mttkrp3_r32<KIND_CSF_BPOS4><<<p->grid_heavy, p->block, 0, st>>>(p->work_heavy, fx);
-        else if (p->bpos)
-          k_mttkrp3_r32<KIND_CSF_BPOS><<<p->grid_heavy, p->block, 0, st>>>(p->work_heavy, fx);
+        if (p->bpos)
+          k_mttkrp3_r32<KIND_CSF_UNI><<<p->grid_heavy, p->block, 0, st>>>(p->work_heavy, fx);
         else
           k_mttkrp3_r32<KIND_CSF><<<p->grid_heavy, p->block, 0, st>>>(p->work_heavy, fx);
       }
