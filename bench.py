@@ -236,9 +236,17 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # HBK_BENCH_BACKEND=gloo runs the N>1 path on fewer GPUs than ranks (ranks
+    # share devices round-robin) to validate the sharded leg on one GPU; the
+    # measured configuration is one rank per GPU over NCCL.
+    backend = os.environ.get("HBK_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_1904_03329_b200 as hb
     from paper_1904_03329_b200 import shard
@@ -260,9 +268,18 @@ def main():
     for mode in range(len(dims)):
         mo = hb.allmode_order(dims, mode)
         if world > 1:
-            rr, part = shard.shard_for_rank(t, mode, rank, world)
+            # this rank's output rows, rebased: its plan writes only them
+            ranges_m = shard.plan_row_ranges(shard.slice_histogram(t, mode).cpu().numpy(), world)
+            rr = ranges_m[rank]
+            part = shard.shard_rows(t, mode, rr[0], rr[1]) if rr[1] > rr[0] else None
         else:
             rr, part = (0, dims[mode]), t
+        if part is None:  # more ranks than non-empty row ranges
+            reps.append(None)
+            ranges.append(rr)
+            censuses.append(None)
+            plans.append(None)
+            continue
         h = hb.split_fibers(hb.build_hbcsf(part, mo), split_cfg)
         reps.append(h)
         ranges.append(rr)
@@ -273,13 +290,19 @@ def main():
 
     f64 = make_factors(dims, cfg["seed"])
     f_dev = [torch.from_numpy(f).float().cuda() for f in f64]
-    outs = [torch.empty((dims[m], RANK), dtype=torch.float32, device="cuda") for m in range(len(dims))]
+    rows_local = [hi - lo for lo, hi in ranges]
+    outs = [torch.empty((max(1, rows_local[m]), RANK), dtype=torch.float32, device="cuda")
+            for m in range(len(dims))]
     ptrs = [_device_factors(f_dev, m)[0] for m in range(len(dims))]
     stream = torch.cuda.current_stream()
 
+    def run_mode(m):
+        if plans[m] is not None:
+            plans[m].execute(ptrs[m], outs[m])
+
     def step():
         for m in range(len(dims)):
-            plans[m].execute(ptrs[m], outs[m])
+            run_mode(m)
 
     for _ in range(args.warmup):
         step()
@@ -297,7 +320,7 @@ def main():
         for s in range(args.steps):
             for m in range(n_modes):
                 ev[m][s][0].record(stream)
-                plans[m].execute(ptrs[m], outs[m])
+                run_mode(m)
                 ev[m][s][1].record(stream)
         stop.record(stream)
         torch.cuda.synchronize()
@@ -315,7 +338,15 @@ def main():
 
     # roofline over the per-mode launches (each step is one launch per mode)
     hbm, hbm_src = peaks()
-    bytes_modes = [b_comp(censuses[m], dims, m) for m in range(n_modes)]
+    # this rank's launches: its own output rows, every input factor row
+    bytes_modes = []
+    for m in range(n_modes):
+        if censuses[m] is None:
+            bytes_modes.append(0)
+            continue
+        dl = list(dims)
+        dl[m] = rows_local[m]
+        bytes_modes.append(b_comp(censuses[m], dl, m))
     achieved = sum(bytes_modes) / (sum(per_mode_ms) * 1e-3) / 1e9
     # DRAM bytes per launch from the committed ncu capture of this workload
     # (profiles/ncu_summary.json, written by scripts/make_profile_summary.py)
@@ -328,28 +359,39 @@ def main():
         except Exception:
             traffic = None
 
-    # end to end through the public API with host buffers (numpy factors in,
-    # numpy float64 rows out), one mttkrp_hbcsf per mode per step
+    # end to end through the public API with host buffers: pinned fp32
+    # factors in, NumPy float64 rows out, one mttkrp_hbcsf per mode per step
+    # (each rank: its own row shard); wall clock, max over ranks
     e2e = None
-    if not args.no_e2e and world == 1:
-        # inputs in page-locked host memory (fp32, the kernel dtype); every
-        # call copies its two factors in and the (dims[mode], R) rows out
+    if not args.no_e2e:
         f_pin = [torch.from_numpy(f).float().pin_memory() for f in f64]
-        for m in range(n_modes):
-            hb.mttkrp_hbcsf(reps[m], f_pin, m)
+
+        def e2e_step():
+            for m in range(n_modes):
+                if reps[m] is not None:
+                    hb.mttkrp_hbcsf(reps[m], f_pin, m)
+
+        e2e_step()
         torch.cuda.synchronize()
         k = max(3, min(args.steps, 10))
+        if world > 1:
+            dist.barrier()
         tic = time.perf_counter()
         for _ in range(k):
-            for m in range(n_modes):
-                y, _ = hb.mttkrp_hbcsf(reps[m], f_pin, m)
+            e2e_step()
         e2e_s = (time.perf_counter() - tic) / k
-        h2d = sum(4 * RANK * sum(d for i, d in enumerate(dims) if i != m) for m in range(n_modes))
-        d2h = sum(4 * RANK * dims[m] for m in range(n_modes))
+        if world > 1:
+            tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        h2d = sum(4 * RANK * sum(d for i, d in enumerate(dims) if i != m)
+                  for m in range(n_modes) if reps[m] is not None)
+        d2h = sum(4 * RANK * rows_local[m] for m in range(n_modes) if reps[m] is not None)
         e2e = {"value": flops_step / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
                "path": "paper_1904_03329_b200.mttkrp_hbcsf(pinned host fp32 factors) -> numpy f64 rows, "
-                       "one call per mode, H2D + kernel + D2H inside the timed region"}
+                       "one call per mode, H2D + kernel + D2H inside the timed region"
+                       + ("; bytes per rank, rank 0" if world > 1 else "")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -399,7 +441,7 @@ def main():
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * sum(int(pl.info.launches) for pl in plans),
+            "gpu_launches": args.steps * sum(int(pl.info.launches) for pl in plans if pl is not None),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -219,6 +219,16 @@ int hbk_plan_execute_f64(const hbk_plan* p, const double* const* factors, double
                          void* stream);
 void hbk_plan_release(hbk_plan* p);
 
+/* ------------------------------------------------------------- CP-ALS --
+ * Row update of one ALS mode on a row shard (cpd.py:157-195), fused:
+ *   F = Y * M                 (cpd.py:172; M = pinv(V), 32x32 row-major fp32)
+ *   gram  = F^T F             (cpd.py:39-42; fp64, overwritten)
+ *   inner = sum_r w_r sum_i Y[i,r] F[i,r]   (cpd.py:176-184 fit term; NULL
+ *                               to skip; colw = w [dev] fp32 [32] or NULL = 1)
+ * Y, F [dev] rows x rank fp32 row-major (may not alias); rank must be 32.   */
+int hbk_als_update(const float* Y, int64_t rows, int rank, const float* M, const float* colw,
+                   float* F, double* gram, double* inner, void* stream);
+
 /* ------------------------------------------------------------ sharding --
  * Multi-GPU partitioner: slice nnz histogram of `mode`.
  * hist [dev] int64 [dims[mode]] is overwritten.                            */

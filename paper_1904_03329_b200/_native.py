@@ -130,6 +130,7 @@ _SIGS = {
     "hbk_coo_slice_histogram": ([vp, C.c_int, vp, vp], C.c_int),
     "hbk_coo_select_rows": ([vp, C.c_int, i64, i64, vp, C.POINTER(vp)], C.c_int),
     "hbk_coo_shard_rows": ([vp, C.c_int, i64, i64, vp, C.POINTER(vp)], C.c_int),
+    "hbk_als_update": ([vp, i64, C.c_int, vp, vp, vp, vp, vp, vp], C.c_int),
 }
 
 EXPORTED = tuple(_SIGS)

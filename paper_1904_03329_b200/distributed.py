@@ -10,16 +10,16 @@ One process per GPU (torchrun), ``torch.distributed`` for the plumbing
   (``hbk_coo_shard_rows``: rebased, so its MTTKRP writes exactly those rows);
 * the MTTKRP of a mode needs no communication (slices are independent,
   kernels.py:154-186);
-* the ALS update ``F_n[rows_g] = Y_g · V†`` is row-local (cpd.py:170-172), V
-  is built from Grams every rank holds;
-* exchanges per mode: one all-gather of the fp32 rows the MTTKRP kernels read
-  (uneven shards padded), one all-reduce of the R×R fp64 Gram partials
-  (cpd.py:39-42), one all-reduce of the finiteness flag; per sweep one scalar
-  all-reduce for ⟨X, X̂⟩ (cpd.py:176-184).
-* fp64 master rows stay on their owner; column norms for the normalisation
-  (cpd.py:187-195) come from the diagonal of the all-reduced Gram, so every
-  rank applies identical scalings.  The full fp64 factors are gathered once,
-  at the end, for the returned KruskalModel.
+* the ALS update ``F_n[rows_g] = Y_g · V†`` is row-local (cpd.py:170-172) and
+  runs fused with the Gram partial and the fit term (``hbk_als_update``);
+  V is built from Grams every rank holds;
+* exchanges per mode: each rank broadcasts its contiguous fp32 rows of the
+  new factor straight into every rank's replicated copy (uneven shards, no
+  padding or reassembly copy), one all-reduce of the R×R fp64 Gram partial
+  (cpd.py:39-42); per sweep one scalar all-reduce for ⟨X, X̂⟩ (cpd.py:176-184).
+* column normalisation (cpd.py:187-195) is kept as per-column scales folded
+  into the next update matrix, so it costs no pass over the factors.
+"""
 """
 from __future__ import annotations
 
@@ -102,7 +102,13 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
     every rank.  ``local_mttkrp(mode, factors32) -> (rows_g, R)`` and
     ``ranges`` (per mode, the row ranges of all ranks) replace the GPU shards
     (used by the CPU tests); by default the HB-CSF shards are built on the GPU
-    and the collectives run on NCCL."""
+    and the collectives run on NCCL.
+
+    Factors are kept in fp32 (the MTTKRP's input precision) as raw matrices
+    with per-column scales s_d: the true factor is F_d diag(s_d).  The scales
+    absorb the column normalisation (cpd.py:187-195) and fold into the 32x32
+    update matrix, so no pass over the factors is spent on it; Grams, fit
+    terms and the pseudo-inverse stay fp64 (cpd.py:39-83,176-184)."""
     import torch
 
     dist = _dist()
@@ -133,64 +139,115 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
     if over:
         warnings.warn(f"rank {rank} exceeds the extent of mode(s) {over}; the problem is "
                       "over-complete and factors will be rank-deficient", RuntimeWarning)
+    fused = device.type == "cuda" and rank == 32
 
     rng = np.random.default_rng(seed)
-    init = [rng.random((dim, rank)) for dim in dims]  # cpd.py:231-232, identical on every rank
+    f32 = [torch.from_numpy(rng.random((dim, rank))).to(device=device, dtype=torch.float32)
+           for dim in dims]  # cpd.py:231-232, identical on every rank
+    scales = [np.ones(rank) for _ in dims]
     own = [ranges[d][me] for d in range(order)]
-    f64 = [torch.from_numpy(init[d][lo:hi].copy()).to(device) for d, (lo, hi) in enumerate(own)]
-    f32 = [torch.from_numpy(init[d]).to(device=device, dtype=torch.float32) for d in range(order)]
 
-    def gram_allreduce(local):
-        g = local.T @ local
-        dist.all_reduce(g, group=group)
-        g = g.cpu().numpy()
+    def allreduce_(x):
+        dist.all_reduce(x, group=group)
+        return x
+
+    def gram_raw(local):
+        g = torch.zeros((rank, rank), dtype=torch.float64, device=device)
+        for a in range(0, local.shape[0], 1 << 20):  # fp32 partials over <= 1M rows
+            c = local[a: a + (1 << 20)]
+            g += (c.T @ c).double()
+        return g
+
+    def true_gram(d, g_raw):
+        s = scales[d]
+        g = (g_raw.cpu().numpy() * np.outer(s, s))
         return (g + g.T) * 0.5
 
-    def scalar_allreduce(x):
-        v = torch.tensor([x], dtype=torch.float64, device=device)
-        dist.all_reduce(v, group=group)
-        return float(v.item())
-
-    def all_true(flag):
-        v = torch.tensor([0.0 if flag else 1.0], dtype=torch.float64, device=device)
-        dist.all_reduce(v, group=group)
-        return float(v.item()) == 0.0
+    def exchange(d):
+        """Replicate factor d's rows: rank r broadcasts its contiguous rows."""
+        if world == 1:
+            return
+        for r, (lo, hi) in enumerate(ranges[d]):
+            if hi > lo:
+                dist.broadcast(f32[d][lo:hi], src=r, group=group)
 
     def sync():
         if device.type == "cuda":
             torch.cuda.synchronize(device)
 
-    grams = [gram_allreduce(f) for f in f64]
+    grams = []
+    for d in range(order):
+        lo, hi = own[d]
+        grams.append(true_gram(d, allreduce_(gram_raw(f32[d][lo:hi]))))
     norm_x = _value_norm(torch, t)
     last = order - 1
 
-    def fit_of(y_local, grams):
+    def fit_value(inner):
         norm_hat_sq = float((hadamard_all_but(grams, last) * grams[last]).sum())
-        inner = scalar_allreduce(float((y_local.double() * f64[last]).sum()))
         err_sq = max(norm_x * norm_x + norm_hat_sq - 2.0 * inner, 0.0)
         return 1.0 - math.sqrt(err_sq) / norm_x
 
-    fit = fit_of(local_mttkrp(last, f32), grams)
-    history = [AlsIteration(0, fit, 0.0, (), ())]
+    def colscale(mode):
+        c = np.ones(rank)
+        for d in range(order):
+            if d != mode:
+                c = c * scales[d]
+        return c
+
+    y0 = local_mttkrp(last, f32).double()
+    lo, hi = own[last]
+    inner0 = float((y0 * torch.from_numpy(colscale(last)).to(device)
+                    * (f32[last][lo:hi].double() * torch.from_numpy(scales[last]).to(device))).sum())
+    history = [AlsIteration(0, fit_value(float(allreduce_(torch.tensor([inner0], dtype=torch.float64,
+                                                                      device=device)).item())),
+                            0.0, (), ())]
+    del y0
     lam = None
+    inner_t = torch.zeros(1, dtype=torch.float64, device=device)
     for it in range(1, max_iters + 1):
         seconds = []
-        y = None
+        inner = 0.0
         for mode in range(order):
             sync()
             tic = time.perf_counter()
-            y = local_mttkrp(mode, f32).double()
-            vinv = torch.from_numpy(pinv_spsd(hadamard_all_but(grams, mode))).to(device)
-            factor = y @ vinv
-            if not all_true(bool(torch.isfinite(factor).all())):
+            y = local_mttkrp(mode, f32).float().contiguous()
+            c = colscale(mode)
+            # F_true = (Y_raw diag(c)) V^+  ->  M = diag(c) V^+, new scales 1
+            m64 = c[:, None] * pinv_spsd(hadamard_all_but(grams, mode))
+            lo, hi = own[mode]
+            dst = f32[mode][lo:hi]
+            if fused and hi > lo:
+                from . import _native as N
+                import ctypes as C
+
+                m32 = torch.from_numpy(m64).to(device=device, dtype=torch.float32).contiguous()
+                w32 = torch.from_numpy(c).to(device=device, dtype=torch.float32)
+                g_raw = torch.empty((rank, rank), dtype=torch.float64, device=device)
+                N.call("hbk_als_update", C.c_void_p(y.data_ptr()), int(hi - lo), int(rank),
+                       C.c_void_p(m32.data_ptr()), C.c_void_p(w32.data_ptr()),
+                       C.c_void_p(dst.data_ptr()), C.c_void_p(g_raw.data_ptr()),
+                       C.c_void_p(inner_t.data_ptr()) if mode == last else None, N.stream_ptr())
+                if mode == last:
+                    inner = inner_t.clone()
+            else:
+                fm = y @ torch.from_numpy(m64).to(device=device, dtype=torch.float32)
+                dst.copy_(fm)
+                g_raw = gram_raw(dst)
+                if mode == last:
+                    inner = ((y.double() * torch.from_numpy(c).to(device)) * fm.double()).sum().reshape(1)
+            scales[mode] = np.ones(rank)
+            g = allreduce_(g_raw).cpu().numpy()
+            if not np.isfinite(g).all():
                 raise NumericalError(f"non-finite factor for mode {mode} in ALS sweep {it}", iteration=it)
-            f64[mode] = factor
-            f32[mode] = allgather_padded(torch, dist, factor.float(), ranges[mode], group)
-            grams[mode] = gram_allreduce(factor)
+            grams[mode] = (g + g.T) * 0.5
+            exchange(mode)
+            del y
             sync()
             seconds.append(time.perf_counter() - tic)
-        new_fit = fit_of(y, grams)
-        lam = _normalize(torch, f64, f32, grams, device)
+        if not torch.is_tensor(inner):
+            inner = torch.zeros(1, dtype=torch.float64, device=device)
+        new_fit = fit_value(float(allreduce_(inner.reshape(1)).item()))
+        lam = _normalize_scales(scales, grams)
         if not math.isfinite(new_fit):
             raise NumericalError(f"non-finite fit in ALS sweep {it}", iteration=it)
         delta = new_fit - history[-1].fit
@@ -198,9 +255,23 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
         if abs(delta) < fit_tol:
             break
     if len(history) == 1:
-        lam = _normalize(torch, f64, f32, grams, device)
-    full = [allgather_padded(torch, dist, f64[d], ranges[d], group).cpu().numpy() for d in range(order)]
+        lam = _normalize_scales(scales, grams)
+    full = [(f32[d].double() * torch.from_numpy(scales[d]).to(device)).cpu().numpy()
+            for d in range(order)]
     return KruskalModel(lam=lam, factors=tuple(full)), history
+
+
+def _normalize_scales(scales, grams):
+    """Column normalisation (cpd.py:187-195) applied to the scale vectors:
+    norms from diag of the true Grams; F_d diag(s_d) -> F_d diag(s_d / n_d)."""
+    lam = None
+    for d in range(len(scales)):
+        n = np.sqrt(np.maximum(np.diag(grams[d]), 0.0))
+        n = np.where(n > 0.0, n, 1.0)
+        scales[d] = scales[d] / n
+        grams[d] = grams[d] / np.outer(n, n)
+        lam = n.copy() if lam is None else lam * n
+    return lam
 
 
 def _value_norm(torch, t: CooTensor) -> float:
@@ -215,17 +286,3 @@ def _value_norm(torch, t: CooTensor) -> float:
                N.stream_ptr())
         return float(torch.linalg.vector_norm(v).item())
     return float(np.linalg.norm(t.values))
-
-
-def _normalize(torch, f64, f32, grams, device):
-    """Column norms from diag(G) of the all-reduced Grams (cpd.py:187-195)."""
-    lam = None
-    for d in range(len(f64)):
-        n = np.sqrt(np.maximum(np.diag(grams[d]), 0.0))
-        n = np.where(n > 0.0, n, 1.0)
-        nt = torch.from_numpy(n).to(device)
-        f64[d] = f64[d] / nt
-        f32[d] = (f32[d].double() / nt).float()
-        grams[d] = grams[d] / np.outer(n, n)
-        lam = n.copy() if lam is None else lam * n
-    return lam
