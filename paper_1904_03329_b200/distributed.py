@@ -20,7 +20,6 @@ One process per GPU (torchrun), ``torch.distributed`` for the plumbing
 * column normalisation (cpd.py:187-195) is kept as per-column scales folded
   into the next update matrix, so it costs no pass over the factors.
 """
-"""
 from __future__ import annotations
 
 import math
