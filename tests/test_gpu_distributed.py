@@ -85,3 +85,34 @@ def test_cp_als_distributed_single_rank_matches_cp_als(hb):
     assert np.allclose(m1.lam, m0.lam, rtol=1e-3)
     fits_ref, _, _ = P.cp_als(idx, vals, dims, rank=8, max_iters=5, fit_tol=1e-14, seed=3)
     assert np.allclose([h.fit for h in h1], fits_ref, atol=1e-5, rtol=0)
+
+
+@pytest.mark.parametrize("rows", [1, 255, 1000, 70000])
+def test_als_update_kernel_matches_fp64(rows):
+    """hbk_als_update: F = Y M, Gram = F^T F, weighted <Y, F> against an fp64
+    torch restatement (fp32 kernel arithmetic, so 1e-5 relative)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1904_03329_b200 import _native as N
+
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    Y = torch.rand((rows, 32), device="cuda", generator=g) - 0.3
+    M = torch.rand((32, 32), device="cuda", generator=g) - 0.5
+    w = torch.rand(32, device="cuda", generator=g) + 0.5
+    F = torch.empty_like(Y)
+    gram = torch.empty((32, 32), dtype=torch.float64, device="cuda")
+    inner = torch.empty(1, dtype=torch.float64, device="cuda")
+    N.call("hbk_als_update", C.c_void_p(Y.data_ptr()), rows, 32, C.c_void_p(M.data_ptr()),
+           C.c_void_p(w.data_ptr()), C.c_void_p(F.data_ptr()), C.c_void_p(gram.data_ptr()),
+           C.c_void_p(inner.data_ptr()), N.stream_ptr())
+    F64 = Y.double() @ M.double()
+    assert torch.allclose(F.double(), F64, rtol=1e-5, atol=1e-5)
+    G64 = F64.T @ F64
+    assert torch.allclose(gram, G64, rtol=1e-5, atol=1e-4 * float(G64.abs().max()) * 1e-2 + 1e-6)
+    I64 = float(((Y.double() * w.double()) * F64).sum())
+    assert abs(float(inner) - I64) <= 1e-5 * max(1.0, abs(I64))
+    with pytest.raises(ValueError):
+        N.call("hbk_als_update", C.c_void_p(Y.data_ptr()), rows, 16, C.c_void_p(M.data_ptr()),
+               None, C.c_void_p(F.data_ptr()), C.c_void_p(gram.data_ptr()), None, N.stream_ptr())
