@@ -219,6 +219,31 @@ int hbk_plan_execute_f64(const hbk_plan* p, const double* const* factors, double
                          void* stream);
 void hbk_plan_release(hbk_plan* p);
 
+/* ------------------------------------------------------- FROSTT text --
+ * parse_frostt / load_frostt / write_frostt, coo.py:117-205, on the host
+ * (multi-threaded; no device needed).  Parsing rules are the reference's:
+ * '#' starts a comment, blank lines are skipped, 1-based indices, order from
+ * the first data line (or `order` + `dims` when dims != NULL).  On a
+ * malformed line the call fails with HBK_EINVAL and, when the failure has a
+ * line, *out is still set so hbk_tns_info can report err_line (release it).
+ * threads: 0 = all cores (>= 1 MiB per chunk), > 0 = at most that many,
+ * < 0 = exactly -threads chunks.                                             */
+typedef struct hbk_tns hbk_tns;
+int hbk_tns_parse(const char* text, int64_t len, int order, const int64_t* dims, int threads,
+                  hbk_tns** out);
+int hbk_tns_load(const char* path, int order, const int64_t* dims, int threads, hbk_tns** out);
+/* order, nnz, dims [HBK_MAX_ORDER] (max index + 1 per mode, or the given
+ * dims), err_line (0 = none); any pointer may be NULL. */
+int hbk_tns_info(const hbk_tns* t, int* order, int64_t* nnz, int64_t* dims, int64_t* err_line);
+/* idx [host] nnz x order uint32 0-based row-major, vals [host] fp64. */
+int hbk_tns_export(const hbk_tns* t, uint32_t* idx, double* vals);
+void hbk_tns_release(hbk_tns* t);
+/* write_frostt text of nnz entries (1-based, "%.17g" values); *text is
+ * malloc'ed, free with hbk_tns_free_text. */
+int hbk_tns_format(const uint32_t* idx, const double* vals, int64_t nnz, int order, int threads,
+                   char** text, int64_t* len);
+void hbk_tns_free_text(char* text);
+
 /* ------------------------------------------------------------- CP-ALS --
  * Row update of one ALS mode on a row shard (cpd.py:157-195), fused:
  *   F = Y * M                 (cpd.py:172; M = pinv(V), 32x32 row-major fp32)

@@ -130,6 +130,13 @@ _SIGS = {
     "hbk_coo_slice_histogram": ([vp, C.c_int, vp, vp], C.c_int),
     "hbk_coo_select_rows": ([vp, C.c_int, i64, i64, vp, C.POINTER(vp)], C.c_int),
     "hbk_coo_shard_rows": ([vp, C.c_int, i64, i64, vp, C.POINTER(vp)], C.c_int),
+    "hbk_tns_parse": ([C.c_char_p, i64, C.c_int, vp, C.c_int, C.POINTER(vp)], C.c_int),
+    "hbk_tns_load": ([C.c_char_p, C.c_int, vp, C.c_int, C.POINTER(vp)], C.c_int),
+    "hbk_tns_info": ([vp, C.POINTER(C.c_int), C.POINTER(i64), vp, C.POINTER(i64)], C.c_int),
+    "hbk_tns_export": ([vp, vp, vp], C.c_int),
+    "hbk_tns_release": ([vp], None),
+    "hbk_tns_format": ([vp, vp, i64, C.c_int, C.c_int, C.POINTER(vp), C.POINTER(i64)], C.c_int),
+    "hbk_tns_free_text": ([vp], None),
     "hbk_als_update": ([vp, i64, C.c_int, vp, vp, vp, vp, vp, vp], C.c_int),
 }
 

@@ -10,6 +10,7 @@ someone reads them.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import Iterator, Sequence
 
 import numpy as np
@@ -256,3 +257,90 @@ def allmode_order(dims: Sequence[int], mode: int) -> tuple[int, ...]:
         raise ValueError(f"mode {mode} out of range for order {n}")
     rest = sorted((d for d in range(n) if d != mode), key=lambda d: (dims[d], d))
     return (mode, *rest)
+
+
+# ---------------------------------------------------------------- FROSTT text
+def _tns_to_tensor(handle) -> "CooTensor":
+    order = C.c_int()
+    nnz = C.c_int64()
+    dims = (C.c_int64 * N.HBK_MAX_ORDER)()
+    N.call("hbk_tns_info", handle, C.byref(order), C.byref(nnz), dims, None)
+    o, m = int(order.value), int(nnz.value)
+    idx = np.empty((m, o), dtype=INDEX_DTYPE)
+    vals = np.empty(m, dtype=VALUE_DTYPE)
+    N.call("hbk_tns_export", handle, idx.ctypes.data_as(C.c_void_p), vals.ctypes.data_as(C.c_void_p))
+    return CooTensor(tuple(int(dims[d]) for d in range(o)), idx, vals)
+
+
+def _tns_call(fn, *args) -> "CooTensor":
+    lib = N.lib()
+    h = C.c_void_p()
+    status = getattr(lib, fn)(*args, C.byref(h))
+    try:
+        if status != N.HBK_OK:
+            msg = lib.hbk_last_error().decode(errors="replace")
+            line = C.c_int64(0)
+            if h:
+                lib.hbk_tns_info(h, None, None, None, C.byref(line))
+            if status == N.HBK_EINVAL:
+                raise ParseError(msg, int(line.value) if line.value else None)
+            N.check(status)
+        return _tns_to_tensor(h)
+    finally:
+        if h:
+            lib.hbk_tns_release(h)
+
+
+def _dims_arg(dims):
+    if dims is None:
+        return 0, None
+    d = tuple(int(x) for x in dims)
+    if len(d) < 3:
+        raise ValueError(f"tensor order must be >= 3, got {len(d)}")
+    return len(d), N.i64_array(d)
+
+
+def parse_frostt(stream, dims: Sequence[int] | None = None, *, threads: int = 0) -> CooTensor:
+    """Parse FROSTT text into a CooTensor (coo.py:117-184), in libhbk's
+    multi-threaded host parser: '#' comments, blank lines skipped, 1-based
+    indices, order from the first data line unless ``dims`` is given.
+    Raises ParseError with the 1-based line of the first malformed line."""
+    order, darr = _dims_arg(dims)
+    text = stream if isinstance(stream, (str, bytes, bytearray)) else stream.read()
+    data = text.encode("utf-8") if isinstance(text, str) else bytes(text)
+    return _tns_call("hbk_tns_parse", data, len(data), order, darr, int(threads))
+
+
+def load_frostt(path: str, dims: Sequence[int] | None = None, *, threads: int = 0) -> CooTensor:
+    """Read and parse a .tns file (coo.py:198-200); the file is read and parsed in C++."""
+    order, darr = _dims_arg(dims)
+    return _tns_call("hbk_tns_load", os.fsencode(path), order, darr, int(threads))
+
+
+def _tns_text(t: CooTensor, threads: int = 0) -> bytes:
+    idx = np.ascontiguousarray(t.indices, dtype=INDEX_DTYPE)
+    vals = np.ascontiguousarray(t.values, dtype=VALUE_DTYPE)
+    ptr = C.c_void_p()
+    n = C.c_int64()
+    N.call("hbk_tns_format", idx.ctypes.data_as(C.c_void_p), vals.ctypes.data_as(C.c_void_p),
+           int(t.nnz), int(t.order), int(threads), C.byref(ptr), C.byref(n))
+    try:
+        return C.string_at(ptr, n.value)
+    finally:
+        N.lib().hbk_tns_free_text(ptr)
+
+
+def write_frostt(t: CooTensor, stream) -> None:
+    """FROSTT text (coo.py:187-195): 1-based indices, values with 17
+    significant digits (round-trip exact), entries in the tensor's order."""
+    text = _tns_text(t)
+    try:
+        stream.write(text.decode("ascii"))
+    except TypeError:
+        stream.write(text)
+
+
+def save_frostt(t: CooTensor, path: str) -> None:
+    """Write a .tns file (coo.py:203-205)."""
+    with open(path, "wb") as fh:
+        fh.write(_tns_text(t))

@@ -1329,6 +1329,13 @@ static HeavyLayout heavy_layout(const hbk_csf* c, const uint32_t* loff, const ui
   hl.ntasks = NG;
   hl.slots = nheavy;
   hl.segments = Fh;
+  if (getenv("HBK_DEBUG")) {
+    uint32_t heavy_nnz = 0;
+    HBK_CUDA(cudaMemcpyAsync(&heavy_nnz, hoff.as<uint32_t>() + S, 4, cudaMemcpyDeviceToHost, st));
+    HBK_CUDA(cudaStreamSynchronize(st));
+    fprintf(stderr, "hbk heavy: slices %u nnz %u segments %u warp-tasks %u positions %u (x4 groups)\n",
+            nheavy, heavy_nnz, G, NW, Mh);
+  }
   HBK_CUDA(cudaStreamSynchronize(st));
   return hl;
 }
