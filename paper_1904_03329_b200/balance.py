@@ -163,3 +163,38 @@ def assign_slice_blocks(t: CsfTensor, cfg: SplitConfig) -> BlockSchedule:
     out = N.new_out()
     N.call("hbk_assign_slice_blocks", t._h.ptr, int(cfg.block_size), N.stream_ptr(), C.byref(out))
     return BlockSchedule(_handle=N.Handle(out, "hbk_sched_release"))
+
+
+@dataclass(frozen=True)
+class ImbalanceMetrics:
+    """Population spread of nonzeros over slices and fibers (balance.py:192-207)."""
+
+    slices: int
+    fibers: int
+    nnz: int
+    mean_nnz_per_slice: float
+    stddev_nnz_per_slice: float
+    max_nnz_per_slice: int
+    mean_nnz_per_fiber: float
+    stddev_nnz_per_fiber: float
+    max_nnz_per_fiber: int
+
+    def to_dict(self) -> dict:
+        return dict(self.__dict__)
+
+
+def imbalance_metrics(t: CsfTensor) -> ImbalanceMetrics:
+    """Mean, population stddev and max of nonzeros per slice and per fiber
+    (per segment once split), balance.py:210-227.  Computed from the tree's
+    pointer arrays (built on the GPU)."""
+    if t.nnz == 0:
+        return ImbalanceMetrics(0, 0, 0, 0.0, 0.0, 0, 0.0, 0.0, 0)
+    slice_nnz = t.slice_nnz()
+    fiber_nnz = t.fiber_sizes()
+    return ImbalanceMetrics(
+        slices=t.num_slices, fibers=t.num_fibers, nnz=t.nnz,
+        mean_nnz_per_slice=float(slice_nnz.mean()), stddev_nnz_per_slice=float(slice_nnz.std()),
+        max_nnz_per_slice=int(slice_nnz.max()),
+        mean_nnz_per_fiber=float(fiber_nnz.mean()), stddev_nnz_per_fiber=float(fiber_nnz.std()),
+        max_nnz_per_fiber=int(fiber_nnz.max()),
+    )
