@@ -202,7 +202,8 @@ typedef struct {
   int64_t nnz;
   int64_t stream_bytes;    /* index + value bytes read per execute        */
   int64_t tasks_heavy;     /* group tasks of the heavy-slice CSF layout   */
-  int64_t hot_rows;        /* factor rows gathered with the L2 evict-last policy */
+  int64_t hot_rows;        /* reserved (0) */
+  int64_t csl_blocks;      /* B-row blocks of the fast CSL task order (0/1 = unblocked) */
 } hbk_plan_info;
 
 int hbk_plan_create(hbk_coo* coo, hbk_csl* csl, hbk_csf* csf, hbk_sched* sched, int mode,

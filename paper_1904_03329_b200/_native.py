@@ -84,6 +84,7 @@ class PlanInfo(C.Structure):
         ("stream_bytes", i64),
         ("tasks_heavy", i64),
         ("hot_rows", i64),
+        ("csl_blocks", i64),
     ]
 
 

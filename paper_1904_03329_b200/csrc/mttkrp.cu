@@ -1232,6 +1232,137 @@ __global__ void k_gather_u32(const uint32_t* __restrict__ src, const uint32_t* _
     dst[i] = src[perm[i]];
 }
 
+// ------------------------------------------------ CSL B-row blocking --
+// In a CSL slice the nonzeros are sorted by rest[0] (the B-row index), so the
+// nonzeros whose B rows fall in one block of BB rows are one contiguous
+// segment of the stream.  When the B factor exceeds the L2 budget, the fast
+// path cuts every slice into its per-block segments and orders the tasks by
+// (block, slice): the persistent kernel pulls tasks in that order, so at any
+// time the warps gather B rows from ~one block, which stays L2-resident
+// (on delicious-3d the near-uniform B factor is 2.5x the L2).  Slices cut into
+// several tasks hand over through the split-slice accumulator.
+__global__ void k_csl_segflags(const uint32_t* __restrict__ j, int64_t M, uint32_t BB,
+                               uint32_t* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
+       i += int64_t(gridDim.x) * blockDim.x)
+    flag[i] = (i == 0) || (j[i] / BB != j[i - 1] / BB);
+}
+__global__ void k_csl_slicestarts(const uint32_t* __restrict__ sptr, int64_t S,
+                                  uint32_t* __restrict__ flag) {
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < S;
+       s += int64_t(gridDim.x) * blockDim.x)
+    flag[sptr[s]] = 1;
+}
+__global__ void k_csl_segs(const uint32_t* __restrict__ pos, int64_t M, uint32_t* __restrict__ start) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
+       i += int64_t(gridDim.x) * blockDim.x)
+    if (pos[i + 1] != pos[i]) start[pos[i]] = uint32_t(i);
+}
+// per segment: slice, block, task count; per slice: task count (atomic)
+__global__ void k_csl_seginfo(const uint32_t* __restrict__ start, int64_t G, uint32_t M,
+                              const uint32_t* __restrict__ sptr, int64_t S,
+                              const uint32_t* __restrict__ j, uint32_t BB, uint32_t T,
+                              uint32_t* __restrict__ sslice, uint32_t* __restrict__ sblock,
+                              uint32_t* __restrict__ sntask, uint32_t* __restrict__ slice_ntask) {
+  for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < G;
+       g += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t a = start[g], b = (g + 1 < G) ? start[g + 1] : M;
+    int64_t lo = 0, hi = S;  // last slice with sptr[s] <= a
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (sptr[mid] <= a) lo = mid; else hi = mid;
+    }
+    const uint32_t nt = (b - a + T - 1) / T;
+    sslice[g] = uint32_t(lo);
+    sblock[g] = j[a] / BB;
+    sntask[g] = nt;
+    atomicAdd(slice_ntask + lo, nt);
+  }
+}
+__global__ void k_select_count(const uint32_t* __restrict__ key, const uint32_t* __restrict__ val,
+                               int64_t n, uint32_t want, uint32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = key[i] == want ? val[i] : 0u;
+}
+__global__ void k_csl_seg_tasks(const uint32_t* __restrict__ start, int64_t G, uint32_t M,
+                                const uint32_t* __restrict__ sslice, const uint32_t* __restrict__ sblock,
+                                const uint32_t* __restrict__ sntask, const uint32_t* __restrict__ pos_in_block,
+                                uint32_t block, uint32_t base, const uint32_t* __restrict__ slice_ntask,
+                                const uint32_t* __restrict__ slice_slot, uint32_t slot_base,
+                                Task* __restrict__ tasks) {
+  for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < G;
+       g += int64_t(gridDim.x) * blockDim.x) {
+    if (sblock[g] != block) continue;
+    const uint32_t a = start[g], b = (g + 1 < G) ? start[g + 1] : M, m = b - a;
+    const uint32_t nt = sntask[g], s = sslice[g], total = slice_ntask[s];
+    Task* out = tasks + base + pos_in_block[g];
+    for (uint32_t c = 0; c < nt; ++c) {
+      Task t{};
+      t.lo = a + uint32_t((uint64_t(m) * c) / nt);
+      t.hi = a + uint32_t((uint64_t(m) * (c + 1)) / nt);
+      t.s = s;
+      t.f = 0;
+      t.slot = total > 1 ? slot_base + slice_slot[s] : NOSLOT;
+      t.nchunk = total;
+      out[c] = t;
+    }
+  }
+}
+__global__ void k_gt1_flags(const uint32_t* __restrict__ n, int64_t S, uint32_t* __restrict__ f) {
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < S;
+       s += int64_t(gridDim.x) * blockDim.x)
+    f[s] = n[s] > 1;
+}
+
+static BucketTasks csl_block_tasks(const hbk_csl* c, uint32_t BB, uint32_t T, uint32_t slot_base,
+                                   int64_t* nblocks_out, cudaStream_t st) {
+  BucketTasks bt;
+  const int64_t M = c->M, S = c->S;
+  const uint32_t* j = c->rest[0].as<uint32_t>();
+  const uint32_t* sptr = c->slice_ptr.as<uint32_t>();
+  const uint32_t nb = uint32_t((c->dims[c->mode_order[1]] + BB - 1) / BB);
+  *nblocks_out = nb;
+  Scratch flag((M + 1) * 4, st);
+  k_csl_segflags<<<grid_for(M, 256), 256, 0, st>>>(j, M, BB, flag.as<uint32_t>());
+  k_csl_slicestarts<<<grid_for(S, 256), 256, 0, st>>>(sptr, S, flag.as<uint32_t>());
+  check_launch("k_csl_segflags");
+  const uint32_t G = exclusive_scan_total(flag.as<uint32_t>(), M, st);
+  Scratch start(size_t(G) * 4, st), sslice(size_t(G) * 4, st), sblock(size_t(G) * 4, st),
+      sntask(size_t(G) * 4, st), pos((size_t(G) + 1) * 4, st), slice_nt((S + 1) * 4, st),
+      slice_slot((S + 1) * 4, st);
+  k_csl_segs<<<grid_for(M, 256), 256, 0, st>>>(flag.as<uint32_t>(), M, start.as<uint32_t>());
+  HBK_CUDA(cudaMemsetAsync(slice_nt.p, 0, (S + 1) * 4, st));
+  k_csl_seginfo<<<grid_for(G, 256), 256, 0, st>>>(start.as<uint32_t>(), G, uint32_t(M), sptr, S, j,
+                                                  BB, T, sslice.as<uint32_t>(),
+                                                  sblock.as<uint32_t>(), sntask.as<uint32_t>(),
+                                                  slice_nt.as<uint32_t>());
+  check_launch("k_csl_seginfo");
+  k_gt1_flags<<<grid_for(S, 256), 256, 0, st>>>(slice_nt.as<uint32_t>(), S, slice_slot.as<uint32_t>());
+  const uint32_t nslot = exclusive_scan_total(slice_slot.as<uint32_t>(), S, st);
+  HBK_CUDA(cudaMemcpyAsync(pos.p, sntask.p, size_t(G) * 4, cudaMemcpyDeviceToDevice, st));
+  const uint32_t ntask = exclusive_scan_total(pos.as<uint32_t>(), G, st);
+  bt.tasks = Scratch(size_t(std::max<uint32_t>(ntask, 1)) * sizeof(Task), st);
+  uint32_t base = 0;
+  for (uint32_t b = 0; b < nb; ++b) {
+    k_select_count<<<grid_for(G, 256), 256, 0, st>>>(sblock.as<uint32_t>(), sntask.as<uint32_t>(),
+                                                     G, b, pos.as<uint32_t>());
+    const uint32_t nb_tasks = exclusive_scan_total(pos.as<uint32_t>(), G, st);
+    if (nb_tasks) {
+      k_csl_seg_tasks<<<grid_for(G, 256), 256, 0, st>>>(
+          start.as<uint32_t>(), G, uint32_t(M), sslice.as<uint32_t>(), sblock.as<uint32_t>(),
+          sntask.as<uint32_t>(), pos.as<uint32_t>(), b, base, slice_nt.as<uint32_t>(),
+          slice_slot.as<uint32_t>(), slot_base, bt.tasks.as<Task>());
+      check_launch("k_csl_seg_tasks");
+    }
+    base += nb_tasks;
+  }
+  HBK_REQUIRE(base == ntask, HBK_ECUDA, "CSL block task accounting mismatch");
+  bt.n = ntask;
+  bt.slots = nslot;
+  return bt;
+}
+
 struct HeavyLayout {
   Buf pairs, fj, tasks;
   int64_t ntasks = 0;  // group tasks (4 per warp task)
@@ -1363,7 +1494,8 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
 
   Work& w = p->work;
   std::memset(&w, 0, sizeof(w));
-  BucketTasks tcsf, tcsl, tcsf_light;
+  BucketTasks tcsf, tcsl, tcsf_light, tcsl_fast;
+  bool csl_blocked = false;
   // heavy-slice layout (fast path): slices with more than H nonzeros
   // B-position streams (default fast CSF path): every slice with more than
   // Tcsf nonzeros goes to the heavy layout, lighter slices form runs
@@ -1521,7 +1653,22 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
                                                            uint32_t(slots));
       check_launch("k_shift_slots");
     }
-    slots += tcsl.slots;
+    // B-row blocking of the fast CSL tasks (opt-in: HBK_CSL_BLOCK_MB = MB of
+    // B rows per block).  Measured on delicious-3d: 96 MB blocks -7% on mode
+    // 0, smaller blocks up to 3x slower (per-slice segments become tiny tasks
+    // with split hand-overs), so it is off by default.
+    if (p->fast) {
+      double mb = 0.0;
+      if (const char* e = getenv("HBK_CSL_BLOCK_MB")) mb = atof(e);
+      const int64_t BB = std::max<int64_t>(1, int64_t(mb * 1e6 / (R * 4.0)));
+      if (mb > 0 && s->dims[s->mode_order[1]] > BB) {
+        int64_t nb = 0;
+        tcsl_fast = csl_block_tasks(s, uint32_t(BB), Tcsl, uint32_t(slots), &nb, st);
+        csl_blocked = nb > 1;
+        p->info.csl_blocks = nb;
+      }
+    }
+    slots += std::max(tcsl.slots, csl_blocked ? tcsl_fast.slots : int64_t(0));
     w.csl_send = s->slice_ptr.as<uint32_t>();
     w.csl_sidx = s->slice_idx.as<uint32_t>();
     w.csl_j = s->rest[0].as<uint32_t>();
@@ -1595,8 +1742,8 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     w.zero_rows = p->zero_rows.as<uint32_t>();
     p->info.tasks_zero = n_zero;
     // assemble [CSF | CSL | COO | ZERO], each padded to a multiple of gpw
-    auto assemble = [&](const BucketTasks& tc, Buf& store, Work& wo) {
-      const int64_t a0 = pad_to(tc.n, gpw), a1 = pad_to(tcsl.n, gpw), a2 = pad_to(n_coo, gpw),
+    auto assemble = [&](const BucketTasks& tc, const BucketTasks& tl, Buf& store, Work& wo) {
+      const int64_t a0 = pad_to(tc.n, gpw), a1 = pad_to(tl.n, gpw), a2 = pad_to(n_coo, gpw),
                     a3 = pad_to(n_zero, gpw);
       const int64_t total = a0 + a1 + a2 + a3;
       store = dalloc(std::max<int64_t>(total, 1) * sizeof(Task), st);
@@ -1607,8 +1754,8 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       }
       if (tc.n)
         HBK_CUDA(cudaMemcpyAsync(T, tc.tasks.p, tc.n * sizeof(Task), cudaMemcpyDeviceToDevice, st));
-      if (tcsl.n)
-        HBK_CUDA(cudaMemcpyAsync(T + a0, tcsl.tasks.p, tcsl.n * sizeof(Task),
+      if (tl.n)
+        HBK_CUDA(cudaMemcpyAsync(T + a0, tl.tasks.p, tl.n * sizeof(Task),
                                  cudaMemcpyDeviceToDevice, st));
       if (n_coo) {
         k_range_tasks<<<grid_for(n_coo, 256), 256, 0, st>>>(T + a0 + a1, n_coo,
@@ -1626,14 +1773,14 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       wo.n3 = uint32_t(total);
       wo.tasks = T;
     };
-    if (heavy_on) {
-      assemble(tcsf_light, p->tasks, w);
-      assemble(tcsf, p->gen_tasks, p->work_gen);
+    if (heavy_on || csl_blocked) {
+      assemble(heavy_on ? tcsf_light : tcsf, csl_blocked ? tcsl_fast : tcsl, p->tasks, w);
+      assemble(tcsf, tcsl, p->gen_tasks, p->work_gen);
     } else {
-      assemble(tcsf, p->tasks, w);
+      assemble(tcsf, tcsl, p->tasks, w);
     }
     p->info.tasks_csf = heavy_on ? tcsf_light.n : tcsf.n;
-    p->info.tasks_csl = tcsl.n;
+    p->info.tasks_csl = csl_blocked ? tcsl_fast.n : tcsl.n;
     p->info.tasks_coo = n_coo;
   }
   // workspace: [ctr(2) pad to 32 words][cnt slots][acc slots x R]
@@ -1645,7 +1792,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   w.ws_ctr = reinterpret_cast<uint32_t*>(p->ws.as<char>());
   w.ws_cnt = reinterpret_cast<uint32_t*>(p->ws.as<char>() + cnt_off);
   w.ws_acc = reinterpret_cast<float*>(p->ws.as<char>() + acc_off);
-  if (!heavy_on) {
+  if (!heavy_on && !csl_blocked) {
     p->work_gen = w;
   } else {
     Work& wg = p->work_gen;

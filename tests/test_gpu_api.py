@@ -306,3 +306,32 @@ def test_pinned_host_factors_match_numpy(hb, rng):
     h = hb.build_hbcsf(t, hb.allmode_order(t.dims, 0))
     with pytest.raises(ValueError):
         hb.mttkrp_hbcsf(h, bad, 0)
+
+
+@pytest.mark.parametrize("block_mb", ["0.002", "0.0005"])
+def test_csl_b_row_blocking_parity(hb, rng, block_mb, monkeypatch):
+    """The fast CSL path cut into per-B-block segments (tasks ordered by
+    block, split slices handed over through the accumulator) gives the
+    oracle's rows.  Tiny blocks force many segments per slice."""
+    monkeypatch.setenv("HBK_CSL_BLOCK_MB", block_mb)
+    dims = (60, 500, 400)
+    # CSL-dominated: distinct (j, k) per slice, so every fiber is a singleton
+    n = 6000
+    i = rng.integers(0, 60, n)
+    j = rng.integers(0, 500, n)
+    k = rng.integers(0, 400, n)
+    idx = np.stack([i, j, k], 1).astype(np.uint32)
+    idx, vals = P.canonical(idx, rng.uniform(0.1, 1.0, n))
+    t = hb.CooTensor(dims, idx, vals)
+    f = [rng.random((d, 32)).astype(np.float32).astype(np.float64) for d in dims]
+    for mode in range(3):
+        mo = hb.allmode_order(dims, mode)
+        h = hb.build_hbcsf(t, mo)
+        from paper_1904_03329_b200.kernels import plan_for
+
+        pl = plan_for(h, mode, 32)
+        if h.csl_part.nnz and dims[mo[1]] * 128 > float(block_mb) * 1e6:
+            assert pl.info.csl_blocks > 1
+        y, _ = hb.mttkrp_hbcsf(h, f, mode)
+        ref, _ = P.mttkrp_hbcsf(P.hbcsf(idx, vals, dims, mo), f, mode)
+        assert P.row_deviation(y, ref) <= 1e-4
