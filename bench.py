@@ -336,6 +336,41 @@ def main():
     flops_step = 3.0 * nnz_total * RANK * n_modes
     value = flops_step / (ms_per_step * 1e-3) / 1e9
 
+    # gather ceiling: the plans' gather-only calibration kernels over the same
+    # task lists and streams (hbk_plan_probe), timed the same way
+    gather = None
+    try:
+        rows = [int(pl.info.gather_rows) if pl is not None else 0 for pl in plans]
+        if all(r > 0 for r, pl in zip(rows, plans) if pl is not None):
+            pev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    for _ in range(args.steps)] for _ in range(n_modes)]
+            for m in range(n_modes):
+                if plans[m] is not None:
+                    plans[m].probe(ptrs[m])
+            torch.cuda.synchronize()
+            for s_ in range(args.steps):
+                for m in range(n_modes):
+                    if plans[m] is None:
+                        continue
+                    pev[m][s_][0].record(stream)
+                    plans[m].probe(ptrs[m])
+                    pev[m][s_][1].record(stream)
+            torch.cuda.synchronize()
+            probe_ms = [statistics.mean(a.elapsed_time(b) for a, b in pev[m]) if plans[m] is not None
+                        else 0.0 for m in range(n_modes)]
+            gather = {
+                "rows_per_step": sum(rows),
+                "kernel_rows_per_s": sum(rows) / (sum(per_mode_ms) * 1e-3),
+                "ceiling_rows_per_s": sum(rows) / (sum(probe_ms) * 1e-3),
+                "frac": sum(probe_ms) / sum(per_mode_ms),
+                "probe_ms_per_mode": probe_ms,
+                "note": ("128-byte factor rows delivered to the SMs (leaf rows + fiber rows, 2 per "
+                         "CSL/COO nonzero); ceiling = gather-only kernel over the same tasks "
+                         "(hbk_plan_probe)"),
+            }
+    except Exception as e:  # calibration is optional; never fail the bench on it
+        gather = {"error": str(e)}
+
     # roofline over the per-mode launches (each step is one launch per mode)
     hbm, hbm_src = peaks()
     # this rank's launches: its own output rows, every input factor row
@@ -438,6 +473,7 @@ def main():
                 "traffic_unit": "DRAM bytes per MTTKRP launch (ncu dram__bytes_read+write, profiles/)",
                 "per_mode_ms": per_mode_ms, "per_mode_bytes": bytes_modes,
                 "per_mode_frac": [b / (ms * 1e-3) / 1e9 / hbm for b, ms in zip(bytes_modes, per_mode_ms)],
+                "gather": gather,
             },
             "cpu_baseline": cpu,
             "e2e": e2e,

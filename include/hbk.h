@@ -204,6 +204,7 @@ typedef struct {
   int64_t tasks_heavy;     /* group tasks of the heavy-slice CSF layout   */
   int64_t hot_rows;        /* reserved (0) */
   int64_t csl_blocks;      /* B-row blocks of the fast CSL task order (0/1 = unblocked) */
+  int64_t gather_rows;     /* factor rows one execute gathers (B-position plans) */
 } hbk_plan_info;
 
 int hbk_plan_create(hbk_coo* coo, hbk_csl* csl, hbk_csf* csf, hbk_sched* sched, int mode,
@@ -219,6 +220,11 @@ int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out,
 int hbk_plan_execute_f64(const hbk_plan* p, const double* const* factors, double* out,
                          void* stream);
 void hbk_plan_release(hbk_plan* p);
+/* Roofline calibration: walk the plan's task lists and streams exactly as
+ * hbk_plan_execute does but only gather the factor rows (no arithmetic, no
+ * output).  Its time is the row-gather ceiling of this plan on this GPU;
+ * info.gather_rows / time = rows per second.  B-position plans only. */
+int hbk_plan_probe(const hbk_plan* p, const float* const* factors, void* stream);
 
 /* ------------------------------------------------------- FROSTT text --
  * parse_frostt / load_frostt / write_frostt, coo.py:117-205, on the host

@@ -568,6 +568,83 @@ __global__ void __launch_bounds__(FAST_BLOCK, (KIND == KIND_CSF_BPOS4 || KIND ==
 }
 
 
+// ------------------------------------------------------- gather probe --
+// Calibration kernel for the roofline: walks exactly the task lists and
+// streams of a plan with the same warp/group structure as k_mttkrp3_r32 but
+// only gathers the factor rows (summing them into one register), so its time
+// is this plan's row-gather ceiling on this GPU — the resource that bounds
+// the MTTKRP when factor rows are L2-resident.
+template <int KIND>
+__global__ void __launch_bounds__(FAST_BLOCK, 4)
+    k_gather_probe(const __grid_constant__ Work w, const __grid_constant__ Factors3 fx,
+                   float4* __restrict__ sink) {
+  const int lane = threadIdx.x & 31, g = lane >> 3, lig = lane & 7;
+  const uint64_t pol_s = policy_evict_first();
+  const uint64_t pol_r = policy_evict_last();
+  const float4* Cl = fx.C + lig;
+  const float4* Bl = fx.B + lig;
+  float4 acc = f4zero();
+  const uint32_t first = KIND == KIND_CSL ? w.n0 : (KIND == KIND_COO ? w.n1 : 0u);
+  const uint32_t last = KIND == KIND_CSL ? w.n1 : (KIND == KIND_COO ? w.n2 : w.n0);
+  uint32_t* ctr = w.ws_ctr + 8;  // probe counters (words 8, 9), self-resetting
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(ctr, 4u);
+    base = __shfl_sync(FULL, base, 0) + first;
+    if (base >= last) break;
+    const Task t = w.tasks[base + g];
+    const uint32_t nbat = __reduce_max_sync(FULL, t.hi > t.lo ? (t.hi - t.lo + 7) / 8 : 0u);
+    uint32_t p0 = t.lo;
+    for (uint32_t it = 0; it < nbat; ++it, p0 += 8) {
+      const bool live = p0 + lig < t.hi;
+      if (KIND == KIND_CSF) {
+        const uint2 pr = live ? ld_stream_u2(w.csf_pairs + p0 + lig, pol_s) : make_uint2(0u, 0u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t xj = __shfl_sync(FULL, pr.x, j, 8);
+          acc = add4(acc, ld_row4(((xj & FB) ? Bl : Cl) + (xj & XMASK), pol_r));
+        }
+      } else if (KIND == KIND_CSL) {
+        const uint2 pr = live ? ld_stream_u2(w.csl_pairs + p0 + lig, pol_s) : make_uint2(0u, 0u);
+        const uint32_t jx = live ? ld_stream_u32(w.csl_j + p0 + lig, pol_s) : 0u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t kj = __shfl_sync(FULL, pr.x, j, 8) & KMASK;
+          const uint32_t bj = __shfl_sync(FULL, jx, j, 8);
+          acc = add4(acc, ld_row4(Cl + size_t(kj) * 8, pol_r));
+          acc = add4(acc, ld_row4(Bl + size_t(bj) * 8, pol_r));
+        }
+      } else {
+        const uint4 q = live ? ld_stream_u4(w.coo_quads + p0 + lig, pol_s) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t bj = __shfl_sync(FULL, q.y, j, 8);
+          const uint32_t cj = __shfl_sync(FULL, q.z, j, 8);
+          acc = add4(acc, ld_row4(Cl + size_t(cj) * 8, pol_r));
+          acc = add4(acc, ld_row4(Bl + size_t(bj) * 8, pol_r));
+        }
+      }
+    }
+  }
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  if (lane == 0) {
+    const uint32_t done = atomicAdd(ctr + 1, 1u);
+    if (done == gridDim.x * (blockDim.x >> 5) - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+  }
+}
+
+__global__ void k_task_span(const Task* __restrict__ t, int64_t n, unsigned long long* __restrict__ out) {
+  unsigned long long s = 0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    s += t[i].hi > t[i].lo ? t[i].hi - t[i].lo : 0u;
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
 // --------------------------------------------------------- generic kernel --
 // Any order, any rank: one warp per task, lanes over rank columns, nonzeros
 // walked one at a time.  Used for order > 3 or R != 32 (parity coverage; the
@@ -958,7 +1035,7 @@ struct hbk_plan {
   hbk::Work work{};      // fast kernels (light CSF tasks when the heavy layout is on)
   hbk::Work work_gen{};  // generic kernel (every CSF slice in tree order)
   hbk::Work work_heavy{};
-  hbk::Buf heavy_pairs, heavy_fj, heavy_tasks, gen_tasks;
+  hbk::Buf heavy_pairs, heavy_fj, heavy_tasks, gen_tasks, probe_sink;
   int grid_heavy = 0;
   bool fast = false;
   int csf_variant = 2;  // 0: smem-slot kernel, 1|2: B-position streams at 3|4 CTAs per SM (HBK_CSF_VARIANT)
@@ -1885,6 +1962,24 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   p->info.op_muls = muls;
   p->info.op_adds = adds;
   p->info.stream_bytes = stream_bytes;
+  // rows one execute gathers (B-position plans): CSF positions + 2 per CSL/COO nonzero
+  if (p->bpos) {
+    Scratch acc(4 * 8, st);
+    HBK_CUDA(cudaMemsetAsync(acc.p, 0, 4 * 8, st));
+    unsigned long long* a = acc.as<unsigned long long>();
+    if (w.n0) k_task_span<<<grid_for(w.n0, 256), 256, 0, st>>>(w.tasks, w.n0, a + 0);
+    if (heavy_ntasks)
+      k_task_span<<<grid_for(heavy_ntasks, 256), 256, 0, st>>>(p->heavy_tasks.as<Task>(),
+                                                              heavy_ntasks, a + 1);
+    if (w.n1 > w.n0) k_task_span<<<grid_for(w.n1 - w.n0, 256), 256, 0, st>>>(w.tasks + w.n0,
+                                                                           w.n1 - w.n0, a + 2);
+    check_launch("k_task_span");
+    unsigned long long h[4] = {0, 0, 0, 0};
+    HBK_CUDA(cudaMemcpyAsync(h, a, sizeof(h), cudaMemcpyDeviceToHost, st));
+    HBK_CUDA(cudaStreamSynchronize(st));
+    p->info.gather_rows = int64_t(h[0] + h[1] + 2 * h[2]) + 2 * (p->coo ? p->coo->nnz : 0);
+    p->probe_sink = dalloc(size_t(sms) * 8 * FAST_BLOCK * sizeof(float4), st);
+  }
   HBK_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -2035,6 +2130,27 @@ int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out,
     } else {
       launch_generic<float>(p, factors, out, st);
     }
+  });
+}
+
+int hbk_plan_probe(const hbk_plan* p, const float* const* factors, void* stream) {
+  return guarded([&] {
+    HBK_REQUIRE(p->bpos, HBK_EINVAL, "the gather probe needs a B-position (fast order-3, R=32) plan");
+    cudaStream_t st = to_stream(stream);
+    Factors3 fx;
+    fx.B = reinterpret_cast<const float4*>(factors[p->mo[1]]);
+    fx.C = reinterpret_cast<const float4*>(factors[p->mo[2]]);
+    fx.out = nullptr;
+    float4* sink = p->probe_sink.as<float4>();
+    int dev = 0, sms = 0;
+    HBK_CUDA(cudaGetDevice(&dev));
+    HBK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int grid = sms * 4;
+    if (p->work.n0) k_gather_probe<KIND_CSF><<<grid, FAST_BLOCK, 0, st>>>(p->work, fx, sink);
+    if (p->grid_heavy) k_gather_probe<KIND_CSF><<<grid, FAST_BLOCK, 0, st>>>(p->work_heavy, fx, sink);
+    if (p->work.n1 > p->work.n0) k_gather_probe<KIND_CSL><<<grid, FAST_BLOCK, 0, st>>>(p->work, fx, sink);
+    if (p->work.n2 > p->work.n1) k_gather_probe<KIND_COO><<<grid, FAST_BLOCK, 0, st>>>(p->work, fx, sink);
+    check_launch("k_gather_probe");
   });
 }
 

@@ -268,6 +268,10 @@ class _Plan:
     def opcount(self) -> OpCount:
         return OpCount(int(self.info.op_muls), int(self.info.op_adds))
 
+    def probe(self, factor_ptrs) -> None:
+        """Launch the plan's gather-only calibration kernels (hbk_plan_probe)."""
+        N.call("hbk_plan_probe", self.h.ptr, factor_ptrs, N.stream_ptr())
+
     def execute(self, factor_ptrs, out=None, precision: str = "fp32"):
         torch = N.require_device()
         dt = torch.float64 if precision == "fp64" else torch.float32
