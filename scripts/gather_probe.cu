@@ -159,6 +159,43 @@ __global__ void k_hot(const float4* __restrict__ F, const uint32_t* __restrict__
   out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = acc;
 }
 
+// cache-hint variants of the 8-lane LDG.128 row gather
+template <int HINT>
+__device__ __forceinline__ float4 ldrow_h(const float4* p) {
+  float4 v;
+  if (HINT == 0)
+    asm("ld.global.nc.L1::evict_last.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  else if (HINT == 1)
+    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  else if (HINT == 2)
+    asm("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  else if (HINT == 3)
+    asm("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  else
+    asm("ld.global.nc.L1::evict_first.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+template <int HINT>
+__global__ void k_ldg_hint(const float4* __restrict__ F, const uint32_t* __restrict__ idx, int64_t n,
+                           float4* __restrict__ out) {
+  const int lane = threadIdx.x & 31, lig = lane & 7;
+  const int64_t gid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 3;
+  const int64_t ngroups = (int64_t(gridDim.x) * blockDim.x) >> 3;
+  float4 acc = make_float4(0, 0, 0, 0);
+  for (int64_t base = gid * 8; base < n; base += ngroups * 8) {
+    uint32_t k = (base + lig < n) ? idx[base + lig] : 0;
+    float4 r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t kj = __shfl_sync(0xffffffffu, k, j, 8);
+      r[j] = ldrow_h<HINT>(F + size_t(kj) * 8 + lig);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { acc.x += r[j].x; acc.y += r[j].y; acc.z += r[j].z; acc.w += r[j].w; }
+  }
+  out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = acc;
+}
+
 // 4 lanes x LDG.256 per row (8 rows per warp instruction)
 struct f8 {
   float v[8];
@@ -408,6 +445,19 @@ int main() {
     printf("  hot all=%d H=%d thr=%d blk/sm=%d : %.3f ms  %.2f Grows/s\n", (int)(ALL), hh,       \
            THREADS, BLOCKS_PER_SM, ms, n / ms / 1e6);                                             \
   }
+#define RUN_HINT(H, BPS)                                                                       \
+  {                                                                                               \
+    int g = sms * BPS;                                                                            \
+    float ms = time_ms([&] { k_ldg_hint<H><<<g, 256>>>(F, idx, n, out); });                      \
+    printf("  hint=%d blk/sm=%d : %.3f ms  %.2f Grows/s\n", H, BPS, ms, n / ms / 1e6);         \
+  }
+    if (getenv("HINTS")) {
+      RUN_HINT(0, 4); RUN_HINT(1, 4); RUN_HINT(2, 4); RUN_HINT(3, 4); RUN_HINT(4, 4);
+      RUN_HINT(0, 8); RUN_HINT(1, 8); RUN_HINT(3, 8);
+      CK(cudaFree(idx));
+      CK(cudaFree(F));
+      continue;
+    }
     RUN_HOT(true, 512, 1024, 1);
     RUN_HOT(true, 1536, 1024, 1);
     RUN_HOT(false, 512, 512, 2);
