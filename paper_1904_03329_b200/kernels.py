@@ -126,8 +126,8 @@ class _HostStage:
     def upload_all(self, torch, items, dt):
         """items: [(d, host array)] -> ({d: CUDA tensor}, deferred checks).
         Page-locked torch tensors of the kernel dtype are copied as they are
-        (their finiteness is checked on the device: (d, flag) pairs the
-        caller tests after the launch).  Other factors are
+        (their finiteness is checked on the device: (d, device tensor) pairs
+        the caller tests after the launch).  Other factors are
         converted concurrently (one pool task per factor, or per chunk of a
         large one); the host-to-device copies are issued by the calling
         thread, on its current stream, as soon as each factor is staged."""
@@ -140,7 +140,7 @@ class _HostStage:
                 dev = torch.empty(tuple(f.shape), dtype=dt, device="cuda")
                 dev.copy_(f, non_blocking=True)
                 out[d] = dev
-                checks.append((d, torch.isfinite(dev).all()))
+                checks.append((d, dev))  # checked after the launch (_finish)
                 continue
             src = np.ascontiguousarray(f)
             if src.ndim != 2:
@@ -301,10 +301,15 @@ def _finish(plan: _Plan, factors, mode: int, out=None, precision: str = "fp32"):
     y = plan.execute(ptrs, out, precision)
     if on_device:
         return y, plan.opcount
-    rows = _host_stage().download(N.require_device(), y)
-    for d, ok in checks:  # pinned host tensors: checked on the device
-        if not bool(ok):
-            raise ValueError(f"factor {d} has non-finite entries")
+    torch = N.require_device()
+    # pinned host tensors are checked on the device, after the launch so the
+    # MTTKRP does not wait for the check kernels; one flag vector comes back
+    flags = torch.stack([torch.isfinite(dev).all() for _, dev in checks]) if checks else None
+    rows = _host_stage().download(torch, y)
+    if flags is not None:
+        for (d, _), ok in zip(checks, flags.cpu().tolist()):
+            if not ok:
+                raise ValueError(f"factor {d} has non-finite entries")
     return rows, plan.opcount
 
 
