@@ -13,9 +13,11 @@ One process per GPU (torchrun), ``torch.distributed`` for the plumbing
 * the ALS update ``F_n[rows_g] = Y_g · V†`` is row-local (cpd.py:170-172) and
   runs fused with the Gram partial and the fit term (``hbk_als_update``);
   V is built from Grams every rank holds;
-* exchanges per mode: each rank broadcasts its contiguous fp32 rows of the
-  new factor straight into every rank's replicated copy (uneven shards, no
-  padding or reassembly copy), one all-reduce of the R×R fp64 Gram partial
+* exchanges per mode: the touched-rows exchange — each rank receives, in one
+  all_to_all, only the rows of the new factor that its own shards of the
+  other modes read (``RowExchange``; index lists agreed once) — or, with
+  ``exchange="full"``, every rank broadcasts its contiguous fp32 rows into
+  every replicated copy; one all-reduce of the R×R fp64 Gram partial
   (cpd.py:39-42); per sweep one scalar all-reduce for ⟨X, X̂⟩ (cpd.py:176-184).
 * column normalisation (cpd.py:187-195) is kept as per-column scales folded
   into the next update matrix, so it costs no pass over the factors.
@@ -58,14 +60,21 @@ def allgather_padded(torch, dist, local, ranges, group=None):
 
 
 class DeviceShards:
-    """Per-mode HB-CSF of this rank's row range, MTTKRP on the GPU."""
+    """Per-mode HB-CSF of this rank's row range, MTTKRP on the GPU, and the
+    factor rows those shards reference (for the touched-rows exchange)."""
 
     def __init__(self, t: CooTensor, world: int, me: int):
+        import ctypes as C
+
+        import torch
+
+        from . import _native as N
         from . import shard
         from .formats import build_hbcsf
 
         self.me = me
         self.ranges, self.reps = [], []
+        refs = [[] for _ in range(t.order)]
         for mode in range(t.order):
             hist = shard.slice_histogram(t, mode).cpu().numpy()
             ranges = plan_row_ranges(hist, world)
@@ -74,8 +83,19 @@ class DeviceShards:
             if hi > lo:
                 part = shard.shard_rows(t, mode, lo, hi)
                 self.reps.append(build_hbcsf(part, allmode_order(t.dims, mode)))
+                if part.nnz:
+                    idx = torch.empty((part.nnz, t.order), dtype=torch.int32, device="cuda")
+                    N.call("hbk_coo_export_device", part._dev().ptr, C.c_void_p(idx.data_ptr()), None,
+                           None, N.stream_ptr())
+                    for d in range(t.order):
+                        if d != mode:
+                            refs[d].append(torch.unique(idx[:, d]).long())
+                    del idx
             else:
                 self.reps.append(None)
+        # rows of factor d this rank's MTTKRPs of the other modes read
+        self.needed = [torch.unique(torch.cat(r)) if r else torch.zeros(0, dtype=torch.long, device="cuda")
+                       for r in refs]
 
     def __call__(self, mode: int, factors32):
         from .kernels import mttkrp_device
@@ -91,9 +111,47 @@ class DeviceShards:
         return y
 
 
+class RowExchange:
+    """Touched-rows exchange of one factor: after factor d is
+    updated, each rank receives only the rows its own shards of the other
+    modes read, from the ranks that own them — one all_to_all of row blocks
+    instead of replicating the whole factor.  The send/receive index lists
+    are agreed once (two small all_to_alls)."""
+
+    def __init__(self, torch, dist, needed, ranges, me: int, group=None):
+        world = len(ranges)
+        self.group = group
+        dev = needed.device
+        parts, splits = [], []
+        for r, (lo, hi) in enumerate(ranges):
+            sel = needed[(needed >= lo) & (needed < hi)] if r != me else needed[:0]
+            parts.append(sel)
+            splits.append(int(sel.numel()))
+        self.recv_idx = torch.cat(parts) if parts else needed[:0]
+        self.recv_splits = splits
+        cnt_out = torch.tensor(splits, dtype=torch.long, device=dev)
+        cnt_in = torch.empty_like(cnt_out)
+        dist.all_to_all_single(cnt_in, cnt_out, group=group)
+        self.send_splits = [int(x) for x in cnt_in.tolist()]
+        send_idx = torch.empty(sum(self.send_splits), dtype=torch.long, device=dev)
+        dist.all_to_all_single(send_idx, self.recv_idx, output_split_sizes=self.send_splits,
+                               input_split_sizes=self.recv_splits, group=group)
+        self.send_idx = send_idx
+        self.rows_in = int(self.recv_idx.numel())
+
+    def __call__(self, torch, dist, F):
+        width = F.shape[1]
+        send = F.index_select(0, self.send_idx)
+        recv = torch.empty((self.rows_in, width), dtype=F.dtype, device=F.device)
+        dist.all_to_all_single(recv, send, output_split_sizes=self.recv_splits,
+                               input_split_sizes=self.send_splits, group=self.group)
+        if self.rows_in:
+            F.index_copy_(0, self.recv_idx, recv)
+
+
 def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_tol: float = 1e-8,
                        seed: int = 0, *, group=None, local_mttkrp=None, ranges=None,
-                       device=None):
+                       device=None, exchange: str = "touched", needed=None):
     """CP-ALS over ``world`` processes, each owning a row range of every mode.
 
     Every rank passes the same tensor ``t`` (it is canonicalised and sharded
@@ -101,7 +159,11 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
     every rank.  ``local_mttkrp(mode, factors32) -> (rows_g, R)`` and
     ``ranges`` (per mode, the row ranges of all ranks) replace the GPU shards
     (used by the CPU tests); by default the HB-CSF shards are built on the GPU
-    and the collectives run on NCCL.
+    and the collectives run on NCCL.  ``exchange``: "touched" (default)
+    moves only the factor rows each rank's shards read (``needed[d]``: the
+    sorted row ids of factor d this rank reads; derived from the GPU shards,
+    or passed with a custom ``local_mttkrp``), "full" replicates every
+    updated factor.
 
     Factors are kept in fp32 (the MTTKRP's input precision) as raw matrices
     with per-column scales s_d: the true factor is F_d diag(s_d).  The scales
@@ -128,6 +190,8 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
         shards = DeviceShards(t, world, me)
         ranges = shards.ranges
         local_mttkrp = shards
+        if needed is None:
+            needed = shards.needed
     else:
         device = torch.device(device or "cpu")
         if ranges is None:
@@ -162,13 +226,26 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
         g = (g_raw.cpu().numpy() * np.outer(s, s))
         return (g + g.T) * 0.5
 
-    def exchange(d):
+    if exchange not in ("touched", "full"):
+        raise ValueError("exchange must be 'touched' or 'full'")
+    touched = None
+    if exchange == "touched" and world > 1 and needed is not None:
+        touched = [RowExchange(torch, dist, torch.as_tensor(needed[d], dtype=torch.long).to(device),
+                               ranges[d], me, group) for d in range(order)]
+
+    def replicate(d):
         """Replicate factor d's rows: rank r broadcasts its contiguous rows."""
         if world == 1:
             return
         for r, (lo, hi) in enumerate(ranges[d]):
             if hi > lo:
                 dist.broadcast(f32[d][lo:hi], src=r, group=group)
+
+    def exchange_rows(d):
+        if touched is not None:
+            touched[d](torch, dist, f32[d])
+        else:
+            replicate(d)
 
     def sync():
         if device.type == "cuda":
@@ -239,7 +316,7 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
             if not np.isfinite(g).all():
                 raise NumericalError(f"non-finite factor for mode {mode} in ALS sweep {it}", iteration=it)
             grams[mode] = (g + g.T) * 0.5
-            exchange(mode)
+            exchange_rows(mode)
             del y
             sync()
             seconds.append(time.perf_counter() - tic)
@@ -255,6 +332,9 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
             break
     if len(history) == 1:
         lam = _normalize_scales(scales, grams)
+    if touched is not None:  # the model needs every row of every factor
+        for d in range(order):
+            replicate(d)
     full = [(f32[d].double() * torch.from_numpy(scales[d]).to(device)).cpu().numpy()
             for d in range(order)]
     return KruskalModel(lam=lam, factors=tuple(full)), history

@@ -90,7 +90,22 @@ def _local_mttkrp_factory(idx, vals, dims, ranges, rank):
     return local
 
 
-def _job_cpd(rank, world):
+def _needed_rows(idx, dims, ranges, rank):
+    """Rows of factor d read by this rank's shards of the other modes."""
+    need = []
+    for d in range(3):
+        rows = set()
+        for n in range(3):
+            if n == d:
+                continue
+            lo, hi = ranges[n][rank]
+            keep = (idx[:, n] >= lo) & (idx[:, n] < hi)
+            rows.update(idx[keep, d].tolist())
+        need.append(np.array(sorted(rows), dtype=np.int64))
+    return need
+
+
+def _job_cpd(rank, world, exchange="full"):
     from paper_1904_03329_b200.coo import CooTensor
     from paper_1904_03329_b200.distributed import cp_als_distributed
     from paper_1904_03329_b200.shard import plan_row_ranges
@@ -100,9 +115,15 @@ def _job_cpd(rank, world):
     t = CooTensor(dims, idx, vals, sorted_under=(0, 1, 2))
     ranges = [plan_row_ranges(np.bincount(idx[:, m], minlength=dims[m]), world) for m in range(3)]
     local = _local_mttkrp_factory(idx, vals, dims, ranges, rank)
+    needed = _needed_rows(idx, dims, ranges, rank) if exchange == "touched" else None
     model, hist = cp_als_distributed(t, rank=4, max_iters=6, fit_tol=1e-14, seed=7,
-                                     local_mttkrp=local, ranges=ranges)
+                                     local_mttkrp=local, ranges=ranges, exchange=exchange,
+                                     needed=needed)
     return [h.fit for h in hist], model.lam, [f for f in model.factors], ranges
+
+
+def _job_cpd_touched(rank, world):
+    return _job_cpd(rank, world, exchange="touched")
 
 
 def test_allgather_padded_uneven_world2():
@@ -127,3 +148,16 @@ def test_cp_als_distributed_matches_single_process_oracle():
     assert len(fits0) == len(fits_ref)
     assert np.allclose(fits0, fits_ref, atol=2e-6, rtol=0)
     assert np.allclose(lam0, lam_ref, rtol=2e-4)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_touched_rows_exchange_matches_full_replication(world):
+    """Touched-rows exchange (each rank receives only the factor rows its
+    shards read) gives the same model as full replication, on every rank."""
+    full = _run(_job_cpd, world)
+    touched = _run(_job_cpd_touched, world)
+    for r in range(world):
+        assert np.allclose(touched[r][0], full[0][0], atol=1e-12, rtol=0)
+        assert np.allclose(touched[r][1], full[0][1], rtol=1e-12)
+        for a, b in zip(touched[r][2], full[0][2]):
+            assert np.allclose(a, b, rtol=1e-10, atol=1e-12)
