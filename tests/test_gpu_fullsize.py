@@ -1,0 +1,51 @@
+"""Parity at benchmark scale through size-independent properties (the CPU
+oracle is too slow here): on the Appendix-A generator's tensors, the fast
+fp32 kernels (B-position streams, padded heavy layout, CSL/COO/zero tasks)
+against libhbk's independent generic kernel run in fp64 — different code,
+different layout, different arithmetic — with the reference's row metric;
+plus linearity in a factor and bit-repeatability of the fast path."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _rowdev(y, ref):
+    import torch
+
+    num = torch.linalg.vector_norm(y.double() - ref, dim=1)
+    return float((num / (1.0 + torch.linalg.vector_norm(ref, dim=1))).max())
+
+
+@pytest.mark.parametrize("config,scale", [("nell-2", 1.0), ("flickr-3d", 0.5),
+                                          ("delicious-3d", 0.5), ("nell-1", 0.5)])
+def test_fast_fp32_matches_generic_fp64_at_scale(config, scale):
+    import torch
+
+    import paper_1904_03329_b200 as hb
+    from paper_1904_03329_b200.generate import CONFIGS, config_tensor
+    from paper_1904_03329_b200.kernels import mttkrp_device
+
+    dims = CONFIGS[config]["dims"]
+    t = config_tensor(config, scale=scale)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    f64 = [torch.rand((d, 32), dtype=torch.float64, device="cuda", generator=g) for d in dims]
+    f32 = [f.float() for f in f64]
+    f64r = [f.double() for f in f32]  # the fp64 kernel sees the fp32-rounded factors
+    for mode in range(3):
+        h = hb.split_fibers(hb.build_hbcsf(t, hb.allmode_order(dims, mode)), hb.SplitConfig())
+        y32, _ = mttkrp_device(h, f32, mode)
+        y64, _ = mttkrp_device(h, f64r, mode)
+        assert y32.dtype == torch.float32 and y64.dtype == torch.float64
+        assert _rowdev(y32, y64) <= 1e-4, (config, mode)
+        # linearity in a factor (exact up to fp32 rounding): Y(2C) = 2 Y(C)
+        fs = list(f32)
+        d = hb.allmode_order(dims, mode)[2]
+        fs[d] = f32[d] * 2.0
+        y2, _ = mttkrp_device(h, fs, mode)
+        assert _rowdev(y2, 2.0 * y32.double()) <= 1e-6
+        # repeatability up to the atomic order of split slices
+        y32b, _ = mttkrp_device(h, f32, mode)
+        assert _rowdev(y32b, y32.double()) <= 1e-6
