@@ -196,6 +196,30 @@ __global__ void k_ldg_hint(const float4* __restrict__ F, const uint32_t* __restr
   out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = acc;
 }
 
+// L1 split by row hotness: rows k < H (the power-law head) evict_last,
+// colder rows HINT2 (1 = L1::no_allocate, 4 = L1::evict_first)
+template <int HINT2>
+__global__ void k_ldg_split(const float4* __restrict__ F, const uint32_t* __restrict__ idx, int64_t n,
+                            uint32_t H, float4* __restrict__ out) {
+  const int lane = threadIdx.x & 31, lig = lane & 7;
+  const int64_t gid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 3;
+  const int64_t ngroups = (int64_t(gridDim.x) * blockDim.x) >> 3;
+  float4 acc = make_float4(0, 0, 0, 0);
+  for (int64_t base = gid * 8; base < n; base += ngroups * 8) {
+    uint32_t k = (base + lig < n) ? idx[base + lig] : 0;
+    float4 r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t kj = __shfl_sync(0xffffffffu, k, j, 8);
+      const float4* p = F + size_t(kj) * 8 + lig;
+      r[j] = kj < H ? ldrow_h<0>(p) : ldrow_h<HINT2>(p);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { acc.x += r[j].x; acc.y += r[j].y; acc.z += r[j].z; acc.w += r[j].w; }
+  }
+  out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = acc;
+}
+
 // 4 lanes x LDG.256 per row (8 rows per warp instruction)
 struct f8 {
   float v[8];
@@ -451,6 +475,19 @@ int main() {
     float ms = time_ms([&] { k_ldg_hint<H><<<g, 256>>>(F, idx, n, out); });                      \
     printf("  hint=%d blk/sm=%d : %.3f ms  %.2f Grows/s\n", H, BPS, ms, n / ms / 1e6);         \
   }
+    if (getenv("SPLIT")) {
+      for (uint32_t H : {256u, 512u, 1024u, 2048u, 4096u, 8192u}) {
+        int g = sms * 4;
+        float ms1 = time_ms([&] { k_ldg_split<1><<<g, 256>>>(F, idx, n, H, out); });
+        float ms4 = time_ms([&] { k_ldg_split<4><<<g, 256>>>(F, idx, n, H, out); });
+        printf("  split H=%u : no_allocate tail %.2f Grows/s, evict_first tail %.2f Grows/s\n", H,
+               n / ms1 / 1e6, n / ms4 / 1e6);
+      }
+      RUN_HINT(0, 4);
+      CK(cudaFree(idx));
+      CK(cudaFree(F));
+      continue;
+    }
     if (getenv("HINTS")) {
       RUN_HINT(0, 4); RUN_HINT(1, 4); RUN_HINT(2, 4); RUN_HINT(3, 4); RUN_HINT(4, 4);
       RUN_HINT(0, 8); RUN_HINT(1, 8); RUN_HINT(3, 8);
