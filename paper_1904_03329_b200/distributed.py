@@ -202,17 +202,61 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
     if over:
         warnings.warn(f"rank {rank} exceeds the extent of mode(s) {over}; the problem is "
                       "over-complete and factors will be rank-deficient", RuntimeWarning)
-    fused = device.type == "cuda" and rank == 32
-
-    rng = np.random.default_rng(seed)
-    f32 = [torch.from_numpy(rng.random((dim, rank))).to(device=device, dtype=torch.float32)
-           for dim in dims]  # cpd.py:231-232, identical on every rank
-    scales = [np.ones(rank) for _ in dims]
+    if exchange not in ("touched", "full"):
+        raise ValueError("exchange must be 'touched' or 'full'")
     own = [ranges[d][me] for d in range(order)]
 
     def allreduce_(x):
         dist.all_reduce(x, group=group)
         return x
+
+    touched = None
+    if exchange == "touched" and world > 1 and needed is not None:
+        touched = [RowExchange(torch, dist, torch.as_tensor(needed[d], dtype=torch.long).to(device),
+                               ranges[d], me, group) for d in range(order)]
+
+    def replicate(d, f32):
+        """Replicate factor d's rows: rank r broadcasts its contiguous rows."""
+        if world == 1:
+            return
+        for r, (lo, hi) in enumerate(ranges[d]):
+            if hi > lo:
+                dist.broadcast(f32[d][lo:hi], src=r, group=group)
+
+    def exchange_rows(d, f32):
+        if touched is not None:
+            touched[d](torch, dist, f32[d])
+        else:
+            replicate(d, f32)
+
+    def finalize(f32):
+        if touched is not None:  # the model needs every row of every factor
+            for d in range(order):
+                replicate(d, f32)
+
+    return als_fp32(torch, dims=dims, rank=rank, max_iters=max_iters, fit_tol=fit_tol, seed=seed,
+                    device=device, own=own, local_mttkrp=local_mttkrp,
+                    norm_x=_value_norm(torch, t), allreduce_=allreduce_,
+                    exchange_rows=exchange_rows, finalize=finalize)
+
+
+def als_fp32(torch, *, dims, rank, max_iters, fit_tol, seed, device, own, local_mttkrp, norm_x,
+             allreduce_=lambda x: x, exchange_rows=lambda d, f32: None, finalize=lambda f32: None):
+    """The CP-ALS sweep loop (cpd.py:198-271) on fp32 factors with folded
+    column scales, for a rank owning rows ``own[d]`` of every factor.
+    ``local_mttkrp(mode, f32)`` returns this rank's (rows, R) MTTKRP (or a
+    (rows, OpCount) pair); the hooks do the collectives (identity on one
+    process).  Used by cp_als_distributed and by cp_als at R = 32."""
+    order = len(dims)
+    fused = device.type == "cuda" and rank == 32
+    rng = np.random.default_rng(seed)
+    f32 = [torch.from_numpy(rng.random((dim, rank))).to(device=device, dtype=torch.float32)
+           for dim in dims]  # cpd.py:231-232, identical on every rank
+    scales = [np.ones(rank) for _ in dims]
+
+    def mttkrp(mode):
+        r = local_mttkrp(mode, f32)
+        return r if isinstance(r, tuple) else (r, None)
 
     def gram_raw(local):
         g = torch.zeros((rank, rank), dtype=torch.float64, device=device)
@@ -226,27 +270,6 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
         g = (g_raw.cpu().numpy() * np.outer(s, s))
         return (g + g.T) * 0.5
 
-    if exchange not in ("touched", "full"):
-        raise ValueError("exchange must be 'touched' or 'full'")
-    touched = None
-    if exchange == "touched" and world > 1 and needed is not None:
-        touched = [RowExchange(torch, dist, torch.as_tensor(needed[d], dtype=torch.long).to(device),
-                               ranges[d], me, group) for d in range(order)]
-
-    def replicate(d):
-        """Replicate factor d's rows: rank r broadcasts its contiguous rows."""
-        if world == 1:
-            return
-        for r, (lo, hi) in enumerate(ranges[d]):
-            if hi > lo:
-                dist.broadcast(f32[d][lo:hi], src=r, group=group)
-
-    def exchange_rows(d):
-        if touched is not None:
-            touched[d](torch, dist, f32[d])
-        else:
-            replicate(d)
-
     def sync():
         if device.type == "cuda":
             torch.cuda.synchronize(device)
@@ -255,7 +278,6 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
     for d in range(order):
         lo, hi = own[d]
         grams.append(true_gram(d, allreduce_(gram_raw(f32[d][lo:hi]))))
-    norm_x = _value_norm(torch, t)
     last = order - 1
 
     def fit_value(inner):
@@ -270,7 +292,7 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
                 c = c * scales[d]
         return c
 
-    y0 = local_mttkrp(last, f32).double()
+    y0 = mttkrp(last)[0].double()
     lo, hi = own[last]
     inner0 = float((y0 * torch.from_numpy(colscale(last)).to(device)
                     * (f32[last][lo:hi].double() * torch.from_numpy(scales[last]).to(device))).sum())
@@ -281,12 +303,14 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
     lam = None
     inner_t = torch.zeros(1, dtype=torch.float64, device=device)
     for it in range(1, max_iters + 1):
-        seconds = []
+        seconds, ops = [], []
         inner = 0.0
         for mode in range(order):
             sync()
             tic = time.perf_counter()
-            y = local_mttkrp(mode, f32).float().contiguous()
+            y, op = mttkrp(mode)
+            y = y.float().contiguous()
+            ops.append(op)
             c = colscale(mode)
             # F_true = (Y_raw diag(c)) V^+  ->  M = diag(c) V^+, new scales 1
             m64 = c[:, None] * pinv_spsd(hadamard_all_but(grams, mode))
@@ -316,7 +340,7 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
             if not np.isfinite(g).all():
                 raise NumericalError(f"non-finite factor for mode {mode} in ALS sweep {it}", iteration=it)
             grams[mode] = (g + g.T) * 0.5
-            exchange_rows(mode)
+            exchange_rows(mode, f32)
             del y
             sync()
             seconds.append(time.perf_counter() - tic)
@@ -327,14 +351,13 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
         if not math.isfinite(new_fit):
             raise NumericalError(f"non-finite fit in ALS sweep {it}", iteration=it)
         delta = new_fit - history[-1].fit
-        history.append(AlsIteration(it, new_fit, delta, tuple(seconds), ()))
+        history.append(AlsIteration(it, new_fit, delta, tuple(seconds),
+                                    tuple(ops) if all(o is not None for o in ops) else ()))
         if abs(delta) < fit_tol:
             break
     if len(history) == 1:
         lam = _normalize_scales(scales, grams)
-    if touched is not None:  # the model needs every row of every factor
-        for d in range(order):
-            replicate(d)
+    finalize(f32)
     full = [(f32[d].double() * torch.from_numpy(scales[d]).to(device)).cpu().numpy()
             for d in range(order)]
     return KruskalModel(lam=lam, factors=tuple(full)), history

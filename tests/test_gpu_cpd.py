@@ -115,3 +115,21 @@ def test_order4(hb):
     _, history = hb.cp_als(t, rank=2, max_iters=30, fit_tol=1e-13, seed=3)
     fits = [h.fit for h in history]
     assert fits[-1] > 0.98
+
+
+def test_rank32_fused_path_tracks_fp64_path(hb):
+    """cp_als at R = 32 (fp32 factors, fused row update) against the same
+    solve with the fp64 MTTKRP and fp64 factors."""
+    rng = np.random.default_rng(21)
+    dims = (120, 90, 150)
+    idx = np.stack([rng.integers(0, d, 20000) for d in dims], 1)
+    t = hb.canonicalize(hb.CooTensor(dims, idx, rng.random(20000) + 0.01))
+    m32, h32 = hb.cp_als(t, rank=32, max_iters=6, fit_tol=1e-14, seed=4)
+    m64, h64 = hb.cp_als(t, rank=32, max_iters=6, fit_tol=1e-14, seed=4, mttkrp_precision="fp64")
+    f32, f64 = np.array([h.fit for h in h32]), np.array([h.fit for h in h64])
+    assert len(f32) == len(f64)
+    assert np.allclose(f32, f64, atol=1e-5, rtol=0)
+    assert np.allclose(m32.lam, m64.lam, rtol=1e-3)
+    assert [[o.muls, o.adds] for o in h32[1].op_counts] == [[o.muls, o.adds] for o in h64[1].op_counts]
+    for f in m32.factors:
+        assert np.allclose(np.linalg.norm(f, axis=0), 1.0, atol=1e-5)
