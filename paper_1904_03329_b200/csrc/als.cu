@@ -3,13 +3,15 @@
 // After a mode's MTTKRP the reference computes F = Y · pinv(V) (cpd.py:172),
 // then G = FᵀF (cpd.py:39-42), and — for the last mode of a sweep — the fit
 // term <Y, F> (cpd.py:176-184).  On a row shard all three are row-local, so
-// one pass over the rows does them: a CTA stages a tile of 256 rows of Y in
-// shared memory, each thread turns its row into F (32x32 matrix M broadcast
-// from shared memory), the tile of F is written back coalesced and reduced
-// into the CTA's Gram partial (register-blocked 4x4 per thread, fp32 within a
-// tile, fp64 across tiles), and sum_r w_r <Y[:, r], F[:, r]> is accumulated
-// alongside (w: column weights of Y, e.g. factor column scales; NULL = 1).  Y and F are
-// read/written once: the pass is HBM-bound (8 bytes per row element).
+// one pass over the rows does them.  Per tile of 256 rows a CTA
+//   1. stages the Y tile in shared memory (coalesced loads),
+//   2. computes the F tile, register-blocked 4 rows x 8 columns per thread
+//      (M broadcast from shared memory as LDS.128), and the column-weighted
+//      sum_r w_r <Y[:, r], F[:, r]> alongside (w: factor column scales),
+//   3. writes the F tile to a second, 16-byte-aligned shared buffer, stores it
+//      coalesced, and reduces it into the CTA's Gram partial, register-blocked
+//      8x8 per thread (fp32 over <= 8 tiles, then fp64 in shared memory).
+// Y and F cross HBM once each (8 bytes per row element).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -19,120 +21,146 @@
 namespace hbk {
 
 static constexpr int ALS_R = 32;
-static constexpr int ALS_TILE = 256;  // rows per tile = threads per CTA
-static constexpr int ALS_LD = ALS_R + 1;
+static constexpr int ALS_TILE = 256;       // rows per tile = threads per CTA
+static constexpr int ALS_LDY = ALS_R + 1;  // Y tile: conflict-free column reads
+static constexpr int ALS_LDF = ALS_R + 4;  // F tile: 16-byte aligned rows for LDS.128
+
+struct AlsSmem {
+  float Ms[ALS_R * ALS_R];
+  float W[ALS_R];
+  float Y[ALS_TILE * ALS_LDY];
+  alignas(16) float F[ALS_TILE * ALS_LDF];
+  double G[ALS_R * ALS_R];
+  double red[ALS_TILE / 32];
+};
 
 __global__ void __launch_bounds__(ALS_TILE, 2)
     k_als_update32(const float* __restrict__ Y, int64_t rows, const float* __restrict__ M,
                    const float* __restrict__ colw, float* __restrict__ F, double* __restrict__ gram,
                    double* __restrict__ inner) {
-  __shared__ float Ms[ALS_R * ALS_R];
-  __shared__ float W[ALS_R];
-  __shared__ float T[ALS_TILE * ALS_LD];
-  __shared__ double red[ALS_TILE / 32];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  AlsSmem& S = *reinterpret_cast<AlsSmem*>(smem_raw);
   const int tid = threadIdx.x;
-  for (int i = tid; i < ALS_R * ALS_R; i += ALS_TILE) Ms[i] = M[i];
-  if (tid < ALS_R) W[tid] = colw ? colw[tid] : 1.f;
-  // Gram blocking: 4 row groups x 64 threads, each thread a 4x4 block of G
-  const int grp = tid >> 6, p = tid & 63;
-  const int a0 = (p >> 3) * 4, b0 = (p & 7) * 4;
-  double g64[16];
-#pragma unroll
-  for (int q = 0; q < 16; ++q) g64[q] = 0.0;
+  for (int i = tid; i < ALS_R * ALS_R; i += ALS_TILE) {
+    S.Ms[i] = M[i];
+    S.G[i] = 0.0;
+  }
+  if (tid < ALS_R) S.W[tid] = colw ? colw[tid] : 1.f;
+  // F-tile blocking 4x8 (row block rb, column block cb); Gram blocking 8x8
+  const int rb = tid >> 2, cb = tid & 3;
+  const int gp = tid & 15, grp = tid >> 4;  // 16 Gram blocks x 16 row groups
+  const int ga = (gp >> 2) * 8, gb = (gp & 3) * 8;
   double in64 = 0.0;
+  // Gram partial in registers (fp32) over up to FLUSH tiles (FLUSH x 16 rows
+  // per thread), then added into the fp64 shared Gram group by group
+  constexpr int FLUSH = 8;
+  float g32[64];
+#pragma unroll
+  for (int q = 0; q < 64; ++q) g32[q] = 0.f;
+  auto flush = [&]() {
+    for (int g = 0; g < ALS_TILE / 16; ++g) {
+      if (grp == g) {
+#pragma unroll
+        for (int q = 0; q < 64; ++q) {
+          S.G[(ga + (q >> 3)) * ALS_R + gb + (q & 7)] += double(g32[q]);
+          g32[q] = 0.f;
+        }
+      }
+      __syncthreads();
+    }
+  };
   const int64_t ntiles = (rows + ALS_TILE - 1) / ALS_TILE;
+  int since = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * ALS_TILE;
     const int nr = int(rows - r0 < ALS_TILE ? rows - r0 : int64_t(ALS_TILE));
-    __syncthreads();  // previous tile's Gram reads are done
-    // coalesced load of the Y tile (rows beyond the end are zero)
-    const float* src = Y + r0 * ALS_R;
-    for (int i = tid; i < ALS_TILE * ALS_R; i += ALS_TILE) {
-      const int r = i / ALS_R, c = i % ALS_R;
-      T[r * ALS_LD + c] = r < nr ? __ldcs(src + i) : 0.f;
+    __syncthreads();  // the previous tile's Y and F reads are done
+    // all 8 float4 loads of a thread are issued before any is stored
+    const float4* src = reinterpret_cast<const float4*>(Y + r0 * ALS_R);
+    float4 ld[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i4 = tid + ALS_TILE * j, r = i4 >> 3;
+      ld[j] = r < nr ? __ldcs(src + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i4 = tid + ALS_TILE * j, r = i4 >> 3, c = (i4 & 7) * 4;
+      float* d = S.Y + r * ALS_LDY + c;
+      d[0] = ld[j].x;
+      d[1] = ld[j].y;
+      d[2] = ld[j].z;
+      d[3] = ld[j].w;
     }
     __syncthreads();
-    // row `tid`: f = y M
-    float y[ALS_R], f[ALS_R];
+    float acc[4][8];
 #pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[i][c] = 0.f;
+#pragma unroll 4
     for (int k = 0; k < ALS_R; ++k) {
-      y[k] = T[tid * ALS_LD + k];
-      f[k] = 0.f;
-    }
+      float yv[4];
 #pragma unroll
-    for (int k = 0; k < ALS_R; ++k) {
-      const float4* mk = reinterpret_cast<const float4*>(Ms + k * ALS_R);
+      for (int i = 0; i < 4; ++i) yv[i] = S.Y[(4 * rb + i) * ALS_LDY + k];
+      const float4 m0 = reinterpret_cast<const float4*>(S.Ms + k * ALS_R + 8 * cb)[0];
+      const float4 m1 = reinterpret_cast<const float4*>(S.Ms + k * ALS_R + 8 * cb)[1];
+      const float mv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
 #pragma unroll
-      for (int c4 = 0; c4 < ALS_R / 4; ++c4) {
-        const float4 m = mk[c4];
-        f[4 * c4 + 0] = fmaf(y[k], m.x, f[4 * c4 + 0]);
-        f[4 * c4 + 1] = fmaf(y[k], m.y, f[4 * c4 + 1]);
-        f[4 * c4 + 2] = fmaf(y[k], m.z, f[4 * c4 + 2]);
-        f[4 * c4 + 3] = fmaf(y[k], m.w, f[4 * c4 + 3]);
-      }
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[i][c] = fmaf(yv[i], mv[c], acc[i][c]);
     }
     if (inner) {
       float d = 0.f;
 #pragma unroll
-      for (int c = 0; c < ALS_R; ++c) d = fmaf(W[c] * y[c], f[c], d);
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          d = fmaf(S.W[8 * cb + c] * S.Y[(4 * rb + i) * ALS_LDY + 8 * cb + c], acc[i][c], d);
       in64 += double(d);
     }
-    __syncthreads();  // every row of Y has been read
 #pragma unroll
-    for (int c = 0; c < ALS_R; ++c) T[tid * ALS_LD + c] = f[c];
-    __syncthreads();
-    // coalesced store of the F tile
-    float* dst = F + r0 * ALS_R;
-    for (int i = tid; i < nr * ALS_R; i += ALS_TILE) dst[i] = T[(i / ALS_R) * ALS_LD + i % ALS_R];
-    // Gram partial of the tile
-    float g32[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) g32[q] = 0.f;
-    for (int r = grp; r < ALS_TILE; r += 4) {
-      const float* row = T + r * ALS_LD;
-      float av[4], bv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        av[u] = row[a0 + u];
-        bv[u] = row[b0 + u];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) g32[u * 4 + v] = fmaf(av[u], bv[v], g32[u * 4 + v]);
+    for (int i = 0; i < 4; ++i) {
+      float4* fr = reinterpret_cast<float4*>(S.F + (4 * rb + i) * ALS_LDF + 8 * cb);
+      fr[0] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+      fr[1] = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
     }
+    __syncthreads();
+    float4* dst = reinterpret_cast<float4*>(F + r0 * ALS_R);
 #pragma unroll
-    for (int q = 0; q < 16; ++q) g64[q] += double(g32[q]);
+    for (int j = 0; j < 8; ++j) {
+      const int i4 = tid + ALS_TILE * j, r = i4 >> 3;
+      if (r < nr) __stcs(dst + i4, reinterpret_cast<const float4*>(S.F + r * ALS_LDF)[i4 & 7]);
+    }
+    // Gram partial of the tile: rows grp, grp+16, ... (rows beyond nr are zero)
+#pragma unroll 2
+    for (int r = grp; r < ALS_TILE; r += 16) {
+      const float4* row = reinterpret_cast<const float4*>(S.F + r * ALS_LDF);
+      const float4 a0 = row[ga / 4], a1 = row[ga / 4 + 1], b0 = row[gb / 4], b1 = row[gb / 4 + 1];
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) g32[u * 8 + v] = fmaf(av[u], bv[v], g32[u * 8 + v]);
+    }
+    if (++since == FLUSH) {
+      flush();
+      since = 0;
+    }
   }
-  // CTA reduction: the 4 row groups' partials through shared memory (reuse T
-  // as doubles: 4 x 64 threads x 16 values = 16384 doubles > T, so go in two
-  // passes of 8 values)
+  flush();
   __syncthreads();
-  double* S = reinterpret_cast<double*>(T);  // 256 * 33 floats = 4224 doubles
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) S[(q * 4 + grp) * 64 + p] = g64[half * 8 + q];
-    __syncthreads();
-    if (grp == 0) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double v = S[(q * 4 + 0) * 64 + p] + S[(q * 4 + 1) * 64 + p] +
-                         S[(q * 4 + 2) * 64 + p] + S[(q * 4 + 3) * 64 + p];
-        const int qq = half * 8 + q, u = qq >> 2, w = qq & 3;
-        atomicAdd(gram + (a0 + u) * ALS_R + (b0 + w), v);
-      }
-    }
-    __syncthreads();
-  }
+  for (int i = tid; i < ALS_R * ALS_R; i += ALS_TILE) atomicAdd(gram + i, S.G[i]);
   if (inner) {
     double v = in64;
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-    if ((tid & 31) == 0) red[tid >> 5] = v;
+    if ((tid & 31) == 0) S.red[tid >> 5] = v;
     __syncthreads();
     if (tid == 0) {
       double s = 0.0;
-      for (int i = 0; i < ALS_TILE / 32; ++i) s += red[i];
+      for (int i = 0; i < ALS_TILE / 32; ++i) s += S.red[i];
       atomicAdd(inner, s);
     }
   }
@@ -148,16 +176,22 @@ extern "C" int hbk_als_update(const float* Y, int64_t rows, int rank, const floa
   return guarded([&] {
     HBK_REQUIRE(rank == ALS_R, HBK_EINVAL, "hbk_als_update supports rank 32");
     HBK_REQUIRE(rows >= 0, HBK_EINVAL, "negative row count");
+    HBK_REQUIRE((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(F)) % 16 == 0,
+                HBK_EINVAL, "Y and F must be 16-byte aligned");
     cudaStream_t st = to_stream(stream);
     HBK_CUDA(cudaMemsetAsync(gram, 0, sizeof(double) * ALS_R * ALS_R, st));
     if (inner) HBK_CUDA(cudaMemsetAsync(inner, 0, sizeof(double), st));
     if (rows == 0) return;
-    int dev = 0, sms = 0;
+    HBK_CUDA(cudaFuncSetAttribute(k_als_update32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(sizeof(AlsSmem))));
+    int dev = 0, sms = 0, per_sm = 0;
     HBK_CUDA(cudaGetDevice(&dev));
     HBK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_update32, ALS_TILE,
+                                                           sizeof(AlsSmem)));
     const int64_t ntiles = (rows + ALS_TILE - 1) / ALS_TILE;
-    const int grid = int(std::min<int64_t>(ntiles, int64_t(sms) * 2));
-    k_als_update32<<<grid, ALS_TILE, 0, st>>>(Y, rows, M, colw, F, gram, inner);
+    const int grid = int(std::min<int64_t>(ntiles, int64_t(sms) * std::max(per_sm, 1)));
+    k_als_update32<<<grid, ALS_TILE, sizeof(AlsSmem), st>>>(Y, rows, M, colw, F, gram, inner);
     check_launch("k_als_update32");
   });
 }

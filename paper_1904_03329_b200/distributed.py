@@ -248,7 +248,9 @@ def als_fp32(torch, *, dims, rank, max_iters, fit_tol, seed, device, own, local_
     (rows, OpCount) pair); the hooks do the collectives (identity on one
     process).  Used by cp_als_distributed and by cp_als at R = 32."""
     order = len(dims)
-    fused = device.type == "cuda" and rank == 32
+    import os
+
+    fused = device.type == "cuda" and rank == 32 and os.environ.get("HBK_ALS_FUSED", "1") != "0"
     rng = np.random.default_rng(seed)
     f32 = [torch.from_numpy(rng.random((dim, rank))).to(device=device, dtype=torch.float32)
            for dim in dims]  # cpd.py:231-232, identical on every rank
@@ -333,8 +335,12 @@ def als_fp32(torch, *, dims, rank, max_iters, fit_tol, seed, device, own, local_
                 fm = y @ torch.from_numpy(m64).to(device=device, dtype=torch.float32)
                 dst.copy_(fm)
                 g_raw = gram_raw(dst)
-                if mode == last:
-                    inner = ((y.double() * torch.from_numpy(c).to(device)) * fm.double()).sum().reshape(1)
+                if mode == last:  # sum_r c_r <Y[:, r], F[:, r]>, fp32 chunks, fp64 total
+                    cw = torch.from_numpy(c).to(device=device, dtype=fm.dtype)
+                    inner = torch.zeros(1, dtype=torch.float64, device=device)
+                    for a in range(0, fm.shape[0], 1 << 20):
+                        inner += ((y[a: a + (1 << 20)] * fm[a: a + (1 << 20)]).sum(0).double()
+                                  * cw.double()).sum()
             scales[mode] = np.ones(rank)
             g = allreduce_(g_raw).cpu().numpy()
             if not np.isfinite(g).all():
