@@ -220,6 +220,46 @@ __global__ void k_ldg_split(const float4* __restrict__ F, const uint32_t* __rest
   out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = acc;
 }
 
+// Index stream staged through shared memory with cp.async (D batches ahead,
+// one 16-byte copy per lane pair), rows gathered 8 lanes x LDG.128 — the
+// north-star's "stream through cp.async staging" against the direct LDG of
+// the index (k_ldg<8>, prefetched one batch ahead by the warp scheduler).
+template <int D>
+__global__ void k_ldg_staged(const float4* __restrict__ F, const uint32_t* __restrict__ idx, int64_t n,
+                             float4* __restrict__ out) {
+  __shared__ __align__(16) uint32_t ring[256 / 8][D][8];  // per group: D batches of 8 indices
+  const int lane = threadIdx.x & 31, lig = lane & 7, grp = threadIdx.x >> 3;
+  const int64_t gid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 3;
+  const int64_t ngroups = (int64_t(gridDim.x) * blockDim.x) >> 3;
+  const int64_t nb = n / 8;  // whole batches only (n is a multiple of 8 here)
+  const int64_t mine = gid < nb ? (nb - 1 - gid) / ngroups + 1 : 0;
+  const int64_t maxb = (nb + ngroups - 1) / ngroups;
+  auto issue = [&](int64_t b) {
+    if (b < mine && lig < 2) {
+      const uint32_t* g = idx + (gid + b * ngroups) * 8 + lig * 4;
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(&ring[grp][b % D][lig * 4]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (int s = 0; s < D - 1; ++s) issue(s);
+  float4 acc = make_float4(0, 0, 0, 0);
+  for (int64_t b = 0; b < maxb; ++b) {
+    issue(b + D - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+    __syncwarp();
+    if (b < mine) {
+      float4 r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = ldrow(F + size_t(ring[grp][b % D][j]) * 8 + lig);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { acc.x += r[j].x; acc.y += r[j].y; acc.z += r[j].z; acc.w += r[j].w; }
+    }
+    __syncwarp();
+  }
+  out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = acc;
+}
+
 // 4 lanes x LDG.256 per row (8 rows per warp instruction)
 struct f8 {
   float v[8];
@@ -475,6 +515,19 @@ int main() {
     float ms = time_ms([&] { k_ldg_hint<H><<<g, 256>>>(F, idx, n, out); });                      \
     printf("  hint=%d blk/sm=%d : %.3f ms  %.2f Grows/s\n", H, BPS, ms, n / ms / 1e6);         \
   }
+    if (getenv("STAGED")) {
+      for (int bps : {4, 8}) {
+        int g = sms * bps;
+        float m0 = time_ms([&] { k_ldg<8><<<g, 256>>>(F, idx, n, out); });
+        float m2 = time_ms([&] { k_ldg_staged<2><<<g, 256>>>(F, idx, n, out); });
+        float m4 = time_ms([&] { k_ldg_staged<4><<<g, 256>>>(F, idx, n, out); });
+        printf("  blk/sm=%d direct LDG idx %.2f | cp.async-staged D=2 %.2f | D=4 %.2f Grows/s\n", bps,
+               n / m0 / 1e6, n / m2 / 1e6, n / m4 / 1e6);
+      }
+      CK(cudaFree(idx));
+      CK(cudaFree(F));
+      continue;
+    }
     if (getenv("SPLIT")) {
       for (uint32_t H : {256u, 512u, 1024u, 2048u, 4096u, 8192u}) {
         int g = sms * 4;
