@@ -11,7 +11,9 @@
 //      sum_r w_r <Y[:, r], F[:, r]> alongside (w: factor column scales),
 //   3. writes the F tile over the consumed Y tile, stores it coalesced, and
 //      reduces it into the CTA's Gram partial, register-blocked 8x8 per
-//      thread (fp32 over <= 8 tiles, then fp64 in shared memory).
+//      thread (fp32 over <= 32 tiles, then fp64 in shared memory; the
+//      sequential per-group flush beats fp64 shared atomics, which are CAS
+//      loops on sm_100).
 // Y and F cross HBM once each (8 bytes per row element).
 #include <cuda_runtime.h>
 
@@ -67,7 +69,7 @@ __global__ void __launch_bounds__(ALS_TILE, 2)
   if (gp >= 9) { A = 3; B = 3; }
   const int ga = A * 8, gb = B * 8;
   double in64 = 0.0;
-  constexpr int FLUSH = 8;
+  constexpr int FLUSH = 32;
   float g32[64];
 #pragma unroll
   for (int q = 0; q < 64; ++q) g32[q] = 0.f;
