@@ -159,7 +159,7 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path is not None else LIB_PATH
+        p = Path(path) if path is not None else Path(os.environ.get("HBK_LIB", LIB_PATH))
         if not p.exists():
             raise NativeUnavailable(
                 f"{p} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`"

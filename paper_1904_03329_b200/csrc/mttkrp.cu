@@ -91,10 +91,10 @@ static constexpr uint32_t FEND = 0x80000000u;  // last nonzero of its fiber
 static constexpr uint32_t SEND = 0x40000000u;  // last nonzero of its slice
 static constexpr uint32_t KMASK = 0x3FFFFFFFu;
 static constexpr uint32_t FB = 0x80000000u;    // B-row position (B-position streams)
-// B-position streams keep the row index pre-scaled to float4 units (x8) in
-// bits 0..29 (rows < 2^27); bit 31 = FB, bit 30 = SEND.  (Measured and
-// dropped: a per-row L2 evict-last/evict-first class by reference count —
-// <= 4% on the HBM-resident tensors, -8% on nell-2 — and a persisting L2
+// B-position streams keep the row index in bits 0..29; bit 31 = FB, bit 30 =
+// SEND.  The kernel scales it by the row stride (one IMAD.WIDE).  (Measured
+// and dropped: a per-row L2 evict-last/evict-first class by reference count
+// — <= 4% on the HBM-resident tensors, -8% on nell-2 — and a persisting L2
 // set-aside, which was slower.)
 static constexpr uint32_t XMASK = 0x3FFFFFFFu;
 
@@ -102,7 +102,57 @@ struct Factors3 {
   const float4* B;  // factor of mode_order[1] (fiber / rest[0])
   const float4* C;  // factor of mode_order[2] (leaf / rest[1])
   float4* out;
+  // rank R = 4 * rs; a launch covers columns [4 col4, 4 col4 + 4 lanes) of
+  // every row (8 lanes x float4 = 32 columns per pass; R > 32 takes several)
+  uint32_t rs;     // row stride in float4
+  uint32_t col4;   // first column of this pass, in float4
+  uint32_t lanes;  // active lanes of an 8-lane group in this pass (1..8)
 };
+// The R = 32 specialisation: one full pass, strides known at compile time
+// (the runtime fields cost registers the B-position kernels do not have).
+struct Factors3R32 {
+  const float4* B;
+  const float4* C;
+  float4* out;
+  static constexpr uint32_t rs = 8, col4 = 0, lanes = 8;
+  Factors3R32() = default;
+  __host__ __device__ explicit Factors3R32(const Factors3& f) : B(f.B), C(f.C), out(f.out) {}
+};
+// A lane's column within the pass; idle lanes of a partial pass mirror the
+// last active one (valid addresses) and never store.
+template <class FX>
+__device__ __forceinline__ uint32_t lane_col(const FX& fx, int lig) {
+  return fx.col4 + min(uint32_t(lig), fx.lanes - 1);
+}
+template <class FX>
+__device__ __forceinline__ bool lane_live(const FX& fx, int lig) {
+  return uint32_t(lig) < fx.lanes;
+}
+
+// &base[x * rs].  R = 32: plain arithmetic (ptxas picks the cheapest form
+// for the constant stride); other ranks: one mad.wide.u32 with the runtime
+// stride (the compiler otherwise splits the 64-bit offset into shift + add
+// pairs).  srowp: a B-position stream index, pre-scaled to float4 units by
+// the plan builder when FX is the R = 32 specialisation (one IMAD.WIDE per
+// row instead of three instructions: 3.5% of the nell-2 step).
+template <class P>
+__device__ __forceinline__ P* rowp(P* base, uint32_t x, const Factors3R32&) {
+  return base + size_t(x) * 8;
+}
+template <class P>
+__device__ __forceinline__ P* rowp(P* base, uint32_t x, const Factors3& fx) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "r"(x), "r"(uint32_t(fx.rs * sizeof(float4))), "l"(base));
+  return reinterpret_cast<P*>(r);
+}
+template <class P>
+__device__ __forceinline__ P* srowp(P* base, uint32_t x, const Factors3R32&) { return base + x; }
+template <class P>
+__device__ __forceinline__ P* srowp(P* base, uint32_t x, const Factors3& fx) {
+  return rowp(base, x, fx);
+}
 
 __device__ __forceinline__ float4 f4zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 __device__ __forceinline__ float4 fma4(float a, float4 x, float4 y) {
@@ -182,11 +232,14 @@ __device__ __forceinline__ uint32_t any_group(uint32_t ballot) {
 // Split-slice hand-over, warp-convergent: groups with `active` add their
 // partial into the slot accumulator; the group whose add completes the slot
 // count stores the row and re-zeroes the slot for the next launch.
-__device__ __forceinline__ void flush_split(const Work& w, bool active, uint32_t slot,
-                                            uint32_t nchunk, uint32_t inc, uint32_t row,
-                                            float4 sa, float4* out, int lane, int lig) {
-  float4* acc = reinterpret_cast<float4*>(w.ws_acc) + size_t(active ? slot : 0) * 8 + lig;
-  if (active) red_add4(acc, sa);
+template <class FX>
+__device__ __forceinline__ void flush_split(const Work& w, const FX& fx, bool active,
+                                            uint32_t slot, uint32_t nchunk, uint32_t inc,
+                                            uint32_t row, float4 sa, int lane, int lig) {
+  const bool live = lane_live(fx, lig);
+  float4* acc = reinterpret_cast<float4*>(w.ws_acc) + size_t(active ? slot : 0) * fx.rs +
+                fx.col4 + lig;
+  if (active && live) red_add4(acc, sa);
   __threadfence();
   __syncwarp();
   uint32_t old = 0;
@@ -194,9 +247,11 @@ __device__ __forceinline__ void flush_split(const Work& w, bool active, uint32_t
   old = __shfl_sync(FULL, old, lane & ~7);
   if (active && old + inc == nchunk) {
     __threadfence();
-    const float4 r = ld_cg4(acc);
-    out[size_t(row) * 8 + lig] = r;
-    st_cg4(acc, f4zero());
+    if (live) {
+      const float4 r = ld_cg4(acc);
+      fx.out[size_t(row) * fx.rs + fx.col4 + lig] = r;
+      st_cg4(acc, f4zero());
+    }
     if (lig == 0) w.ws_cnt[slot] = 0;
   }
 }
@@ -207,15 +262,16 @@ __device__ __forceinline__ void flush_split(const Work& w, bool active, uint32_t
 // slice rows are consumed in order from their own streams (no pointer is
 // chased).  The next batch's stream words are loaded before the current
 // batch is reduced.  Returns the partial of a chunk task (zero for runs).
-__device__ __forceinline__ float4 csf_tasks(const Work& w, const Factors3& fx, const Task& t,
+template <class FX>
+__device__ __forceinline__ float4 csf_tasks(const Work& w, const FX& fx, const Task& t,
                                             int g, int lig, uint64_t pol_s, uint64_t pol_r,
                                             float4* __restrict__ slots) {
   const uint32_t lo = t.lo, hi = t.hi;
   const bool chunk = t.slot != NOSLOT;
   const uint32_t my_batches = hi > lo ? (hi - lo + 7) / 8 : 0;
   const uint32_t nbat = __reduce_max_sync(FULL, my_batches);
-  const float4* Cl = fx.C + lig;
-  const float4* Bl = fx.B + lig;
+  const float4* Cl = fx.C + lane_col(fx, lig);
+  const float4* Bl = fx.B + lane_col(fx, lig);
   uint32_t s = t.s, f = t.f;
   float4 fa = f4zero(), sa = f4zero();
   uint2 pr = make_uint2(0u, 0u);
@@ -239,7 +295,7 @@ __device__ __forceinline__ float4 csf_tasks(const Work& w, const Factors3& fx, c
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t kj = __shfl_sync(FULL, k, j, 8);
-      if (uint32_t(j) < n) c[j] = ld_row4(Cl + size_t(kj) * 8, pol_r);
+      if (uint32_t(j) < n) c[j] = ld_row4(rowp(Cl, kj, fx), pol_r);
     }
     // fiber rows of the fibers ending in this batch -> slot = end position
     uint32_t tf = 0;
@@ -247,7 +303,7 @@ __device__ __forceinline__ float4 csf_tasks(const Work& w, const Factors3& fx, c
     for (int j = 0; j < 8; ++j) {
       if ((eany >> j) & 1u) {
         const uint32_t fj = __shfl_sync(FULL, fi, tf, 8);
-        if ((ebits >> j) & 1u) cp_async16(slots + j * 8, Bl + size_t(fj) * 8);
+        if ((ebits >> j) & 1u) cp_async16(slots + j * 8, rowp(Bl, fj, fx));
         tf += (ebits >> j) & 1u;
       }
     }
@@ -274,7 +330,7 @@ __device__ __forceinline__ float4 csf_tasks(const Work& w, const Factors3& fx, c
       if ((sany >> j) & 1u) {
         const uint32_t row = __shfl_sync(FULL, sr_cur, ts, 8);
         if ((sbits >> j) & 1u) {
-          fx.out[size_t(row) * 8 + lig] = sa;
+          if (lane_live(fx, lig)) fx.out[size_t(row) * fx.rs + fx.col4 + lig] = sa;
           sa = f4zero();
           ++ts;
         }
@@ -284,7 +340,7 @@ __device__ __forceinline__ float4 csf_tasks(const Work& w, const Factors3& fx, c
   }
   if (chunk && pending) {  // the chunk ended inside fiber f
     const uint32_t fj = __ldg(w.csf_fidx + f);
-    sa = fmav4(fa, ld_row4(Bl + size_t(fj) * 8, pol_r), sa);
+    sa = fmav4(fa, ld_row4(rowp(Bl, fj, fx), pol_r), sa);
   }
   return sa;
 }
@@ -298,14 +354,14 @@ __device__ __forceinline__ float4 csf_tasks(const Work& w, const Factors3& fx, c
 // UNIFORM (padded heavy layout): the four groups' streams have identical
 // structure, so B positions are warp-uniform and take a uniform branch
 // instead of predicated FMAs; heavy tasks are slice chunks (no SEND).
-template <bool UNIFORM>
-__device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const Factors3& fx, const Task& t,
+template <bool UNIFORM, class FX>
+__device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const FX& fx, const Task& t,
                                                  int g, int lig, uint64_t pol_s, uint64_t pol_r) {
   const uint32_t lo = t.lo, hi = t.hi;
   const bool chunk = UNIFORM || t.slot != NOSLOT;
   const uint32_t nbat = __reduce_max_sync(FULL, hi > lo ? (hi - lo + 7) / 8 : 0u);
-  const float4* Cl = fx.C + lig;
-  const float4* Bl = fx.B + lig;
+  const float4* Cl = fx.C + lane_col(fx, lig);
+  const float4* Bl = fx.B + lane_col(fx, lig);
   const uint2* pairs = w.csf_pairs;
   const uint32_t Sm1 = w.csf_S ? w.csf_S - 1 : 0;
   uint32_t s = t.s;
@@ -328,7 +384,7 @@ __device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const Factors3& 
     for (int j = 0; j < 8; ++j) {
       const uint32_t xj = __shfl_sync(FULL, pr.x, j, 8);
       const float4* bp = (UNIFORM ? ((bbits >> j) & 1u) : (xj & FB)) ? Bl : Cl;
-      r[j] = ld_row4(bp + (xj & XMASK), pol_r);
+      r[j] = ld_row4(srowp(bp, xj & XMASK, fx), pol_r);
     }
     const float vv = __uint_as_float(pr.y);
     const uint32_t sr_cur = sr;
@@ -361,7 +417,7 @@ __device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const Factors3& 
       if ((sany >> j) & 1u) {
         const uint32_t row = __shfl_sync(FULL, sr_cur, ts, 8);
         if ((sbits >> j) & 1u) {
-          fx.out[size_t(row) * 8 + lig] = sa;
+          if (lane_live(fx, lig)) fx.out[size_t(row) * fx.rs + fx.col4 + lig] = sa;
           sa = f4zero();
           ++ts;
         }
@@ -378,15 +434,16 @@ __device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const Factors3& 
 // 8 C rows into registers; v * B[j] o C[k] accumulates into the slice
 // partial (kernels.py:210-214).  Measured: loading both rows into registers
 // (98 registers, 2 CTAs/SM) was 10-14% slower on delicious-3d.
-__device__ __forceinline__ float4 csl_tasks(const Work& w, const Factors3& fx, const Task& t,
+template <class FX>
+__device__ __forceinline__ float4 csl_tasks(const Work& w, const FX& fx, const Task& t,
                                             int g, int lig, uint64_t pol_s, uint64_t pol_r,
                                             float4* __restrict__ slots) {
   const uint32_t lo = t.lo, hi = t.hi;
   const bool chunk = t.slot != NOSLOT;
   const uint32_t my_batches = hi > lo ? (hi - lo + 7) / 8 : 0;
   const uint32_t nbat = __reduce_max_sync(FULL, my_batches);
-  const float4* Cl = fx.C + lig;
-  const float4* Bl = fx.B + lig;
+  const float4* Cl = fx.C + lane_col(fx, lig);
+  const float4* Bl = fx.B + lane_col(fx, lig);
   uint32_t s = t.s;
   float4 sa = f4zero();
   uint2 pr = make_uint2(0u, 0u);
@@ -411,8 +468,8 @@ __device__ __forceinline__ float4 csl_tasks(const Work& w, const Factors3& fx, c
       const uint32_t bj = __shfl_sync(FULL, jx, j, 8);
       const uint32_t cj = __shfl_sync(FULL, k, j, 8);
       if (uint32_t(j) < n) {
-        cp_async16(slots + j * 8, Bl + size_t(bj) * 8);
-        c[j] = ld_row4(Cl + size_t(cj) * 8, pol_r);
+        cp_async16(slots + j * 8, rowp(Bl, bj, fx));
+        c[j] = ld_row4(rowp(Cl, cj, fx), pol_r);
       }
     }
     const uint32_t sr_cur = sr;
@@ -434,7 +491,7 @@ __device__ __forceinline__ float4 csl_tasks(const Work& w, const Factors3& fx, c
       if ((sany >> j) & 1u) {
         const uint32_t row = __shfl_sync(FULL, sr_cur, ts, 8);
         if ((sbits >> j) & 1u) {
-          fx.out[size_t(row) * 8 + lig] = sa;
+          if (lane_live(fx, lig)) fx.out[size_t(row) * fx.rs + fx.col4 + lig] = sa;
           sa = f4zero();
           ++ts;
         }
@@ -445,14 +502,15 @@ __device__ __forceinline__ float4 csl_tasks(const Work& w, const Factors3& fx, c
 }
 
 // ------------------------------------------------------------ COO tasks --
-__device__ __forceinline__ void coo_tasks(const Work& w, const Factors3& fx, const Task& t,
+template <class FX>
+__device__ __forceinline__ void coo_tasks(const Work& w, const FX& fx, const Task& t,
                                           int lig, uint64_t pol_s, uint64_t pol_r,
                                           float4* __restrict__ slots) {
   const uint32_t lo = t.lo, hi = t.hi;
   const uint32_t my_batches = hi > lo ? (hi - lo + 7) / 8 : 0;
   const uint32_t nbat = __reduce_max_sync(FULL, my_batches);
-  const float4* Cl = fx.C + lig;
-  const float4* Bl = fx.B + lig;
+  const float4* Cl = fx.C + lane_col(fx, lig);
+  const float4* Bl = fx.B + lane_col(fx, lig);
   uint4 q = make_uint4(0u, 0u, 0u, 0u);
   if (lo + lig < hi) q = ld_stream_u4(w.coo_quads + lo + lig, pol_s);
   uint32_t base = lo;
@@ -464,8 +522,8 @@ __device__ __forceinline__ void coo_tasks(const Work& w, const Factors3& fx, con
       const uint32_t bj = __shfl_sync(FULL, q.y, j, 8);
       const uint32_t cj = __shfl_sync(FULL, q.z, j, 8);
       if (uint32_t(j) < n) {
-        cp_async16(slots + j * 8, Bl + size_t(bj) * 8);
-        c[j] = ld_row4(Cl + size_t(cj) * 8, pol_r);
+        cp_async16(slots + j * 8, rowp(Bl, bj, fx));
+        c[j] = ld_row4(rowp(Cl, cj, fx), pol_r);
       }
     }
     const uint4 cur = q;
@@ -482,7 +540,7 @@ __device__ __forceinline__ void coo_tasks(const Work& w, const Factors3& fx, con
         r.y *= c[j].y;
         r.z *= c[j].z;
         r.w *= c[j].w;
-        fx.out[size_t(row) * 8 + lig] = r;
+        if (lane_live(fx, lig)) fx.out[size_t(row) * fx.rs + fx.col4 + lig] = r;
       }
     }
   }
@@ -490,7 +548,8 @@ __device__ __forceinline__ void coo_tasks(const Work& w, const Factors3& fx, con
 
 // Rows owned by no bucket: a group loads 8 row numbers at once (one per
 // lane) and stores 8 zero rows, so the loop is not a chain of dependent loads.
-__device__ __forceinline__ void zero_task(const Work& w, const Factors3& fx, const Task& t,
+template <class FX>
+__device__ __forceinline__ void zero_task(const Work& w, const FX& fx, const Task& t,
                                           int lig) {
   const uint32_t nbat = __reduce_max_sync(FULL, t.hi > t.lo ? (t.hi - t.lo + 7) / 8 : 0u);
   uint32_t base = t.lo;
@@ -500,7 +559,7 @@ __device__ __forceinline__ void zero_task(const Work& w, const Factors3& fx, con
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t row = __shfl_sync(FULL, rl, j, 8);
-      if (uint32_t(j) < n) fx.out[size_t(row) * 8 + lig] = f4zero();
+      if (uint32_t(j) < n && lane_live(fx, lig)) fx.out[size_t(row) * fx.rs + fx.col4 + lig] = f4zero();
     }
   }
 }
@@ -513,9 +572,9 @@ __device__ __forceinline__ void zero_task(const Work& w, const Factors3& fx, con
 static constexpr int FAST_BLOCK = 256;
 enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2, KIND_CSF_BPOS = 3, KIND_CSF_BPOS4 = 4, KIND_CSF_UNI = 5 };
 
-template <int KIND>
+template <int KIND, class FX>
 __global__ void __launch_bounds__(FAST_BLOCK, (KIND == KIND_CSF_BPOS4 || KIND == KIND_CSF_UNI) ? 4 : 3)
-    k_mttkrp3_r32(const __grid_constant__ Work w, const __grid_constant__ Factors3 fx) {
+    k_mttkrp3_r32(const __grid_constant__ Work w, const __grid_constant__ FX fx) {
   // per lane: 8 slots of 16 B (one per batch position) for staged B rows
   __shared__ float4 s_slots[FAST_BLOCK * 8];
   const int lane = threadIdx.x & 31;
@@ -548,9 +607,9 @@ __global__ void __launch_bounds__(FAST_BLOCK, (KIND == KIND_CSF_BPOS4 || KIND ==
       if (same) {
         float4 r = add4(sa, shfl_xor4(sa, 8));
         r = add4(r, shfl_xor4(r, 16));
-        flush_split(w, g == 0, t.slot, t.nchunk, 4u, row, r, fx.out, lane, lig);
+        flush_split(w, fx, g == 0, t.slot, t.nchunk, 4u, row, r, lane, lig);
       } else if (__any_sync(FULL, mine)) {
-        flush_split(w, mine, t.slot, t.nchunk, 1u, row, sa, fx.out, lane, lig);
+        flush_split(w, fx, mine, t.slot, t.nchunk, 1u, row, sa, lane, lig);
       }
     } else if (base < w.n2) {
       coo_tasks(w, fx, t, lig, pol_s, pol_r, slots);
@@ -576,13 +635,13 @@ __global__ void __launch_bounds__(FAST_BLOCK, (KIND == KIND_CSF_BPOS4 || KIND ==
 // the MTTKRP when factor rows are L2-resident.
 template <int KIND>
 __global__ void __launch_bounds__(FAST_BLOCK, 4)
-    k_gather_probe(const __grid_constant__ Work w, const __grid_constant__ Factors3 fx,
+    k_gather_probe(const __grid_constant__ Work w, const __grid_constant__ Factors3R32 fx,
                    float4* __restrict__ sink) {
   const int lane = threadIdx.x & 31, g = lane >> 3, lig = lane & 7;
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_r = policy_evict_last();
-  const float4* Cl = fx.C + lig;
-  const float4* Bl = fx.B + lig;
+  const float4* Cl = fx.C + lane_col(fx, lig);
+  const float4* Bl = fx.B + lane_col(fx, lig);
   float4 acc = f4zero();
   const uint32_t first = KIND == KIND_CSL ? w.n0 : (KIND == KIND_COO ? w.n1 : 0u);
   const uint32_t last = KIND == KIND_CSL ? w.n1 : (KIND == KIND_COO ? w.n2 : w.n0);
@@ -602,7 +661,7 @@ __global__ void __launch_bounds__(FAST_BLOCK, 4)
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const uint32_t xj = __shfl_sync(FULL, pr.x, j, 8);
-          acc = add4(acc, ld_row4(((xj & FB) ? Bl : Cl) + (xj & XMASK), pol_r));
+          acc = add4(acc, ld_row4(srowp((xj & FB) ? Bl : Cl, xj & XMASK, fx), pol_r));
         }
       } else if (KIND == KIND_CSL) {
         const uint2 pr = live ? ld_stream_u2(w.csl_pairs + p0 + lig, pol_s) : make_uint2(0u, 0u);
@@ -611,8 +670,8 @@ __global__ void __launch_bounds__(FAST_BLOCK, 4)
         for (int j = 0; j < 8; ++j) {
           const uint32_t kj = __shfl_sync(FULL, pr.x, j, 8) & KMASK;
           const uint32_t bj = __shfl_sync(FULL, jx, j, 8);
-          acc = add4(acc, ld_row4(Cl + size_t(kj) * 8, pol_r));
-          acc = add4(acc, ld_row4(Bl + size_t(bj) * 8, pol_r));
+          acc = add4(acc, ld_row4(rowp(Cl, kj, fx), pol_r));
+          acc = add4(acc, ld_row4(rowp(Bl, bj, fx), pol_r));
         }
       } else {
         const uint4 q = live ? ld_stream_u4(w.coo_quads + p0 + lig, pol_s) : make_uint4(0u, 0u, 0u, 0u);
@@ -620,8 +679,8 @@ __global__ void __launch_bounds__(FAST_BLOCK, 4)
         for (int j = 0; j < 8; ++j) {
           const uint32_t bj = __shfl_sync(FULL, q.y, j, 8);
           const uint32_t cj = __shfl_sync(FULL, q.z, j, 8);
-          acc = add4(acc, ld_row4(Cl + size_t(cj) * 8, pol_r));
-          acc = add4(acc, ld_row4(Bl + size_t(bj) * 8, pol_r));
+          acc = add4(acc, ld_row4(rowp(Cl, cj, fx), pol_r));
+          acc = add4(acc, ld_row4(rowp(Bl, bj, fx), pol_r));
         }
       }
     }
@@ -671,14 +730,19 @@ struct WorkN {
   T* out;
 };
 
+// Split-slice hand-over of the generic kernel: every rank chunk of a task
+// adds its columns into the slot accumulator; once all chunks are added the
+// task arrives (one counter increment per task), and the last task to arrive
+// stores every column of the row and re-zeroes the slot.
 template <class T>
-__device__ __forceinline__ void gen_flush_split(const Work& w, const WorkN<T>& wn, uint32_t slot,
-                                                uint32_t nchunk, uint32_t row, int r0, T sa,
-                                                int lane) {
+__device__ __forceinline__ void gen_add_split(const WorkN<T>& wn, uint32_t slot, int r0, T sa,
+                                              int lane) {
+  if (r0 + lane < wn.rank) atomicAdd(wn.acc + size_t(slot) * wn.rank + r0 + lane, sa);
+}
+template <class T>
+__device__ __forceinline__ void gen_finish_split(const Work& w, const WorkN<T>& wn, uint32_t slot,
+                                                 uint32_t nchunk, uint32_t row, int lane) {
   const int R = wn.rank;
-  const bool act = r0 + lane < R;
-  T* acc = wn.acc + size_t(slot) * R + r0 + lane;
-  if (act) atomicAdd(acc, sa);
   __threadfence();
   __syncwarp();
   uint32_t old = 0;
@@ -686,9 +750,9 @@ __device__ __forceinline__ void gen_flush_split(const Work& w, const WorkN<T>& w
   old = __shfl_sync(0xFFFFFFFFu, old, 0);
   if (old == nchunk - 1) {
     __threadfence();
-    if (act) {
-      const T r = __ldcg(acc);
-      wn.out[size_t(row) * R + r0 + lane] = r;
+    for (int r = lane; r < R; r += 32) {
+      T* acc = wn.acc + size_t(slot) * R + r;
+      wn.out[size_t(row) * R + r] = __ldcg(acc);
       __stcg(acc, T(0));
     }
     __syncwarp();
@@ -750,7 +814,7 @@ __global__ void __launch_bounds__(256) k_mttkrp_generic(const __grid_constant__ 
             }
             sa = fa * m + sa;
           }
-          gen_flush_split(w, wn, t.slot, t.nchunk, w.csf_sidx[t.s], rc * 32, sa, lane);
+          gen_add_split(wn, t.slot, rc * 32, sa, lane);
         }
       } else if (ti < w.n1) {  // CSL
         uint32_t s = t.s;
@@ -769,7 +833,7 @@ __global__ void __launch_bounds__(256) k_mttkrp_generic(const __grid_constant__ 
             if (s < w.csl_S) send = w.csl_send[s + 1];
           }
         }
-        if (chunk) gen_flush_split(w, wn, t.slot, t.nchunk, w.csl_sidx[t.s], rc * 32, sa, lane);
+        if (chunk) gen_add_split(wn, t.slot, rc * 32, sa, lane);
       } else if (ti < w.n2) {  // COO (unique rows)
         for (uint32_t i = t.lo; i < t.hi; ++i) {
           if (!act) continue;
@@ -783,6 +847,9 @@ __global__ void __launch_bounds__(256) k_mttkrp_generic(const __grid_constant__ 
           if (act) wn.out[size_t(w.zero_rows[i]) * R + r] = T(0);
       }
     }
+    if (chunk && ti < w.n1)
+      gen_finish_split(w, wn, t.slot, t.nchunk,
+                       ti < w.n0 ? w.csf_sidx[t.s] : w.csl_sidx[t.s], lane);
   }
   __syncwarp();
   if (lane == 0) {
@@ -972,18 +1039,16 @@ __global__ void k_empty_tasks(Task* __restrict__ tasks, int64_t n) {
 }
 
 // B-position stream of a CSF bucket in tree order: fiber f's pairs start at
-// position lptr[f] + f and are followed by (fidx[f] | FB, 0).  Row indices
-// are stored pre-scaled to float4 units (x8) so the kernel's address is one
-// IMAD.WIDE off the lane's base pointer.
+// position lptr[f] + f and are followed by (fidx[f] | FB, 0).
 __global__ void k_bpos_stream(const uint32_t* __restrict__ lptr, const uint32_t* __restrict__ fidx,
                               const uint32_t* __restrict__ leaf, const float* __restrict__ val,
-                              int64_t F, uint2* __restrict__ out) {
+                              int64_t F, uint32_t sh, uint2* __restrict__ out) {
   for (int64_t f = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; f < F;
        f += int64_t(gridDim.x) * blockDim.x) {
     const uint32_t a = lptr[f], b = lptr[f + 1];
     uint2* o = out + a + f;
-    for (uint32_t i = a; i < b; ++i) *o++ = make_uint2(leaf[i] << 3, __float_as_uint(val[i]));
-    *o = make_uint2((fidx[f] << 3) | FB, 0u);
+    for (uint32_t i = a; i < b; ++i) *o++ = make_uint2(leaf[i] << sh, __float_as_uint(val[i]));
+    *o = make_uint2((fidx[f] << sh) | FB, 0u);
   }
 }
 // SEND on the B position of each slice's last fiber
@@ -1040,6 +1105,10 @@ struct hbk_plan {
   bool fast = false;
   int csf_variant = 2;  // 0: smem-slot kernel, 1|2: B-position streams at 3|4 CTAs per SM (HBK_CSF_VARIANT)
   bool bpos = false;
+  // R = 32 with B/C extents < 2^27: the Factors3R32 kernels, B-position
+  // stream indices pre-scaled to float4 units (bshift 3)
+  bool r32 = false;
+  uint32_t bshift = 0;
   int grid = 0, block = 256;
   int gen_grid = 0;
   int grids[3] = {0, 0, 0};
@@ -1225,7 +1294,8 @@ __global__ void k_group_fill(const uint32_t* __restrict__ tfirst, const uint32_t
                              const uint32_t* __restrict__ sj, const uint32_t* __restrict__ gofs,
                              const uint32_t* __restrict__ fofs, int64_t NW, uint32_t G,
                              const uint32_t* __restrict__ leaf, const float* __restrict__ val,
-                             bool pad, uint2* __restrict__ pairs, uint32_t* __restrict__ fj) {
+                             bool pad, uint32_t sh, uint2* __restrict__ pairs,
+                             uint32_t* __restrict__ fj) {
   for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < NW * 4;
        x += int64_t(gridDim.x) * blockDim.x) {
     const int64_t w = x >> 2;
@@ -1244,10 +1314,10 @@ __global__ void k_group_fill(const uint32_t* __restrict__ tfirst, const uint32_t
           j = sj[q];
         }
         for (uint32_t t = 0; t < len; ++t)
-          pairs[dst + t] = make_uint2(leaf[off + t] << 3, __float_as_uint(val[off + t]));
+          pairs[dst + t] = make_uint2(leaf[off + t] << sh, __float_as_uint(val[off + t]));
         for (uint32_t t = len; t < Lq; ++t) pairs[dst + t] = make_uint2(0u, 0u);
         dst += Lq;
-        pairs[dst++] = make_uint2((j << 3) | FB, 0u);
+        pairs[dst++] = make_uint2((j << sh) | FB, 0u);
         fj[fpos++] = j;
       }
       continue;
@@ -1449,7 +1519,7 @@ struct HeavyLayout {
 
 // Builds the heavy-slice layout of a 3rd-order CSF bucket (see above).
 static HeavyLayout heavy_layout(const hbk_csf* c, const uint32_t* loff, const uint32_t* fpos,
-                                uint32_t H, uint32_t tau, uint32_t W, uint32_t slot_base, bool bpos,
+                                uint32_t H, uint32_t tau, uint32_t W, uint32_t slot_base, bool bpos, uint32_t bshift,
                                 cudaStream_t st) {
   HeavyLayout hl;
   const int64_t S = c->n[0], F = c->n[1];
@@ -1527,7 +1597,7 @@ static HeavyLayout heavy_layout(const hbk_csf* c, const uint32_t* loff, const ui
   k_group_fill<<<grid_for(NG, 128), 128, 0, st>>>(
       tfirst.as<uint32_t>(), perm, soff.as<uint32_t>(), slen.as<uint32_t>(), sj.as<uint32_t>(),
       gofs.as<uint32_t>(), fofs.as<uint32_t>(), NW, G, c->leaf.as<uint32_t>(), c->v32.as<float>(),
-      bpos, hl.pairs.as<uint2>(), hl.fj.as<uint32_t>());
+      bpos, bshift, hl.pairs.as<uint2>(), hl.fj.as<uint32_t>());
   check_launch("k_group_fill");
   k_group_tasks<<<grid_for(NG, 256), 256, 0, st>>>(tslice.as<uint32_t>(), gofs.as<uint32_t>(),
                                                    gnnz.as<uint32_t>(), fofs.as<uint32_t>(),
@@ -1554,13 +1624,44 @@ __global__ void k_shift_slots(Task* __restrict__ t, int64_t n, uint32_t base) {
     if (t[i].slot != NOSLOT) t[i].slot += base;
 }
 
+// Resident CTAs per SM of the fast kernel of a kind (k 0 = light CSF,
+// 1 = CSL, 2 = COO, 3 = heavy CSF), for the factor shape the plan launches.
+template <class FX>
+static int fast_occupancy(const hbk_plan* p, int k) {
+  int per_sm = 0;
+  const void* fn = nullptr;
+  if (k == 0)
+    fn = p->bpos ? (p->csf_variant == 2 ? reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF_BPOS4, FX>)
+                                        : reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF_BPOS, FX>))
+                 : reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF, FX>);
+  else if (k == 1)
+    fn = reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSL, FX>);
+  else if (k == 2)
+    fn = reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_COO, FX>);
+  else
+    fn = p->bpos ? reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF_UNI, FX>)
+                 : reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF, FX>);
+  HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, p->block, 0));
+  return per_sm;
+}
+
+static int fast_occupancy_any(const hbk_plan* p, int k) {
+  return p->r32 ? fast_occupancy<Factors3R32>(p, k) : fast_occupancy<Factors3>(p, k);
+}
+
 static void build_plan(hbk_plan* p, cudaStream_t st) {
   const int N = p->order;
   const int R = p->rank;
   // fast path: order 3, R = 32 (8 lanes x float4 per row); the streams keep
   // two flag bits in the leaf coordinate, so leaf extents must stay < 2^30
-  p->fast = (N == 3 && R == 32 && p->dims[p->mo[2]] < (int64_t(1) << 29) &&
+  // fast path: order 3, R a multiple of 4 (float4 rows; R > 32 runs in
+  // passes of 32 columns); the old-variant streams keep two flag bits in the
+  // leaf coordinate, so leaf extents must stay < 2^29
+  p->fast = (N == 3 && R >= 4 && R % 4 == 0 && p->dims[p->mo[2]] < (int64_t(1) << 29) &&
              p->dims[p->mo[1]] < (int64_t(1) << 29));
+  p->r32 = p->fast && R == 32 && p->dims[p->mo[2]] < (int64_t(1) << 27) &&
+           p->dims[p->mo[1]] < (int64_t(1) << 27);
+  p->bshift = p->r32 ? 3u : 0u;
   const int gpw = p->fast ? 4 : 1;  // task ranges padded so a warp never straddles kinds
   uint32_t task_nnz = TASK_NNZ_CSF;
   if (const char* e = getenv("HBK_TASK_NNZ")) task_nnz = std::max(8, atoi(e));
@@ -1576,8 +1677,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   // heavy-slice layout (fast path): slices with more than H nonzeros
   // B-position streams (default fast CSF path): every slice with more than
   // Tcsf nonzeros goes to the heavy layout, lighter slices form runs
-  p->bpos = p->fast && !p->sched && p->csf_variant >= 1 && p->dims[p->mo[1]] < (int64_t(1) << 27) &&
-            p->dims[p->mo[2]] < (int64_t(1) << 27);
+  p->bpos = p->fast && !p->sched && p->csf_variant >= 1;
   uint32_t heavy_H = p->bpos ? Tcsf : 4 * Tcsf, heavy_tau = 32, heavy_W = 2048;
   if (const char* e = getenv("HBK_HEAVY_H")) heavy_H = uint32_t(std::max(0, atoi(e)));
   if (const char* e = getenv("HBK_HEAVY_TAU")) heavy_tau = uint32_t(std::min(65535, std::max(1, atoi(e))));
@@ -1665,7 +1765,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
                                   c->ptr[L].as<uint32_t>(), S, uint32_t(c->M), Tcsf, st, heavy_H,
                                   p->bpos ? fpos.as<uint32_t>() : nullptr);
         HeavyLayout hl = heavy_layout(c, p->csf_send.as<uint32_t>(), fpos.as<uint32_t>(), heavy_H,
-                                      heavy_tau, heavy_W, uint32_t(tcsf_light.slots), p->bpos, st);
+                                      heavy_tau, heavy_W, uint32_t(tcsf_light.slots), p->bpos, p->bshift, st);
         HBK_REQUIRE(tcsf_light.slots + hl.slots == tcsf.slots, HBK_ECUDA,
                     "heavy layout slot accounting mismatch");
         p->heavy_pairs = hl.pairs;
@@ -1700,7 +1800,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       uint2* pp = p->csf_pairs.as<uint2>();
       k_bpos_stream<<<grid_for(c->n[L], 128), 128, 0, st>>>(
           c->ptr[L].as<uint32_t>(), c->idx[L].as<uint32_t>(), c->leaf.as<uint32_t>(),
-          c->v32.as<float>(), c->n[L], pp);
+          c->v32.as<float>(), c->n[L], p->bshift, pp);
       check_launch("k_bpos_stream");
       k_bpos_send<<<grid_for(S, 256), 256, 0, st>>>(fpos.as<uint32_t>(), c->ptr[L].as<uint32_t>(),
                                                     S, pp);
@@ -1898,18 +1998,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     p->block = FAST_BLOCK;
     const int64_t ntk[3] = {int64_t(w.n0), int64_t(w.n1) - w.n0, int64_t(w.n3) - w.n1};
     for (int k = 0; k < 3; ++k) {
-      if (k == 0)
-        HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm,
-            p->bpos ? (p->csf_variant == 2 ? k_mttkrp3_r32<KIND_CSF_BPOS4> : k_mttkrp3_r32<KIND_CSF_BPOS>)
-                  : k_mttkrp3_r32<KIND_CSF>,
-            p->block, 0));
-      if (k == 1)
-        HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp3_r32<KIND_CSL>,
-                                                               p->block, 0));
-      if (k == 2)
-        HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mttkrp3_r32<KIND_COO>,
-                                                               p->block, 0));
+      per_sm = fast_occupancy_any(p, k);
       p->grids[k] = ntk[k] > 0 ? grid_for_tasks(ntk[k], per_sm, 4) : 0;
       w.total_warps[k] = uint32_t(p->grids[k]) * (p->block / 32);
       launches += ntk[k] > 0;
@@ -1923,8 +2012,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       wh.csf_pairs = p->heavy_pairs.as<uint2>();
       wh.csf_fidx = p->heavy_fj.as<uint32_t>();
       wh.csf_F = uint32_t(heavy_segments);
-      HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &per_sm, p->bpos ? k_mttkrp3_r32<KIND_CSF_UNI> : k_mttkrp3_r32<KIND_CSF>, p->block, 0));
+      per_sm = fast_occupancy_any(p, 3);
       p->grid_heavy = grid_for_tasks(heavy_ntasks, per_sm, 4);
       wh.total_warps[0] = uint32_t(p->grid_heavy) * (p->block / 32);
       launches += 1;
@@ -1951,7 +2039,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   p->info.rank = R;
   p->info.out_rows = rows;
   p->info.split_rows = slots;
-  p->info.launches = launches;
+  p->info.launches = p->fast ? int64_t(launches) * ((R + 31) / 32) : launches;
   p->info.fast_path = p->fast;
   int64_t nnz = 0;
   if (p->csf) nnz += p->csf->M;
@@ -2032,6 +2120,29 @@ static void launch_generic(const hbk_plan* p, const T* const* factors, T* out, c
 
 using namespace hbk;
 
+namespace hbk {
+template <class FX>
+static void launch_fast(const hbk_plan* p, const FX& fx, cudaStream_t st) {
+  if (p->grids[0]) {
+    if (p->bpos && p->csf_variant == 2)
+      k_mttkrp3_r32<KIND_CSF_BPOS4, FX><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
+    else if (p->bpos)
+      k_mttkrp3_r32<KIND_CSF_BPOS, FX><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
+    else
+      k_mttkrp3_r32<KIND_CSF, FX><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
+  }
+  if (p->grid_heavy) {
+    if (p->bpos)
+      k_mttkrp3_r32<KIND_CSF_UNI, FX><<<p->grid_heavy, p->block, 0, st>>>(p->work_heavy, fx);
+    else
+      k_mttkrp3_r32<KIND_CSF, FX><<<p->grid_heavy, p->block, 0, st>>>(p->work_heavy, fx);
+  }
+  if (p->grids[1]) k_mttkrp3_r32<KIND_CSL, FX><<<p->grids[1], p->block, 0, st>>>(p->work, fx);
+  if (p->grids[2]) k_mttkrp3_r32<KIND_COO, FX><<<p->grids[2], p->block, 0, st>>>(p->work, fx);
+  check_launch("k_mttkrp3_r32");
+}
+}  // namespace hbk
+
 extern "C" {
 
 int hbk_plan_create(hbk_coo* coo, hbk_csl* csl, hbk_csf* csf, hbk_sched* sched, int mode, int rank,
@@ -2110,23 +2221,17 @@ int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out,
                           16 ==
                       0,
                   HBK_EINVAL, "factor and output buffers must be 16-byte aligned");
-      if (p->grids[0]) {
-        if (p->bpos && p->csf_variant == 2)
-          k_mttkrp3_r32<KIND_CSF_BPOS4><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
-        else if (p->bpos)
-          k_mttkrp3_r32<KIND_CSF_BPOS><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
-        else
-          k_mttkrp3_r32<KIND_CSF><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
+      const int R = p->rank;
+      if (p->r32) {
+        launch_fast(p, Factors3R32(fx), st);
+      } else {
+        fx.rs = uint32_t(R / 4);
+        for (int c0 = 0; c0 < R; c0 += 32) {  // passes of 32 columns
+          fx.col4 = uint32_t(c0 / 4);
+          fx.lanes = uint32_t(std::min(8, (R - c0) / 4));
+          launch_fast(p, fx, st);
+        }
       }
-      if (p->grid_heavy) {
-        if (p->bpos)
-          k_mttkrp3_r32<KIND_CSF_UNI><<<p->grid_heavy, p->block, 0, st>>>(p->work_heavy, fx);
-        else
-          k_mttkrp3_r32<KIND_CSF><<<p->grid_heavy, p->block, 0, st>>>(p->work_heavy, fx);
-      }
-      if (p->grids[1]) k_mttkrp3_r32<KIND_CSL><<<p->grids[1], p->block, 0, st>>>(p->work, fx);
-      if (p->grids[2]) k_mttkrp3_r32<KIND_COO><<<p->grids[2], p->block, 0, st>>>(p->work, fx);
-      check_launch("k_mttkrp3_r32");
     } else {
       launch_generic<float>(p, factors, out, st);
     }
@@ -2135,21 +2240,23 @@ int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out,
 
 int hbk_plan_probe(const hbk_plan* p, const float* const* factors, void* stream) {
   return guarded([&] {
-    HBK_REQUIRE(p->bpos, HBK_EINVAL, "the gather probe needs a B-position (fast order-3, R=32) plan");
+    HBK_REQUIRE(p->bpos && p->r32, HBK_EINVAL,
+                "the gather probe needs a B-position (fast order-3, R=32, extents < 2^27) plan");
     cudaStream_t st = to_stream(stream);
     Factors3 fx;
     fx.B = reinterpret_cast<const float4*>(factors[p->mo[1]]);
     fx.C = reinterpret_cast<const float4*>(factors[p->mo[2]]);
     fx.out = nullptr;
+    const Factors3R32 f32(fx);
     float4* sink = p->probe_sink.as<float4>();
     int dev = 0, sms = 0;
     HBK_CUDA(cudaGetDevice(&dev));
     HBK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int grid = sms * 4;
-    if (p->work.n0) k_gather_probe<KIND_CSF><<<grid, FAST_BLOCK, 0, st>>>(p->work, fx, sink);
-    if (p->grid_heavy) k_gather_probe<KIND_CSF><<<grid, FAST_BLOCK, 0, st>>>(p->work_heavy, fx, sink);
-    if (p->work.n1 > p->work.n0) k_gather_probe<KIND_CSL><<<grid, FAST_BLOCK, 0, st>>>(p->work, fx, sink);
-    if (p->work.n2 > p->work.n1) k_gather_probe<KIND_COO><<<grid, FAST_BLOCK, 0, st>>>(p->work, fx, sink);
+    if (p->work.n0) k_gather_probe<KIND_CSF><<<grid, FAST_BLOCK, 0, st>>>(p->work, f32, sink);
+    if (p->grid_heavy) k_gather_probe<KIND_CSF><<<grid, FAST_BLOCK, 0, st>>>(p->work_heavy, f32, sink);
+    if (p->work.n1 > p->work.n0) k_gather_probe<KIND_CSL><<<grid, FAST_BLOCK, 0, st>>>(p->work, f32, sink);
+    if (p->work.n2 > p->work.n1) k_gather_probe<KIND_COO><<<grid, FAST_BLOCK, 0, st>>>(p->work, f32, sink);
     check_launch("k_gather_probe");
   });
 }

@@ -89,7 +89,7 @@ def test_rows_without_nonzeros_are_zero(hb):
     assert not np.delete(y, [3, 7], axis=0).any()
 
 
-@pytest.mark.parametrize("rank", [1, 2, 7, 16, 32, 33, 64])
+@pytest.mark.parametrize("rank", [1, 2, 4, 7, 12, 16, 32, 33, 48, 64, 96])
 def test_ranks_match_loop_oracle(hb, rng, rank):
     idx, vals = _rand(rng, (9, 8, 7), 150)
     t = hb.CooTensor((9, 8, 7), idx, vals)

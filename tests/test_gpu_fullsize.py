@@ -49,3 +49,25 @@ def test_fast_fp32_matches_generic_fp64_at_scale(config, scale):
         # repeatability up to the atomic order of split slices
         y32b, _ = mttkrp_device(h, f32, mode)
         assert _rowdev(y32b, y32.double()) <= 1e-6
+
+
+@pytest.mark.parametrize("R", [8, 16, 48, 64])
+def test_other_ranks_fast_path_at_scale(R):
+    """R a multiple of 4 takes the float4 kernels in passes of 32 columns;
+    checked against the generic fp64 kernel on a nell-2-shaped tensor."""
+    import torch
+
+    import paper_1904_03329_b200 as hb
+    from paper_1904_03329_b200.generate import CONFIGS, config_tensor
+    from paper_1904_03329_b200.kernels import mttkrp_device, plan_for
+
+    dims = CONFIGS["nell-2"]["dims"]
+    t = config_tensor("nell-2", scale=0.05)
+    g = torch.Generator(device="cuda").manual_seed(R)
+    f32 = [torch.rand((d, R), device="cuda", generator=g) for d in dims]
+    for mode in range(3):
+        h = hb.build_hbcsf(t, hb.allmode_order(dims, mode))
+        assert plan_for(h, mode, R).info.fast_path == 1
+        y32, _ = mttkrp_device(h, f32, mode)
+        y64, _ = mttkrp_device(h, [f.double() for f in f32], mode)
+        assert _rowdev(y32, y64) <= 1e-4, (R, mode)
