@@ -249,6 +249,7 @@ def main():
             dist.init_process_group(backend)
 
     import paper_1904_03329_b200 as hb
+    from paper_1904_03329_b200 import kernels as K
     from paper_1904_03329_b200 import shard
     from paper_1904_03329_b200.generate import CONFIGS, config_tensor
     from paper_1904_03329_b200.kernels import _device_factors, plan_for
@@ -421,7 +422,11 @@ def main():
             e2e_s = float(tt.item())
         h2d = sum(4 * RANK * sum(d for i, d in enumerate(dims) if i != m)
                   for m in range(n_modes) if reps[m] is not None)
-        d2h = sum(4 * RANK * rows_local[m] for m in range(n_modes) if reps[m] is not None)
+        # rows come back as float64 when the output fits the pinned-return
+        # path (device widening), else as fp32 widened on the host
+        cap = K._HostStage.PINNED_OUT_BYTES
+        d2h = sum((8 if 8 * RANK * rows_local[m] <= cap else 4) * RANK * rows_local[m]
+                  for m in range(n_modes) if reps[m] is not None)
         e2e = {"value": flops_step / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
                "path": "paper_1904_03329_b200.mttkrp_hbcsf(pinned host fp32 factors) -> numpy f64 rows, "

@@ -225,6 +225,12 @@ void hbk_plan_release(hbk_plan* p);
  * output).  Its time is the row-gather ceiling of this plan on this GPU;
  * info.gather_rows / time = rows per second.  B-position plans only. */
 int hbk_plan_probe(const hbk_plan* p, const float* const* factors, void* stream);
+/* Finiteness scan for the host calling convention (replaces the per-call
+ * np.isfinite of kernels.py:82-86 on factors already uploaded): async, one
+ * launch; flags[i] (device int32) = 1 if bufs[i][0..counts[i]) holds a NaN or
+ * Inf, else 0.  n <= 8. */
+int hbk_nonfinite_f32(const float* const* bufs, const int64_t* counts, int n, int32_t* flags,
+                      void* stream);
 
 /* ------------------------------------------------------- FROSTT text --
  * parse_frostt / load_frostt / write_frostt, coo.py:117-205, on the host

@@ -2238,6 +2238,63 @@ int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out,
   });
 }
 
+namespace hbk {
+// Finiteness scan of up to 8 fp32 buffers in one launch (the host calling
+// convention's kernels.py:82-86 check, run on the uploaded copies).  float4
+// loads over the 16-byte-aligned body, scalar head/tail.
+struct FiniteArgs {
+  const float* p[8];
+  int64_t n[8];
+  int count;
+};
+__global__ void __launch_bounds__(256) k_nonfinite(const __grid_constant__ FiniteArgs a,
+                                                   int32_t* __restrict__ flags) {
+  const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t nth = int64_t(gridDim.x) * blockDim.x;
+  for (int i = 0; i < a.count; ++i) {
+    const float* p = a.p[i];
+    const int64_t n = a.n[i];
+    const int64_t head = std::min<int64_t>(n, ((16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15) / 4);
+    const int64_t n4 = (n - head) / 4;
+    const float4* q = reinterpret_cast<const float4*>(p + head);
+    bool bad = false;
+    for (int64_t k = tid; k < n4; k += nth) {
+      const float4 v = __ldcs(q + k);
+      bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+    }
+    for (int64_t k = tid; k < head; k += nth) bad |= !isfinite(p[k]);
+    for (int64_t k = head + n4 * 4 + tid; k < n; k += nth) bad |= !isfinite(p[k]);
+    if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) flags[i] = 1;
+  }
+}
+}  // namespace hbk
+
+int hbk_nonfinite_f32(const float* const* bufs, const int64_t* counts, int n, int32_t* flags,
+                      void* stream) {
+  return guarded([&] {
+    HBK_REQUIRE(n >= 0 && n <= 8, HBK_EINVAL, "at most 8 buffers per finiteness scan");
+    HBK_REQUIRE(n == 0 || (bufs && counts && flags), HBK_EINVAL, "null pointer");
+    cudaStream_t st = to_stream(stream);
+    if (n == 0) return;
+    FiniteArgs a{};
+    a.count = n;
+    int64_t total = 0;
+    for (int i = 0; i < n; ++i) {
+      HBK_REQUIRE(counts[i] >= 0 && (counts[i] == 0 || bufs[i]), HBK_EINVAL, "bad buffer");
+      a.p[i] = bufs[i];
+      a.n[i] = counts[i];
+      total += counts[i];
+    }
+    HBK_CUDA(cudaMemsetAsync(flags, 0, size_t(n) * 4, st));
+    int dev = 0, sms = 0;
+    HBK_CUDA(cudaGetDevice(&dev));
+    HBK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(sms) * 8, (total / 4 + 255) / 256)));
+    k_nonfinite<<<grid, 256, 0, st>>>(a, flags);
+    check_launch("k_nonfinite");
+  });
+}
+
 int hbk_plan_probe(const hbk_plan* p, const float* const* factors, void* stream) {
   return guarded([&] {
     HBK_REQUIRE(p->bpos && p->r32, HBK_EINVAL,

@@ -189,23 +189,43 @@ class _HostStage:
                 raise ValueError(f"factor {bad} has non-finite entries")
         return out, checks
 
-    def download(self, torch, y):
-        out = np.empty(tuple(y.shape), dtype=np.float64)
-        if y.numel() == 0:
-            return out
-        rows = int(y.shape[0])
-        width = y.numel() // max(1, rows)
+    # outputs up to this size are widened on the device and copied straight
+    # into a page-locked float64 array (torch's caching host allocator) that
+    # is returned as the NumPy result; larger ones come back as fp32 into a
+    # reused pinned buffer and are widened on host threads
+    PINNED_OUT_BYTES = 256 << 20
+
+    def download(self, torch, y, flags=None):
+        """Device rows -> NumPy float64 rows (+ the host copy of the device
+        int32 ``flags`` vector, read back under the same synchronisation)."""
+        n = y.numel()
         with self.lock:
-            buf = self._pinned(torch, ("out",), y.numel(), y.dtype)
-            buf[: y.numel()].view(y.shape).copy_(y, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            src = buf.numpy()[: y.numel()].reshape(rows, width)
-            dst = out.reshape(rows, width)
-            step = max(1, (2 << 20) // max(1, width * 8))
-            spans = [(a, min(rows, a + step)) for a in range(0, rows, step)]
-            self._map(lambda a, b: np.copyto(dst[a:b], src[a:b]), spans)
-            self.bufs[("out",)] = (buf, None)
-        return out
+            fbuf = None
+            if flags is not None and flags.numel():
+                fbuf = self._pinned(torch, ("flags",), flags.numel(), flags.dtype)
+                fbuf[: flags.numel()].copy_(flags, non_blocking=True)
+            if n * 8 <= self.PINNED_OUT_BYTES:
+                host = torch.empty(tuple(y.shape), dtype=torch.float64, pin_memory=n > 0)
+                if n:
+                    host.copy_(y if y.dtype == torch.float64 else y.to(torch.float64),
+                               non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                out = host.numpy()
+            else:
+                out = np.empty(tuple(y.shape), dtype=np.float64)
+                rows = int(y.shape[0])
+                width = n // max(1, rows)
+                buf = self._pinned(torch, ("out",), n, y.dtype)
+                buf[:n].view(y.shape).copy_(y, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                src = buf.numpy()[:n].reshape(rows, width)
+                dst = out.reshape(rows, width)
+                step = max(1, (2 << 20) // max(1, width * 8))
+                spans = [(a, min(rows, a + step)) for a in range(0, rows, step)]
+                self._map(lambda a, b: np.copyto(dst[a:b], src[a:b]), spans)
+                self.bufs[("out",)] = (buf, None)
+            fl = fbuf[: flags.numel()].tolist() if fbuf is not None else []
+        return out, fl
 
 
 _stage = None
@@ -296,20 +316,35 @@ def _check_precision(precision: str) -> str:
     return precision
 
 
+def _nonfinite_flags(torch, tensors):
+    """Device int32 vector: 1 where the tensor holds a NaN/Inf (fp32 tensors:
+    one hbk_nonfinite_f32 launch over all of them)."""
+    flags = torch.empty(len(tensors), dtype=torch.int32, device="cuda")
+    if all(t.dtype == torch.float32 for t in tensors) and len(tensors) <= 8:
+        ptrs = (C.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
+        counts = (C.c_int64 * len(tensors))(*[t.numel() for t in tensors])
+        N.call("hbk_nonfinite_f32", ptrs, counts, len(tensors), C.c_void_p(flags.data_ptr()),
+               N.stream_ptr())
+    else:
+        for i, t in enumerate(tensors):
+            flags[i] = (~torch.isfinite(t)).any().to(torch.int32)
+    return flags
+
+
 def _finish(plan: _Plan, factors, mode: int, out=None, precision: str = "fp32"):
     ptrs, keep, on_device, checks = _device_factors(factors, mode, _check_precision(precision))
     y = plan.execute(ptrs, out, precision)
     if on_device:
         return y, plan.opcount
     torch = N.require_device()
-    # pinned host tensors are checked on the device, after the launch so the
-    # MTTKRP does not wait for the check kernels; one flag vector comes back
-    flags = torch.stack([torch.isfinite(dev).all() for _, dev in checks]) if checks else None
-    rows = _host_stage().download(torch, y)
-    if flags is not None:
-        for (d, _), ok in zip(checks, flags.cpu().tolist()):
-            if not ok:
-                raise ValueError(f"factor {d} has non-finite entries")
+    # pinned host tensors are checked on the device (one hbk_nonfinite_f32
+    # launch), after the MTTKRP launch so it does not wait for the scan; the
+    # flags come back with the rows
+    flags = _nonfinite_flags(torch, [dev for _, dev in checks]) if checks else None
+    rows, bad = _host_stage().download(torch, y, flags)
+    for (d, _), b in zip(checks, bad):
+        if b:
+            raise ValueError(f"factor {d} has non-finite entries")
     return rows, plan.opcount
 
 

@@ -1,5 +1,5 @@
-"""Per-call timeline of the host-array MTTKRP (pinned fp32 factors in,
-float64 rows out) on nell-2: host time per phase, averaged over calls."""
+"""Host-array MTTKRP call time (pinned fp32 factors in, float64 rows out) on
+nell-2, against the device time of the same call's kernel."""
 import statistics
 import sys
 import time
@@ -21,31 +21,17 @@ fp = [torch.from_numpy(rng.random((d, 32))).float().pin_memory() for d in dims]
 for m in range(3):
     hb.mttkrp_hbcsf(reps[m], fp, m)
 torch.cuda.synchronize()
-ph = {k: [] for k in ("check", "plan", "upload", "launch", "d2h+sync", "widen", "flags", "total")}
-for it in range(20):
+t0 = time.perf_counter()
+for it in range(10):
     for m in range(3):
-        t0 = time.perf_counter()
-        r = K._check_factors(reps[m].dims, fp, m, check_finite="staged")
-        t1 = time.perf_counter()
-        plan = K.plan_for(reps[m], m, r)
-        t2 = time.perf_counter()
-        ptrs, keep, on_dev, checks = K._device_factors(fp, m)
-        t3 = time.perf_counter()
-        y = plan.execute(ptrs)
-        t4 = time.perf_counter()
-        st = K._host_stage()
-        buf = st._pinned(torch, ("out",), y.numel(), y.dtype)
-        buf[: y.numel()].view(y.shape).copy_(y, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        t5 = time.perf_counter()
-        out = np.empty(tuple(y.shape))
-        np.copyto(out, buf.numpy()[: y.numel()].reshape(y.shape))
-        t6 = time.perf_counter()
-        for d, ok in checks:
-            bool(ok)
-        t7 = time.perf_counter()
-        for k, a, b in (("check", t0, t1), ("plan", t1, t2), ("upload", t2, t3), ("launch", t3, t4),
-                        ("d2h+sync", t4, t5), ("widen", t5, t6), ("flags", t6, t7), ("total", t0, t7)):
-            ph[k].append((b - a) * 1e3)
-for k, v in ph.items():
-    print(f"{k:10s} {statistics.median(v):7.3f} ms")
+        hb.mttkrp_hbcsf(reps[m], fp, m)
+print(f"api call  {(time.perf_counter() - t0) / 30 * 1e3:7.3f} ms")
+dev = [torch.from_numpy(np.asarray(f)).cuda() for f in fp]
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+ev[0].record()
+for it in range(10):
+    for m in range(3):
+        hb.mttkrp_device(reps[m], dev, m)
+ev[1].record()
+torch.cuda.synchronize()
+print(f"device    {ev[0].elapsed_time(ev[1]) / 30:7.3f} ms")

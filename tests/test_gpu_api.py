@@ -306,6 +306,41 @@ def test_pinned_host_factors_match_numpy(hb, rng):
     h = hb.build_hbcsf(t, hb.allmode_order(t.dims, 0))
     with pytest.raises(ValueError):
         hb.mttkrp_hbcsf(h, bad, 0)
+    # returned rows own their memory: a later call does not overwrite them
+    y_a, _ = hb.mttkrp_hbcsf(h, pinned, 0)
+    keep = y_a.copy()
+    hb.mttkrp_hbcsf(h, [2 * p for p in pinned], 0)
+    assert np.array_equal(y_a, keep)
+
+
+@pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 37, 4096 + 3, 1 << 20])
+@pytest.mark.parametrize("offset", [0, 1, 2, 3])
+def test_nonfinite_scan(n, offset):
+    """hbk_nonfinite_f32 over unaligned heads, float4 bodies and tails: a NaN
+    or Inf at the first, a middle and the last position is found, clean
+    buffers are not flagged; several buffers in one launch."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1904_03329_b200 import _native as N
+    from paper_1904_03329_b200.kernels import _nonfinite_flags
+
+    base = torch.rand(n + offset + 8, device="cuda")
+    view = base[offset: offset + n]
+    clean = torch.rand(777, device="cuda")
+    assert _nonfinite_flags(torch, [view, clean]).tolist() == [0, 0]
+    for pos in sorted({0, n // 2, n - 1}) if n else []:
+        for bad in (float("nan"), float("inf"), float("-inf")):
+            v = base.clone()[offset: offset + n]
+            v[pos] = bad
+            assert _nonfinite_flags(torch, [clean, v, clean]).tolist() == [0, 1, 0]
+    # neighbours outside the buffer are not read
+    base[:offset] = float("nan")
+    base[offset + n:] = float("nan")
+    assert _nonfinite_flags(torch, [view]).tolist() == [0]
+    with pytest.raises(ValueError):
+        N.call("hbk_nonfinite_f32", None, None, 9, None, N.stream_ptr())
 
 
 @pytest.mark.parametrize("block_mb", ["0.002", "0.0005"])
