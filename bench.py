@@ -472,12 +472,20 @@ def main():
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
+                # the DRAM bytes the kernels actually move (ncu, cold caches per
+                # replay) over their time: how close to the HBM peak the
+                # traffic runs, as opposed to the compulsory-bytes fraction
+                "traffic_gbs": (traffic / (statistics.mean(per_mode_ms) * 1e-3) / 1e9
+                                if traffic else None),
+                "traffic_frac": (traffic / (statistics.mean(per_mode_ms) * 1e-3) / 1e9 / hbm
+                                 if traffic else None),
                 "kernel": "k_mttkrp3_r32<kind> (one launch per non-empty bucket kind per mode)",
                 "algorithmic_bytes_per_step": sum(bytes_modes),
                 "algorithmic_bytes_per_launch": sum(bytes_modes) / n_modes,
                 "traffic_unit": "DRAM bytes per MTTKRP launch (ncu dram__bytes_read+write, profiles/)",
                 "per_mode_ms": per_mode_ms, "per_mode_bytes": bytes_modes,
                 "per_mode_frac": [b / (ms * 1e-3) / 1e9 / hbm for b, ms in zip(bytes_modes, per_mode_ms)],
+                "launches_per_mode": [int(pl.info.launches) if pl is not None else 0 for pl in plans],
                 "gather": gather,
             },
             "cpu_baseline": cpu,
