@@ -34,6 +34,7 @@ def test_large_extent(big, rank):
     import torch
 
     import paper_1904_03329_b200 as hb
+    from paper_1904_03329_b200.kernels import plan_for
 
     free, _ = torch.cuda.mem_get_info()
     need = 2 * big * rank * 4 + (4 << 30)
@@ -52,6 +53,9 @@ def test_large_extent(big, rank):
     for mode in range(3):
         h = hb.build_hbcsf(t, hb.allmode_order(dims, mode))
         y, _ = hb.mttkrp_device(h, f, mode)
+        # leaf / fiber extents >= 2^29 leave the float4 kernels for the generic one
+        wide = big >= (1 << 29) and mode != 2
+        assert plan_for(h, mode, rank).info.fast_path == (0 if wide else 1)
         rows, ref = _entries_mttkrp(torch, idx, vals, f, mode)
         sel = torch.from_numpy(rows.astype(np.int64)).cuda()
         assert row_dev(y.index_select(0, sel).double().cpu().numpy(), ref) <= 1e-4
