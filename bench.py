@@ -265,12 +265,13 @@ def main():
     # preprocessing (reported separately, like cli.py preprocessing_seconds)
     t0 = time.perf_counter()
     split_cfg = hb.SplitConfig()
-    reps, censuses, plans, ranges = [], [], [], []
+    reps, censuses, plans, ranges, all_ranges = [], [], [], [], []
     for mode in range(len(dims)):
         mo = hb.allmode_order(dims, mode)
         if world > 1:
             # this rank's output rows, rebased: its plan writes only them
             ranges_m = shard.plan_row_ranges(shard.slice_histogram(t, mode).cpu().numpy(), world)
+            all_ranges.append(ranges_m)
             rr = ranges_m[rank]
             part = shard.shard_rows(t, mode, rr[0], rr[1]) if rr[1] > rr[0] else None
         else:
@@ -336,6 +337,37 @@ def main():
     ms_per_step = elapsed_ms / args.steps
     flops_step = 3.0 * nnz_total * RANK * n_modes
     value = flops_step / (ms_per_step * 1e-3) / 1e9
+
+    # N > 1: the same steps followed by the replication of every mode's output
+    # rows on all ranks (all-gather over NCCL) — the standalone MTTKRP with
+    # and without the output exchange
+    with_ag = None
+    if world > 1:
+        from paper_1904_03329_b200.distributed import allgather_padded
+
+        def step_ag():
+            for m in range(n_modes):
+                run_mode(m)
+                rows_m = outs[m][: rows_local[m]]
+                allgather_padded(torch, dist, rows_m, all_ranges[m])
+
+        for _ in range(max(1, args.warmup)):
+            step_ag()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_ev.record(stream)
+        for _ in range(args.steps):
+            step_ag()
+        b_ev.record(stream)
+        torch.cuda.synchronize()
+        tt = torch.tensor([a_ev.elapsed_time(b_ev) / args.steps], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ag_ms = float(tt.item())
+        with_ag = {"ms_per_step": ag_ms, "value": flops_step / (ag_ms * 1e-3) / 1e9,
+                   "unit": "GFLOP/s",
+                   "gathered_bytes_per_step": sum(4 * RANK * d for d in dims),
+                   "note": "each step + all_gather of every mode's output rows to every rank"}
 
     # gather ceiling: the plans' gather-only calibration kernels over the same
     # task lists and streams (hbk_plan_probe), timed the same way
@@ -490,6 +522,7 @@ def main():
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "with_output_allgather": with_ag,
             "gpu_launches": args.steps * sum(int(pl.info.launches) for pl in plans if pl is not None),
             "clocks": clk.summary(),
         }

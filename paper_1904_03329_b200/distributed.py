@@ -52,7 +52,7 @@ def allgather_padded(torch, dist, local, ranges, group=None):
     buf = torch.zeros((cap, width), dtype=local.dtype, device=local.device)
     buf[: local.shape[0]] = local
     out = torch.empty((world * cap, width), dtype=local.dtype, device=local.device)
-    if hasattr(dist, "all_gather_into_tensor") and local.device.type == "cuda":
+    if local.device.type == "cuda" and dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, buf, group=group)
     else:
         dist.all_gather(list(out.chunk(world)), buf, group=group)
