@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <string>
 
@@ -429,18 +430,22 @@ extern "C" int hbk_als_update(const float* Y, int64_t rows, int rank, const floa
       // G_Y accumulates in `gram`; the one-CTA epilogue reads it whole, then
       // overwrites it with M^T G_Y M
       HBK_CUDA(cudaMemsetAsync(gram, 0, sizeof(double) * ALS_R * ALS_R, st));
-      static int attr_dev = -1, per_sm_mma = 0;
-      if (attr_dev != dev) {
+      // per-device launch setup, done once (concurrent first calls just
+      // repeat the idempotent attribute call)
+      static std::atomic<int> occ[64];
+      int per_sm_mma = dev < 64 ? occ[dev].load(std::memory_order_relaxed) : 0;
+      if (per_sm_mma == 0) {
         HBK_CUDA(cudaFuncSetAttribute(k_als_update32_mma,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(sizeof(AlsMmaSmem))));
         HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &per_sm_mma, k_als_update32_mma, MMA_WARPS * 32, sizeof(AlsMmaSmem)));
-        attr_dev = dev;
+        per_sm_mma = std::max(per_sm_mma, 1);
+        if (dev < 64) occ[dev].store(per_sm_mma, std::memory_order_relaxed);
       }
       const int64_t nsub = (rows + MMA_ROWS - 1) / MMA_ROWS;
       const int grid = int(std::min<int64_t>((nsub + MMA_WARPS - 1) / MMA_WARPS,
-                                             int64_t(sms) * std::max(per_sm_mma, 1)));
+                                             int64_t(sms) * per_sm_mma));
       k_als_update32_mma<<<grid, MMA_WARPS * 32, sizeof(AlsMmaSmem), st>>>(Y, rows, M, F, gram);
       check_launch("k_als_update32_mma");
       k_als_finish<<<1, 1024, 0, st>>>(M, colw, gram, inner);

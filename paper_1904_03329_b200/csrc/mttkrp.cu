@@ -1652,8 +1652,6 @@ static int fast_occupancy_any(const hbk_plan* p, int k) {
 static void build_plan(hbk_plan* p, cudaStream_t st) {
   const int N = p->order;
   const int R = p->rank;
-  // fast path: order 3, R = 32 (8 lanes x float4 per row); the streams keep
-  // two flag bits in the leaf coordinate, so leaf extents must stay < 2^30
   // fast path: order 3, R a multiple of 4 (float4 rows; R > 32 runs in
   // passes of 32 columns); the old-variant streams keep two flag bits in the
   // leaf coordinate, so leaf extents must stay < 2^29
