@@ -218,8 +218,10 @@ def run_reference(args, world, rank):
         "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (SURVEY Appendix A power-law generator)",
-        "config": {"workload": f"{args.config} HB-CSF MTTKRP, all modes, R=32", "dims": list(dims),
-                   "nnz": t.nnz, "rank": RANK},
+        "config": {"workload": f"{args.config}-shaped HB-CSF MTTKRP, all {len(dims)} modes per step, R=32",
+                   "dims": list(dims), "nnz": t.nnz, "rank": RANK, "scale": args.scale,
+                   "split": {"fiber_threshold": 128, "block_size": 512},
+                   "parallelism": "host CPU (rank 0)"},
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "port",
                          "sample": sample_desc},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
