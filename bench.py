@@ -47,6 +47,10 @@ def parse_args():
     ap.add_argument("--config", default="nell-2")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # the format comparison of the paper (cpd.py:141-149
+    # TENSOR_FORMATS): hbcsf (default, the headline), bcsf = split CSF, csf,
+    # coo = the whole tensor as a coordinate list
+    ap.add_argument("--format", default="hbcsf", choices=["hbcsf", "bcsf", "csf", "coo"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-nnz", type=int, default=300_000)
     return ap.parse_args()
@@ -116,7 +120,16 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+FORMAT_NAME = {"hbcsf": "HB-CSF", "bcsf": "B-CSF", "csf": "CSF", "coo": "COO"}
+
+
 def census_of(h):
+    if not hasattr(h, "coo_part"):  # standalone formats
+        if hasattr(h, "num_fibers"):  # CsfTensor (csf / bcsf)
+            return {"coo_nnz": 0, "csl_slices": 0, "csl_nnz": 0, "csf_slices": h.num_slices,
+                    "csf_fibers": h.num_fibers, "csf_nnz": h.nnz}
+        return {"coo_nnz": h.nnz, "csl_slices": 0, "csl_nnz": 0, "csf_slices": 0,
+                "csf_fibers": 0, "csf_nnz": 0}
     return {
         "coo_nnz": h.coo_part.nnz,
         "csl_slices": h.csl_part.num_slices,
@@ -284,7 +297,14 @@ def main():
             censuses.append(None)
             plans.append(None)
             continue
-        h = hb.split_fibers(hb.build_hbcsf(part, mo), split_cfg)
+        if args.format == "hbcsf":
+            h = hb.split_fibers(hb.build_hbcsf(part, mo), split_cfg)
+        elif args.format == "bcsf":
+            h = hb.split_fibers(hb.build_csf(part, mo), split_cfg)
+        elif args.format == "csf":
+            h = hb.build_csf(part, mo)
+        else:
+            h = part
         reps.append(h)
         ranges.append(rr)
         censuses.append(census_of(h))
@@ -439,7 +459,7 @@ def main():
         def e2e_step():
             for m in range(n_modes):
                 if reps[m] is not None:
-                    hb.mttkrp_hbcsf(reps[m], f_pin, m)
+                    hb.mttkrp(reps[m], f_pin, m)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -463,7 +483,7 @@ def main():
                   for m in range(n_modes) if reps[m] is not None)
         e2e = {"value": flops_step / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
-               "path": "paper_1904_03329_b200.mttkrp_hbcsf(pinned host fp32 factors) -> numpy f64 rows, "
+               "path": f"paper_1904_03329_b200.mttkrp({args.format} rep, pinned host fp32 factors) -> numpy f64 rows, "
                        "one call per mode, H2D + kernel + D2H inside the timed region"
                        + ("; bytes per rank, rank 0" if world > 1 else "")}
 
@@ -495,7 +515,8 @@ def main():
             "dtype": "f32",
             "data": "synthetic (SURVEY Appendix A power-law generator, seeded, on device)",
             "config": {
-                "workload": f"{args.config}-shaped HB-CSF MTTKRP, all {n_modes} modes per step, R=32",
+                "workload": (f"{args.config}-shaped {FORMAT_NAME[args.format]} MTTKRP, all {n_modes} "
+                             "modes per step, R=32"),
                 "dims": list(dims), "nnz": nnz_total, "rank": RANK, "scale": args.scale,
                 "split": {"fiber_threshold": 128, "block_size": 512},
                 "l2": "inputs larger than L2 (index/value streams 0.75+ GB per mode); factors L2-resident by design",
