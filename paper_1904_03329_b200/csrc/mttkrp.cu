@@ -573,7 +573,7 @@ static constexpr int FAST_BLOCK = 256;
 enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2, KIND_CSF_BPOS = 3, KIND_CSF_BPOS4 = 4, KIND_CSF_UNI = 5 };
 
 template <int KIND, class FX>
-__global__ void __launch_bounds__(FAST_BLOCK, (KIND == KIND_CSF_BPOS4 || KIND == KIND_CSF_UNI) ? 4 : 3)
+__global__ void __launch_bounds__(FAST_BLOCK, KIND == KIND_CSF_UNI ? 3 : (KIND == KIND_CSF_BPOS4 ? 4 : 3))
     k_mttkrp3_r32(const __grid_constant__ Work w, const __grid_constant__ FX fx) {
   // per lane: 8 slots of 16 B (one per batch position) for staged B rows
   __shared__ float4 s_slots[FAST_BLOCK * 8];
