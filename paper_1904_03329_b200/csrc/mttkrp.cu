@@ -2011,6 +2011,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       wh.csf_fidx = p->heavy_fj.as<uint32_t>();
       wh.csf_F = uint32_t(heavy_segments);
       per_sm = fast_occupancy_any(p, 3);
+      if (const char* e = getenv("HBK_HEAVY_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
       p->grid_heavy = grid_for_tasks(heavy_ntasks, per_sm, 4);
       wh.total_warps[0] = uint32_t(p->grid_heavy) * (p->block / 32);
       launches += 1;
