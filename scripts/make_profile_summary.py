@@ -84,8 +84,12 @@ def main(tag, config, rep, launches):
     out.write_text("\n".join(lines) + "\n")
     js = ROOT / "profiles" / "ncu_summary.json"
     d = json.loads(js.read_text()) if js.exists() else {}
-    d[config] = {"tag": tag, "dram_bytes_per_launch": traffic,
-                 "note": "dram__bytes_read.sum + dram__bytes_write.sum of the captured MTTKRP launches"}
+    entry = d.setdefault(config, {})
+    entry["full_capture"] = {"tag": tag, "dram_bytes_per_launch": traffic,
+                             "note": "dram__bytes_read.sum + dram__bytes_write.sum of the launches "
+                                     "captured with --set full"}
+    if "dram_bytes_per_launch" not in entry:  # no per-mode pass (scripts/ncu_traffic.py) yet
+        entry["dram_bytes_per_launch"] = traffic
     js.write_text(json.dumps(d, indent=1) + "\n")
     print(out)
 
