@@ -196,17 +196,21 @@ __global__ void __launch_bounds__(ALS_TILE, 2)
 
 
 // ---------------------------------------------------------------------------
-// Tensor-core variant (default).  F = Y M and the Gram are 32-wide GEMMs, so
-// they run on the warp-level tensor-core path (mma.sync m16n8k8 TF32, fp32
-// accumulate; measured 273 TFLOP/s on B200 vs 72 for FFMA) in 3xTF32 form —
-// x = hi + lo with hi = tf32(x), lo = tf32(x - hi), and a·b ≈ hi·hi' +
-// hi·lo' + lo·hi' — which keeps fp32 accuracy (dropped term ~2^-22 relative).
-// Instead of F^T F the kernel accumulates G_Y = Y^T Y (upper 16x8 tiles only);
-// a one-CTA epilogue forms Gram = M^T G_Y M and the fit term
-// sum_r w_r (G_Y M)_rr = sum_r w_r <Y[:, r], F[:, r]> in fp64.  Each warp
-// streams its own 16-row subtiles through a 3-stage cp.async ring (no
-// CTA-wide barrier in the loop) and stores F straight from the MMA
-// accumulators (each 32-byte sector fully written).
+// Tensor-core variant (default).  F = Y M and the Gram F^T F are 32-wide
+// GEMMs, so they run on the warp-level tensor-core path (mma.sync m16n8k8
+// TF32, fp32 accumulate; measured 273 TFLOP/s on B200 vs 72 for FFMA) in
+// 3xTF32 form — x = hi + lo with hi = tf32(x), lo = tf32(x - hi), and
+// a·b ≈ hi·hi' + hi·lo' + lo·hi' — which keeps fp32 accuracy (dropped term
+// ~2^-22 relative).  The Gram is taken from F itself, not as M^T (Y^T Y) M:
+// early in ALS, M = pinv(V) is large and F = Y M cancels, and the
+// algebraically equal form loses the cancellation to rounding (measured: a
+// 1e-6..1e-5 fit drift on nell-2).  Each warp streams its own 16-row
+// subtiles through a 3-stage cp.async ring (no CTA-wide barrier in the loop):
+// F from the MMA accumulators goes to global memory and over the consumed Y
+// subtile in shared memory, where the Gram MMAs read it (upper 16x8 tiles,
+// fp32 in registers, flushed to per-warp fp64 every 32 subtiles); the fit
+// term sum_r w_r Y[i,r] F[i,r] is accumulated alongside.  A one-CTA epilogue
+// mirrors the upper tiles into the symmetric Gram.
 static constexpr int MMA_WARPS = 8;
 static constexpr int MMA_ROWS = 16;
 static constexpr int MMA_STAGES = 3;
@@ -218,6 +222,7 @@ struct AlsMmaSmem {
   alignas(16) float y[MMA_WARPS][MMA_STAGES][MMA_ROWS * MMA_LD];
   uint4 mfrag[16][32];  // (nt * 4 + ks, lane) -> {hi(b0), hi(b1), lo(b0), lo(b1)}
   double g[MMA_WARPS][MMA_GT][32][4];
+  double inner[MMA_WARPS];
 };
 
 __device__ __forceinline__ uint32_t to_tf32(float x) {
@@ -246,7 +251,8 @@ __device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4], con
 
 __global__ void __launch_bounds__(MMA_WARPS * 32, 2)
     k_als_update32_mma(const float* __restrict__ Y, int64_t rows, const float* __restrict__ M,
-                       float* __restrict__ F, double* __restrict__ gy) {
+                       const float* __restrict__ colw, float* __restrict__ F,
+                       double* __restrict__ gupper, double* __restrict__ inner) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   AlsMmaSmem& S = *reinterpret_cast<AlsMmaSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -258,6 +264,12 @@ __global__ void __launch_bounds__(MMA_WARPS * 32, 2)
     S.mfrag[nt * 4 + ks][ln] = make_uint4(h0, h1, l0, l1);
   }
   for (int i = lane; i < MMA_GT * 32 * 4; i += 32) (&S.g[warp][0][0][0])[i] = 0.0;
+  // fit-term column weights of this thread's accumulator columns nt*8 + 2t (+1)
+  float wc[4][2];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) wc[nt][e] = colw ? colw[nt * 8 + 2 * t + e] : 1.f;
   __syncthreads();
 
   const int64_t nsub = (rows + MMA_ROWS - 1) / MMA_ROWS;
@@ -284,6 +296,8 @@ __global__ void __launch_bounds__(MMA_WARPS * 32, 2)
   for (int i = 0; i < MMA_GT; ++i)
 #pragma unroll
     for (int q = 0; q < 4; ++q) gacc[i][q] = 0.f;
+  float in32 = 0.f;
+  double in64 = 0.0;
   auto flush = [&]() {
 #pragma unroll
     for (int i = 0; i < MMA_GT; ++i)
@@ -292,6 +306,8 @@ __global__ void __launch_bounds__(MMA_WARPS * 32, 2)
         S.g[warp][i][lane][q] += double(gacc[i][q]);
         gacc[i][q] = 0.f;
       }
+    in64 += double(in32);
+    in32 = 0.f;
   };
   int stage = 0, since = 0;
   for (; sub < nsub; sub += wstride) {
@@ -300,7 +316,7 @@ __global__ void __launch_bounds__(MMA_WARPS * 32, 2)
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group %0;" ::"n"(MMA_STAGES - 1) : "memory");
     __syncwarp();
-    const float* T = ring + stage * (MMA_ROWS * MMA_LD);
+    float* T = ring + stage * (MMA_ROWS * MMA_LD);
     const int64_t r0 = sub * MMA_ROWS;
 
     // ---- F = Y M: 16 rows x 32 columns, K = 32
@@ -322,18 +338,33 @@ __global__ void __launch_bounds__(MMA_WARPS * 32, 2)
         mma3(d[nt], ah, al, b.x, b.y, b.z, b.w);
       }
     }
-    // ---- store F straight from the accumulators
+    // ---- fit term: w_c * Y[i, c] * F[i, c] at this thread's accumulator slots
+    if (inner) {
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const float2 ya = *reinterpret_cast<const float2*>(T + g * MMA_LD + nt * 8 + 2 * t);
+        const float2 yb = *reinterpret_cast<const float2*>(T + (g + 8) * MMA_LD + nt * 8 + 2 * t);
+        in32 = fmaf(wc[nt][0] * ya.x, d[nt][0], in32);
+        in32 = fmaf(wc[nt][1] * ya.y, d[nt][1], in32);
+        in32 = fmaf(wc[nt][0] * yb.x, d[nt][2], in32);
+        in32 = fmaf(wc[nt][1] * yb.y, d[nt][3], in32);
+      }
+    }
+    __syncwarp();  // every lane has read its Y values
+    // ---- F to global memory and over the Y subtile
     {
       const int64_t ra = r0 + g, rb = r0 + g + 8;
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
-        if (ra < rows) __stcs(reinterpret_cast<float2*>(F + ra * ALS_R + nt * 8 + 2 * t),
-                              make_float2(d[nt][0], d[nt][1]));
-        if (rb < rows) __stcs(reinterpret_cast<float2*>(F + rb * ALS_R + nt * 8 + 2 * t),
-                              make_float2(d[nt][2], d[nt][3]));
+        const float2 fa = make_float2(d[nt][0], d[nt][1]), fb = make_float2(d[nt][2], d[nt][3]);
+        *reinterpret_cast<float2*>(T + g * MMA_LD + nt * 8 + 2 * t) = fa;
+        *reinterpret_cast<float2*>(T + (g + 8) * MMA_LD + nt * 8 + 2 * t) = fb;
+        if (ra < rows) __stcs(reinterpret_cast<float2*>(F + ra * ALS_R + nt * 8 + 2 * t), fa);
+        if (rb < rows) __stcs(reinterpret_cast<float2*>(F + rb * ALS_R + nt * 8 + 2 * t), fb);
       }
     }
-    // ---- G_Y += Y^T Y over the 16 rows (upper tiles)
+    __syncwarp();
+    // ---- Gram += F^T F over the 16 rows (upper tiles; rows past the end are 0)
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
       uint32_t vh[4][2], vl[4][2];
@@ -362,8 +393,13 @@ __global__ void __launch_bounds__(MMA_WARPS * 32, 2)
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   flush();
+  if (inner) {
+    double v = in64;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if (lane == 0) S.inner[warp] = v;
+  }
   __syncthreads();
-  // CTA reduction of the warps' fp64 tiles -> global G_Y (upper tiles)
+  // CTA reduction of the warps' fp64 tiles -> global upper tiles
   for (int i = threadIdx.x; i < MMA_GT * 32 * 4; i += blockDim.x) {
     const int ti = i >> 7, ln = (i >> 2) & 31, q = i & 3;
     double v = 0.0;
@@ -371,35 +407,22 @@ __global__ void __launch_bounds__(MMA_WARPS * 32, 2)
     for (int w = 0; w < MMA_WARPS; ++w) v += S.g[w][ti][ln][q];
     const int mt = ti < 4 ? 0 : 1, nt = ti < 4 ? ti : ti - 2;
     const int row = 16 * mt + (ln >> 2) + (q >= 2 ? 8 : 0), col = 8 * nt + 2 * (ln & 3) + (q & 1);
-    atomicAdd(gy + row * ALS_R + col, v);
+    atomicAdd(gupper + row * ALS_R + col, v);
+  }
+  if (inner && threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < MMA_WARPS; ++w) v += S.inner[w];
+    atomicAdd(inner, v);
   }
 }
 
-// Gram = M^T G_Y M (exactly symmetric), inner = sum_r w_r (G_Y M)_rr, fp64.
-__global__ void __launch_bounds__(1024) k_als_finish(const float* __restrict__ M,
-                                                     const float* __restrict__ colw,
-                                                     double* __restrict__ gram,
-                                                     double* __restrict__ inner) {
-  const double* gy = gram;  // read whole before it is overwritten
-  __shared__ double G[ALS_R][ALS_R + 1], Md[ALS_R][ALS_R + 1], T[ALS_R][ALS_R + 1];
+// The Gram holds the upper 16x8 tiles ((c / 8) >= 2 (r / 16)); mirror the rest.
+__global__ void __launch_bounds__(1024) k_als_mirror(double* __restrict__ gram) {
+  __shared__ double G[ALS_R][ALS_R + 1];
   const int r = threadIdx.x >> 5, c = threadIdx.x & 31;
-  // G_Y holds tiles with (c / 8) >= 2 (r / 16); the rest mirrors
-  G[r][c] = (c / 8 >= 2 * (r / 16)) ? gy[r * ALS_R + c] : gy[c * ALS_R + r];
-  Md[r][c] = double(M[r * ALS_R + c]);
+  G[r][c] = gram[r * ALS_R + c];
   __syncthreads();
-  double v = 0.0;
-  for (int k = 0; k < ALS_R; ++k) v += G[r][k] * Md[k][c];
-  T[r][c] = v;
-  __syncthreads();
-  const int a = r <= c ? r : c, b = r <= c ? c : r;
-  double s2 = 0.0;
-  for (int k = 0; k < ALS_R; ++k) s2 += Md[k][a] * T[k][b];
-  gram[r * ALS_R + c] = s2;
-  if (inner && threadIdx.x < 32) {
-    double d = (colw ? double(colw[c]) : 1.0) * T[c][c];
-    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xFFFFFFFFu, d, o);
-    if (c == 0) *inner = d;
-  }
+  gram[r * ALS_R + c] = (c / 8 >= 2 * (r / 16)) ? G[r][c] : G[c][r];
 }
 }  // namespace hbk
 
@@ -427,9 +450,9 @@ extern "C" int hbk_als_update(const float* Y, int64_t rows, int rank, const floa
         if (inner) HBK_CUDA(cudaMemsetAsync(inner, 0, sizeof(double), st));
         return;
       }
-      // G_Y accumulates in `gram`; the one-CTA epilogue reads it whole, then
-      // overwrites it with M^T G_Y M
+      // the upper Gram tiles accumulate in `gram`, then are mirrored
       HBK_CUDA(cudaMemsetAsync(gram, 0, sizeof(double) * ALS_R * ALS_R, st));
+      if (inner) HBK_CUDA(cudaMemsetAsync(inner, 0, sizeof(double), st));
       // per-device launch setup, done once (concurrent first calls just
       // repeat the idempotent attribute call)
       static std::atomic<int> occ[64];
@@ -446,10 +469,11 @@ extern "C" int hbk_als_update(const float* Y, int64_t rows, int rank, const floa
       const int64_t nsub = (rows + MMA_ROWS - 1) / MMA_ROWS;
       const int grid = int(std::min<int64_t>((nsub + MMA_WARPS - 1) / MMA_WARPS,
                                              int64_t(sms) * per_sm_mma));
-      k_als_update32_mma<<<grid, MMA_WARPS * 32, sizeof(AlsMmaSmem), st>>>(Y, rows, M, F, gram);
+      k_als_update32_mma<<<grid, MMA_WARPS * 32, sizeof(AlsMmaSmem), st>>>(Y, rows, M, colw, F,
+                                                                           gram, inner);
       check_launch("k_als_update32_mma");
-      k_als_finish<<<1, 1024, 0, st>>>(M, colw, gram, inner);
-      check_launch("k_als_finish");
+      k_als_mirror<<<1, 1024, 0, st>>>(gram);
+      check_launch("k_als_mirror");
       return;
     }
     HBK_CUDA(cudaMemsetAsync(gram, 0, sizeof(double) * ALS_R * ALS_R, st));
