@@ -586,7 +586,9 @@ __global__ void __launch_bounds__(FAST_BLOCK, KIND == KIND_CSF_UNI ? 3 : (KIND =
   constexpr int K = (KIND == KIND_CSF_BPOS || KIND == KIND_CSF_BPOS4 || KIND == KIND_CSF_UNI) ? KIND_CSF : KIND;
   const uint32_t first = K == KIND_CSF ? 0u : (K == KIND_CSL ? w.n0 : w.n1);
   const uint32_t last = K == KIND_CSF ? w.n0 : (K == KIND_CSL ? w.n1 : w.n3);
-  uint32_t* ctr = w.ws_ctr + 2 * K;
+  // the heavy-slice launch has its own counter pair (words 6, 7) so it can
+  // run concurrently with the light-slice launch
+  uint32_t* ctr = w.ws_ctr + 2 * (KIND == KIND_CSF_UNI ? 3 : K);
   for (;;) {
     uint32_t base = 0;
     if (lane == 0) base = atomicAdd(ctr, 4u);
@@ -1101,6 +1103,11 @@ struct hbk_plan {
   hbk::Work work_gen{};  // generic kernel (every CSF slice in tree order)
   hbk::Work work_heavy{};
   hbk::Buf heavy_pairs, heavy_fj, heavy_tasks, gen_tasks, probe_sink;
+  // B-position plans launch their bucket kernels on forked streams so each
+  // kernel's CTAs fill the tail of the one before (HBK_CONCURRENT=0: serial)
+  bool concurrent = false;
+  cudaStream_t side[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
   int grid_heavy = 0;
   bool fast = false;
   int csf_variant = 2;  // 0: smem-slot kernel, 1|2: B-position streams at 3|4 CTAs per SM (HBK_CSF_VARIANT)
@@ -1114,6 +1121,11 @@ struct hbk_plan {
   int grids[3] = {0, 0, 0};
   hbk_plan_info info{};
   ~hbk_plan() {
+    for (int i = 0; i < 3; ++i) {
+      if (side[i]) cudaStreamDestroy(side[i]);
+      if (ev_join[i]) cudaEventDestroy(ev_join[i]);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
     hbk_coo_release(coo);
     hbk_csl_release(csl);
     hbk_csf_release(csf);
@@ -2039,6 +2051,17 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   p->info.out_rows = rows;
   p->info.split_rows = slots;
   p->info.launches = p->fast ? int64_t(launches) * ((R + 31) / 32) : launches;
+  {
+    const char* e = getenv("HBK_CONCURRENT");
+    p->concurrent = p->fast && p->bpos && launches > 1 && !(e && atoi(e) == 0);
+    if (p->concurrent) {
+      HBK_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+      for (int i = 0; i < 3; ++i) {
+        HBK_CUDA(cudaStreamCreateWithFlags(&p->side[i], cudaStreamNonBlocking));
+        HBK_CUDA(cudaEventCreateWithFlags(&p->ev_join[i], cudaEventDisableTiming));
+      }
+    }
+  }
   p->info.fast_path = p->fast;
   int64_t nnz = 0;
   if (p->csf) nnz += p->csf->M;
@@ -2122,23 +2145,51 @@ using namespace hbk;
 namespace hbk {
 template <class FX>
 static void launch_fast(const hbk_plan* p, const FX& fx, cudaStream_t st) {
-  if (p->grids[0]) {
-    if (p->bpos && p->csf_variant == 2)
-      k_mttkrp3_r32<KIND_CSF_BPOS4, FX><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
-    else if (p->bpos)
-      k_mttkrp3_r32<KIND_CSF_BPOS, FX><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
-    else
-      k_mttkrp3_r32<KIND_CSF, FX><<<p->grids[0], p->block, 0, st>>>(p->work, fx);
-  }
+  // kernels in launch order: heavy slices first (the longest), then light
+  // CSF, CSL, COO/zero; with p->concurrent each after the first goes to its
+  // own forked stream
+  int n = 0;
+  auto next_stream = [&]() -> cudaStream_t {
+    if (!p->concurrent || n == 0) {
+      ++n;
+      return st;
+    }
+    cudaStream_t s2 = p->side[n - 1];
+    HBK_CUDA(cudaStreamWaitEvent(s2, p->ev_fork, 0));
+    ++n;
+    return s2;
+  };
+  if (p->concurrent) HBK_CUDA(cudaEventRecord(p->ev_fork, st));
   if (p->grid_heavy) {
+    cudaStream_t s2 = next_stream();
     if (p->bpos)
-      k_mttkrp3_r32<KIND_CSF_UNI, FX><<<p->grid_heavy, p->block, 0, st>>>(p->work_heavy, fx);
+      k_mttkrp3_r32<KIND_CSF_UNI, FX><<<p->grid_heavy, p->block, 0, s2>>>(p->work_heavy, fx);
     else
-      k_mttkrp3_r32<KIND_CSF, FX><<<p->grid_heavy, p->block, 0, st>>>(p->work_heavy, fx);
+      k_mttkrp3_r32<KIND_CSF, FX><<<p->grid_heavy, p->block, 0, s2>>>(p->work_heavy, fx);
   }
-  if (p->grids[1]) k_mttkrp3_r32<KIND_CSL, FX><<<p->grids[1], p->block, 0, st>>>(p->work, fx);
-  if (p->grids[2]) k_mttkrp3_r32<KIND_COO, FX><<<p->grids[2], p->block, 0, st>>>(p->work, fx);
+  if (p->grids[0]) {
+    cudaStream_t s2 = next_stream();
+    if (p->bpos && p->csf_variant == 2)
+      k_mttkrp3_r32<KIND_CSF_BPOS4, FX><<<p->grids[0], p->block, 0, s2>>>(p->work, fx);
+    else if (p->bpos)
+      k_mttkrp3_r32<KIND_CSF_BPOS, FX><<<p->grids[0], p->block, 0, s2>>>(p->work, fx);
+    else
+      k_mttkrp3_r32<KIND_CSF, FX><<<p->grids[0], p->block, 0, s2>>>(p->work, fx);
+  }
+  if (p->grids[1]) {
+    cudaStream_t s2 = next_stream();
+    k_mttkrp3_r32<KIND_CSL, FX><<<p->grids[1], p->block, 0, s2>>>(p->work, fx);
+  }
+  if (p->grids[2]) {
+    cudaStream_t s2 = next_stream();
+    k_mttkrp3_r32<KIND_COO, FX><<<p->grids[2], p->block, 0, s2>>>(p->work, fx);
+  }
   check_launch("k_mttkrp3_r32");
+  if (p->concurrent)
+    for (int i = 0; i + 1 < n; ++i) {
+      HBK_CUDA(cudaEventRecord(p->ev_join[i], p->side[i]));
+      HBK_CUDA(cudaStreamWaitEvent(st, p->ev_join[i], 0));
+    }
 }
 }  // namespace hbk
 
