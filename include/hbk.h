@@ -189,7 +189,11 @@ void hbk_sched_release(hbk_sched* s);
  *   sched: optional BlockSchedule of csf; its units become the CSF work
  *          units (one 8-lane group per unit) exactly as mttkrp_scheduled.
  * The output (dims[mode] x rank fp32, row-major, caller-owned) is fully
- * written: rows owned by no part are zero-filled inside the same launch.  */
+ * written: rows owned by no part are zero-filled inside the same launch.
+ * A plan owns its split-slice workspace, task counters and fork/join
+ * streams, so executions of ONE plan must be ordered (same stream, or
+ * externally synchronised); distinct plans may run concurrently.  An
+ * execute is capturable into a CUDA graph.                                 */
 typedef struct {
   int mode;
   int rank;
