@@ -921,37 +921,41 @@ __device__ __forceinline__ uint32_t fiber_of(const uint32_t* __restrict__ lptr, 
   return lo;
 }
 
+// One thread per task: its slice is the last s with toff[s] <= i (slices
+// without tasks have empty ranges), so a heavy slice's thousands of chunks
+// are filled in parallel rather than by one thread.
 __global__ void k_task_fill(const uint32_t* __restrict__ loff, const uint32_t* __restrict__ fpos,
-                            const uint32_t* __restrict__ lptr, int64_t S, uint32_t T, uint32_t H,
+                            const uint32_t* __restrict__ lptr, int64_t S, uint32_t T,
                             const uint32_t* __restrict__ toff, const uint32_t* __restrict__ slot,
-                            const uint32_t* __restrict__ posoff, Task* __restrict__ tasks) {
-  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < S;
-       s += int64_t(gridDim.x) * blockDim.x) {
-    uint32_t a = loff[s], m = loff[s + 1] - a;
-    if (m > H) continue;
-    uint32_t nt = toff[s + 1] - toff[s];
-    if (m > T) {
-      for (uint32_t c = 0; c < nt; ++c) {
-        Task t{};
-        t.lo = a + uint32_t((uint64_t(m) * c) / nt);
-        t.hi = a + uint32_t((uint64_t(m) * (c + 1)) / nt);
-        t.s = uint32_t(s);
-        t.f = fpos ? fiber_of(lptr, fpos[s], fpos[s + 1], t.lo) : 0;
-        t.slot = slot[s];
-        t.nchunk = nt;
-        tasks[toff[s] + c] = t;
-      }
-      continue;
+                            const uint32_t* __restrict__ posoff, uint32_t ntask,
+                            Task* __restrict__ tasks) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < ntask;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int64_t lo = 0, hi = S;  // largest s in [0, S) with toff[s] <= i
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (toff[mid] <= uint32_t(i)) lo = mid;
+      else hi = mid;
     }
-    if (nt) {
-      Task t{};
+    const int64_t s = lo;
+    const uint32_t a = loff[s], m = loff[s + 1] - a;
+    const uint32_t nt = toff[s + 1] - toff[s];
+    Task t{};
+    t.s = uint32_t(s);
+    if (m > T) {
+      const uint32_t c = uint32_t(i) - toff[s];
+      t.lo = a + uint32_t((uint64_t(m) * c) / nt);
+      t.hi = a + uint32_t((uint64_t(m) * (c + 1)) / nt);
+      t.f = fpos ? fiber_of(lptr, fpos[s], fpos[s + 1], t.lo) : 0;
+      t.slot = slot[s];
+      t.nchunk = nt;
+    } else {
       t.lo = a + (posoff ? posoff[s] : 0u);
-      t.s = uint32_t(s);
       t.f = fpos ? fpos[s] : 0;
       t.slot = NOSLOT;
       t.nchunk = 1;
-      tasks[toff[s]] = t;
     }
+    tasks[i] = t;
   }
 }
 
@@ -1160,8 +1164,9 @@ static BucketTasks bucket_tasks(const uint32_t* loff, const uint32_t* fpos, cons
   uint32_t nslot = exclusive_scan_total(slot.as<uint32_t>(), S, st);
   bt.tasks = Scratch(size_t(std::max<uint32_t>(n, 1)) * sizeof(Task), st);
   if (n) {
-    k_task_fill<<<grid_for(S, 128), 128, 0, st>>>(loff, fpos, lptr, S, T, H, cnt.as<uint32_t>(),
-                                                  slot.as<uint32_t>(), posoff, bt.tasks.as<Task>());
+    k_task_fill<<<grid_for(n, 256), 256, 0, st>>>(loff, fpos, lptr, S, T, cnt.as<uint32_t>(),
+                                                  slot.as<uint32_t>(), posoff, n,
+                                                  bt.tasks.as<Task>());
     check_launch("k_task_fill");
     k_run_hi<<<grid_for(S, 256), 256, 0, st>>>(loff, S, T, H, cnt.as<uint32_t>(), posoff,
                                                bt.tasks.as<Task>());
