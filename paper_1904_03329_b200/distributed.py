@@ -151,7 +151,7 @@ class RowExchange:
 
 def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_tol: float = 1e-8,
                        seed: int = 0, *, group=None, local_mttkrp=None, ranges=None,
-                       device=None, exchange: str = "touched", needed=None):
+                       device=None, exchange: str = "touched", needed=None, sweep_hook=None):
     """CP-ALS over ``world`` processes, each owning a row range of every mode.
 
     Every rank passes the same tensor ``t`` (it is canonicalised and sharded
@@ -237,11 +237,12 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
     return als_fp32(torch, dims=dims, rank=rank, max_iters=max_iters, fit_tol=fit_tol, seed=seed,
                     device=device, own=own, local_mttkrp=local_mttkrp,
                     norm_x=_value_norm(torch, t), allreduce_=allreduce_,
-                    exchange_rows=exchange_rows, finalize=finalize)
+                    exchange_rows=exchange_rows, finalize=finalize, sweep_hook=sweep_hook)
 
 
 def als_fp32(torch, *, dims, rank, max_iters, fit_tol, seed, device, own, local_mttkrp, norm_x,
-             allreduce_=lambda x: x, exchange_rows=lambda d, f32: None, finalize=lambda f32: None):
+             allreduce_=lambda x: x, exchange_rows=lambda d, f32: None, finalize=lambda f32: None,
+             sweep_hook=None):
     """The CP-ALS sweep loop (cpd.py:198-271) on fp32 factors with folded
     column scales, for a rank owning rows ``own[d]`` of every factor.
     ``local_mttkrp(mode, f32)`` returns this rank's (rows, R) MTTKRP (or a
@@ -304,58 +305,137 @@ def als_fp32(torch, *, dims, rank, max_iters, fit_tol, seed, device, own, local_
     del y0
     lam = None
     inner_t = torch.zeros(1, dtype=torch.float64, device=device)
-    for it in range(1, max_iters + 1):
-        seconds, ops = [], []
-        inner = 0.0
-        for mode in range(order):
-            sync()
-            tic = time.perf_counter()
-            y, op = mttkrp(mode)
-            y = y.float().contiguous()
-            ops.append(op)
-            c = colscale(mode)
-            # F_true = (Y_raw diag(c)) V^+  ->  M = diag(c) V^+, new scales 1
-            m64 = c[:, None] * pinv_spsd(hadamard_all_but(grams, mode))
-            lo, hi = own[mode]
-            dst = f32[mode][lo:hi]
-            if fused and hi > lo:
-                from . import _native as N
-                import ctypes as C
+    # CUDA + fused: the sweep is pipelined — mode n+1's MTTKRP (which needs
+    # only the factors) is queued right behind mode n's row update, and the
+    # host reads mode n's Gram and forms M_{n+1} = pinv(V) while that MTTKRP
+    # runs, so the GPU does not idle on host round trips.  mode_seconds are
+    # then device times (CUDA events, MTTKRP start -> update end).
+    pipelined = fused
+    if pipelined:
+        m_pin = torch.empty((rank, rank), dtype=torch.float32, pin_memory=True)
+        w_pin = torch.empty(rank, dtype=torch.float32, pin_memory=True)
+        g_pin = torch.empty((rank, rank), dtype=torch.float64, pin_memory=True)
+        m_dev = torch.empty((rank, rank), dtype=torch.float32, device=device)
+        w_dev = torch.empty(rank, dtype=torch.float32, device=device)
+        ev_g = torch.cuda.Event()
+        in_pin = torch.empty(1, dtype=torch.float64, pin_memory=True)
+    ahead = None
 
+    def update(mode, y, with_inner):
+        """F_mode <- Y M (rows this rank owns), the raw Gram of the new rows;
+        the fit term into inner_t when with_inner."""
+        c = colscale(mode)
+        # F_true = (Y_raw diag(c)) V^+  ->  M = diag(c) V^+, new scales 1
+        m64 = c[:, None] * pinv_spsd(hadamard_all_but(grams, mode))
+        lo, hi = own[mode]
+        dst = f32[mode][lo:hi]
+        g_raw = torch.zeros((rank, rank), dtype=torch.float64, device=device)
+        if fused:
+            from . import _native as N
+            import ctypes as C
+
+            if pipelined:  # page-locked staging, no host-side wait on the stream
+                m_pin.copy_(torch.from_numpy(m64))
+                w_pin.copy_(torch.from_numpy(c))
+                m_dev.copy_(m_pin, non_blocking=True)
+                w_dev.copy_(w_pin, non_blocking=True)
+                m32, w32 = m_dev, w_dev
+            else:
                 m32 = torch.from_numpy(m64).to(device=device, dtype=torch.float32).contiguous()
                 w32 = torch.from_numpy(c).to(device=device, dtype=torch.float32)
-                g_raw = torch.empty((rank, rank), dtype=torch.float64, device=device)
+            if hi > lo:
                 N.call("hbk_als_update", C.c_void_p(y.data_ptr()), int(hi - lo), int(rank),
                        C.c_void_p(m32.data_ptr()), C.c_void_p(w32.data_ptr()),
                        C.c_void_p(dst.data_ptr()), C.c_void_p(g_raw.data_ptr()),
-                       C.c_void_p(inner_t.data_ptr()) if mode == last else None, N.stream_ptr())
-                if mode == last:
-                    inner = inner_t.clone()
+                       C.c_void_p(inner_t.data_ptr()) if with_inner else None, N.stream_ptr())
+            elif with_inner:
+                inner_t.zero_()
+            return g_raw, (inner_t.clone() if with_inner else None)
+        fm = y @ torch.from_numpy(m64).to(device=device, dtype=torch.float32)
+        dst.copy_(fm)
+        g_raw = gram_raw(dst)
+        inner_m = None
+        if with_inner:  # sum_r c_r <Y[:, r], F[:, r]>, fp32 chunks, fp64 total
+            cw = torch.from_numpy(c).to(device=device, dtype=fm.dtype)
+            inner_m = torch.zeros(1, dtype=torch.float64, device=device)
+            for a in range(0, fm.shape[0], 1 << 20):
+                inner_m += ((y[a: a + (1 << 20)] * fm[a: a + (1 << 20)]).sum(0).double()
+                            * cw.double()).sum()
+        return g_raw, inner_m
+
+    def set_gram(mode, g, it):
+        if not np.isfinite(g).all():
+            raise NumericalError(f"non-finite factor for mode {mode} in ALS sweep {it}", iteration=it)
+        scales[mode] = np.ones(rank)
+        grams[mode] = (g + g.T) * 0.5
+
+    for it in range(1, max_iters + 1):
+        seconds, ops = [], []
+        inner = 0.0
+        sweep_tic = time.perf_counter()
+        if pipelined:
+            # mode_seconds[n]: from mode n's MTTKRP launch to mode n+1's (its
+            # update, Gram read-back and row exchange included); the last mode
+            # runs to the end of the sweep's exchange
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(order + 1)]
+            if ahead is not None:  # mode 0 was launched during the previous sweep's fit
+                evs[0], pending = ahead
+                ahead = None
             else:
-                fm = y @ torch.from_numpy(m64).to(device=device, dtype=torch.float32)
-                dst.copy_(fm)
-                g_raw = gram_raw(dst)
-                if mode == last:  # sum_r c_r <Y[:, r], F[:, r]>, fp32 chunks, fp64 total
-                    cw = torch.from_numpy(c).to(device=device, dtype=fm.dtype)
-                    inner = torch.zeros(1, dtype=torch.float64, device=device)
-                    for a in range(0, fm.shape[0], 1 << 20):
-                        inner += ((y[a: a + (1 << 20)] * fm[a: a + (1 << 20)]).sum(0).double()
-                                  * cw.double()).sum()
-            scales[mode] = np.ones(rank)
-            g = allreduce_(g_raw).cpu().numpy()
-            if not np.isfinite(g).all():
-                raise NumericalError(f"non-finite factor for mode {mode} in ALS sweep {it}", iteration=it)
-            grams[mode] = (g + g.T) * 0.5
-            exchange_rows(mode, f32)
-            del y
-            sync()
-            seconds.append(time.perf_counter() - tic)
-        if not torch.is_tensor(inner):
-            inner = torch.zeros(1, dtype=torch.float64, device=device)
-        new_fit = fit_value(float(allreduce_(inner.reshape(1)).item()))
+                evs[0].record()
+                pending = mttkrp(0)
+            for mode in range(order):
+                y, op = pending
+                y = y.float().contiguous()
+                ops.append(op)
+                g_raw, inner_m = update(mode, y, mode == last)
+                if inner_m is not None:
+                    inner = inner_m
+                g_pin.copy_(allreduce_(g_raw), non_blocking=True)
+                ev_g.record()
+                exchange_rows(mode, f32)
+                if mode == last:
+                    in_pin.copy_(allreduce_(inner.reshape(1)), non_blocking=True)
+                evs[mode + 1].record()
+                if mode + 1 < order:
+                    pending = mttkrp(mode + 1)
+                elif it < max_iters:
+                    # the next sweep's first MTTKRP needs only the factors:
+                    # queue it now, so it runs while the host computes the fit
+                    # (if the fit converges, its output is simply dropped)
+                    ev0 = torch.cuda.Event(enable_timing=True)
+                    ev0.record()
+                    ahead = (ev0, mttkrp(0))
+                ev_g.synchronize()
+                set_gram(mode, g_pin.numpy().copy(), it)
+                del y
+            evs[order].synchronize()
+            seconds = [evs[m].elapsed_time(evs[m + 1]) * 1e-3 for m in range(order)]
+            inner_val = float(in_pin[0])
+        else:
+            for mode in range(order):
+                sync()
+                tic = time.perf_counter()
+                y, op = mttkrp(mode)
+                y = y.float().contiguous()
+                ops.append(op)
+                g_raw, inner_m = update(mode, y, mode == last)
+                if inner_m is not None:
+                    inner = inner_m
+                set_gram(mode, allreduce_(g_raw).cpu().numpy(), it)
+                exchange_rows(mode, f32)
+                del y
+                sync()
+                seconds.append(time.perf_counter() - tic)
+            if not torch.is_tensor(inner):
+                inner = torch.zeros(1, dtype=torch.float64, device=device)
+            inner_val = float(allreduce_(inner.reshape(1)).item())
+        new_fit = fit_value(inner_val)
         lam = _normalize_scales(scales, grams)
         if not math.isfinite(new_fit):
             raise NumericalError(f"non-finite fit in ALS sweep {it}", iteration=it)
+        if sweep_hook is not None:  # host wall clock of the whole sweep
+            sweep_hook(it, time.perf_counter() - sweep_tic)
         delta = new_fit - history[-1].fit
         history.append(AlsIteration(it, new_fit, delta, tuple(seconds),
                                     tuple(ops) if all(o is not None for o in ops) else ()))
