@@ -229,6 +229,10 @@ void hbk_plan_release(hbk_plan* p);
  * output).  Its time is the row-gather ceiling of this plan on this GPU;
  * info.gather_rows / time = rows per second.  B-position plans only. */
 int hbk_plan_probe(const hbk_plan* p, const float* const* factors, void* stream);
+/* The output rows a plan's buckets own (rows the MTTKRP can make nonzero),
+ * ascending.  *count = their number; rows [dev] u32 (capacity >= *count) or
+ * NULL to only count.  Synchronises the stream (the count comes back).      */
+int hbk_plan_rows(const hbk_plan* p, uint32_t* rows, int64_t* count, void* stream);
 /* Finiteness scan for the host calling convention (replaces the per-call
  * np.isfinite of kernels.py:82-86 on factors already uploaded): async, one
  * launch; flags[i] (device int32) = 1 if bufs[i][0..counts[i]) holds a NaN or
@@ -270,6 +274,13 @@ void hbk_tns_free_text(char* text);
  * Y, F [dev] rows x rank fp32 row-major (may not alias); rank must be 32.   */
 int hbk_als_update(const float* Y, int64_t rows, int rank, const float* M, const float* colw,
                    float* F, double* gram, double* inner, void* stream);
+/* The same update restricted to the listed rows (ascending u32 row ids [dev],
+ * nlist of them): only those rows of Y are read and of F written — for modes
+ * whose other rows are known to be zero in Y (and already zero in F), e.g.
+ * rows no bucket owns (hbk_plan_rows).  Gram and fit term as above.         */
+int hbk_als_update_rows(const float* Y, const uint32_t* list, int64_t nlist, int rank,
+                        const float* M, const float* colw, float* F, double* gram, double* inner,
+                        void* stream);
 
 /* ------------------------------------------------------------ sharding --
  * Multi-GPU partitioner: slice nnz histogram of `mode`.

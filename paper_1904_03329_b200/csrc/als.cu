@@ -249,10 +249,14 @@ __device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4], con
   mma_tf32(d, ah[0], ah[1], ah[2], ah[3], bh0, bh1);
 }
 
+// LIST: process the rows list[0..rows) (ascending ids) instead of 0..rows.
+template <bool LIST>
 __global__ void __launch_bounds__(MMA_WARPS * 32, 2)
-    k_als_update32_mma(const float* __restrict__ Y, int64_t rows, const float* __restrict__ M,
-                       const float* __restrict__ colw, float* __restrict__ F,
-                       double* __restrict__ gupper, double* __restrict__ inner) {
+    k_als_update32_mma(const float* __restrict__ Y, int64_t rows, const uint32_t* __restrict__ list,
+                       const float* __restrict__ M, const float* __restrict__ colw,
+                       float* __restrict__ F, double* __restrict__ gupper,
+                       double* __restrict__ inner) {
+  auto rid = [&](int64_t i) -> int64_t { return LIST ? int64_t(__ldg(list + i)) : i; };
   extern __shared__ __align__(16) unsigned char smem_raw[];
   AlsMmaSmem& S = *reinterpret_cast<AlsMmaSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -282,7 +286,7 @@ __global__ void __launch_bounds__(MMA_WARPS * 32, 2)
       const int c = lane + 32 * j, r = c >> 3, c4 = (c & 7) * 4;
       const bool ok = r0 + r < rows;
       cp16_zfill(ring + stage * (MMA_ROWS * MMA_LD) + r * MMA_LD + c4,
-                 Y + (ok ? (r0 + r) * ALS_R + c4 : 0), ok);
+                 Y + (ok ? rid(r0 + r) * ALS_R + c4 : 0), ok);
     }
   };
   int64_t sub = int64_t(blockIdx.x) * MMA_WARPS + warp;
@@ -354,13 +358,14 @@ __global__ void __launch_bounds__(MMA_WARPS * 32, 2)
     // ---- F to global memory and over the Y subtile
     {
       const int64_t ra = r0 + g, rb = r0 + g + 8;
+      const int64_t fa_row = ra < rows ? rid(ra) : 0, fb_row = rb < rows ? rid(rb) : 0;
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
         const float2 fa = make_float2(d[nt][0], d[nt][1]), fb = make_float2(d[nt][2], d[nt][3]);
         *reinterpret_cast<float2*>(T + g * MMA_LD + nt * 8 + 2 * t) = fa;
         *reinterpret_cast<float2*>(T + (g + 8) * MMA_LD + nt * 8 + 2 * t) = fb;
-        if (ra < rows) __stcs(reinterpret_cast<float2*>(F + ra * ALS_R + nt * 8 + 2 * t), fa);
-        if (rb < rows) __stcs(reinterpret_cast<float2*>(F + rb * ALS_R + nt * 8 + 2 * t), fb);
+        if (ra < rows) __stcs(reinterpret_cast<float2*>(F + fa_row * ALS_R + nt * 8 + 2 * t), fa);
+        if (rb < rows) __stcs(reinterpret_cast<float2*>(F + fb_row * ALS_R + nt * 8 + 2 * t), fb);
       }
     }
     __syncwarp();
@@ -416,13 +421,49 @@ __global__ void __launch_bounds__(MMA_WARPS * 32, 2)
   }
 }
 
-// The Gram holds the upper 16x8 tiles ((c / 8) >= 2 (r / 16)); mirror the rest.
+// The Gram holds the upper 16x8 tiles, which cover every r <= c; mirror the
+// upper triangle (the diagonal tiles computed both (r, c) and (c, r), which
+// may differ in the last bit) so the result is exactly symmetric.
 __global__ void __launch_bounds__(1024) k_als_mirror(double* __restrict__ gram) {
   __shared__ double G[ALS_R][ALS_R + 1];
   const int r = threadIdx.x >> 5, c = threadIdx.x & 31;
   G[r][c] = gram[r * ALS_R + c];
   __syncthreads();
-  gram[r * ALS_R + c] = (c / 8 >= 2 * (r / 16)) ? G[r][c] : G[c][r];
+  gram[r * ALS_R + c] = r <= c ? G[r][c] : G[c][r];
+}
+
+// Tensor-core update over rows 0..n (or list[0..n)): Gram upper tiles and the
+// fit term accumulate in gram / inner (zeroed here), then the Gram is mirrored.
+template <bool LIST>
+static void launch_als_mma(const float* Y, const uint32_t* list, int64_t n, const float* M,
+                           const float* colw, float* F, double* gram, double* inner,
+                           cudaStream_t st) {
+  HBK_CUDA(cudaMemsetAsync(gram, 0, sizeof(double) * ALS_R * ALS_R, st));
+  if (inner) HBK_CUDA(cudaMemsetAsync(inner, 0, sizeof(double), st));
+  if (n == 0) return;
+  int dev = 0, sms = 0;
+  HBK_CUDA(cudaGetDevice(&dev));
+  HBK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // per-device launch setup, done once (concurrent first calls just repeat
+  // the idempotent attribute call)
+  static std::atomic<int> occ[64];
+  int per_sm = dev < 64 ? occ[dev].load(std::memory_order_relaxed) : 0;
+  if (per_sm == 0) {
+    HBK_CUDA(cudaFuncSetAttribute(k_als_update32_mma<LIST>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(sizeof(AlsMmaSmem))));
+    HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_update32_mma<LIST>,
+                                                           MMA_WARPS * 32, sizeof(AlsMmaSmem)));
+    per_sm = std::max(per_sm, 1);
+    if (dev < 64) occ[dev].store(per_sm, std::memory_order_relaxed);
+  }
+  const int64_t nsub = (n + MMA_ROWS - 1) / MMA_ROWS;
+  const int grid = int(std::min<int64_t>((nsub + MMA_WARPS - 1) / MMA_WARPS, int64_t(sms) * per_sm));
+  k_als_update32_mma<LIST><<<grid, MMA_WARPS * 32, sizeof(AlsMmaSmem), st>>>(Y, n, list, M, colw,
+                                                                              F, gram, inner);
+  check_launch("k_als_update32_mma");
+  k_als_mirror<<<1, 1024, 0, st>>>(gram);
+  check_launch("k_als_mirror");
 }
 }  // namespace hbk
 
@@ -445,35 +486,7 @@ extern "C" int hbk_als_update(const float* Y, int64_t rows, int rank, const floa
       return e && std::string(e) == "fma";
     }();
     if (!use_fma) {
-      if (rows == 0) {
-        HBK_CUDA(cudaMemsetAsync(gram, 0, sizeof(double) * ALS_R * ALS_R, st));
-        if (inner) HBK_CUDA(cudaMemsetAsync(inner, 0, sizeof(double), st));
-        return;
-      }
-      // the upper Gram tiles accumulate in `gram`, then are mirrored
-      HBK_CUDA(cudaMemsetAsync(gram, 0, sizeof(double) * ALS_R * ALS_R, st));
-      if (inner) HBK_CUDA(cudaMemsetAsync(inner, 0, sizeof(double), st));
-      // per-device launch setup, done once (concurrent first calls just
-      // repeat the idempotent attribute call)
-      static std::atomic<int> occ[64];
-      int per_sm_mma = dev < 64 ? occ[dev].load(std::memory_order_relaxed) : 0;
-      if (per_sm_mma == 0) {
-        HBK_CUDA(cudaFuncSetAttribute(k_als_update32_mma,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(sizeof(AlsMmaSmem))));
-        HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm_mma, k_als_update32_mma, MMA_WARPS * 32, sizeof(AlsMmaSmem)));
-        per_sm_mma = std::max(per_sm_mma, 1);
-        if (dev < 64) occ[dev].store(per_sm_mma, std::memory_order_relaxed);
-      }
-      const int64_t nsub = (rows + MMA_ROWS - 1) / MMA_ROWS;
-      const int grid = int(std::min<int64_t>((nsub + MMA_WARPS - 1) / MMA_WARPS,
-                                             int64_t(sms) * per_sm_mma));
-      k_als_update32_mma<<<grid, MMA_WARPS * 32, sizeof(AlsMmaSmem), st>>>(Y, rows, M, colw, F,
-                                                                           gram, inner);
-      check_launch("k_als_update32_mma");
-      k_als_mirror<<<1, 1024, 0, st>>>(gram);
-      check_launch("k_als_mirror");
+      launch_als_mma<false>(Y, nullptr, rows, M, colw, F, gram, inner, st);
       return;
     }
     HBK_CUDA(cudaMemsetAsync(gram, 0, sizeof(double) * ALS_R * ALS_R, st));
@@ -487,5 +500,18 @@ extern "C" int hbk_als_update(const float* Y, int64_t rows, int rank, const floa
     const int grid = int(std::min<int64_t>(ntiles, int64_t(sms) * std::max(per_sm, 1)));
     k_als_update32<<<grid, ALS_TILE, sizeof(AlsSmem), st>>>(Y, rows, M, colw, F, gram, inner);
     check_launch("k_als_update32");
+  });
+}
+
+extern "C" int hbk_als_update_rows(const float* Y, const uint32_t* list, int64_t nlist, int rank,
+                                   const float* M, const float* colw, float* F, double* gram,
+                                   double* inner, void* stream) {
+  return guarded([&] {
+    HBK_REQUIRE(rank == ALS_R, HBK_EINVAL, "hbk_als_update_rows supports rank 32");
+    HBK_REQUIRE(nlist >= 0, HBK_EINVAL, "negative row count");
+    HBK_REQUIRE(nlist == 0 || list, HBK_EINVAL, "null row list");
+    HBK_REQUIRE((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(F)) % 16 == 0,
+                HBK_EINVAL, "Y and F must be 16-byte aligned");
+    launch_als_mma<true>(Y, list, nlist, M, colw, F, gram, inner, to_stream(stream));
   });
 }

@@ -1022,6 +1022,12 @@ __global__ void k_unmarked_emit(const uint32_t* __restrict__ pos, int64_t n,
        i += int64_t(gridDim.x) * blockDim.x)
     if (pos[i + 1] != pos[i]) rows[pos[i]] = uint32_t(i);
 }
+__global__ void k_marked_flags(const uint8_t* __restrict__ mark, int64_t n,
+                               uint32_t* __restrict__ f) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    f[i] = mark[i] != 0;
+}
 __global__ void k_range_tasks(Task* __restrict__ tasks, int64_t ntask, uint32_t total,
                               uint32_t step) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < ntask;
@@ -2323,6 +2329,40 @@ __global__ void __launch_bounds__(256) k_nonfinite(const __grid_constant__ Finit
   }
 }
 }  // namespace hbk
+
+int hbk_plan_rows(const hbk_plan* p, uint32_t* rows_out, int64_t* count, void* stream) {
+  return guarded([&] {
+    HBK_REQUIRE(p && count, HBK_EINVAL, "null pointer");
+    cudaStream_t st = to_stream(stream);
+    const int64_t rows = p->dims[p->mode];
+    if (rows == 0) {
+      *count = 0;
+      return;
+    }
+    Scratch mark(rows, st);
+    HBK_CUDA(cudaMemsetAsync(mark.p, 0, rows, st));
+    if (p->csf && p->csf->n[0])
+      k_mark_rows<<<grid_for(p->csf->n[0], 256), 256, 0, st>>>(p->csf->idx[0].as<uint32_t>(),
+                                                               p->csf->n[0], mark.as<uint8_t>());
+    if (p->csl && p->csl->S)
+      k_mark_rows<<<grid_for(p->csl->S, 256), 256, 0, st>>>(p->csl->slice_idx.as<uint32_t>(),
+                                                            p->csl->S, mark.as<uint8_t>());
+    if (p->coo && p->coo->nnz)
+      k_mark_rows<<<grid_for(p->coo->nnz, 256), 256, 0, st>>>(
+          p->coo->cols[p->mode].as<uint32_t>(), p->coo->nnz, mark.as<uint8_t>());
+    check_launch("k_mark_rows");
+    Scratch pos((rows + 1) * sizeof(uint32_t), st);
+    k_marked_flags<<<grid_for(rows, 256), 256, 0, st>>>(mark.as<uint8_t>(), rows,
+                                                        pos.as<uint32_t>());
+    check_launch("k_marked_flags");
+    const uint32_t n = exclusive_scan_total(pos.as<uint32_t>(), rows, st);
+    *count = n;
+    if (rows_out && n) {
+      k_unmarked_emit<<<grid_for(rows, 256), 256, 0, st>>>(pos.as<uint32_t>(), rows, rows_out);
+      check_launch("k_unmarked_emit");
+    }
+  });
+}
 
 int hbk_nonfinite_f32(const float* const* bufs, const int64_t* counts, int n, int32_t* flags,
                       void* stream) {

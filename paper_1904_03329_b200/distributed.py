@@ -110,6 +110,14 @@ class DeviceShards:
         y, _ = mttkrp_device(rep, fs, mode)
         return y
 
+    def owned_rows(self, mode: int, rank: int = 32):
+        """This rank's output rows of ``mode`` that some bucket owns (local
+        indices, device int32), or None."""
+        from .kernels import plan_for
+
+        rep = self.reps[mode]
+        return None if rep is None else plan_for(rep, mode, rank).owned_rows()
+
 
 class RowExchange:
     """Touched-rows exchange of one factor: after factor d is
@@ -179,6 +187,7 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
         raise ValueError("rank must be at least 1")
     if max_iters < 0:
         raise ValueError("max_iters must be nonnegative")
+    owned_rows = None
     if local_mttkrp is None:
         from . import _native as N
 
@@ -190,6 +199,7 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
         shards = DeviceShards(t, world, me)
         ranges = shards.ranges
         local_mttkrp = shards
+        owned_rows = lambda mode: shards.owned_rows(mode, rank)  # noqa: E731
         if needed is None:
             needed = shards.needed
     else:
@@ -237,12 +247,13 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
     return als_fp32(torch, dims=dims, rank=rank, max_iters=max_iters, fit_tol=fit_tol, seed=seed,
                     device=device, own=own, local_mttkrp=local_mttkrp,
                     norm_x=_value_norm(torch, t), allreduce_=allreduce_,
-                    exchange_rows=exchange_rows, finalize=finalize, sweep_hook=sweep_hook)
+                    exchange_rows=exchange_rows, finalize=finalize, sweep_hook=sweep_hook,
+                    owned_rows=owned_rows)
 
 
 def als_fp32(torch, *, dims, rank, max_iters, fit_tol, seed, device, own, local_mttkrp, norm_x,
              allreduce_=lambda x: x, exchange_rows=lambda d, f32: None, finalize=lambda f32: None,
-             sweep_hook=None):
+             sweep_hook=None, owned_rows=None):
     """The CP-ALS sweep loop (cpd.py:198-271) on fp32 factors with folded
     column scales, for a rank owning rows ``own[d]`` of every factor.
     ``local_mttkrp(mode, f32)`` returns this rank's (rows, R) MTTKRP (or a
@@ -321,9 +332,11 @@ def als_fp32(torch, *, dims, rank, max_iters, fit_tol, seed, device, own, local_
         in_pin = torch.empty(1, dtype=torch.float64, pin_memory=True)
     ahead = None
 
-    def update(mode, y, with_inner):
+    def update(mode, y, with_inner, use_list=False):
         """F_mode <- Y M (rows this rank owns), the raw Gram of the new rows;
-        the fit term into inner_t when with_inner."""
+        the fit term into inner_t when with_inner.  use_list: only the rows
+        some bucket owns (owned_rows(mode)); the others are zero in Y and
+        have been zero in F since the first sweep wrote them."""
         c = colscale(mode)
         # F_true = (Y_raw diag(c)) V^+  ->  M = diag(c) V^+, new scales 1
         m64 = c[:, None] * pinv_spsd(hadamard_all_but(grams, mode))
@@ -343,7 +356,14 @@ def als_fp32(torch, *, dims, rank, max_iters, fit_tol, seed, device, own, local_
             else:
                 m32 = torch.from_numpy(m64).to(device=device, dtype=torch.float32).contiguous()
                 w32 = torch.from_numpy(c).to(device=device, dtype=torch.float32)
-            if hi > lo:
+            rows_l = owned_rows(mode) if (use_list and owned_rows is not None) else None
+            if rows_l is not None and hi > lo and rows_l.numel() < 0.9 * (hi - lo):
+                N.call("hbk_als_update_rows", C.c_void_p(y.data_ptr()),
+                       C.c_void_p(rows_l.data_ptr()), int(rows_l.numel()), int(rank),
+                       C.c_void_p(m32.data_ptr()), C.c_void_p(w32.data_ptr()),
+                       C.c_void_p(dst.data_ptr()), C.c_void_p(g_raw.data_ptr()),
+                       C.c_void_p(inner_t.data_ptr()) if with_inner else None, N.stream_ptr())
+            elif hi > lo:
                 N.call("hbk_als_update", C.c_void_p(y.data_ptr()), int(hi - lo), int(rank),
                        C.c_void_p(m32.data_ptr()), C.c_void_p(w32.data_ptr()),
                        C.c_void_p(dst.data_ptr()), C.c_void_p(g_raw.data_ptr()),
@@ -388,7 +408,7 @@ def als_fp32(torch, *, dims, rank, max_iters, fit_tol, seed, device, own, local_
                 y, op = pending
                 y = y.float().contiguous()
                 ops.append(op)
-                g_raw, inner_m = update(mode, y, mode == last)
+                g_raw, inner_m = update(mode, y, mode == last, use_list=it > 1)
                 if inner_m is not None:
                     inner = inner_m
                 g_pin.copy_(allreduce_(g_raw), non_blocking=True)

@@ -271,7 +271,7 @@ def _device_factors(factors: Factors, mode: int, precision: str = "fp32"):
 class _Plan:
     """A libhbk plan (work list for one mode/rank/bucket set) plus its info."""
 
-    __slots__ = ("h", "info", "rows", "rank")
+    __slots__ = ("h", "info", "rows", "rank", "_owned")
 
     def __init__(self, coo, csl, csf, sched, mode: int, rank: int, rows: int):
         out = N.new_out()
@@ -283,10 +283,24 @@ class _Plan:
         self.info = info
         self.rows = rows
         self.rank = rank
+        self._owned = None
 
     @property
     def opcount(self) -> OpCount:
         return OpCount(int(self.info.op_muls), int(self.info.op_adds))
+
+    def owned_rows(self):
+        """Device int32 tensor of the output rows the buckets own, ascending
+        (hbk_plan_rows); rows outside it are zero in every MTTKRP result."""
+        if self._owned is None:
+            torch = N.require_device()
+            n = C.c_int64(0)
+            N.call("hbk_plan_rows", self.h.ptr, None, C.byref(n), N.stream_ptr())
+            out = torch.empty(max(1, n.value), dtype=torch.int32, device="cuda")
+            N.call("hbk_plan_rows", self.h.ptr, C.c_void_p(out.data_ptr()), C.byref(n),
+                   N.stream_ptr())
+            self._owned = out[: n.value]
+        return self._owned
 
     def probe(self, factor_ptrs) -> None:
         """Launch the plan's gather-only calibration kernels (hbk_plan_probe)."""

@@ -116,3 +116,47 @@ def test_als_update_kernel_matches_fp64(rows):
     with pytest.raises(ValueError):
         N.call("hbk_als_update", C.c_void_p(Y.data_ptr()), rows, 16, C.c_void_p(M.data_ptr()),
                None, C.c_void_p(F.data_ptr()), C.c_void_p(gram.data_ptr()), None, N.stream_ptr())
+
+
+@pytest.mark.parametrize("rows", [1, 37, 5000, 70001])
+def test_als_update_rows_matches_full_update(rows):
+    """hbk_als_update_rows over the nonzero rows of Y equals hbk_als_update
+    over all rows when the other rows are zero (F, Gram, fit term); rows not
+    listed keep their previous F contents."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1904_03329_b200 import _native as N
+
+    g = torch.Generator(device="cuda").manual_seed(rows + 1)
+    Y = torch.rand((rows, 32), device="cuda", generator=g) - 0.3
+    keep = torch.rand(rows, device="cuda", generator=g) < 0.6
+    keep[0] = True
+    Y[~keep] = 0.0
+    lst = torch.nonzero(keep).flatten().to(torch.int32)
+    M = torch.rand((32, 32), device="cuda", generator=g) - 0.5
+    w = torch.rand(32, device="cuda", generator=g) + 0.5
+    outs = []
+    for use_list in (False, True):
+        F = torch.full_like(Y, 7.0)
+        gram = torch.empty((32, 32), dtype=torch.float64, device="cuda")
+        inner = torch.empty(1, dtype=torch.float64, device="cuda")
+        if use_list:
+            N.call("hbk_als_update_rows", C.c_void_p(Y.data_ptr()), C.c_void_p(lst.data_ptr()),
+                   int(lst.numel()), 32, C.c_void_p(M.data_ptr()), C.c_void_p(w.data_ptr()),
+                   C.c_void_p(F.data_ptr()), C.c_void_p(gram.data_ptr()),
+                   C.c_void_p(inner.data_ptr()), N.stream_ptr())
+        else:
+            N.call("hbk_als_update", C.c_void_p(Y.data_ptr()), rows, 32, C.c_void_p(M.data_ptr()),
+                   C.c_void_p(w.data_ptr()), C.c_void_p(F.data_ptr()), C.c_void_p(gram.data_ptr()),
+                   C.c_void_p(inner.data_ptr()), N.stream_ptr())
+        outs.append((F, gram, inner))
+    (F0, g0, i0), (F1, g1, i1) = outs
+    assert torch.equal(F1[keep], F0[keep])  # same MMA arithmetic per row
+    assert bool((F1[~keep] == 7.0).all())   # unlisted rows untouched
+    # the listed rows form different 16-row MMA subtiles: the Gram and the fit
+    # term agree to fp32 accumulation order
+    assert torch.allclose(g1, g0, rtol=1e-6, atol=1e-6 * float(g0.abs().max()))
+    assert abs(float(i1) - float(i0)) <= 1e-6 * max(1.0, abs(float(i0)))
+    assert torch.equal(g1, g1.T)
