@@ -218,6 +218,12 @@ int hbk_plan_info_get(const hbk_plan* p, hbk_plan_info* info);
  * dims[d] x rank fp32 (factors[mode] is not read, kernels.py:62-66).
  * out: [dev] dims[mode] x rank fp32.                                       */
 int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out, void* stream);
+/* hbk_plan_execute with flags.  HBK_EXEC_SKIP_UNOWNED: rows no bucket owns
+ * (see hbk_plan_rows) may be left unwritten instead of zero-filled — for
+ * callers that only read the owned rows (the CP-ALS row update).           */
+#define HBK_EXEC_SKIP_UNOWNED 1
+int hbk_plan_execute_ex(const hbk_plan* p, const float* const* factors, float* out, int flags,
+                        void* stream);
 /* fp64 mode: factors/out fp64, the buckets' original fp64 values, fp64
  * accumulation (generic kernel).  For accuracy-sensitive callers, e.g. the
  * CP-ALS fit, whose algebraic form amplifies fp32 rounding near convergence. */

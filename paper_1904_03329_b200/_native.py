@@ -135,6 +135,7 @@ _SIGS = {
     "hbk_plan_probe": ([vp, vp, vp], C.c_int),
     "hbk_nonfinite_f32": ([vp, vp, C.c_int, vp, vp], C.c_int),
     "hbk_plan_rows": ([vp, vp, C.POINTER(C.c_int64), vp], C.c_int),
+    "hbk_plan_execute_ex": ([vp, vp, vp, C.c_int, vp], C.c_int),
     "hbk_als_update_rows": ([vp, vp, C.c_int64, C.c_int, vp, vp, vp, vp, vp, vp], C.c_int),
     "hbk_tns_parse": ([C.c_char_p, i64, C.c_int, vp, C.c_int, C.POINTER(vp)], C.c_int),
     "hbk_tns_load": ([C.c_char_p, C.c_int, vp, C.c_int, C.POINTER(vp)], C.c_int),

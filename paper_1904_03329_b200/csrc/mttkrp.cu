@@ -2155,7 +2155,7 @@ using namespace hbk;
 
 namespace hbk {
 template <class FX>
-static void launch_fast(const hbk_plan* p, const FX& fx, cudaStream_t st) {
+static void launch_fast(const hbk_plan* p, const FX& fx, cudaStream_t st, bool skip_zero = false) {
   // kernels in launch order: heavy slices first (the longest), then light
   // CSF, CSL, COO/zero; with p->concurrent each after the first goes to its
   // own forked stream
@@ -2191,9 +2191,12 @@ static void launch_fast(const hbk_plan* p, const FX& fx, cudaStream_t st) {
     cudaStream_t s2 = next_stream();
     k_mttkrp3_r32<KIND_CSL, FX><<<p->grids[1], p->block, 0, s2>>>(p->work, fx);
   }
-  if (p->grids[2]) {
+  // skip_zero: the rows no bucket owns are left unwritten (COO tasks only)
+  Work wc = p->work;
+  if (skip_zero) wc.n3 = wc.n2;
+  if (p->grids[2] && wc.n3 > wc.n1) {
     cudaStream_t s2 = next_stream();
-    k_mttkrp3_r32<KIND_COO, FX><<<p->grids[2], p->block, 0, s2>>>(p->work, fx);
+    k_mttkrp3_r32<KIND_COO, FX><<<p->grids[2], p->block, 0, s2>>>(wc, fx);
   }
   check_launch("k_mttkrp3_r32");
   if (p->concurrent)
@@ -2266,7 +2269,13 @@ int hbk_plan_info_get(const hbk_plan* p, hbk_plan_info* info) {
 }
 
 int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out, void* stream) {
+  return hbk_plan_execute_ex(p, factors, out, 0, stream);
+}
+
+int hbk_plan_execute_ex(const hbk_plan* p, const float* const* factors, float* out, int flags,
+                        void* stream) {
   return guarded([&] {
+    const bool skip_zero = (flags & HBK_EXEC_SKIP_UNOWNED) != 0;
     cudaStream_t st = to_stream(stream);
     const int N = p->order;
     for (int d = 0; d < N; ++d)
@@ -2284,13 +2293,13 @@ int hbk_plan_execute(const hbk_plan* p, const float* const* factors, float* out,
                   HBK_EINVAL, "factor and output buffers must be 16-byte aligned");
       const int R = p->rank;
       if (p->r32) {
-        launch_fast(p, Factors3R32(fx), st);
+        launch_fast(p, Factors3R32(fx), st, skip_zero);
       } else {
         fx.rs = uint32_t(R / 4);
         for (int c0 = 0; c0 < R; c0 += 32) {  // passes of 32 columns
           fx.col4 = uint32_t(c0 / 4);
           fx.lanes = uint32_t(std::min(8, (R - c0) / 4));
-          launch_fast(p, fx, st);
+          launch_fast(p, fx, st, skip_zero);
         }
       }
     } else {

@@ -97,7 +97,7 @@ class DeviceShards:
         self.needed = [torch.unique(torch.cat(r)) if r else torch.zeros(0, dtype=torch.long, device="cuda")
                        for r in refs]
 
-    def __call__(self, mode: int, factors32):
+    def __call__(self, mode: int, factors32, skip_unowned: bool = False):
         from .kernels import mttkrp_device
 
         lo, hi = self.ranges[mode][self.me]
@@ -107,7 +107,7 @@ class DeviceShards:
             return ref.new_zeros((0, ref.shape[1]))
         fs = list(factors32)
         fs[mode] = factors32[mode][: hi - lo]  # shape only; factors[mode] is not read
-        y, _ = mttkrp_device(rep, fs, mode)
+        y, _ = mttkrp_device(rep, fs, mode, skip_unowned=skip_unowned)
         return y
 
     def owned_rows(self, mode: int, rank: int = 32):
@@ -268,8 +268,11 @@ def als_fp32(torch, *, dims, rank, max_iters, fit_tol, seed, device, own, local_
            for dim in dims]  # cpd.py:231-232, identical on every rank
     scales = [np.ones(rank) for _ in dims]
 
-    def mttkrp(mode):
-        r = local_mttkrp(mode, f32)
+    def mttkrp(mode, skip_unowned=False):
+        # skip_unowned (with owned_rows): rows no bucket owns are not written —
+        # the row update then reads only the owned rows
+        skip_unowned = skip_unowned and os.environ.get("HBK_SKIP_UNOWNED", "1") != "0"
+        r = local_mttkrp(mode, f32, skip_unowned=True) if skip_unowned else local_mttkrp(mode, f32)
         return r if isinstance(r, tuple) else (r, None)
 
     def gram_raw(local):
@@ -357,7 +360,8 @@ def als_fp32(torch, *, dims, rank, max_iters, fit_tol, seed, device, own, local_
                 m32 = torch.from_numpy(m64).to(device=device, dtype=torch.float32).contiguous()
                 w32 = torch.from_numpy(c).to(device=device, dtype=torch.float32)
             rows_l = owned_rows(mode) if (use_list and owned_rows is not None) else None
-            if rows_l is not None and hi > lo and rows_l.numel() < 0.9 * (hi - lo):
+            # (the MTTKRP of such a sweep leaves unowned rows of Y unwritten)
+            if rows_l is not None and hi > lo:
                 N.call("hbk_als_update_rows", C.c_void_p(y.data_ptr()),
                        C.c_void_p(rows_l.data_ptr()), int(rows_l.numel()), int(rank),
                        C.c_void_p(m32.data_ptr()), C.c_void_p(w32.data_ptr()),
@@ -398,17 +402,19 @@ def als_fp32(torch, *, dims, rank, max_iters, fit_tol, seed, device, own, local_
             # update, Gram read-back and row exchange included); the last mode
             # runs to the end of the sweep's exchange
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(order + 1)]
+            # from the second sweep on the row update reads only owned rows
+            lists = owned_rows is not None and it > 1
             if ahead is not None:  # mode 0 was launched during the previous sweep's fit
                 evs[0], pending = ahead
                 ahead = None
             else:
                 evs[0].record()
-                pending = mttkrp(0)
+                pending = mttkrp(0, lists)
             for mode in range(order):
                 y, op = pending
                 y = y.float().contiguous()
                 ops.append(op)
-                g_raw, inner_m = update(mode, y, mode == last, use_list=it > 1)
+                g_raw, inner_m = update(mode, y, mode == last, use_list=lists)
                 if inner_m is not None:
                     inner = inner_m
                 g_pin.copy_(allreduce_(g_raw), non_blocking=True)
@@ -418,14 +424,14 @@ def als_fp32(torch, *, dims, rank, max_iters, fit_tol, seed, device, own, local_
                     in_pin.copy_(allreduce_(inner.reshape(1)), non_blocking=True)
                 evs[mode + 1].record()
                 if mode + 1 < order:
-                    pending = mttkrp(mode + 1)
+                    pending = mttkrp(mode + 1, lists)
                 elif it < max_iters:
                     # the next sweep's first MTTKRP needs only the factors:
                     # queue it now, so it runs while the host computes the fit
                     # (if the fit converges, its output is simply dropped)
                     ev0 = torch.cuda.Event(enable_timing=True)
                     ev0.record()
-                    ahead = (ev0, mttkrp(0))
+                    ahead = (ev0, mttkrp(0, owned_rows is not None))
                 ev_g.synchronize()
                 set_gram(mode, g_pin.numpy().copy(), it)
                 del y

@@ -306,13 +306,19 @@ class _Plan:
         """Launch the plan's gather-only calibration kernels (hbk_plan_probe)."""
         N.call("hbk_plan_probe", self.h.ptr, factor_ptrs, N.stream_ptr())
 
-    def execute(self, factor_ptrs, out=None, precision: str = "fp32"):
+    def execute(self, factor_ptrs, out=None, precision: str = "fp32", skip_unowned: bool = False):
+        """skip_unowned: rows no bucket owns may be left unwritten (fp32 fast
+        path; callers that read only owned_rows())."""
         torch = N.require_device()
         dt = torch.float64 if precision == "fp64" else torch.float32
         if out is None:
             out = torch.empty((self.rows, self.rank), dtype=dt, device="cuda")
-        fn = "hbk_plan_execute_f64" if precision == "fp64" else "hbk_plan_execute"
-        N.call(fn, self.h.ptr, factor_ptrs, C.c_void_p(out.data_ptr()), N.stream_ptr())
+        if precision == "fp64":
+            N.call("hbk_plan_execute_f64", self.h.ptr, factor_ptrs, C.c_void_p(out.data_ptr()),
+                   N.stream_ptr())
+        else:
+            N.call("hbk_plan_execute_ex", self.h.ptr, factor_ptrs, C.c_void_p(out.data_ptr()),
+                   1 if skip_unowned else 0, N.stream_ptr())
         return out
 
 
@@ -450,7 +456,8 @@ def mttkrp(rep, factors: Factors, mode: int, **kwargs):
     raise TypeError(f"no MTTKRP kernel for {type(rep).__name__}")
 
 
-def mttkrp_device(rep, factors, mode: int, out=None, schedule=None, precision: str | None = None):
+def mttkrp_device(rep, factors, mode: int, out=None, schedule=None, precision: str | None = None,
+                  skip_unowned: bool = False):
     """Device fast path: CUDA factors in, CUDA (dims[mode], R) out, no host
     synchronisation and no finiteness scan.  The kernel precision follows the
     factors' dtype (float64 -> fp64 kernel) unless given.  Returns (out, OpCount)."""
@@ -462,4 +469,4 @@ def mttkrp_device(rep, factors, mode: int, out=None, schedule=None, precision: s
         precision = "fp64" if str(getattr(ref, "dtype", "")) == "torch.float64" else "fp32"
     plan = plan_for(rep, mode, r, schedule)
     ptrs, keep, _, _ = _device_factors(factors, mode, _check_precision(precision))
-    return plan.execute(ptrs, out, precision), plan.opcount
+    return plan.execute(ptrs, out, precision, skip_unowned), plan.opcount
