@@ -396,3 +396,27 @@ def test_execute_captures_into_cuda_graph(hb, rng):
         torch.cuda.synchronize()
         ref, _ = mttkrp_device(h, f, 0)
         assert row_dev(out.double().cpu().numpy(), ref.double().cpu().numpy()) <= 1e-6
+
+
+def test_skip_unowned_rows_and_owned_rows_list(hb, rng):
+    """hbk_plan_rows lists exactly the rows with nonzeros; an execute with
+    HBK_EXEC_SKIP_UNOWNED writes those rows as the plain execute does and
+    leaves every other row untouched."""
+    import torch
+
+    from paper_1904_03329_b200.kernels import mttkrp_device, plan_for
+
+    dims = (20000, 60, 80)  # Zipf rows: many of the 20000 stay empty
+    idx, vals = _powerlaw(rng, dims, 20000)
+    t = hb.CooTensor(dims, idx, vals)
+    h = hb.build_hbcsf(t, hb.allmode_order(dims, 0))
+    owned = plan_for(h, 0, 32).owned_rows()
+    assert owned.tolist() == sorted(set(int(i) for i in idx[:, 0]))
+    f = [torch.rand((d, 32), device="cuda") for d in dims]
+    full, _ = mttkrp_device(h, f, 0)
+    out = torch.full((dims[0], 32), 3.0, device="cuda")
+    mttkrp_device(h, f, 0, out=out, skip_unowned=True)
+    mask = torch.zeros(dims[0], dtype=torch.bool, device="cuda")
+    mask[owned.long()] = True
+    assert torch.equal(out[mask], full[mask])
+    assert bool((out[~mask] == 3.0).all()) and int((~mask).sum()) > 0
