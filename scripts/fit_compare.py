@@ -1,3 +1,6 @@
+"""CP-ALS fit history of the fused fp32 path (R=32: fast MTTKRP + tensor-core
+row update) against the fp64 MTTKRP path on nell-2 (first four sweeps).
+    python scripts/fit_compare.py"""
 import sys, numpy as np
 sys.path.insert(0, '.')
 import paper_1904_03329_b200 as hb
