@@ -1699,7 +1699,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   // B-position streams (default fast CSF path): every slice with more than
   // Tcsf nonzeros goes to the heavy layout, lighter slices form runs
   p->bpos = p->fast && !p->sched && p->csf_variant >= 1;
-  uint32_t heavy_H = p->bpos ? Tcsf : 4 * Tcsf, heavy_tau = 32, heavy_W = 2048;
+  uint32_t heavy_H = p->bpos ? Tcsf : 4 * Tcsf, heavy_tau = 32, heavy_W = 1024;
   if (const char* e = getenv("HBK_HEAVY_H")) heavy_H = uint32_t(std::max(0, atoi(e)));
   if (const char* e = getenv("HBK_HEAVY_TAU")) heavy_tau = uint32_t(std::min(65535, std::max(1, atoi(e))));
   if (const char* e = getenv("HBK_HEAVY_W")) heavy_W = uint32_t(std::max(1, atoi(e)));

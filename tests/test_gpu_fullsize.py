@@ -40,15 +40,18 @@ def test_fast_fp32_matches_generic_fp64_at_scale(config, scale):
         y64, _ = mttkrp_device(h, f64r, mode)
         assert y32.dtype == torch.float32 and y64.dtype == torch.float64
         assert _rowdev(y32, y64) <= 1e-4, (config, mode)
-        # linearity in a factor (exact up to fp32 rounding): Y(2C) = 2 Y(C)
+        # linearity in a factor: Y(2C) = 2 Y(C) exactly, except that the
+        # chunks of a split slice (thousands for the 3M-nonzero nell-2 slices)
+        # meet in red.global.add order, which varies run to run: fp32
+        # reassociation, ~1e-6 of the row norm (a bug would show as O(1))
         fs = list(f32)
         d = hb.allmode_order(dims, mode)[2]
         fs[d] = f32[d] * 2.0
         y2, _ = mttkrp_device(h, fs, mode)
-        assert _rowdev(y2, 2.0 * y32.double()) <= 1e-6
-        # repeatability up to the atomic order of split slices
+        assert _rowdev(y2, 2.0 * y32.double()) <= 1e-5
+        # repeatability up to the same atomic order
         y32b, _ = mttkrp_device(h, f32, mode)
-        assert _rowdev(y32b, y32.double()) <= 1e-6
+        assert _rowdev(y32b, y32.double()) <= 1e-5
 
 
 @pytest.mark.parametrize("R", [8, 16, 48, 64])
