@@ -987,15 +987,18 @@ __global__ void k_slot_flags(const uint32_t* __restrict__ cnt, int64_t S,
        s += int64_t(gridDim.x) * blockDim.x)
     f[s] = cnt[s] > 1;
 }
+// bpos: ranges in B-position stream positions (fiber f's leaves start at
+// lptr[f] + f); units are fiber-aligned, so a unit ends on a B position.
 __global__ void k_units_to_tasks(const uint32_t* __restrict__ units, int64_t U,
                                  const uint32_t* __restrict__ lptr, const uint32_t* __restrict__ cnt,
-                                 const uint32_t* __restrict__ slot, Task* __restrict__ tasks) {
+                                 const uint32_t* __restrict__ slot, int bpos,
+                                 Task* __restrict__ tasks) {
   for (int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; u < U;
        u += int64_t(gridDim.x) * blockDim.x) {
     uint32_t sp = units[3 * u], fs = units[3 * u + 1], ft = units[3 * u + 2];
     Task t{};
-    t.lo = lptr[fs];
-    t.hi = lptr[ft];
+    t.lo = lptr[fs] + (bpos ? fs : 0u);
+    t.hi = lptr[ft] + (bpos ? ft : 0u);
     t.s = sp;
     t.f = fs;
     t.slot = cnt[sp] > 1 ? slot[sp] : NOSLOT;
@@ -1694,11 +1697,12 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   Work& w = p->work;
   std::memset(&w, 0, sizeof(w));
   BucketTasks tcsf, tcsl, tcsf_light, tcsl_fast;
-  bool csl_blocked = false;
+  bool csl_blocked = false, sched_bpos = false;
   // heavy-slice layout (fast path): slices with more than H nonzeros
   // B-position streams (default fast CSF path): every slice with more than
   // Tcsf nonzeros goes to the heavy layout, lighter slices form runs
-  p->bpos = p->fast && !p->sched && p->csf_variant >= 1;
+  // (schedule units run through the same light-slice B-position kernel)
+  p->bpos = p->fast && p->csf_variant >= 1;
   uint32_t heavy_H = p->bpos ? Tcsf : 4 * Tcsf, heavy_tau = 32, heavy_W = 1024;
   if (const char* e = getenv("HBK_HEAVY_H")) heavy_H = uint32_t(std::max(0, atoi(e)));
   if (const char* e = getenv("HBK_HEAVY_TAU")) heavy_tau = uint32_t(std::min(65535, std::max(1, atoi(e))));
@@ -1743,11 +1747,23 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       if (sc->U) {
         k_units_to_tasks<<<grid_for(sc->U, 256), 256, 0, st>>>(
             sc->units.as<uint32_t>(), sc->U, c->ptr[L].as<uint32_t>(), cnt.as<uint32_t>(),
-            slot.as<uint32_t>(), tcsf.tasks.as<Task>());
+            slot.as<uint32_t>(), 0, tcsf.tasks.as<Task>());
         check_launch("k_units_to_tasks");
       }
       tcsf.n = sc->U;
       tcsf.slots = nslot;
+      if (p->bpos) {  // the fast kernel's copy in stream positions; tcsf stays for the generic one
+        tcsf_light.tasks = Scratch(size_t(std::max<int64_t>(sc->U, 1)) * sizeof(Task), st);
+        if (sc->U) {
+          k_units_to_tasks<<<grid_for(sc->U, 256), 256, 0, st>>>(
+              sc->units.as<uint32_t>(), sc->U, c->ptr[L].as<uint32_t>(), cnt.as<uint32_t>(),
+              slot.as<uint32_t>(), 1, tcsf_light.tasks.as<Task>());
+          check_launch("k_units_to_tasks");
+        }
+        tcsf_light.n = sc->U;
+        tcsf_light.slots = nslot;
+        sched_bpos = true;
+      }
       // OpCount of mttkrp_scheduled (kernels.py:283-298, 325-330)
       int64_t mid = 0;
       if (N > 3) {
@@ -1971,13 +1987,14 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       wo.n3 = uint32_t(total);
       wo.tasks = T;
     };
-    if (heavy_on || csl_blocked) {
-      assemble(heavy_on ? tcsf_light : tcsf, csl_blocked ? tcsl_fast : tcsl, p->tasks, w);
+    if (heavy_on || csl_blocked || sched_bpos) {
+      assemble((heavy_on || sched_bpos) ? tcsf_light : tcsf, csl_blocked ? tcsl_fast : tcsl,
+               p->tasks, w);
       assemble(tcsf, tcsl, p->gen_tasks, p->work_gen);
     } else {
       assemble(tcsf, tcsl, p->tasks, w);
     }
-    p->info.tasks_csf = heavy_on ? tcsf_light.n : tcsf.n;
+    p->info.tasks_csf = (heavy_on || sched_bpos) ? tcsf_light.n : tcsf.n;
     p->info.tasks_csl = csl_blocked ? tcsl_fast.n : tcsl.n;
     p->info.tasks_coo = n_coo;
   }
@@ -1990,7 +2007,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   w.ws_ctr = reinterpret_cast<uint32_t*>(p->ws.as<char>());
   w.ws_cnt = reinterpret_cast<uint32_t*>(p->ws.as<char>() + cnt_off);
   w.ws_acc = reinterpret_cast<float*>(p->ws.as<char>() + acc_off);
-  if (!heavy_on && !csl_blocked) {
+  if (!heavy_on && !csl_blocked && !sched_bpos) {
     p->work_gen = w;
   } else {
     Work& wg = p->work_gen;
