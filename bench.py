@@ -521,7 +521,7 @@ def main():
                 "split": {"fiber_threshold": 128, "block_size": 512},
                 "l2": "inputs larger than L2 (index/value streams 0.75+ GB per mode); factors L2-resident by design",
                 "parallelism": f"slice-sharded dp{world}" if world > 1 else "1 GPU",
-                "census": censuses if world == 1 else None,
+                "census": censuses if world == 1 else {"rank0_shards": censuses},
                 "preprocessing_s": prep_s, "generate_s": gen_s,
             },
             "roofline": {
