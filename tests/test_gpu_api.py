@@ -350,6 +350,7 @@ def test_csl_b_row_blocking_parity(hb, rng, block_mb, monkeypatch):
     block, split slices handed over through the accumulator) gives the
     oracle's rows.  Tiny blocks force many segments per slice."""
     monkeypatch.setenv("HBK_CSL_BLOCK_MB", block_mb)
+    monkeypatch.setenv("HBK_CSL_AS_CSF", "0")  # the CSL kernel itself
     dims = (60, 500, 400)
     # CSL-dominated: distinct (j, k) per slice, so every fiber is a singleton
     n = 6000
@@ -421,3 +422,32 @@ def test_skip_unowned_rows_and_owned_rows_list(hb, rng):
     mask[owned.long()] = True
     assert torch.equal(out[mask], full[mask])
     assert bool((out[~mask] == 3.0).all()) and int((~mask).sum()) > 0
+
+
+@pytest.mark.parametrize("nnz", [6000, 40000])
+def test_csl_slices_through_csf_kernels(hb, rng, nnz, monkeypatch):
+    """HB-CSF plans may run their CSL slices as singleton-fiber CSF slices
+    (HBK_CSL_AS_CSF; automatic for heavy CSL slices): same rows as the CSL
+    kernel and the oracle, same OpCount, for HB-CSF and standalone CSL."""
+    dims = (60, 5000, 4000)
+    per = nnz // 60  # distinct j within a slice: every fiber is a singleton (CSL)
+    i = np.repeat(np.arange(60), per)
+    j = np.concatenate([rng.choice(5000, per, replace=False) for _ in range(60)])
+    k = rng.integers(0, 4000, 60 * per)
+    idx = np.stack([i, j, k], 1).astype(np.uint32)
+    idx, vals = P.canonical(idx, rng.uniform(0.1, 1.0, 60 * per))
+    t = hb.CooTensor(dims, idx, vals)
+    f = [rng.random((d, 32)).astype(np.float32).astype(np.float64) for d in dims]
+    ref = loops.mttkrp_entries(idx, vals, dims, f, 0)
+    outs = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("HBK_CSL_AS_CSF", flag)
+        h = hb.build_hbcsf(t, (0, 1, 2))  # fresh rep: plans are cached per rep
+        assert h.csl_part.nnz > 0
+        y, ops = hb.mttkrp_hbcsf(h, f, 0)
+        y2, ops2 = hb.mttkrp_csl(h.csl_part, f, 0)
+        assert row_dev(y, ref) <= TOL
+        outs[flag] = (y, (ops.muls, ops.adds), y2, (ops2.muls, ops2.adds))
+    assert row_dev(outs["1"][0], outs["0"][0]) <= 1e-5
+    assert row_dev(outs["1"][2], outs["0"][2]) <= 1e-5
+    assert outs["1"][1] == outs["0"][1] and outs["1"][3] == outs["0"][3]
