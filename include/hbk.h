@@ -235,6 +235,9 @@ void hbk_plan_release(hbk_plan* p);
  * output).  Its time is the row-gather ceiling of this plan on this GPU;
  * info.gather_rows / time = rows per second.  B-position plans only. */
 int hbk_plan_probe(const hbk_plan* p, const float* const* factors, void* stream);
+/* cudaStreamSynchronize on the caller's stream (the host calling convention
+ * waits for its result copy without a Python-level stream object).        */
+int hbk_stream_synchronize(void* stream);
 /* The output rows a plan's buckets own (rows the MTTKRP can make nonzero),
  * ascending.  *count = their number; rows [dev] u32 (capacity >= *count) or
  * NULL to only count.  Synchronises the stream (the count comes back).      */

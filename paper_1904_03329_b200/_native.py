@@ -135,6 +135,7 @@ _SIGS = {
     "hbk_plan_probe": ([vp, vp, vp], C.c_int),
     "hbk_nonfinite_f32": ([vp, vp, C.c_int, vp, vp], C.c_int),
     "hbk_plan_rows": ([vp, vp, C.POINTER(C.c_int64), vp], C.c_int),
+    "hbk_stream_synchronize": ([vp], C.c_int),
     "hbk_plan_execute_ex": ([vp, vp, vp, C.c_int, vp], C.c_int),
     "hbk_als_update_rows": ([vp, vp, C.c_int64, C.c_int, vp, vp, vp, vp, vp, vp], C.c_int),
     "hbk_tns_parse": ([C.c_char_p, i64, C.c_int, vp, C.c_int, C.POINTER(vp)], C.c_int),
@@ -221,7 +222,13 @@ def require_device():
 
 
 def stream_ptr():
+    """cudaStream_t of torch's current stream on the current device (the
+    raw-stream accessor: torch.cuda.current_stream() costs ~15 us of Python
+    per call, a measurable share of a small host-array MTTKRP call)."""
     torch = require_device()
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return C.c_void_p(raw(torch._C._cuda_getDevice()))
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 

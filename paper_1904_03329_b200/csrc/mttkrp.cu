@@ -2446,6 +2446,10 @@ __global__ void __launch_bounds__(256) k_nonfinite(const __grid_constant__ Finit
 }
 }  // namespace hbk
 
+int hbk_stream_synchronize(void* stream) {
+  return guarded([&] { HBK_CUDA(cudaStreamSynchronize(to_stream(stream))); });
+}
+
 int hbk_plan_rows(const hbk_plan* p, uint32_t* rows_out, int64_t* count, void* stream) {
   return guarded([&] {
     HBK_REQUIRE(p && count, HBK_EINVAL, "null pointer");

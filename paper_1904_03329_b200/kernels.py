@@ -209,7 +209,7 @@ class _HostStage:
                 if n:
                     host.copy_(y if y.dtype == torch.float64 else y.to(torch.float64),
                                non_blocking=True)
-                torch.cuda.current_stream().synchronize()
+                N.call("hbk_stream_synchronize", N.stream_ptr())
                 out = host.numpy()
             else:
                 out = np.empty(tuple(y.shape), dtype=np.float64)
@@ -217,7 +217,7 @@ class _HostStage:
                 width = n // max(1, rows)
                 buf = self._pinned(torch, ("out",), n, y.dtype)
                 buf[:n].view(y.shape).copy_(y, non_blocking=True)
-                torch.cuda.current_stream().synchronize()
+                N.call("hbk_stream_synchronize", N.stream_ptr())
                 src = buf.numpy()[:n].reshape(rows, width)
                 dst = out.reshape(rows, width)
                 step = max(1, (2 << 20) // max(1, width * 8))
