@@ -1691,7 +1691,13 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   if (const char* e = getenv("HBK_TASK_NNZ")) task_nnz = std::max(8, atoi(e));
   if (const char* e = getenv("HBK_CSF_VARIANT")) p->csf_variant = atoi(e);
   const uint32_t Tcsf = p->fast ? task_nnz : GEN_TASK_NNZ;
-  const uint32_t Tcsl = p->fast ? TASK_NNZ_CSL : GEN_TASK_NNZ;
+  // CSL runs: 256 nonzeros when the CSL slices average >= 48 (delicious-3d
+  // mode 2, 56 per slice: -5%), else 128 (flickr / nell-1, 4-36 per slice)
+  uint32_t Tcsl = GEN_TASK_NNZ;
+  if (p->fast) {
+    Tcsl = (p->csl && p->csl->S && p->csl->M >= 48 * p->csl->S) ? 2 * TASK_NNZ_CSL : TASK_NNZ_CSL;
+    if (const char* e = getenv("HBK_TASK_NNZ_CSL")) Tcsl = uint32_t(std::max(8, atoi(e)));
+  }
   const uint32_t Tcoo = p->fast ? TASK_NNZ_COO : GEN_TASK_NNZ;
 
   Work& w = p->work;
