@@ -1698,7 +1698,11 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     Tcsl = (p->csl && p->csl->S && p->csl->M >= 48 * p->csl->S) ? 2 * TASK_NNZ_CSL : TASK_NNZ_CSL;
     if (const char* e = getenv("HBK_TASK_NNZ_CSL")) Tcsl = uint32_t(std::max(8, atoi(e)));
   }
-  const uint32_t Tcoo = p->fast ? TASK_NNZ_COO : GEN_TASK_NNZ;
+  uint32_t Tcoo = p->fast ? TASK_NNZ_COO : GEN_TASK_NNZ;
+  if (const char* e = getenv("HBK_TASK_NNZ_COO"))
+    if (p->fast) Tcoo = uint32_t(std::max(8, atoi(e)));
+  uint32_t Tzero = TASK_ROWS_ZERO;
+  if (const char* e = getenv("HBK_TASK_ROWS_ZERO")) Tzero = uint32_t(std::max(8, atoi(e)));
 
   Work& w = p->work;
   std::memset(&w, 0, sizeof(w));
@@ -1958,7 +1962,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
                                                            p->zero_rows.as<uint32_t>());
       check_launch("k_unmarked_emit");
     }
-    n_zero = (Z + TASK_ROWS_ZERO - 1) / TASK_ROWS_ZERO;
+    n_zero = (Z + Tzero - 1) / Tzero;
     w.zero_rows = p->zero_rows.as<uint32_t>();
     p->info.tasks_zero = n_zero;
     // assemble [CSF | CSL | COO | ZERO], each padded to a multiple of gpw
@@ -1984,7 +1988,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       }
       if (n_zero) {
         k_range_tasks<<<grid_for(n_zero, 256), 256, 0, st>>>(T + a0 + a1 + a2, n_zero, Z,
-                                                             TASK_ROWS_ZERO);
+                                                             Tzero);
         check_launch("k_range_tasks");
       }
       wo.n0 = uint32_t(a0);
