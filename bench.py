@@ -1,21 +1,31 @@
 """HB-CSF MTTKRP benchmark (BASELINE.json metric: GFLOP/s on the 3·nnz·R basis,
-R=32, and % of the HBM roofline).
+R=32, and % of the HBM roofline, at 1/2/4/8 B200 vs the host CPU).
 
 A step = one HB-CSF MTTKRP per mode (all three modes) of the configuration's
 tensor, inputs resident in HBM.  Default workload: BASELINE.json configs[1]
-(nell-2-shaped synthetic, 76.9M nnz, all 3 modes on 1 B200).
+(nell-2-shaped, 76.9M nnz, all 3 modes on 1 B200) at N=1, configs[2]
+(flickr-3d-shaped, 112.9M nnz) at N>1 — the metric's multi-GPU configuration.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config nell-2|flickr-3d|delicious-3d|nell-1|config1] [--scale S]
+                    [--also C1,C2] [--cpd nell-1|none]
 
-N>1 is launched by torchrun: output slices of each mode are sharded across
-ranks by nonzero count (no collective in the timed region); time = max over
-ranks; value = all ranks' flops / that time.
+N>1: launched by torchrun (one rank per GPU, NCCL) — or, when WORLD_SIZE is
+unset, bench.py launches torchrun itself.  Each mode's output slices are
+sharded across ranks by nonzero count (contiguous row ranges; no collective
+in the timed region); time = max over ranks; value = all ranks' flops / that
+time.  ``with_output_allgather`` repeats the steps with the all-gather of
+every mode's output rows.  ``cpd``: the config-5 CP-ALS sweep (nell-1,
+MTTKRP of all modes + row update + factor-row exchange) on the same N ranks.
+``also``: further configurations measured the same way (1 GPU: flickr-3d and
+delicious-3d, the metric's other configurations).
 
-``--impl reference`` times the reference algorithm on the host CPU (the
-oracle port, oracle/tenkit_port.py, with all host threads through its
-scheduled path, as ``tenkit mttkrp --threads N``) on a bounded slice sample of
-the same tensor; rank 0 alone prints it.
+``--impl reference`` times the reference algorithm on the host CPU: the
+restated reference (oracle/tenkit_port.py) on a stratified whole-slice
+sample of the same tensor, with all host threads through its scheduled path
+(``tenkit mttkrp --threads N``, cli.py:256-266) and single-threaded.  The
+input comes from oracle/gen_torch.py (pure torch, bit-identical to the
+product generator); libhbk is never loaded on that arm.  Rank 0 alone runs it.
 """
 from __future__ import annotations
 
@@ -36,6 +46,7 @@ sys.path.insert(0, str(ROOT))
 
 RANK = 32
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+METRIC = "MTTKRP GFLOP/s (3*nnz*R, R=32)"
 
 
 def parse_args():
@@ -44,7 +55,7 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="nell-2")
+    ap.add_argument("--config", default=None, help="default: nell-2 at N=1, flickr-3d at N>1")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     # the format comparison of the paper (cpd.py:141-149
@@ -52,8 +63,23 @@ def parse_args():
     # coo = the whole tensor as a coordinate list
     ap.add_argument("--format", default="hbcsf", choices=["hbcsf", "bcsf", "csf", "coo"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample-nnz", type=int, default=300_000)
-    return ap.parse_args()
+    ap.add_argument("--cpu-sample-nnz", type=int, default=1_000_000,
+                    help="nonzeros per mode in the CPU baseline's stratified slice sample")
+    ap.add_argument("--also", default=None,
+                    help="comma list of extra configs (default: flickr-3d,delicious-3d at N=1, none at N>1)")
+    ap.add_argument("--cpd", default="nell-1", help="CP-ALS sweep config, or 'none'")
+    ap.add_argument("--cpd-iters", type=int, default=5)
+    a = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    n = max(world, a.gpus)
+    if a.config is None:
+        a.config = "nell-2" if n == 1 else "flickr-3d"
+    if a.also is None:
+        a.also = "flickr-3d,delicious-3d" if n == 1 and a.scale == 1.0 else ""
+    a.also = [c for c in a.also.split(",") if c and c != a.config]
+    if a.cpd == "none":
+        a.cpd = None
+    return a
 
 
 def peaks():
@@ -63,6 +89,18 @@ def peaks():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
     except Exception:
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def host_cpu():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
 
 
 class Clocks:
@@ -149,409 +187,619 @@ def b_comp(c, dims, mode, r=RANK):
     return stream + factors + out
 
 
-def dist_env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
-
-
 def make_factors(dims, seed):
     rng = np.random.default_rng(seed)  # cli.py:274-276 convention
     return [rng.random((d, RANK)) for d in dims]
 
 
-def cpu_sample(t, dims, mode, target_nnz):
-    """Every K-th slice of `mode` (whole slices, so the per-slice structure is
-    the workload's), exported to the host for the CPU oracle."""
-    import ctypes as C
-
-    import torch
-
-    from paper_1904_03329_b200 import _native as N
-
-    idx = torch.empty((t.nnz, t.order), dtype=torch.int32, device="cuda")
-    vals = torch.empty(t.nnz, dtype=torch.float64, device="cuda")
-    N.call("hbk_coo_export_device", t._dev().ptr, C.c_void_p(idx.data_ptr()),
-           C.c_void_p(vals.data_ptr()), None, N.stream_ptr())
-    k = max(1, int(round(t.nnz / max(1, target_nnz))))
-    keep = (idx[:, mode] % k) == 0
-    si = idx[keep].cpu().numpy().view(np.uint32)
-    sv = vals[keep].cpu().numpy()
-    del idx, vals
-    return si, sv, k
-
-
-def time_oracle(si, sv, dims, mode, factors, threads, runs=3):
+# ------------------------------------------------------------------ CPU legs
+def time_oracle(si, sv, dims, mode, factors, threads, runs=3, warm=True):
+    """Median seconds of the restated reference's mttkrp_hbcsf over the
+    sample (cli.py:220-228 protocol: warm-up, then the median of ``runs``),
+    split τ=128; threads > 1 runs the scheduled path (cli.py:256-266)."""
     from oracle import tenkit_port as P
 
     mo = P.allmode_order(dims, mode)
     h = P.split_hbcsf(P.hbcsf(si, sv, dims, mo), 128)
-    units = None
-    if threads > 1:
-        units, _ = P.block_schedule(h["csf"], 512)
-    P.mttkrp_hbcsf(h, factors, mode, units=units, threads=threads)  # warm-up (cli.py:220-228)
+    units = P.block_schedule(h["csf"], 512)[0] if threads > 1 else None
+    y = None
+    if warm:
+        y, _ = P.mttkrp_hbcsf(h, factors, mode, units=units, threads=threads)
     ts = []
     for _ in range(runs):
         tic = time.perf_counter()
-        P.mttkrp_hbcsf(h, factors, mode, units=units, threads=threads)
+        y, _ = P.mttkrp_hbcsf(h, factors, mode, units=units, threads=threads)
         ts.append(time.perf_counter() - tic)
-    return statistics.median(ts), len(sv)
+    return statistics.median(ts), len(sv), h, y
+
+
+def sample_rows(hist, target, mode):
+    from oracle.shard_parity import stratified_slices
+
+    return stratified_slices(hist, target, seed=101 + mode)
+
+
+def sample_desc(samples, target):
+    return (f"stratified whole-slice sample per mode (every K-th slice by nnz rank, slices above "
+            f"{target // 4} nnz excluded; target {target} nnz/mode): "
+            f"{[int(s['slices']) for s in samples]} slices, {[int(s['nnz']) for s in samples]} nnz, "
+            f"largest sampled slice {[int(s['max_slice']) for s in samples]} nnz")
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference algorithm on the host CPU cores."""
-    import torch
-
+    """--impl reference: the reference algorithm on the host CPU cores.  No
+    libhbk: the tensor comes from the pure-torch generator restatement."""
     if rank != 0:
         return
-    from paper_1904_03329_b200.generate import CONFIGS, config_tensor
+    import torch
+
+    from oracle import gen_torch as G
 
     torch.cuda.set_device(0)
-    cfg = CONFIGS[args.config]
+    cfg = G.CONFIGS[args.config]
     dims = cfg["dims"]
-    t = config_tensor(args.config, scale=args.scale)
+    idx, vals = G.config_tensor(args.config, scale=args.scale)
+    nnz = int(idx.shape[0])
     factors = make_factors(dims, cfg["seed"])
+    f_oracle = [f.astype(np.float32).astype(np.float64) for f in factors]
+    samples = []
+    for m in range(len(dims)):
+        hist = G.slice_histogram(idx, m, dims[m])
+        rows = sample_rows(hist, args.cpu_sample_nnz, m)
+        si, sv = G.host_shard(idx, vals, m, rows)
+        samples.append({"si": si, "sv": sv, "slices": len(rows), "nnz": len(sv),
+                        "max_slice": int(hist[rows].max()) if len(rows) else 0})
+    del idx, vals
+    torch.cuda.empty_cache()
     threads = os.cpu_count() or 1
-    samples = [cpu_sample(t, dims, m, args.cpu_sample_nnz) for m in range(len(dims))]
-    steps = []
-    for s in range(args.warmup + args.steps):
+
+    def step(th):
         flops = secs = 0.0
-        for m, (si, sv, _) in enumerate(samples):
-            sec, m_nnz = time_oracle(si, sv, dims, m, factors, threads, runs=1)
+        for m, s in enumerate(samples):
+            sec, m_nnz, _, _ = time_oracle(s["si"], s["sv"], dims, m, f_oracle, th, runs=1, warm=False)
             flops += 3.0 * m_nnz * RANK
             secs += sec
+        return flops / secs / 1e9, secs
+
+    vals_n, secs_n = [], []
+    for s in range(args.warmup + args.steps):
+        v, sec = step(threads)
         if s >= args.warmup:
-            steps.append(flops / secs / 1e9)
-    value = statistics.median(steps)
-    sample_desc = (f"every K-th output slice per mode (K={[s[2] for s in samples]}, "
-                   f"{[len(s[1]) for s in samples]} nnz), split tau=128, schedule block 512")
+            vals_n.append(v)
+            secs_n.append(sec)
+    v1, _ = step(1)  # the single-thread variant (tenkit mttkrp --format hbcsf defaults)
+    value = statistics.median(vals_n)
+    desc = sample_desc(samples, args.cpu_sample_nnz)
     line = {
-        "impl": "reference", "metric": "MTTKRP GFLOP/s (3*nnz*R, R=32)", "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (SURVEY Appendix A power-law generator)",
+        "ms_per_step": statistics.median(secs_n) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (SURVEY Appendix A power-law generator; oracle/gen_torch.py)",
         "config": {"workload": f"{args.config}-shaped HB-CSF MTTKRP, all {len(dims)} modes per step, R=32",
-                   "dims": list(dims), "nnz": t.nnz, "rank": RANK, "scale": args.scale,
+                   "dims": list(dims), "nnz": nnz, "rank": RANK, "scale": args.scale,
                    "split": {"fiber_threshold": 128, "block_size": 512},
                    "parallelism": "host CPU (rank 0)"},
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "port",
-                         "sample": sample_desc},
+                         "sample": desc + f"; oracle mttkrp_hbcsf threads={threads}, scheduled "
+                                          "(assign_slice_blocks, block 512) as `tenkit mttkrp --threads N`",
+                         "threads1_value": v1, "host": host_cpu(),
+                         "ms_per_step_note": "ms_per_step = CPU seconds for the sample, not the full tensor"},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "native_libraries": "none (libhbk not loaded on this arm)",
     }
+    assert not any("libhbk" in l for l in open("/proc/self/maps")), "libhbk mapped on the reference arm"
     print(json.dumps(line), flush=True)
 
 
-def main():
-    args = parse_args()
-    world, rank, local = dist_env()
-    if args.impl == "reference":
-        run_reference(args, world, rank)
-        return
-    import torch
-    import torch.distributed as dist
+# -------------------------------------------------------------- GPU timing
+class Env:
+    """Process-group plumbing for one or many ranks."""
 
-    # HBK_BENCH_BACKEND=gloo runs the N>1 path on fewer GPUs than ranks (ranks
-    # share devices round-robin) to validate the sharded leg on one GPU; the
-    # measured configuration is one rank per GPU over NCCL.
-    backend = os.environ.get("HBK_BENCH_BACKEND", "nccl")
-    local = local % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(local)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
 
+        self.torch, self.dist = torch, dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # HBK_BENCH_BACKEND=gloo runs the N>1 path on fewer GPUs than ranks
+        # (ranks share devices round-robin) — a validation mode, flagged in
+        # the line; the measured configuration is one rank per GPU over NCCL
+        self.backend = os.environ.get("HBK_BENCH_BACKEND", "nccl")
+        self.device = self.local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(self.device)
+        self.ranks = None
+        if self.world > 1:
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.device))
+            else:
+                dist.init_process_group(self.backend)
+            props = torch.cuda.get_device_properties(self.device)
+            me = {"rank": self.rank, "device": self.device, "name": props.name,
+                  "pci_bus_id": getattr(props, "pci_bus_id", None), "host": os.uname().nodename}
+            allr = [None] * self.world
+            dist.all_gather_object(allr, me)
+            self.ranks = allr
+            print(f"[bench] rank {self.rank}/{self.world} on cuda:{self.device} backend={self.backend} "
+                  f"comm size={dist.get_world_size()}", file=sys.stderr, flush=True)
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+
+def prepare(env, name, args, fmt="hbcsf"):
+    """Generate the config tensor, cut this rank's row shard of every mode and
+    build its representation + plan (preprocessing, reported separately like
+    cli.py preprocessing_seconds)."""
+    torch = env.torch
     import paper_1904_03329_b200 as hb
-    from paper_1904_03329_b200 import kernels as K
     from paper_1904_03329_b200 import shard
     from paper_1904_03329_b200.generate import CONFIGS, config_tensor
     from paper_1904_03329_b200.kernels import _device_factors, plan_for
 
-    cfg = CONFIGS[args.config]
+    cfg = CONFIGS[name]
     dims = cfg["dims"]
     t0 = time.perf_counter()
-    t = config_tensor(args.config, scale=args.scale)
+    t = config_tensor(name, scale=args.scale)
     torch.cuda.synchronize()
     gen_s = time.perf_counter() - t0
-    nnz_total = t.nnz
-
-    # preprocessing (reported separately, like cli.py preprocessing_seconds)
     t0 = time.perf_counter()
     split_cfg = hb.SplitConfig()
-    reps, censuses, plans, ranges, all_ranges = [], [], [], [], []
+    st = {"name": name, "dims": dims, "t": t, "nnz": t.nnz, "reps": [], "census": [], "plans": [],
+          "ranges": [], "all_ranges": [], "gen_s": gen_s}
     for mode in range(len(dims)):
         mo = hb.allmode_order(dims, mode)
-        if world > 1:
+        if env.world > 1:
             # this rank's output rows, rebased: its plan writes only them
-            ranges_m = shard.plan_row_ranges(shard.slice_histogram(t, mode).cpu().numpy(), world)
-            all_ranges.append(ranges_m)
-            rr = ranges_m[rank]
+            ranges_m = shard.plan_row_ranges(shard.slice_histogram(t, mode).cpu().numpy(), env.world)
+            st["all_ranges"].append(ranges_m)
+            rr = ranges_m[env.rank]
             part = shard.shard_rows(t, mode, rr[0], rr[1]) if rr[1] > rr[0] else None
         else:
             rr, part = (0, dims[mode]), t
+        st["ranges"].append(rr)
         if part is None:  # more ranks than non-empty row ranges
-            reps.append(None)
-            ranges.append(rr)
-            censuses.append(None)
-            plans.append(None)
+            st["reps"].append(None)
+            st["census"].append(None)
+            st["plans"].append(None)
             continue
-        if args.format == "hbcsf":
+        if fmt == "hbcsf":
             h = hb.split_fibers(hb.build_hbcsf(part, mo), split_cfg)
-        elif args.format == "bcsf":
+        elif fmt == "bcsf":
             h = hb.split_fibers(hb.build_csf(part, mo), split_cfg)
-        elif args.format == "csf":
+        elif fmt == "csf":
             h = hb.build_csf(part, mo)
         else:
             h = part
-        reps.append(h)
-        ranges.append(rr)
-        censuses.append(census_of(h))
-        plans.append(plan_for(h, mode, RANK))
+        st["reps"].append(h)
+        st["census"].append(census_of(h))
+        st["plans"].append(plan_for(h, mode, RANK))
     torch.cuda.synchronize()
-    prep_s = time.perf_counter() - t0
+    st["prep_s"] = time.perf_counter() - t0
+    st["f64"] = make_factors(dims, cfg["seed"])
+    st["f_dev"] = [torch.from_numpy(f).float().cuda() for f in st["f64"]]
+    st["rows_local"] = [hi - lo for lo, hi in st["ranges"]]
+    st["outs"] = [torch.empty((max(1, st["rows_local"][m]), RANK), dtype=torch.float32, device="cuda")
+                  for m in range(len(dims))]
+    st["ptrs"] = [_device_factors(st["f_dev"], m)[0] for m in range(len(dims))]
+    return st
 
-    f64 = make_factors(dims, cfg["seed"])
-    f_dev = [torch.from_numpy(f).float().cuda() for f in f64]
-    rows_local = [hi - lo for lo, hi in ranges]
-    outs = [torch.empty((max(1, rows_local[m]), RANK), dtype=torch.float32, device="cuda")
-            for m in range(len(dims))]
-    ptrs = [_device_factors(f_dev, m)[0] for m in range(len(dims))]
+
+def time_steps(env, st, args, clocks=False):
+    """W warm-up steps, then K timed steps bracketed by barrier + synchronize,
+    CUDA events on the launch stream (per mode and whole), max over ranks."""
+    torch = env.torch
+    n_modes = len(st["dims"])
     stream = torch.cuda.current_stream()
+    plans, ptrs, outs = st["plans"], st["ptrs"], st["outs"]
 
     def run_mode(m):
         if plans[m] is not None:
             plans[m].execute(ptrs[m], outs[m])
 
-    def step():
-        for m in range(len(dims)):
-            run_mode(m)
-
     for _ in range(args.warmup):
-        step()
+        for m in range(n_modes):
+            run_mode(m)
     torch.cuda.synchronize()
-
-    n_modes = len(dims)
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)] for _ in range(n_modes)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
+    env.barrier()
     torch.cuda.synchronize()
-    with Clocks(local) as clk:
-        start.record(stream)
-        for s in range(args.steps):
-            for m in range(n_modes):
-                ev[m][s][0].record(stream)
-                run_mode(m)
-                ev[m][s][1].record(stream)
-        stop.record(stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    elapsed_ms = start.elapsed_time(stop)
+    clk = Clocks(env.device) if clocks else None
+    if clk:
+        clk.__enter__()
+    start.record(stream)
+    for s in range(args.steps):
+        for m in range(n_modes):
+            ev[m][s][0].record(stream)
+            run_mode(m)
+            ev[m][s][1].record(stream)
+    stop.record(stream)
+    torch.cuda.synchronize()
+    if clk:
+        clk.__exit__(None, None, None)
+    env.barrier()
+    elapsed_ms = env.max(start.elapsed_time(stop))
     per_mode_ms = [statistics.mean(a.elapsed_time(b) for a, b in ev[m]) for m in range(n_modes)]
-    if world > 1:
-        tt = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(tt.item())
     ms_per_step = elapsed_ms / args.steps
-    flops_step = 3.0 * nnz_total * RANK * n_modes
-    value = flops_step / (ms_per_step * 1e-3) / 1e9
+    flops_step = 3.0 * st["nnz"] * RANK * n_modes
+    res = {"ms_per_step": ms_per_step, "value": flops_step / (ms_per_step * 1e-3) / 1e9,
+           "per_mode_ms": per_mode_ms, "flops_step": flops_step}
+    if clk:
+        res["clocks"] = clk.summary()
+    return res
 
-    # N > 1: the same steps followed by the replication of every mode's output
-    # rows on all ranks (all-gather over NCCL) — the standalone MTTKRP with
-    # and without the output exchange (SURVEY §8e)
-    with_ag = None
-    if world > 1:
-        from paper_1904_03329_b200.distributed import allgather_padded
 
-        def step_ag():
-            for m in range(n_modes):
-                run_mode(m)
-                rows_m = outs[m][: rows_local[m]]
-                allgather_padded(torch, dist, rows_m, all_ranges[m])
-
-        for _ in range(max(1, args.warmup)):
-            step_ag()
-        torch.cuda.synchronize()
-        dist.barrier()
-        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a_ev.record(stream)
-        for _ in range(args.steps):
-            step_ag()
-        b_ev.record(stream)
-        torch.cuda.synchronize()
-        tt = torch.tensor([a_ev.elapsed_time(b_ev) / args.steps], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ag_ms = float(tt.item())
-        with_ag = {"ms_per_step": ag_ms, "value": flops_step / (ag_ms * 1e-3) / 1e9,
-                   "unit": "GFLOP/s",
-                   "gathered_bytes_per_step": sum(4 * RANK * d for d in dims),
-                   "note": "each step + all_gather of every mode's output rows to every rank"}
-
-    # gather ceiling: the plans' gather-only calibration kernels over the same
-    # task lists and streams (hbk_plan_probe), timed the same way
-    gather = None
-    try:
-        rows = [int(pl.info.gather_rows) if pl is not None else 0 for pl in plans]
-        if all(r > 0 for r, pl in zip(rows, plans) if pl is not None):
-            pev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                    for _ in range(args.steps)] for _ in range(n_modes)]
-            for m in range(n_modes):
-                if plans[m] is not None:
-                    plans[m].probe(ptrs[m])
-            torch.cuda.synchronize()
-            for s_ in range(args.steps):
-                for m in range(n_modes):
-                    if plans[m] is None:
-                        continue
-                    pev[m][s_][0].record(stream)
-                    plans[m].probe(ptrs[m])
-                    pev[m][s_][1].record(stream)
-            torch.cuda.synchronize()
-            probe_ms = [statistics.mean(a.elapsed_time(b) for a, b in pev[m]) if plans[m] is not None
-                        else 0.0 for m in range(n_modes)]
-            gather = {
-                "rows_per_step": sum(rows),
-                "kernel_rows_per_s": sum(rows) / (sum(per_mode_ms) * 1e-3),
-                "ceiling_rows_per_s": sum(rows) / (sum(probe_ms) * 1e-3),
-                "frac": sum(probe_ms) / sum(per_mode_ms),
-                "probe_ms_per_mode": probe_ms,
-                "note": ("128-byte factor rows delivered to the SMs (leaf rows + fiber rows, 2 per "
-                         "CSL/COO nonzero); ceiling = gather-only kernel over the same tasks "
-                         "(hbk_plan_probe)"),
-            }
-    except Exception as e:  # calibration is optional; never fail the bench on it
-        gather = {"error": str(e)}
-
-    # roofline over the per-mode launches (each step is one launch per mode)
+def roofline_of(st, per_mode_ms):
     hbm, hbm_src = peaks()
-    # this rank's launches: its own output rows, every input factor row
+    dims = st["dims"]
     bytes_modes = []
-    for m in range(n_modes):
-        if censuses[m] is None:
+    for m in range(len(dims)):
+        if st["census"][m] is None:
             bytes_modes.append(0)
             continue
         dl = list(dims)
-        dl[m] = rows_local[m]
-        bytes_modes.append(b_comp(censuses[m], dl, m))
+        dl[m] = st["rows_local"][m]  # this rank's output rows, every input factor row
+        bytes_modes.append(b_comp(st["census"][m], dl, m))
     achieved = sum(bytes_modes) / (sum(per_mode_ms) * 1e-3) / 1e9
-    # DRAM bytes per launch from the committed ncu capture of this workload
-    # (profiles/ncu_summary.json, written by scripts/make_profile_summary.py)
-    traffic = None
+    return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "peak_source": hbm_src, "frac_of_nominal_8tbs": achieved / 8000.0,
+            "algorithmic_bytes_per_step": sum(bytes_modes),
+            "algorithmic_bytes_per_launch": sum(bytes_modes) / len(dims),
+            "per_mode_ms": per_mode_ms, "per_mode_bytes": bytes_modes,
+            "per_mode_frac": [b / (ms * 1e-3) / 1e9 / hbm if ms else 0.0
+                              for b, ms in zip(bytes_modes, per_mode_ms)],
+            "launches_per_mode": [int(pl.info.launches) if pl is not None else 0 for pl in st["plans"]]}
+
+
+def ncu_traffic(name, args):
+    """DRAM bytes per launch and L2 hit rate from the committed ncu capture of
+    this workload (profiles/ncu_summary.json, scripts/make_profile_summary.py)."""
     prof = ROOT / "profiles" / "ncu_summary.json"
-    if prof.exists() and args.scale == 1.0:
-        try:
-            per = json.loads(prof.read_text()).get(args.config, {}).get("dram_bytes_per_launch")
-            traffic = statistics.mean(per) if per else None
-        except Exception:
-            traffic = None
+    if not prof.exists() or args.scale != 1.0:
+        return None, None
+    try:
+        d = json.loads(prof.read_text()).get(name, {})
+        per = d.get("dram_bytes_per_launch")
+        return (statistics.mean(per) if per else None), d.get("l2_hit_rate_pct")
+    except Exception:
+        return None, None
 
-    # end to end through the public API with host buffers: pinned fp32
-    # factors in, NumPy float64 rows out, one mttkrp_hbcsf per mode per step
-    # (each rank: its own row shard); wall clock, max over ranks
-    e2e = None
-    if not args.no_e2e:
-        f_pin = [torch.from_numpy(f).float().pin_memory() for f in f64]
 
+def gather_ceiling(env, st, args, per_mode_ms):
+    """Gather-only calibration kernels over the plans' task lists and streams
+    (hbk_plan_probe), timed the same way."""
+    torch = env.torch
+    plans, ptrs = st["plans"], st["ptrs"]
+    n_modes = len(plans)
+    stream = torch.cuda.current_stream()
+    try:
+        rows = [int(pl.info.gather_rows) if pl is not None else 0 for pl in plans]
+        pev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(args.steps)] for _ in range(n_modes)]
+        for m in range(n_modes):
+            if plans[m] is not None:
+                plans[m].probe(ptrs[m])
+        torch.cuda.synchronize()
+        for s_ in range(args.steps):
+            for m in range(n_modes):
+                if plans[m] is None:
+                    continue
+                pev[m][s_][0].record(stream)
+                plans[m].probe(ptrs[m])
+                pev[m][s_][1].record(stream)
+        torch.cuda.synchronize()
+        probe_ms = [statistics.mean(a.elapsed_time(b) for a, b in pev[m]) if plans[m] is not None
+                    else 0.0 for m in range(n_modes)]
+        return {
+            "rows_per_step": sum(rows),
+            "kernel_rows_per_s": sum(rows) / (sum(per_mode_ms) * 1e-3),
+            "ceiling_rows_per_s": sum(rows) / (sum(probe_ms) * 1e-3),
+            "frac": sum(probe_ms) / sum(per_mode_ms),
+            "probe_ms_per_mode": probe_ms,
+            "note": ("128-byte factor rows delivered to the SMs (leaf rows + fiber rows, 2 per "
+                     "CSL/COO nonzero); ceiling = gather-only kernel over the same tasks "
+                     "(hbk_plan_probe)"),
+        }
+    except Exception as e:  # calibration is optional; never fail the bench on it
+        return {"error": str(e)}
+
+
+def with_allgather(env, st, args, flops_step):
+    """N > 1: the same steps followed by the replication of every mode's
+    output rows on all ranks (all-gather over NCCL) — the standalone MTTKRP
+    with and without the output exchange."""
+    torch, dist = env.torch, env.dist
+    from paper_1904_03329_b200.distributed import allgather_padded
+
+    n_modes = len(st["dims"])
+    stream = torch.cuda.current_stream()
+
+    def step_ag():
+        for m in range(n_modes):
+            if st["plans"][m] is not None:
+                st["plans"][m].execute(st["ptrs"][m], st["outs"][m])
+            allgather_padded(torch, dist, st["outs"][m][: st["rows_local"][m]], st["all_ranges"][m])
+
+    for _ in range(max(1, args.warmup)):
+        step_ag()
+    torch.cuda.synchronize()
+    env.barrier()
+    a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a_ev.record(stream)
+    for _ in range(args.steps):
+        step_ag()
+    b_ev.record(stream)
+    torch.cuda.synchronize()
+    ag_ms = env.max(a_ev.elapsed_time(b_ev) / args.steps)
+    return {"ms_per_step": ag_ms, "value": flops_step / (ag_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+            "gathered_bytes_per_step": sum(4 * RANK * d for d in st["dims"]),
+            "note": "each step + all_gather of every mode's output rows to every rank"}
+
+
+def end_to_end(env, st, args, flops_step):
+    """The same metric through the public API with HOST buffers, in the
+    reference's calling convention: NumPy float64 factors in, NumPy float64
+    rows out (kernels.py:62-88 contract), one ``mttkrp`` call per mode per
+    step; the f64->f32 conversion, H2D, kernel, D2H and widening are inside
+    the timed region (wall clock, max over ranks).  The same with page-locked
+    fp32 torch factors is reported beside it."""
+    torch = env.torch
+    import paper_1904_03329_b200 as hb
+    from paper_1904_03329_b200 import kernels as K
+
+    n_modes = len(st["dims"])
+    reps, dims = st["reps"], st["dims"]
+
+    def timed(factors):
         def e2e_step():
             for m in range(n_modes):
                 if reps[m] is not None:
-                    hb.mttkrp(reps[m], f_pin, m)
+                    fs = list(factors)
+                    if env.world > 1:  # shard rep: its own (rebased) output rows
+                        fs[m] = factors[m][: st["rows_local"][m]]
+                    hb.mttkrp(reps[m], fs, m)
 
         e2e_step()
         torch.cuda.synchronize()
         k = max(3, min(args.steps, 10))
-        if world > 1:
-            dist.barrier()
+        env.barrier()
         tic = time.perf_counter()
         for _ in range(k):
             e2e_step()
-        e2e_s = (time.perf_counter() - tic) / k
-        if world > 1:
-            tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_s = float(tt.item())
-        h2d = sum(4 * RANK * sum(d for i, d in enumerate(dims) if i != m)
-                  for m in range(n_modes) if reps[m] is not None)
-        # rows come back as float64 when the output fits the pinned-return
-        # path (device widening), else as fp32 widened on the host
-        cap = K._HostStage.PINNED_OUT_BYTES
-        d2h = sum((8 if 8 * RANK * rows_local[m] <= cap else 4) * RANK * rows_local[m]
-                  for m in range(n_modes) if reps[m] is not None)
-        e2e = {"value": flops_step / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
-               "path": f"paper_1904_03329_b200.mttkrp({args.format} rep, pinned host fp32 factors) -> numpy f64 rows, "
-                       "one call per mode, H2D + kernel + D2H inside the timed region"
-                       + ("; bytes per rank, rank 0" if world > 1 else "")}
+        return env.max((time.perf_counter() - tic) / k)
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        samples = [cpu_sample(t, dims, m, args.cpu_sample_nnz) for m in range(n_modes)]
-        flops = secs = 0.0
-        for m, (si, sv, _) in enumerate(samples):
-            sec, m_nnz = time_oracle(si, sv, dims, m, f64, threads=1, runs=3)
-            flops += 3.0 * m_nnz * RANK
-            secs += sec
-        cpu = {"value": flops / secs / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "port",
-               "sample": (f"every K-th output slice per mode (K={[s[2] for s in samples]}, "
-                          f"{[len(s[1]) for s in samples]} nnz); oracle mttkrp_hbcsf threads=1, "
-                          "split tau=128, median of 3 after 1 warm-up")}
+    s64 = timed(st["f64"])
+    f_pin = [torch.from_numpy(f).float().pin_memory() for f in st["f64"]]
+    s32 = timed(f_pin)
+    h2d64 = sum(8 * RANK * sum(d for i, d in enumerate(dims) if i != m)
+                for m in range(n_modes) if reps[m] is not None)
+    cap = K._HostStage.PINNED_OUT_BYTES
+    d2h = sum((8 if 8 * RANK * st["rows_local"][m] <= cap else 4) * RANK * st["rows_local"][m]
+              for m in range(n_modes) if reps[m] is not None)
+    return {"value": flops_step / s64 / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d64 // 2,
+            "d2h_bytes_per_step": d2h, "ms_per_step": s64 * 1e3,
+            "host_input_bytes_per_step": h2d64,
+            "path": ("paper_1904_03329_b200.mttkrp(rep, NumPy float64 factors) -> NumPy float64 rows, "
+                     "one call per mode (f64->f32 staging, H2D, kernel, D2H inside the timed region; "
+                     "h2d bytes = the fp32 copies sent)" + ("; bytes per rank, rank 0" if env.world > 1 else "")),
+            "pinned_fp32": {"value": flops_step / s32 / 1e9, "ms_per_step": s32 * 1e3,
+                            "path": "same calls with page-locked fp32 torch factors"}}
 
-    if rank == 0:
+
+def cpu_leg(env, st, args):
+    """Rank 0, N=1: the restated reference on a stratified whole-slice sample
+    of the same tensor, one core; and the parity of the GPU's full-size
+    arrays and rows on that sample (oracle/shard_parity.py)."""
+    torch = env.torch
+    from oracle import shard_parity as S
+    from oracle import tenkit_port as P
+    from paper_1904_03329_b200 import shard
+
+    dims = st["dims"]
+    t = st["t"]
+    f_oracle = [f.astype(np.float32).astype(np.float64) for f in st["f64"]]
+    idx_all, val_all = t.indices, t.values
+    flops = secs = 0.0
+    samples, bit_exact, devs = [], [], []
+    for m in range(len(dims)):
+        hist = shard.slice_histogram(t, m).cpu().numpy()
+        rows = sample_rows(hist, args.cpu_sample_nnz, m)
+        si, sv = S.shard_entries(idx_all, val_all, m, rows)
+        sec, m_nnz, h_o, y_o = time_oracle(si, sv, dims, m, f_oracle, threads=1, runs=3)
+        flops += 3.0 * m_nnz * RANK
+        secs += sec
+        samples.append({"slices": len(rows), "nnz": m_nnz,
+                        "max_slice": int(hist[rows].max()) if len(rows) else 0})
+        rep = st["reps"][m]
+        if hasattr(rep, "coo_part"):
+            res = S.compare_hbcsf(S.gpu_arrays(rep), h_o, rows)
+            bit_exact.append(bool(all(res.values())))
+        st["plans"][m].execute(st["ptrs"][m], st["outs"][m])
+        y = st["outs"][m][torch.from_numpy(rows).cuda()].double().cpu().numpy()
+        devs.append(P.row_deviation(y, y_o[rows]))
+    cpu = {"value": flops / secs / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "port",
+           "sample": sample_desc(samples, args.cpu_sample_nnz)
+           + "; oracle mttkrp_hbcsf threads=1, split tau=128, median of 3 after 1 warm-up",
+           "host": host_cpu()}
+    parity = {"format_bit_exact": all(bit_exact) if bit_exact else None,
+              "max_row_dev": max(devs), "tolerance": 1e-4,
+              "metric": "max_i ||y_i - o_i|| / (1 + ||o_i||) (cli.py:231-234) on the sampled slices, "
+                        "GPU full-size rows vs the restated reference on the sample",
+              "format_arrays": "labels-implied buckets, CSL/COO/split-CSF ptr/idx/values of the sampled "
+                               "slices, restricted from the GPU's full-size build"}
+    return cpu, parity
+
+
+def measure_cpd(env, name, args):
+    """Config 5: CP-ALS sweeps (MTTKRP of every mode + fused row update +
+    factor-row exchange) on the same ranks; median sweep wall time after the
+    first (plans built), max over ranks."""
+    torch = env.torch
+    from paper_1904_03329_b200.cpd import cp_als
+    from paper_1904_03329_b200.distributed import cp_als_distributed
+    from paper_1904_03329_b200.generate import CONFIGS, config_tensor
+
+    if env.world > 1 and env.backend != "nccl":
+        return {"skipped": "CP-ALS exchange needs one GPU per rank over NCCL"}
+    cfg = CONFIGS[name]
+    t = config_tensor(name, scale=args.scale)
+    walls = []
+    tic = time.perf_counter()
+    if env.world > 1:
+        _, hist = cp_als_distributed(t, rank=RANK, max_iters=args.cpd_iters + 1, fit_tol=0.0,
+                                     seed=cfg["seed"], sweep_hook=lambda it, s: walls.append(s))
+    else:
+        _, hist = cp_als(t, rank=RANK, max_iters=args.cpd_iters + 1, fit_tol=0.0, seed=cfg["seed"],
+                         sweep_hook=lambda it, s: walls.append(s))
+    total = time.perf_counter() - tic
+    sweep = env.max(statistics.median(walls[1:]) if len(walls) > 1 else walls[0])
+    flops = 3 * 3.0 * t.nnz * RANK
+    out = {"workload": f"{name}-shaped CP-ALS sweep, R=32 (MTTKRP of all 3 modes + row update + "
+                       "factor-row exchange)", "nnz": t.nnz, "ms_per_sweep": sweep * 1e3,
+           "value": flops / sweep / 1e9, "unit": "GFLOP/s (MTTKRP-equivalent, 3 modes x 3*nnz*R per sweep)",
+           "sweeps_timed": max(1, len(walls) - 1), "fits": [h.fit for h in hist], "total_s": total,
+           "timing": "host wall clock per sweep (median after the first), max over ranks"}
+    del t
+    torch.cuda.empty_cache()
+    return out
+
+
+def free(st):
+    import torch
+
+    for k in list(st):
+        st[k] = None
+    torch.cuda.empty_cache()
+
+
+def run_ours(args):
+    env = Env()
+    torch = env.torch
+    st = prepare(env, args.config, args, args.format)
+    res = time_steps(env, st, args, clocks=True)
+    flops_step = res["flops_step"]
+    roof = roofline_of(st, res["per_mode_ms"])
+    traffic, l2hit = ncu_traffic(args.config, args)
+    mean_ms = statistics.mean(res["per_mode_ms"])
+    roof.update({"traffic": traffic, "l2_hit_rate_pct": l2hit,
+                 "traffic_gbs": traffic / (mean_ms * 1e-3) / 1e9 if traffic else None,
+                 "traffic_frac": traffic / (mean_ms * 1e-3) / 1e9 / roof["peak"] if traffic else None,
+                 "kernel": "k_mttkrp3_r32<kind> (one launch per non-empty bucket kind per mode)",
+                 "traffic_unit": "DRAM bytes per MTTKRP launch (ncu dram__bytes_read+write, profiles/)"})
+    roof["gather"] = gather_ceiling(env, st, args, res["per_mode_ms"])
+    with_ag = with_allgather(env, st, args, flops_step) if env.world > 1 else None
+    e2e = None if args.no_e2e else end_to_end(env, st, args, flops_step)
+    cpu = parity = None
+    if env.rank == 0 and env.world == 1 and not args.no_cpu_baseline:
+        cpu, parity = cpu_leg(env, st, args)
+    launches = args.steps * sum(int(pl.info.launches) for pl in st["plans"] if pl is not None)
+    census = st["census"]
+    header = {k: st[k] for k in ("dims", "nnz", "prep_s", "gen_s")}
+    free(st)
+
+    also = []
+    for name in args.also:
+        s2 = prepare(env, name, args, args.format)
+        r2 = time_steps(env, s2, args)
+        rf = roofline_of(s2, r2["per_mode_ms"])
+        tr, hit = ncu_traffic(name, args)
+        also.append({"config": name, "nnz": s2["nnz"], "value": r2["value"], "unit": "GFLOP/s",
+                     "ms_per_step": r2["ms_per_step"], "per_mode_ms": r2["per_mode_ms"],
+                     "roofline_frac": rf["frac"], "per_mode_frac": rf["per_mode_frac"],
+                     "algorithmic_bytes_per_step": rf["algorithmic_bytes_per_step"],
+                     "ncu_dram_bytes_per_launch": tr, "l2_hit_rate_pct": hit,
+                     "census": s2["census"] if env.world == 1 else None})
+        free(s2)
+    cpd = measure_cpd(env, args.cpd, args) if args.cpd else None
+
+    if env.rank == 0:
+        dims = header["dims"]
         line = {
-            "metric": "MTTKRP GFLOP/s (3*nnz*R, R=32)",
-            "value": value,
+            "metric": METRIC,
+            "value": res["value"],
             "unit": "GFLOP/s",
-            "n_gpus": world,
+            "n_gpus": env.world,
             "steps": args.steps,
             "warmup": args.warmup,
-            "ms_per_step": ms_per_step,
+            "ms_per_step": res["ms_per_step"],
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic (SURVEY Appendix A power-law generator, seeded, on device)",
             "config": {
-                "workload": (f"{args.config}-shaped {FORMAT_NAME[args.format]} MTTKRP, all {n_modes} "
+                "workload": (f"{args.config}-shaped {FORMAT_NAME[args.format]} MTTKRP, all {len(dims)} "
                              "modes per step, R=32"),
-                "dims": list(dims), "nnz": nnz_total, "rank": RANK, "scale": args.scale,
+                "dims": list(dims), "nnz": header["nnz"], "rank": RANK, "scale": args.scale,
                 "split": {"fiber_threshold": 128, "block_size": 512},
                 "l2": "inputs larger than L2 (index/value streams 0.75+ GB per mode); factors L2-resident by design",
-                "parallelism": f"slice-sharded dp{world}" if world > 1 else "1 GPU",
-                "census": censuses if world == 1 else {"rank0_shards": censuses},
-                "preprocessing_s": prep_s, "generate_s": gen_s,
+                "parallelism": f"slice-sharded dp{env.world}" if env.world > 1 else "1 GPU",
+                "backend": env.backend if env.world > 1 else None,
+                "ranks": env.ranks,
+                "census": census if env.world == 1 else {"rank0_shards": census},
+                "preprocessing_s": header["prep_s"], "generate_s": header["gen_s"],
             },
-            "roofline": {
-                "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
-                # the DRAM bytes the kernels actually move (ncu, cold caches per
-                # replay) over their time: how close to the HBM peak the
-                # traffic runs, as opposed to the compulsory-bytes fraction
-                "traffic_gbs": (traffic / (statistics.mean(per_mode_ms) * 1e-3) / 1e9
-                                if traffic else None),
-                "traffic_frac": (traffic / (statistics.mean(per_mode_ms) * 1e-3) / 1e9 / hbm
-                                 if traffic else None),
-                "kernel": "k_mttkrp3_r32<kind> (one launch per non-empty bucket kind per mode)",
-                "algorithmic_bytes_per_step": sum(bytes_modes),
-                "algorithmic_bytes_per_launch": sum(bytes_modes) / n_modes,
-                "traffic_unit": "DRAM bytes per MTTKRP launch (ncu dram__bytes_read+write, profiles/)",
-                "per_mode_ms": per_mode_ms, "per_mode_bytes": bytes_modes,
-                "per_mode_frac": [b / (ms * 1e-3) / 1e9 / hbm for b, ms in zip(bytes_modes, per_mode_ms)],
-                "launches_per_mode": [int(pl.info.launches) if pl is not None else 0 for pl in plans],
-                "gather": gather,
-            },
+            "roofline": roof,
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": e2e,
             "with_output_allgather": with_ag,
-            "gpu_launches": args.steps * sum(int(pl.info.launches) for pl in plans if pl is not None),
-            "clocks": clk.summary(),
+            "also": also,
+            "cpd": cpd,
+            "gpu_launches": launches,
+            "clocks": res["clocks"],
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    if env.world > 1:
+        env.dist.destroy_process_group()
+
+
+def self_launch(args) -> int:
+    """``--gpus N`` without a torchrun environment: launch N ranks here (one
+    per GPU over NCCL; with fewer GPUs than ranks, gloo ranks sharing the
+    GPUs — a validation mode, labelled in the line)."""
+    import socket
+
+    import torch
+
+    env = dict(os.environ)
+    if torch.cuda.device_count() < args.gpus:
+        env["HBK_BENCH_BACKEND"] = "gloo"
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), *sys.argv[1:]]
+    print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
+
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if args.impl == "reference":  # rank 0 alone runs the CPU arm
+            run_reference(args, args.gpus, 0)
+            return
+        sys.exit(self_launch(args))
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    run_ours(args)
 
 
 if __name__ == "__main__":

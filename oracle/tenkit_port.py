@@ -140,6 +140,7 @@ def hbcsf(indices, values, dims, mode_order):
     return {
         "dims": tuple(dims),
         "mode_order": mo,
+        "labels": lab,
         "coo": (idx[sel[COO_LABEL]], val[sel[COO_LABEL]]),
         "csl": csl,
         "csf": csf_tree(idx[sel[CSF_LABEL]], val[sel[CSF_LABEL]], dims, mo),

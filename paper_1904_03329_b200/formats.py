@@ -248,35 +248,6 @@ def classify_slices(c: CsfTensor) -> np.ndarray:
     return labels
 
 
-def flatten_csf(c: CsfTensor) -> CooTensor:
-    """Expand a CSF tree back to COO (formats.py:171-191); parity helper over the
-    exported arrays."""
-    n = c.order
-    m = c.nnz
-    permuted = np.empty((m, n), dtype=INDEX_DTYPE)
-    permuted[:, n - 1] = c.leaf_idx
-    off = c.ptrs[n - 2]
-    permuted[:, n - 2] = np.repeat(c.idxs[n - 2], np.diff(off))
-    for d in range(n - 3, -1, -1):
-        off = off[c.ptrs[d]]
-        permuted[:, d] = np.repeat(c.idxs[d], np.diff(off))
-    indices = np.empty_like(permuted)
-    indices[:, list(c.mode_order)] = permuted
-    return CooTensor(c.dims, indices, c.values, sorted_under=c.mode_order)
-
-
-def flatten_hbcsf(h: HbCsfTensor) -> CooTensor:
-    """Concatenate the three buckets back into one COO list (formats.py:302-312)."""
-    s = h.csl_part
-    csl_indices = np.empty((s.nnz, h.order), dtype=INDEX_DTYPE)
-    csl_indices[:, h.mode_order[0]] = np.repeat(s.slice_idx, np.diff(s.slice_ptr))
-    csl_indices[:, list(h.mode_order[1:])] = s.rest_idx
-    csf_flat = flatten_csf(h.csf_part)
-    indices = np.concatenate([h.coo_part.indices, csl_indices, csf_flat.indices])
-    values = np.concatenate([h.coo_part.values, s.values, csf_flat.values])
-    return CooTensor(h.dims, indices, values)
-
-
 def slice_census(x) -> dict[str, int]:
     """Slices per bucket (formats.py:315-328)."""
     if isinstance(x, CsfTensor):

@@ -91,96 +91,3 @@ def config_tensor(name: str, scale: float = 1.0) -> CooTensor:
     c = CONFIGS[name]
     alpha = c["alpha"] if c["alpha"] is not None else (0.0,) * len(c["dims"])
     return powerlaw_tensor(c["dims"], c["nnz"], alpha, c["seed"], scale=scale)
-
-
-# ------------------------------------------------------------------------
-# The reference's own generator (generate.py:62-115), restated so that
-# config 1 — tenkit.generate_tensor((1000,)*3, 100_000, skew=0.0, seed=0) —
-# can be produced here bit for bit.  It consumes numpy's Generator in the
-# same order as the reference (multinomial slice counts, then per slice a
-# Zipf-weighted first coordinate and uniform rest, de-duplicated keeping the
-# first occurrence), so the tensor is identical for a given seed.  A host
-# input generator, not part of the kernel path; the result is canonicalised
-# on the GPU.
-def _powers(n: int, skew: float):
-    import numpy as np
-
-    w = np.arange(1, n + 1, dtype=np.float64) ** (-skew)
-    return w / w.sum()
-
-
-def _slice_codes(rng, sub, count: int, skew: float):
-    """``count`` distinct mixed-radix codes over ``sub`` (first mode fastest),
-    first coordinate Zipf(skew)-weighted (generate.py:25-59)."""
-    import numpy as np
-
-    from .coo import CapacityError
-
-    cap = math.prod(sub)
-    if count > cap:
-        raise ValueError("slice cannot hold that many nonzeros")
-    if count > cap // 2:
-        if cap > 20_000_000:
-            raise CapacityError(f"refusing to enumerate {cap} cells to fill a near-complete slice")
-        return rng.permutation(cap)[:count].astype(np.int64)
-    p = _powers(sub[0], skew)
-    have = np.empty(0, dtype=np.int64)
-    rounds = 0
-    while have.size < count:
-        draw = max(2 * (count - have.size), 256)
-        lead = (rng.choice(sub[0], size=draw, p=p) if rounds < 12
-                else rng.integers(0, sub[0], size=draw)).astype(np.int64)
-        code, radix = lead, sub[0]
-        for d in sub[1:]:
-            code = code + rng.integers(0, d, size=draw).astype(np.int64) * radix
-            radix *= d
-        pool = np.concatenate([have, code])
-        _, first = np.unique(pool, return_index=True)
-        have = pool[np.sort(first)]
-        rounds += 1
-    return have[:count]
-
-
-def _generate_raw(dims, nnz: int, skew: float, seed: int):
-    """Coordinates and values before canonicalisation (generate.py:76-114)."""
-    import numpy as np
-
-    dims = tuple(int(d) for d in dims)
-    if len(dims) < 3:
-        raise ValueError("tensor order must be >= 3")
-    if skew < 0:
-        raise ValueError("skew must be nonnegative")
-    cells = math.prod(dims)
-    if not 0 <= nnz <= cells:
-        raise ValueError(f"nnz must lie in [0, {cells}], got {nnz}")
-    rng = np.random.default_rng(seed)
-    sub = dims[1:]
-    room = math.prod(sub)
-    per_slice = np.minimum(rng.multinomial(nnz, _powers(dims[0], skew)), room)
-    spill = nnz - int(per_slice.sum())
-    for i in range(dims[0]):  # overflow goes to the first slices with room
-        if spill <= 0:
-            break
-        add = min(room - int(per_slice[i]), spill)
-        per_slice[i] += add
-        spill -= add
-    rows, codes = [], []
-    for i, c in enumerate(per_slice.tolist()):
-        if c:
-            codes.append(_slice_codes(rng, sub, int(c), skew))
-            rows.append(np.full(int(c), i, dtype=np.int64))
-    cols = [np.concatenate(rows)] if rows else [np.zeros(0, dtype=np.int64)]
-    code = np.concatenate(codes) if codes else np.zeros(0, dtype=np.int64)
-    for d in sub:
-        cols.append(code % d)
-        code = code // d
-    idx = np.stack(cols, axis=1)
-    vals = 1.0 - rng.random(idx.shape[0])
-    return dims, idx, vals
-
-
-def generate_tensor(dims, nnz: int, skew: float = 1.0, seed: int = 0) -> CooTensor:
-    """Canonical random tensor with Zipf(skew) slice and second-mode skew,
-    uniform values in (0, 1] (generate.py:62-115; same result per seed)."""
-    dims, idx, vals = _generate_raw(dims, nnz, skew, seed)
-    return canonicalize(CooTensor(dims, idx, vals))

@@ -1,7 +1,7 @@
-"""The restated reference generator (paper_1904_03329_b200.generate,
+"""The restated reference generator (oracle/ref_generate.py,
 generate.py:62-115) against tensors the reference itself produced
-(tests/golden/generate.npz, config1.npz).  Canonicalisation here uses the
-pinned oracle; on the GPU generate_tensor canonicalises with libhbk."""
+(tests/golden/generate.npz, config1.npz).  Canonicalisation uses the pinned
+oracle."""
 from __future__ import annotations
 
 import numpy as np
@@ -9,7 +9,7 @@ import pytest
 
 from conftest import golden
 from oracle import tenkit_port as P
-from paper_1904_03329_b200.generate import _generate_raw
+from oracle.ref_generate import generate_raw as _generate_raw
 
 CASES = ["skew12", "skew0_4d", "dense_slices", "overflow"]
 

@@ -40,6 +40,21 @@ def test_gpu_arm_json_line():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] == 3 * sum(r["launches_per_mode"])
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    p = d["parity"]
+    assert p["format_bit_exact"] is True and p["max_row_dev"] <= 1e-4
+    assert d["e2e"]["pinned_fp32"]["value"] > 0
+    assert d["cpd"]["ms_per_sweep"] > 0 and len(d["cpd"]["fits"]) >= 2
+
+
+def test_two_ranks_on_one_gpu():
+    """--gpus 2 without torchrun: bench.py launches the ranks itself (gloo,
+    sharing the one GPU here) and reports the 2-rank job."""
+    d = _run("--gpus", "2", "--steps", "3", "--warmup", "3", "--scale", "0.05", "--cpd", "none")
+    assert d["n_gpus"] == 2 and len(d["config"]["ranks"]) == 2
+    assert d["config"]["workload"].startswith("flickr-3d")
+    assert d["config"]["parallelism"] == "slice-sharded dp2"
+    assert d["with_output_allgather"]["value"] > 0
+    assert d["value"] > 0
 
 
 def test_reference_arm_json_line():
@@ -49,3 +64,5 @@ def test_reference_arm_json_line():
     assert d["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["threads1_value"] > 0
+    assert d["native_libraries"].startswith("none")
