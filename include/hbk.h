@@ -191,9 +191,13 @@ void hbk_sched_release(hbk_sched* s);
  * The output (dims[mode] x rank fp32, row-major, caller-owned) is fully
  * written: rows owned by no part are zero-filled inside the same launch.
  * A plan owns its split-slice workspace, task counters and fork/join
- * streams, so executions of ONE plan must be ordered (same stream, or
- * externally synchronised); distinct plans may run concurrently.  An
- * execute is capturable into a CUDA graph.                                 */
+ * streams; executions of ONE plan are therefore ordered by the library:
+ * each execute/probe makes its stream wait for the previous execution of
+ * the same plan (an event recorded on whatever stream issued it, under a
+ * per-plan lock), so concurrent calls from several host threads or streams
+ * are safe and serialise on the device; distinct plans run concurrently.
+ * An execute is capturable into a CUDA graph (inside a capture the
+ * capturing stream provides the order).                                    */
 typedef struct {
   int mode;
   int rank;

@@ -9,6 +9,7 @@ its units.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass
 from functools import singledispatch
 
@@ -80,7 +81,7 @@ class BlockSchedule:
     def __init__(self, units=None, multiplicities=None, num_slices: int = 0, num_fibers: int = 0,
                  *, _handle: N.Handle | None = None):
         self._handle = _handle
-        self._bound = {}
+        self._bound = weakref.WeakKeyDictionary()  # tree -> device schedule
         if _handle is not None:
             info = N.SchedInfo()
             N.call("hbk_sched_info_get", _handle.ptr, C.byref(info))
@@ -135,7 +136,7 @@ class BlockSchedule:
         """Device schedule usable with tree t (uploaded for host-built schedules)."""
         if self._handle is not None:
             return self._handle
-        h = self._bound.get(id(t))
+        h = self._bound.get(t)
         if h is None:
             raw = np.ascontiguousarray(self.units_array())
             mult = np.ascontiguousarray(self._mult, dtype=np.int64)
@@ -144,7 +145,7 @@ class BlockSchedule:
                    mult.ctypes.data_as(C.c_void_p) if mult.size else None, N.stream_ptr(),
                    C.byref(out))
             h = N.Handle(out, "hbk_sched_release")
-            self._bound[id(t)] = h
+            self._bound[t] = h
         return h
 
     def validate_for(self, t: CsfTensor) -> None:

@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <cstdio>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -1133,7 +1134,14 @@ struct hbk_plan {
   int gen_grid = 0;
   int grids[3] = {0, 0, 0};
   hbk_plan_info info{};
+  // Executions of one plan share its workspace (task counters, split-slice
+  // accumulators, side streams), so they are ordered: each execution's
+  // stream waits for the previous execution's completion event, whatever
+  // stream or host thread issued it (include/hbk.h, "Plans").
+  mutable std::mutex exec_mu;
+  cudaEvent_t ev_last = nullptr;
   ~hbk_plan() {
+    if (ev_last) cudaEventDestroy(ev_last);
     for (int i = 0; i < 3; ++i) {
       if (side[i]) cudaStreamDestroy(side[i]);
       if (ev_join[i]) cudaEventDestroy(ev_join[i]);
@@ -2232,6 +2240,24 @@ static void launch_fast(const hbk_plan* p, const FX& fx, cudaStream_t st, bool s
       HBK_CUDA(cudaStreamWaitEvent(st, p->ev_join[i], 0));
     }
 }
+// Orders executions of one plan (see hbk_plan::exec_mu).  Inside a CUDA
+// graph capture the capturing stream already orders the replays, and an
+// event recorded outside the capture may not be waited on, so capture skips it.
+struct ExecOrder {
+  const hbk_plan* p;
+  cudaStream_t st;
+  bool capturing = false;
+  std::lock_guard<std::mutex> lk;
+  ExecOrder(const hbk_plan* plan, cudaStream_t s) : p(plan), st(s), lk(plan->exec_mu) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    HBK_CUDA(cudaStreamIsCapturing(st, &cs));
+    capturing = cs != cudaStreamCaptureStatusNone;
+    if (!capturing) HBK_CUDA(cudaStreamWaitEvent(st, p->ev_last, 0));
+  }
+  void done() {
+    if (!capturing) HBK_CUDA(cudaEventRecord(p->ev_last, st));
+  }
+};
 }  // namespace hbk
 
 extern "C" {
@@ -2339,6 +2365,7 @@ int hbk_plan_create(hbk_coo* coo, hbk_csl* csl, hbk_csf* csf, hbk_sched* sched, 
                   "a COO bucket must be an HB-CSF coo_part of this mode");
     hbk_plan* p = new hbk_plan();
     std::unique_ptr<hbk_plan> guard(p);
+    HBK_CUDA(cudaEventCreateWithFlags(&p->ev_last, cudaEventDisableTiming));
     p->order = order;
     p->mode = mode;
     p->rank = rank;
@@ -2398,6 +2425,7 @@ int hbk_plan_execute_ex(const hbk_plan* p, const float* const* factors, float* o
     for (int d = 0; d < N; ++d)
       HBK_REQUIRE(d == p->mode || factors[d] != nullptr, HBK_EINVAL, "null factor pointer");
     HBK_REQUIRE(out != nullptr || p->dims[p->mode] == 0, HBK_EINVAL, "null output pointer");
+    ExecOrder order(p, st);
     if (p->fast) {
       Factors3 fx;
       fx.B = reinterpret_cast<const float4*>(factors[p->mo[1]]);
@@ -2422,6 +2450,7 @@ int hbk_plan_execute_ex(const hbk_plan* p, const float* const* factors, float* o
     } else {
       launch_generic<float>(p, factors, out, st);
     }
+    order.done();
   });
 }
 
@@ -2525,6 +2554,7 @@ int hbk_plan_probe(const hbk_plan* p, const float* const* factors, void* stream)
     HBK_REQUIRE(p->bpos && p->r32, HBK_EINVAL,
                 "the gather probe needs a B-position (fast order-3, R=32, extents < 2^27) plan");
     cudaStream_t st = to_stream(stream);
+    ExecOrder order(p, st);
     Factors3 fx;
     fx.B = reinterpret_cast<const float4*>(factors[p->mo[1]]);
     fx.C = reinterpret_cast<const float4*>(factors[p->mo[2]]);
@@ -2540,6 +2570,7 @@ int hbk_plan_probe(const hbk_plan* p, const float* const* factors, void* stream)
     if (p->work.n1 > p->work.n0) k_gather_probe<KIND_CSL><<<grid, FAST_BLOCK, 0, st>>>(p->work, f32, sink);
     if (p->work.n2 > p->work.n1) k_gather_probe<KIND_COO><<<grid, FAST_BLOCK, 0, st>>>(p->work, f32, sink);
     check_launch("k_gather_probe");
+    order.done();
   });
 }
 
@@ -2550,7 +2581,10 @@ int hbk_plan_execute_f64(const hbk_plan* p, const double* const* factors, double
       HBK_REQUIRE(d == p->mode || factors[d] != nullptr, HBK_EINVAL, "null factor pointer");
     HBK_REQUIRE(out != nullptr, HBK_EINVAL, "null output pointer");
     HBK_REQUIRE(p->gen_grid > 0, HBK_EINVAL, "plan has no fp64 launch configuration");
-    launch_generic<double>(p, factors, out, to_stream(stream));
+    cudaStream_t st = to_stream(stream);
+    ExecOrder order(p, st);
+    launch_generic<double>(p, factors, out, st);
+    order.done();
   });
 }
 

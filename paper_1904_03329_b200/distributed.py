@@ -231,7 +231,9 @@ def cp_als_distributed(t: CooTensor, rank: int = 32, max_iters: int = 50, fit_to
             return
         for r, (lo, hi) in enumerate(ranges[d]):
             if hi > lo:
-                dist.broadcast(f32[d][lo:hi], src=r, group=group)
+                # ranges are indexed by group rank; broadcast wants the global rank
+                src = dist.get_global_rank(group, r) if group is not None else r
+                dist.broadcast(f32[d][lo:hi], src=src, group=group)
 
     def exchange_rows(d, f32):
         if touched is not None:

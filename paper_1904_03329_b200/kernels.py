@@ -89,12 +89,14 @@ class _HostStage:
     factors) are converted concurrently on a host thread pool (NumPy releases
     the GIL in these loops), and each factor's host-to-device copy is issued
     asynchronously as soon as it is staged.  The finiteness check of
-    kernels.py:82-86 runs on the converted data (half the bytes) and falls
-    back to the exact check of the source only when that fails.  The result
-    comes back through one async device-to-host copy into a pinned buffer,
-    widened to float64 on the host."""
+    kernels.py:82-86 runs on the device over the uploaded copies (one
+    hbk_nonfinite_f32 launch after the MTTKRP, flags returned with the rows);
+    only when it fires is the host source examined, to tell a non-finite
+    entry from a finite one beyond the float32 range.  The result comes back
+    through one async device-to-host copy into a pinned buffer, widened to
+    float64 on the host."""
 
-    CHUNK_BYTES = 8 << 20  # conversion work unit (bytes of the source factor)
+    CHUNK_BYTES = 1 << 20  # conversion work unit (bytes of the source factor)
 
     def __init__(self):
         import os
@@ -102,7 +104,7 @@ class _HostStage:
         from concurrent.futures import ThreadPoolExecutor
 
         self.lock = threading.Lock()
-        self.workers = max(1, min(8, (os.cpu_count() or 1)))
+        self.workers = max(1, min(16, (os.cpu_count() or 1)))
         self.pool = ThreadPoolExecutor(self.workers, thread_name_prefix="hbk-stage")
         self.bufs = {}
 
@@ -125,9 +127,10 @@ class _HostStage:
 
     def upload_all(self, torch, items, dt):
         """items: [(d, host array)] -> ({d: CUDA tensor}, deferred checks).
-        Page-locked torch tensors of the kernel dtype are copied as they are
-        (their finiteness is checked on the device: (d, device tensor) pairs
-        the caller tests after the launch).  Other factors are
+        Every uploaded copy is returned in ``checks`` as (d, device tensor,
+        host source) for the device finiteness scan after the launch.
+        Page-locked torch tensors of the kernel dtype are copied as they are.
+        Other factors are
         converted concurrently (one pool task per factor, or per chunk of a
         large one); the host-to-device copies are issued by the calling
         thread, on its current stream, as soon as each factor is staged."""
@@ -140,7 +143,7 @@ class _HostStage:
                 dev = torch.empty(tuple(f.shape), dtype=dt, device="cuda")
                 dev.copy_(f, non_blocking=True)
                 out[d] = dev
-                checks.append((d, dev))  # checked after the launch (_finish)
+                checks.append((d, dev, None))  # checked after the launch (_finish)
                 continue
             src = np.ascontiguousarray(f)
             if src.ndim != 2:
@@ -158,35 +161,29 @@ class _HostStage:
                 return out, checks
 
             def convert(d, a, b):
-                src, stage = srcs[d], stages[d][1]
-                np.copyto(stage[a:b], src[a:b], casting="unsafe")
-                return bool(np.isfinite(stage[a:b]).all()) or bool(np.isfinite(src[a:b]).all())
+                np.copyto(stages[d][1][a:b], srcs[d][a:b], casting="unsafe")
 
             if len(jobs) == 1:
                 futs = [None]
-                results = [convert(*jobs[0])]
+                convert(*jobs[0])
             else:
                 futs = [self.pool.submit(convert, *j) for j in jobs]
-                results = None
             left = {d: sum(1 for j in jobs if j[0] == d) for d in srcs}
-            bad = None
             for i, (d, a, b) in enumerate(jobs):
-                ok = results[i] if results is not None else futs[i].result()
-                if not ok and bad is None:
-                    bad = d
+                if futs[i] is not None:
+                    futs[i].result()
                 left[d] -= 1
-                if left[d] == 0 and bad is None:
+                if left[d] == 0:
                     rows, width = srcs[d].shape
                     dev = torch.empty((rows, width), dtype=dt, device="cuda")
                     if rows * width:
                         dev.copy_(stages[d][0][: rows * width].view(rows, width), non_blocking=True)
                     out[d] = dev
+                    checks.append((d, dev, srcs[d]))
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream())
             for d in srcs:
                 self.bufs[("in", d)] = (stages[d][0], ev)
-            if bad is not None:
-                raise ValueError(f"factor {bad} has non-finite entries")
         return out, checks
 
     # outputs up to this size are widened on the device and copied straight
@@ -360,10 +357,13 @@ def _finish(plan: _Plan, factors, mode: int, out=None, precision: str = "fp32"):
     # pinned host tensors are checked on the device (one hbk_nonfinite_f32
     # launch), after the MTTKRP launch so it does not wait for the scan; the
     # flags come back with the rows
-    flags = _nonfinite_flags(torch, [dev for _, dev in checks]) if checks else None
+    flags = _nonfinite_flags(torch, [dev for _, dev, _ in checks]) if checks else None
     rows, bad = _host_stage().download(torch, y, flags)
-    for (d, _), b in zip(checks, bad):
+    for (d, _, src), b in sorted(zip(checks, bad), key=lambda x: x[0][0]):
         if b:
+            if src is not None and np.isfinite(src).all():
+                raise ValueError(f"factor {d} has entries outside the float32 range of the fp32 "
+                                 "kernel; pass precision='fp64'")
             raise ValueError(f"factor {d} has non-finite entries")
     return rows, plan.opcount
 

@@ -105,7 +105,7 @@ def _needed_rows(idx, dims, ranges, rank):
     return need
 
 
-def _job_cpd(rank, world, exchange="full"):
+def _job_cpd(rank, world, exchange="full", group=None):
     from paper_1904_03329_b200.coo import CooTensor
     from paper_1904_03329_b200.distributed import cp_als_distributed
     from paper_1904_03329_b200.shard import plan_row_ranges
@@ -118,12 +118,24 @@ def _job_cpd(rank, world, exchange="full"):
     needed = _needed_rows(idx, dims, ranges, rank) if exchange == "touched" else None
     model, hist = cp_als_distributed(t, rank=4, max_iters=6, fit_tol=1e-14, seed=7,
                                      local_mttkrp=local, ranges=ranges, exchange=exchange,
-                                     needed=needed)
+                                     needed=needed, group=group)
     return [h.fit for h in hist], model.lam, [f for f in model.factors], ranges
 
 
 def _job_cpd_touched(rank, world):
     return _job_cpd(rank, world, exchange="touched")
+
+
+def _job_cpd_subgroup(rank, world):
+    """Global ranks 1..2 of a world-3 job decompose in a subgroup (group
+    ranks 0..1); global rank 0 stays out."""
+    sub = dist.new_group([1, 2])
+    if rank == 0:
+        return None
+    res = {}
+    for ex in ("full", "touched"):
+        res[ex] = _job_cpd(dist.get_rank(sub), 2, exchange=ex, group=sub)
+    return res
 
 
 def test_allgather_padded_uneven_world2():
@@ -161,3 +173,19 @@ def test_touched_rows_exchange_matches_full_replication(world):
         assert np.allclose(touched[r][1], full[0][1], rtol=1e-12)
         for a, b in zip(touched[r][2], full[0][2]):
             assert np.allclose(a, b, rtol=1e-10, atol=1e-12)
+
+
+def test_cp_als_distributed_in_a_subgroup():
+    """ADVICE r1: with a non-default group the row owners are group ranks;
+    the broadcasts must address them by global rank.  A subgroup {1, 2} of
+    a world-3 job reproduces the world-2 default-group model."""
+    ref = _run(_job_cpd, 2)
+    sub = _run(_job_cpd_subgroup, 3)
+    assert sub[0] is None
+    for r in (1, 2):
+        for ex in ("full", "touched"):
+            fits, lam, fac, _ = sub[r][ex]
+            assert np.allclose(fits, ref[0][0], atol=1e-12, rtol=0)
+            assert np.allclose(lam, ref[0][1], rtol=1e-12)
+            for a, b in zip(fac, ref[0][2]):
+                assert np.allclose(a, b, rtol=1e-10, atol=1e-12)

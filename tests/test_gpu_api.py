@@ -451,3 +451,75 @@ def test_csl_slices_through_csf_kernels(hb, rng, nnz, monkeypatch):
     assert row_dev(outs["1"][0], outs["0"][0]) <= 1e-5
     assert row_dev(outs["1"][2], outs["0"][2]) <= 1e-5
     assert outs["1"][1] == outs["0"][1] and outs["1"][3] == outs["0"][3]
+
+
+def test_concurrent_calls_on_one_plan_are_ordered(hb, rng):
+    """executions of one plan share its task counters and
+    split-slice accumulators.  Calls on one rep from several host threads on
+    distinct streams must each produce the full result (libhbk orders them
+    on the device), like the reference's mttkrp, which is safe to call
+    concurrently."""
+    import threading
+
+    import torch
+
+    from paper_1904_03329_b200.kernels import mttkrp_device
+
+    dims = (60, 500, 800)
+    idx, vals = _powerlaw(rng, dims, 200000)  # heavy slices: split-slice accumulators
+    t = hb.CooTensor(dims, idx, vals)
+    h = hb.split_fibers(hb.build_hbcsf(t, hb.allmode_order(dims, 0)), hb.SplitConfig())
+    f = [torch.rand((d, 32), device="cuda") for d in dims]
+    ref, _ = mttkrp_device(h, f, 0)
+    ref = ref.double().cpu().numpy()
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    outs = [[torch.empty((dims[0], 32), device="cuda") for _ in range(6)] for _ in streams]
+    errors = []
+
+    def work(i):
+        try:
+            with torch.cuda.stream(streams[i]):
+                for o in outs[i]:
+                    mttkrp_device(h, f, 0, out=o)
+        except Exception as e:  # pragma: no cover - surfaced below
+            errors.append(e)
+
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(len(streams))]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    torch.cuda.synchronize()
+    assert not errors, errors
+    for per_stream in outs:
+        for o in per_stream:
+            assert row_dev(o.double().cpu().numpy(), ref) <= 1e-5
+    # host-array calls from threads (the reference calling convention)
+    fh = [x.double().cpu().numpy() for x in f]
+    res = [None] * 4
+
+    def host_call(i):
+        res[i] = hb.mttkrp_hbcsf(h, fh, 0)[0]
+
+    ths = [threading.Thread(target=host_call, args=(i,)) for i in range(4)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    for y in res:
+        assert row_dev(y, ref) <= 1e-5
+
+
+def test_finite_factor_beyond_fp32_range_is_rejected(hb, rng):
+    """a finite float64 factor with |x| > FLT_MAX would reach the
+    fp32 kernel as inf; the host calling convention raises instead (the fp64
+    kernel takes it)."""
+    idx, vals = _powerlaw(rng, (30, 20, 40), 2000)
+    t = hb.CooTensor((30, 20, 40), idx, vals)
+    h = hb.build_hbcsf(t, (0, 1, 2))
+    f = [rng.random((d, 32)) for d in t.dims]
+    f[2][3, 5] = 1e39
+    with pytest.raises(ValueError, match="float32 range"):
+        hb.mttkrp_hbcsf(h, f, 0)
+    y, _ = hb.mttkrp_hbcsf(h, f, 0, precision="fp64")
+    assert np.isfinite(y).all()
