@@ -161,7 +161,8 @@ class _HostStage:
                 return out, checks
 
             def convert(d, a, b):
-                np.copyto(stages[d][1][a:b], srcs[d][a:b], casting="unsafe")
+                with np.errstate(over="ignore", invalid="ignore"):  # reported by the device scan
+                    np.copyto(stages[d][1][a:b], srcs[d][a:b], casting="unsafe")
 
             if len(jobs) == 1:
                 futs = [None]

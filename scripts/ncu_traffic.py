@@ -24,7 +24,7 @@ def run(cfg):
     cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
            "-k", "regex:k_mttkrp3", "--csv", "--log-file", str(out),
            sys.executable, str(ROOT / "bench.py"), "--config", cfg, "--steps", str(K),
-           "--warmup", str(W), "--no-e2e", "--no-cpu-baseline"]
+           "--warmup", str(W), "--no-e2e", "--no-cpu-baseline", "--also", "", "--cpd", "none"]
     r = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT)
     line = [l for l in r.stdout.splitlines() if l.startswith("{")]
     if not line:
