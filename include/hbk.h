@@ -150,6 +150,20 @@ int hbk_build_hbcsf(hbk_coo* t, const int* mode_order, void* stream, hbk_coo** c
                     hbk_csl** csl_part, hbk_csf** csf_part);
 /* classify_slices, formats.py:194-204: labels [host] int8 [num_slices]. */
 int hbk_classify_slices(const hbk_csf* c, int8_t* labels, void* stream);
+/* Slice / fiber populations of a tree, reduced on the device (the inspect
+ * statistics of coo.py:281-325 compute_stats, balance.py:210-227
+ * imbalance_metrics and formats.py:315-328 slice_census, without exporting
+ * the pointer arrays).  Slice sizes are nonzeros per slice, fiber sizes
+ * nonzeros per leaf-parent node (per segment once split).  Sums of squares
+ * are exact integers (sum <= nnz * max < 2^64), so the caller forms the
+ * population variance exactly.  Slice classes follow classify_slices.      */
+typedef struct {
+  int64_t slices, fibers, nnz;
+  int64_t max_slice, max_fiber;
+  uint64_t sumsq_slice, sumsq_fiber;
+  int64_t coo_slices, csl_slices, csf_slices;
+} hbk_population;
+int hbk_csf_population(const hbk_csf* c, hbk_population* out, void* stream);
 /* split_fibers, balance.py:65-90.  *out = NULL (status OK) when no fiber
  * exceeds fiber_threshold (the reference returns the input object).        */
 int hbk_split_fibers(const hbk_csf* c, int64_t fiber_threshold, void* stream, hbk_csf** out);

@@ -57,6 +57,15 @@ class CsfInfo(C.Structure):
     ]
 
 
+class Population(C.Structure):
+    _fields_ = [
+        ("slices", i64), ("fibers", i64), ("nnz", i64),
+        ("max_slice", i64), ("max_fiber", i64),
+        ("sumsq_slice", C.c_uint64), ("sumsq_fiber", C.c_uint64),
+        ("coo_slices", i64), ("csl_slices", i64), ("csf_slices", i64),
+    ]
+
+
 class SchedInfo(C.Structure):
     _fields_ = [
         ("num_units", i64),
@@ -114,6 +123,7 @@ _SIGS = {
     "hbk_build_csf": ([vp, vp, vp, C.POINTER(vp)], C.c_int),
     "hbk_build_hbcsf": ([vp, vp, vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)], C.c_int),
     "hbk_classify_slices": ([vp, vp, vp], C.c_int),
+    "hbk_csf_population": ([vp, vp, vp], C.c_int),
     "hbk_split_fibers": ([vp, i64, vp, C.POINTER(vp)], C.c_int),
     "hbk_csf_retain": ([vp], None),
     "hbk_csf_release": ([vp], None),

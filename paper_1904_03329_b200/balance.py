@@ -186,16 +186,17 @@ class ImbalanceMetrics:
 
 def imbalance_metrics(t: CsfTensor) -> ImbalanceMetrics:
     """Mean, population stddev and max of nonzeros per slice and per fiber
-    (per segment once split), balance.py:210-227.  Computed from the tree's
-    pointer arrays (built on the GPU)."""
+    (per segment once split), balance.py:210-227.  Reduced on the GPU over
+    the tree's pointer arrays (hbk_csf_population, exact integer moments)."""
+    from .formats import mean_std, population
+
     if t.nnz == 0:
         return ImbalanceMetrics(0, 0, 0, 0.0, 0.0, 0, 0.0, 0.0, 0)
-    slice_nnz = t.slice_nnz()
-    fiber_nnz = t.fiber_sizes()
+    pop = population(t)
+    ms, ss = mean_std(pop.nnz, pop.sumsq_slice, pop.slices)
+    mf, sf = mean_std(pop.nnz, pop.sumsq_fiber, pop.fibers)
     return ImbalanceMetrics(
-        slices=t.num_slices, fibers=t.num_fibers, nnz=t.nnz,
-        mean_nnz_per_slice=float(slice_nnz.mean()), stddev_nnz_per_slice=float(slice_nnz.std()),
-        max_nnz_per_slice=int(slice_nnz.max()),
-        mean_nnz_per_fiber=float(fiber_nnz.mean()), stddev_nnz_per_fiber=float(fiber_nnz.std()),
-        max_nnz_per_fiber=int(fiber_nnz.max()),
+        slices=int(pop.slices), fibers=int(pop.fibers), nnz=int(pop.nnz),
+        mean_nnz_per_slice=ms, stddev_nnz_per_slice=ss, max_nnz_per_slice=int(pop.max_slice),
+        mean_nnz_per_fiber=mf, stddev_nnz_per_fiber=sf, max_nnz_per_fiber=int(pop.max_fiber),
     )

@@ -1136,6 +1136,84 @@ int hbk_classify_slices(const hbk_csf* c, int8_t* labels, void* stream) {
   });
 }
 
+namespace hbk {
+// Slice and fiber population reductions (hbk_csf_population): per thread a
+// grid-stride share of slices and fibers; u64 sums of squares, u32 maxima and
+// class counts reduced per warp, then one atomic per warp.
+// acc: [0] slice sumsq, [1] fiber sumsq, [2] COO slices, [3] CSL slices;
+// mx: [0] max slice, [1] max fiber.
+__global__ void k_population(const uint32_t* __restrict__ fpos, const uint32_t* __restrict__ loff,
+                             int64_t S, const uint32_t* __restrict__ lptr, int64_t F,
+                             unsigned long long* __restrict__ acc, unsigned int* __restrict__ mx) {
+  unsigned long long sq_s = 0, sq_f = 0, n_coo = 0, n_csl = 0;
+  unsigned int m_s = 0, m_f = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < S; i += stride) {
+    const unsigned int x = loff[i + 1] - loff[i];
+    const unsigned int nf = fpos[i + 1] - fpos[i];
+    sq_s += (unsigned long long)x * x;
+    m_s = max(m_s, x);
+    n_coo += x == 1u;
+    n_csl += (x >= 2u && x == nf);
+  }
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < F; i += stride) {
+    const unsigned int x = lptr[i + 1] - lptr[i];
+    sq_f += (unsigned long long)x * x;
+    m_f = max(m_f, x);
+  }
+  for (int o = 16; o; o >>= 1) {
+    sq_s += __shfl_xor_sync(0xFFFFFFFFu, sq_s, o);
+    sq_f += __shfl_xor_sync(0xFFFFFFFFu, sq_f, o);
+    n_coo += __shfl_xor_sync(0xFFFFFFFFu, n_coo, o);
+    n_csl += __shfl_xor_sync(0xFFFFFFFFu, n_csl, o);
+  }
+  m_s = __reduce_max_sync(0xFFFFFFFFu, m_s);
+  m_f = __reduce_max_sync(0xFFFFFFFFu, m_f);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(acc + 0, sq_s);
+    atomicAdd(acc + 1, sq_f);
+    atomicAdd(acc + 2, n_coo);
+    atomicAdd(acc + 3, n_csl);
+    atomicMax(mx + 0, m_s);
+    atomicMax(mx + 1, m_f);
+  }
+}
+}  // namespace hbk
+
+int hbk_csf_population(const hbk_csf* c, hbk_population* out, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = to_stream(stream);
+    std::memset(out, 0, sizeof(*out));
+    const int64_t S = c->n[0], F = c->n[c->order - 2];
+    out->slices = S;
+    out->fibers = F;
+    out->nnz = c->M;
+    if (S == 0) return;
+    Scratch fpos((S + 1) * sizeof(uint32_t), st), loff((S + 1) * sizeof(uint32_t), st);
+    Scratch red(6 * sizeof(unsigned long long), st);
+    HBK_CUDA(cudaMemsetAsync(red.p, 0, 6 * sizeof(unsigned long long), st));
+    k_slice_meta<<<grid_for(S + 1, 256), 256, 0, st>>>(chain_of(c), S, fpos.as<uint32_t>(),
+                                                       loff.as<uint32_t>());
+    check_launch("k_slice_meta");
+    auto* acc = red.as<unsigned long long>();
+    k_population<<<grid_for(std::max(S, F), 256), 256, 0, st>>>(
+        fpos.as<uint32_t>(), loff.as<uint32_t>(), S, c->ptr[c->order - 2].as<uint32_t>(), F, acc,
+        reinterpret_cast<unsigned int*>(acc + 4));
+    check_launch("k_population");
+    unsigned long long h[6];
+    HBK_CUDA(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, st));
+    HBK_CUDA(cudaStreamSynchronize(st));
+    const unsigned int* hm = reinterpret_cast<const unsigned int*>(h + 4);
+    out->sumsq_slice = h[0];
+    out->sumsq_fiber = h[1];
+    out->coo_slices = int64_t(h[2]);
+    out->csl_slices = int64_t(h[3]);
+    out->csf_slices = S - out->coo_slices - out->csl_slices;
+    out->max_slice = hm[0];
+    out->max_fiber = hm[1];
+  });
+}
+
 int hbk_build_hbcsf(hbk_coo* t, const int* mo, void* stream, hbk_coo** coo_part,
                     hbk_csl** csl_part, hbk_csf** csf_part) {
   return guarded([&] {

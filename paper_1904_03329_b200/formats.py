@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import math
 from dataclasses import dataclass
 from functools import singledispatch
 from typing import Sequence
@@ -248,15 +249,28 @@ def classify_slices(c: CsfTensor) -> np.ndarray:
     return labels
 
 
+def population(c: CsfTensor) -> N.Population:
+    """Slice/fiber population counts of a tree, reduced on the GPU
+    (hbk_csf_population): sizes, maxima, exact sums of squares, classes."""
+    pop = N.Population()
+    N.call("hbk_csf_population", c._h.ptr, C.byref(pop), N.stream_ptr())
+    return pop
+
+
+def mean_std(total: int, sumsq: int, count: int) -> tuple[float, float]:
+    """Mean and population standard deviation from exact integer moments."""
+    if count == 0:
+        return 0.0, 0.0
+    var_num = count * int(sumsq) - int(total) * int(total)  # exact: count^2 * variance
+    return total / count, math.sqrt(max(var_num, 0) / (count * count))
+
+
 def slice_census(x) -> dict[str, int]:
-    """Slices per bucket (formats.py:315-328)."""
+    """Slices per bucket (formats.py:315-328); a tree's classes are counted
+    on the GPU."""
     if isinstance(x, CsfTensor):
-        labels = classify_slices(x)
-        return {
-            "coo": int((labels == SliceKind.COO).sum()),
-            "csl": int((labels == SliceKind.CSL).sum()),
-            "csf": int((labels == SliceKind.CSF).sum()),
-        }
+        pop = population(x)
+        return {"coo": int(pop.coo_slices), "csl": int(pop.csl_slices), "csf": int(pop.csf_slices)}
     return {"coo": x.coo_part.nnz, "csl": x.csl_part.num_slices, "csf": x.csf_part.num_slices}
 
 
@@ -301,10 +315,11 @@ def _(x: CooTensor) -> StorageReport:
     if x.nnz == 0:
         s = f = 0
     else:
+        # distinct leading coordinates / leading (order-1)-tuples under the
+        # tensor's order = the level sizes of its CSF tree, built on the GPU
         mo = x.sorted_under if x.sorted_under is not None else tuple(range(x.order))
-        permuted = x.indices[:, mo]
-        s = len(np.unique(permuted[:, 0]))
-        f = len(np.unique(permuted[:, : x.order - 1], axis=0))
+        ls = build_csf(x, mo).level_sizes()
+        s, f = ls[0], ls[-1]
     return StorageReport("coo", words, (StoragePart("coo", s, f, x.nnz, words),))
 
 

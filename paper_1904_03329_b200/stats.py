@@ -2,8 +2,9 @@
 
 ``compute_stats`` mirrors the reference's TensorStats: the tensor is sorted
 and compressed under the mode order by libhbk's CSF builder on the GPU (K1,
-K2), and the statistics are reductions over its pointer arrays — the
-reference's group counting (coo.py:304-311) without a host sort.
+K2), and the statistics are device reductions over its pointer arrays
+(hbk_csf_population) — the reference's group counting (coo.py:304-311)
+without a host sort or an export.
 """
 from __future__ import annotations
 
@@ -12,7 +13,7 @@ from dataclasses import dataclass
 from typing import Sequence
 
 from .coo import CooTensor, _check_mode_order
-from .formats import build_csf
+from .formats import build_csf, mean_std, population
 
 
 @dataclass(frozen=True)
@@ -51,14 +52,12 @@ def compute_stats(t: CooTensor, mode_order: Sequence[int] | None = None) -> Tens
                            slice_count=0, fiber_count=0, mean_nnz_per_slice=0.0,
                            stddev_nnz_per_slice=0.0, max_nnz_per_slice=0, mean_nnz_per_fiber=0.0,
                            stddev_nnz_per_fiber=0.0, max_nnz_per_fiber=0)
-    c = build_csf(t, mo)
-    sl = c.slice_nnz()
-    fb = c.fiber_sizes()
+    pop = population(build_csf(t, mo))
+    ms, ss = mean_std(pop.nnz, pop.sumsq_slice, pop.slices)
+    mf, sf = mean_std(pop.nnz, pop.sumsq_fiber, pop.fibers)
     return TensorStats(
         order=t.order, dims=t.dims, nnz=t.nnz, density=density, mode_order=mo,
-        slice_count=int(len(sl)), fiber_count=int(len(fb)),
-        mean_nnz_per_slice=float(sl.mean()), stddev_nnz_per_slice=float(sl.std()),
-        max_nnz_per_slice=int(sl.max()),
-        mean_nnz_per_fiber=float(fb.mean()), stddev_nnz_per_fiber=float(fb.std()),
-        max_nnz_per_fiber=int(fb.max()),
+        slice_count=int(pop.slices), fiber_count=int(pop.fibers),
+        mean_nnz_per_slice=ms, stddev_nnz_per_slice=ss, max_nnz_per_slice=int(pop.max_slice),
+        mean_nnz_per_fiber=mf, stddev_nnz_per_fiber=sf, max_nnz_per_fiber=int(pop.max_fiber),
     )
