@@ -1,0 +1,270 @@
+// L1 / L2 gather probe for the L2-resident MTTKRP pattern (nell-2 mode 0:
+// leaf rows C[k], Zipf(1) over 28,818 rows of 128 B; fiber rows B[j], Zipf(1)
+// over 9,184 rows, about one per 4.6 leaf rows).  What bounds the row rate:
+// the L1 data pipe (row wavefronts + index shuffles), the L2 (bytes / cycle)
+// or the L1 hit rate?  Variants (rows/s, then ncu counters per kernel):
+//   g8     : 8 lanes x LDG.128 per row, index + value broadcast by SHFL (the
+//            product kernel's mapping), W warps per SM
+//   g4     : 4 lanes x LDG.256 per row (ld.global.v8.f32), SHFL over 4 lanes:
+//            half the shuffles per row
+//   g8hot  : g8, rows of the H hottest ids read from a per-CTA shared-memory
+//            copy (LDS.128) instead of L1/L2 (one CTA of 768 threads per SM)
+//   g4hot  : g4 with the shared-memory hot rows (LDS.256 = 2 x LDS.128)
+// Build/run on the box:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -o /tmp/l1p scripts/l1_probe.cu && /tmp/l1p
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <cmath>
+#include <random>
+#include <vector>
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e = (x);                                                             \
+    if (e != cudaSuccess) {                                                          \
+      printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+      exit(1);                                                                       \
+    }                                                                                \
+  } while (0)
+
+static constexpr int HOT_MAX = 1536;  // rows kept in shared memory (192 KB)
+static constexpr int CH = 1024;      // stream positions per task
+
+__device__ __forceinline__ float4 ld128(const float4* p) {
+  float4 v;
+  asm("ld.global.nc.L1::evict_last.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p));
+  return v;
+}
+struct f8 {
+  float a[8];
+};
+__device__ __forceinline__ f8 ld256(const float* p) {
+  f8 v;
+  asm("ld.global.nc.L1::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(v.a[0]), "=f"(v.a[1]), "=f"(v.a[2]), "=f"(v.a[3]), "=f"(v.a[4]), "=f"(v.a[5]),
+        "=f"(v.a[6]), "=f"(v.a[7])
+      : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float4 ld128_ef(const float4* p) {
+  float4 v;
+  asm("ld.global.nc.L1::evict_first.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float4 ld128_na(const float4* p) {
+  float4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint2 ldstream(const uint2* p) {
+  uint2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+
+// stream: (row id, value bits) pairs; rows 0..H-1 are the hottest (ids are
+// frequency ranks), so "hot" is id < H
+template <bool HOT, int SCAN = 0>
+__global__ void k_g8(const float4* __restrict__ F, const uint2* __restrict__ s, int64_t n, int H,
+                     float4* __restrict__ sink) {
+  extern __shared__ float4 hot[];
+  const int lane = threadIdx.x & 31, lig = lane & 7;
+  if (HOT) {
+    for (int i = threadIdx.x; i < H * 8; i += blockDim.x) hot[i] = F[i];
+    __syncthreads();
+  }
+  const int64_t gid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 3;
+  const int64_t ng = (int64_t(gridDim.x) * blockDim.x) >> 3;
+  float4 acc = make_float4(0, 0, 0, 0);
+  // a group owns contiguous chunks of CH stream positions (the product's
+  // ~1024-nonzero tasks), dealt round-robin
+  const int64_t nch = (n + CH - 1) / CH;
+  const int64_t my = gid < nch ? (nch - 1 - gid) / ng + 1 : 0;
+  const int64_t iters = __reduce_max_sync(0xffffffffu, uint32_t(my)) * (CH / 8);
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t base = (gid + (it / (CH / 8)) * ng) * CH + (it % (CH / 8)) * 8;
+    uint2 q = base + lig < n ? ldstream(s + base + lig) : make_uint2(0, 0);
+    float4 r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t kf = __shfl_sync(0xffffffffu, q.x, j, 8);
+      const uint32_t k = kf & 0x7FFFFFFFu;
+      if (HOT && int(k) < H)
+        r[j] = hot[k * 8 + lig];
+      else if (SCAN == 1 && (kf >> 31))
+        r[j] = ld128_ef(F + size_t(k) * 8 + lig);
+      else if (SCAN == 2 && (kf >> 31))
+        r[j] = ld128_na(F + size_t(k) * 8 + lig);
+      else
+        r[j] = ld128(F + size_t(k) * 8 + lig);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float v = __uint_as_float(__shfl_sync(0xffffffffu, q.y, j, 8));
+      acc.x = fmaf(v, r[j].x, acc.x);
+      acc.y = fmaf(v, r[j].y, acc.y);
+      acc.z = fmaf(v, r[j].z, acc.z);
+      acc.w = fmaf(v, r[j].w, acc.w);
+    }
+  }
+  if (acc.x == 1234.5f) sink[threadIdx.x] = acc;
+}
+
+template <bool HOT>
+__global__ void k_g4(const float* __restrict__ F, const uint2* __restrict__ s, int64_t n, int H,
+                     float4* __restrict__ sink) {
+  extern __shared__ float4 hot[];
+  const int lane = threadIdx.x & 31, lig = lane & 3;
+  if (HOT) {
+    const float4* F4 = reinterpret_cast<const float4*>(F);
+    for (int i = threadIdx.x; i < H * 8; i += blockDim.x) hot[i] = F4[i];
+    __syncthreads();
+  }
+  const int64_t gid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 2;
+  const int64_t ng = (int64_t(gridDim.x) * blockDim.x) >> 2;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int64_t nch = (n + CH - 1) / CH;
+  const int64_t my = gid < nch ? (nch - 1 - gid) / ng + 1 : 0;
+  const int64_t iters = __reduce_max_sync(0xffffffffu, uint32_t(my)) * (CH / 4);
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t base = (gid + (it / (CH / 4)) * ng) * CH + (it % (CH / 4)) * 4;
+    uint2 q = base + lig < n ? ldstream(s + base + lig) : make_uint2(0, 0);
+    f8 r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t k = __shfl_sync(0xffffffffu, q.x, j, 4) & 0x7FFFFFFFu;
+      if (HOT && int(k) < H) {
+        const float4 a = hot[k * 8 + 2 * lig], b = hot[k * 8 + 2 * lig + 1];
+        r[j].a[0] = a.x; r[j].a[1] = a.y; r[j].a[2] = a.z; r[j].a[3] = a.w;
+        r[j].a[4] = b.x; r[j].a[5] = b.y; r[j].a[6] = b.z; r[j].a[7] = b.w;
+      } else {
+        r[j] = ld256(F + size_t(k) * 32 + 8 * lig);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float v = __uint_as_float(__shfl_sync(0xffffffffu, q.y, j, 4));
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = fmaf(v, r[j].a[c], acc[c]);
+    }
+  }
+  float t = 0;
+  for (int c = 0; c < 8; ++c) t += acc[c];
+  if (t == 1234.5f) sink[threadIdx.x] = make_float4(t, 0, 0, 0);
+}
+
+int main(int argc, char** argv) {
+  const int rowsC = 28818, rowsB = 9184;
+  int64_t n = argc > 1 ? atoll(argv[1]) : 93600000;  // rows per "mode"
+  // argv[2]: a binary stream file (uint32 count, then (id, value bits)
+  // pairs, ids ranked by frequency) — the real tensor's B-position order
+  // written by scripts/l1_probe_stream.py; replaces the synthetic stream
+  const char* path = argc > 2 ? argv[2] : nullptr;
+  // mixed stream: leaf ids Zipf over C, fiber ids Zipf over B, as one id
+  // space [C | B]; ids are frequency ranks within each matrix, the hot set is
+  // the union of both heads (remapped to [0, H) by weight)
+  std::mt19937_64 rng(7);
+  std::uniform_real_distribution<double> U(0.0, 1.0);
+  const int rows = rowsC + rowsB;
+  std::vector<double> w(rows);
+  for (int i = 0; i < rowsC; ++i) w[i] = (77.0 / 93.6) / (i + 1) / std::log(rowsC + 1.0);
+  for (int i = 0; i < rowsB; ++i) w[rowsC + i] = (16.6 / 93.6) / (i + 1) / std::log(rowsB + 1.0);
+  // relabel by descending weight so "hot" = id < H
+  std::vector<int> order(rows);
+  for (int i = 0; i < rows; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return w[a] > w[b]; });
+  std::vector<int> rank(rows);
+  for (int i = 0; i < rows; ++i) rank[order[i]] = i;
+  std::vector<uint2> s;
+  int nrows_file = 0;
+  if (path) {
+    FILE* fp = fopen(path, "rb");
+    if (!fp) { printf("cannot open %s\n", path); return 1; }
+    uint32_t hdr[2];
+    if (fread(hdr, 4, 2, fp) != 2) return 1;
+    n = hdr[0];
+    nrows_file = int(hdr[1]);
+    s.resize(n);
+    if (fread(s.data(), sizeof(uint2), n, fp) != size_t(n)) return 1;
+    fclose(fp);
+  } else {
+    s.resize(n);
+  }
+  for (int64_t i = 0; i < (path ? 0 : n); ++i) {
+    const bool leaf = U(rng) < 77.0 / 93.6;
+    const int D = leaf ? rowsC : rowsB;
+    int id = std::min(D - 1, int(std::floor(std::exp(U(rng) * std::log(D + 1.0)))) - 1);
+    id = std::max(0, id);
+    const int gidx = leaf ? id : rowsC + id;
+    float v = float(U(rng));
+    s[i] = make_uint2(uint32_t(rank[gidx]), *reinterpret_cast<uint32_t*>(&v));
+  }
+  float* F;
+  uint2* ds;
+  float4* sink;
+  const int frows = std::max(rows, nrows_file);
+  CK(cudaMalloc(&F, size_t(frows) * 128));
+  CK(cudaMemset(F, 0, size_t(frows) * 128));
+  CK(cudaMalloc(&ds, n * sizeof(uint2)));
+  CK(cudaMemcpy(ds, s.data(), n * sizeof(uint2), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&sink, 4096 * sizeof(float4)));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const size_t hot_bytes = size_t(HOT_MAX) * 128;
+  CK(cudaFuncSetAttribute(k_g8<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hot_bytes)));
+  CK(cudaFuncSetAttribute(k_g4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hot_bytes)));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  auto run = [&](const char* name, auto launch) {
+    launch();
+    CK(cudaDeviceSynchronize());
+    float best = 1e9;
+    for (int r = 0; r < 5; ++r) {
+      CK(cudaEventRecord(a));
+      launch();
+      CK(cudaEventRecord(b));
+      CK(cudaEventSynchronize(b));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, a, b));
+      best = std::min(best, ms);
+    }
+    printf("%-28s %8.3f ms  %7.1f G rows/s\n", name, best, n / (best * 1e-3) / 1e9);
+  };
+  for (int wps : {16, 24, 32}) {
+    char nm[64];
+    snprintf(nm, sizeof nm, "g8  %d warps/SM", wps);
+    run(nm, [&] { k_g8<false><<<sms * (wps / 8), 256>>>(reinterpret_cast<float4*>(F), ds, n, 0, sink); });
+    snprintf(nm, sizeof nm, "g4  %d warps/SM", wps);
+    run(nm, [&] { k_g4<false><<<sms * (wps / 8), 256>>>(F, ds, n, 0, sink); });
+  }
+  if (argc > 3) {  // scan-flagged stream: evict-first / no-allocate for the flagged loads
+    for (int wps : {24, 32}) {
+      char nm[64];
+      snprintf(nm, sizeof nm, "g8 scan-EF %d warps/SM", wps);
+      run(nm, [&] { k_g8<false, 1><<<sms * (wps / 8), 256>>>(reinterpret_cast<float4*>(F), ds, n, 0, sink); });
+      snprintf(nm, sizeof nm, "g8 scan-NA %d warps/SM", wps);
+      run(nm, [&] { k_g8<false, 2><<<sms * (wps / 8), 256>>>(reinterpret_cast<float4*>(F), ds, n, 0, sink); });
+      snprintf(nm, sizeof nm, "g8 plain %d warps/SM", wps);
+      run(nm, [&] { k_g8<false, 0><<<sms * (wps / 8), 256>>>(reinterpret_cast<float4*>(F), ds, n, 0, sink); });
+    }
+    return 0;
+  }
+  for (int H : {512, 1024, 1536}) {
+    char nm[64];
+    snprintf(nm, sizeof nm, "g8hot H=%d 24w", H);
+    run(nm, [&] { k_g8<true><<<sms, 768, size_t(H) * 128>>>(reinterpret_cast<float4*>(F), ds, n, H, sink); });
+    snprintf(nm, sizeof nm, "g4hot H=%d 24w", H);
+    run(nm, [&] { k_g4<true><<<sms, 768, size_t(H) * 128>>>(F, ds, n, H, sink); });
+  }
+  return 0;
+}

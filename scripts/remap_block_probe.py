@@ -45,6 +45,7 @@ def timed(h, f, mode, reps=10):
 def main():
     cfg, mode, which = sys.argv[1], int(sys.argv[2]), sys.argv[3]
     nbs = [int(x) for x in sys.argv[4].split(",")]
+    reps = int(sys.argv[5]) if len(sys.argv) > 5 else 10
     dims = CONFIGS[cfg]["dims"]
     t = config_tensor(cfg)
     idx = torch.empty((t.nnz, 3), dtype=torch.int32, device="cuda")
@@ -60,7 +61,7 @@ def main():
         bs = math.ceil(dims[x] / nb)
         if nb == 1:
             h = hb.split_fibers(hb.build_hbcsf(t, mo), hb.SplitConfig())
-            ms, y = timed(h, f, mode)
+            ms, y = timed(h, f, mode, reps)
             base = y.double()
             print(f"{cfg} mode {mode} nb=1: {ms:.3f} ms  (launches {plan_for(h, mode, R).info.launches})",
                   flush=True)
@@ -74,7 +75,7 @@ def main():
         h2 = hb.split_fibers(hb.build_hbcsf(t2, mo), hb.SplitConfig())
         f2 = list(f)
         f2[mode] = torch.empty((d2[mode], R), device="cuda")
-        ms, y2 = timed(h2, f2, mode)
+        ms, y2 = timed(h2, f2, mode, reps)
         ys = y2.view(nb, dims[mode], R).double().sum(0)
         dev = None
         if base is not None:

@@ -98,7 +98,8 @@ def test_device_census_and_coo_storage_match_host_counting(mo):
     census = hb.slice_census(c)
     assert census == {"coo": int((labels == 0).sum()), "csl": int((labels == 1).sum()),
                       "csf": int((labels == 2).sum())}
-    assert census["coo"] > 0 and census["csl"] > 0 and census["csf"] > 0
+    if mo[0] == 0:  # the skewed mode: every class occurs
+        assert census["coo"] > 0 and census["csl"] > 0 and census["csf"] > 0
     ts = hb.sort_by_mode_order(t, mo)
     p = hb.storage_words(ts).parts[0]
     keys = ts.indices[:, list(mo)]
