@@ -1715,7 +1715,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   Work& w = p->work;
   std::memset(&w, 0, sizeof(w));
   BucketTasks tcsf, tcsl, tcsf_light, tcsl_fast;
-  bool csl_blocked = false, sched_bpos = false;
+  bool csl_blocked = false;
   // heavy-slice layout (fast path): slices with more than H nonzeros
   // B-position streams (default fast CSF path): every slice with more than
   // Tcsf nonzeros goes to the heavy layout, lighter slices form runs
@@ -1727,7 +1727,14 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   if (const char* e = getenv("HBK_HEAVY_W")) heavy_W = uint32_t(std::max(1, atoi(e)));
   heavy_W = std::max(heavy_W, heavy_tau);
   if (p->bpos) heavy_H = Tcsf;
-  const bool heavy_on = p->fast && !p->sched && heavy_H > 0 && heavy_H >= Tcsf;
+  // A schedule (mttkrp_scheduled / mttkrp_hbcsf(schedule=...)) fixes the
+  // OpCount and which slices are split; on the B-position path its slices run
+  // through the same layout as the default plan: single-unit slices whole,
+  // multi-unit slices (> block_size nonzeros) as ~1024-nonzero warp tasks of
+  // the heavy layout (two 512-nonzero units' worth across four 8-lane groups)
+  // instead of one light task per unit (nell-2: 1.00 -> 0.72 ms per mode).
+  const bool units_as_tasks = p->sched && !p->bpos;
+  const bool heavy_on = p->fast && !units_as_tasks && heavy_H > 0 && heavy_H >= Tcsf;
   int64_t heavy_ntasks = 0, heavy_segments = 0;
 
   int64_t n_coo = 0, n_zero = 0;
@@ -1747,40 +1754,31 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     k_csf_slice_offsets<<<grid_for(S + 1, 256), 256, 0, st>>>(ch, S, fpos.as<uint32_t>(),
                                                               p->csf_send.as<uint32_t>());
     check_launch("k_csf_slice_offsets");
+    int64_t sched_muls = 0, sched_adds = 0;
     if (p->sched) {
       hbk_sched* sc = p->sched;
       HBK_REQUIRE(sc->S == S && sc->F == c->n[L], HBK_EINVAL,
                   "schedule was built for a different tree");
-      Scratch cnt((S + 1) * sizeof(uint32_t), st), slot((S + 1) * sizeof(uint32_t), st);
-      HBK_CUDA(cudaMemsetAsync(cnt.p, 0, (S + 1) * sizeof(uint32_t), st));
-      if (sc->U) {
-        k_units_per_slice<<<grid_for(sc->U, 256), 256, 0, st>>>(sc->units.as<uint32_t>(), sc->U,
-                                                                cnt.as<uint32_t>());
-        check_launch("k_units_per_slice");
-      }
-      k_slot_flags<<<grid_for(S, 256), 256, 0, st>>>(cnt.as<uint32_t>(), S, slot.as<uint32_t>());
-      check_launch("k_slot_flags");
-      uint32_t nslot = exclusive_scan_total(slot.as<uint32_t>(), S, st);
-      tcsf.tasks = Scratch(size_t(sc->U) * sizeof(Task), st);
-      if (sc->U) {
-        k_units_to_tasks<<<grid_for(sc->U, 256), 256, 0, st>>>(
-            sc->units.as<uint32_t>(), sc->U, c->ptr[L].as<uint32_t>(), cnt.as<uint32_t>(),
-            slot.as<uint32_t>(), 0, tcsf.tasks.as<Task>());
-        check_launch("k_units_to_tasks");
-      }
-      tcsf.n = sc->U;
-      tcsf.slots = nslot;
-      if (p->bpos) {  // the fast kernel's copy in stream positions; tcsf stays for the generic one
-        tcsf_light.tasks = Scratch(size_t(std::max<int64_t>(sc->U, 1)) * sizeof(Task), st);
+      if (units_as_tasks) {
+        Scratch cnt((S + 1) * sizeof(uint32_t), st), slot((S + 1) * sizeof(uint32_t), st);
+        HBK_CUDA(cudaMemsetAsync(cnt.p, 0, (S + 1) * sizeof(uint32_t), st));
+        if (sc->U) {
+          k_units_per_slice<<<grid_for(sc->U, 256), 256, 0, st>>>(sc->units.as<uint32_t>(), sc->U,
+                                                                  cnt.as<uint32_t>());
+          check_launch("k_units_per_slice");
+        }
+        k_slot_flags<<<grid_for(S, 256), 256, 0, st>>>(cnt.as<uint32_t>(), S, slot.as<uint32_t>());
+        check_launch("k_slot_flags");
+        uint32_t nslot = exclusive_scan_total(slot.as<uint32_t>(), S, st);
+        tcsf.tasks = Scratch(size_t(sc->U) * sizeof(Task), st);
         if (sc->U) {
           k_units_to_tasks<<<grid_for(sc->U, 256), 256, 0, st>>>(
               sc->units.as<uint32_t>(), sc->U, c->ptr[L].as<uint32_t>(), cnt.as<uint32_t>(),
-              slot.as<uint32_t>(), 1, tcsf_light.tasks.as<Task>());
+              slot.as<uint32_t>(), 0, tcsf.tasks.as<Task>());
           check_launch("k_units_to_tasks");
         }
-        tcsf_light.n = sc->U;
-        tcsf_light.slots = nslot;
-        sched_bpos = true;
+        tcsf.n = sc->U;
+        tcsf.slots = nslot;
       }
       // OpCount of mttkrp_scheduled (kernels.py:283-298, 325-330)
       int64_t mid = 0;
@@ -1810,8 +1808,12 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
           }
         }
       }
-      muls += (c->M + c->n[L] + mid) * R;
-      adds += (c->M + mid + sc->U) * R;
+      sched_muls = (c->M + c->n[L] + mid) * R;
+      sched_adds = (c->M + mid + sc->U) * R;
+    }
+    if (units_as_tasks) {
+      muls += sched_muls;
+      adds += sched_adds;
     } else {
       tcsf = bucket_tasks(p->csf_send.as<uint32_t>(), fpos.as<uint32_t>(),
                           c->ptr[L].as<uint32_t>(), S, uint32_t(c->M), Tcsf, st);
@@ -1830,15 +1832,15 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
         heavy_segments = hl.segments;
         p->info.tasks_heavy = hl.ntasks;
       }
-      // OpCount of mttkrp_csf (kernels.py:173-185)
+      // OpCount of mttkrp_csf (kernels.py:173-185), or of the schedule
       int64_t m = c->M, a = c->M;
       for (int d = N - 2; d >= 1; --d) {
         m += c->n[d];
         if (d < N - 2) a += c->n[d];
       }
       a += c->n[0];
-      muls += m * R;
-      adds += a * R;
+      muls += p->sched ? sched_muls : m * R;
+      adds += p->sched ? sched_adds : a * R;
     }
     slots += tcsf.slots;
     w.csf_send = p->csf_send.as<uint32_t>();
@@ -2005,14 +2007,14 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       wo.n3 = uint32_t(total);
       wo.tasks = T;
     };
-    if (heavy_on || csl_blocked || sched_bpos) {
-      assemble((heavy_on || sched_bpos) ? tcsf_light : tcsf, csl_blocked ? tcsl_fast : tcsl,
+    if (heavy_on || csl_blocked) {
+      assemble(heavy_on ? tcsf_light : tcsf, csl_blocked ? tcsl_fast : tcsl,
                p->tasks, w);
       assemble(tcsf, tcsl, p->gen_tasks, p->work_gen);
     } else {
       assemble(tcsf, tcsl, p->tasks, w);
     }
-    p->info.tasks_csf = (heavy_on || sched_bpos) ? tcsf_light.n : tcsf.n;
+    p->info.tasks_csf = heavy_on ? tcsf_light.n : tcsf.n;
     p->info.tasks_csl = csl_blocked ? tcsl_fast.n : tcsl.n;
     p->info.tasks_coo = n_coo;
   }
@@ -2025,7 +2027,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   w.ws_ctr = reinterpret_cast<uint32_t*>(p->ws.as<char>());
   w.ws_cnt = reinterpret_cast<uint32_t*>(p->ws.as<char>() + cnt_off);
   w.ws_acc = reinterpret_cast<float*>(p->ws.as<char>() + acc_off);
-  if (!heavy_on && !csl_blocked && !sched_bpos) {
+  if (!heavy_on && !csl_blocked) {
     p->work_gen = w;
   } else {
     Work& wg = p->work_gen;

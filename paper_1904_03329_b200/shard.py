@@ -1,14 +1,12 @@
-"""Multi-GPU partitioner and factor exchange.
+"""Multi-GPU row partitioner.
 
 Output-mode slices are independent (each output row depends only on its
 slice's nonzeros, kernels.py:154-186), so a mode is sharded into contiguous
 row ranges balanced by nonzero count; each rank builds the HB-CSF of its
-shard and produces its rows with no data-path collective.  Between CP-ALS
-modes the updated factor rows are replicated with an all-gather over NCCL
-(uneven row counts are padded to the largest shard, one collective).
+shard and produces its rows with no data-path collective.  The exchanges of
+the row-sharded CP-ALS live in distributed.py.
 
-The range planner is a pure function (unit-tested on CPU); the exchange works
-on any torch.distributed backend (gloo tests on CPU, NCCL on the GPUs).
+The range planner is a pure function (unit-tested on CPU).
 """
 from __future__ import annotations
 
@@ -64,30 +62,3 @@ def shard_rows(t: CooTensor, mode: int, lo: int, hi: int) -> CooTensor:
     N.call("hbk_coo_shard_rows", t._dev().ptr, int(mode), int(lo), int(hi), N.stream_ptr(),
            C.byref(out))
     return CooTensor._from_handle(N.Handle(out, "hbk_coo_release"))
-
-
-def shard_for_rank(t: CooTensor, mode: int, rank: int, world: int):
-    """(row range, shard tensor) owned by `rank` for `mode`."""
-    ranges = plan_row_ranges(slice_histogram(t, mode).cpu().numpy(), world)
-    lo, hi = ranges[rank]
-    return (lo, hi), select_rows(t, mode, lo, hi)
-
-
-def allgather_rows(local, ranges, group=None):
-    """Replicate a row-sharded matrix: rank g holds rows ranges[g] of a
-    (rows, R) matrix in `local`; returns the full matrix on every rank.  One
-    all_gather of max-shard-sized buffers (uneven shards padded)."""
-    import torch
-    import torch.distributed as dist
-
-    world = len(ranges)
-    width = local.shape[1]
-    cap = max(hi - lo for lo, hi in ranges)
-    buf = torch.zeros((cap, width), dtype=local.dtype, device=local.device)
-    buf[: local.shape[0]] = local
-    outs = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(outs, buf, group=group)
-    full = torch.empty((ranges[-1][1], width), dtype=local.dtype, device=local.device)
-    for g, (lo, hi) in enumerate(ranges):
-        full[lo:hi] = outs[g][: hi - lo]
-    return full
