@@ -105,6 +105,18 @@ def _needed_rows(idx, dims, ranges, rank):
     return need
 
 
+def _needed_by(idx, dims, ranges, rank):
+    """Rows of factor d read by this rank's shard of each mode."""
+    out = [[None] * 3 for _ in range(3)]
+    for n in range(3):
+        lo, hi = ranges[n][rank]
+        keep = (idx[:, n] >= lo) & (idx[:, n] < hi)
+        for d in range(3):
+            if d != n:
+                out[n][d] = np.unique(idx[keep, d]).astype(np.int64)
+    return out
+
+
 def _job_cpd(rank, world, exchange="full", group=None):
     from paper_1904_03329_b200.coo import CooTensor
     from paper_1904_03329_b200.distributed import cp_als_distributed
@@ -116,14 +128,21 @@ def _job_cpd(rank, world, exchange="full", group=None):
     ranges = [plan_row_ranges(np.bincount(idx[:, m], minlength=dims[m]), world) for m in range(3)]
     local = _local_mttkrp_factory(idx, vals, dims, ranges, rank)
     needed = _needed_rows(idx, dims, ranges, rank) if exchange == "touched" else None
+    needed_by = None
+    if exchange == "split":
+        exchange, needed_by = "touched", _needed_by(idx, dims, ranges, rank)
     model, hist = cp_als_distributed(t, rank=4, max_iters=6, fit_tol=1e-14, seed=7,
                                      local_mttkrp=local, ranges=ranges, exchange=exchange,
-                                     needed=needed, group=group)
+                                     needed=needed, needed_by=needed_by, group=group)
     return [h.fit for h in hist], model.lam, [f for f in model.factors], ranges
 
 
 def _job_cpd_touched(rank, world):
     return _job_cpd(rank, world, exchange="touched")
+
+
+def _job_cpd_split(rank, world):
+    return _job_cpd(rank, world, exchange="split")
 
 
 def _job_cpd_subgroup(rank, world):
@@ -133,7 +152,7 @@ def _job_cpd_subgroup(rank, world):
     if rank == 0:
         return None
     res = {}
-    for ex in ("full", "touched"):
+    for ex in ("full", "touched", "split"):
         res[ex] = _job_cpd(dist.get_rank(sub), 2, exchange=ex, group=sub)
     return res
 
@@ -165,14 +184,17 @@ def test_cp_als_distributed_matches_single_process_oracle():
 @pytest.mark.parametrize("world", [2, 3])
 def test_touched_rows_exchange_matches_full_replication(world):
     """Touched-rows exchange (each rank receives only the factor rows its
-    shards read) gives the same model as full replication, on every rank."""
+    shards read) — in one piece, and split into the rows the next mode reads
+    plus a deferred remainder overlapping that mode (SplitExchange) — gives
+    the same model as full replication, on every rank."""
     full = _run(_job_cpd, world)
-    touched = _run(_job_cpd_touched, world)
-    for r in range(world):
-        assert np.allclose(touched[r][0], full[0][0], atol=1e-12, rtol=0)
-        assert np.allclose(touched[r][1], full[0][1], rtol=1e-12)
-        for a, b in zip(touched[r][2], full[0][2]):
-            assert np.allclose(a, b, rtol=1e-10, atol=1e-12)
+    for job in (_job_cpd_touched, _job_cpd_split):
+        touched = _run(job, world)
+        for r in range(world):
+            assert np.allclose(touched[r][0], full[0][0], atol=1e-12, rtol=0)
+            assert np.allclose(touched[r][1], full[0][1], rtol=1e-12)
+            for a, b in zip(touched[r][2], full[0][2]):
+                assert np.allclose(a, b, rtol=1e-10, atol=1e-12)
 
 
 def test_cp_als_distributed_in_a_subgroup():
@@ -183,7 +205,7 @@ def test_cp_als_distributed_in_a_subgroup():
     sub = _run(_job_cpd_subgroup, 3)
     assert sub[0] is None
     for r in (1, 2):
-        for ex in ("full", "touched"):
+        for ex in ("full", "touched", "split"):
             fits, lam, fac, _ = sub[r][ex]
             assert np.allclose(fits, ref[0][0], atol=1e-12, rtol=0)
             assert np.allclose(lam, ref[0][1], rtol=1e-12)
