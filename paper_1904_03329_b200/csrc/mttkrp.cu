@@ -258,94 +258,6 @@ __device__ __forceinline__ void flush_split(const Work& w, const FX& fx, bool ac
 }
 
 // ------------------------------------------------------------ CSF tasks --
-// Walks the (leaf|flags, value) stream in batches of 8 nonzeros per group.
-// Fiber and slice boundaries come from the flag bits; fiber coordinates and
-// slice rows are consumed in order from their own streams (no pointer is
-// chased).  The next batch's stream words are loaded before the current
-// batch is reduced.  Returns the partial of a chunk task (zero for runs).
-template <class FX>
-__device__ __forceinline__ float4 csf_tasks(const Work& w, const FX& fx, const Task& t,
-                                            int g, int lig, uint64_t pol_s, uint64_t pol_r,
-                                            float4* __restrict__ slots) {
-  const uint32_t lo = t.lo, hi = t.hi;
-  const bool chunk = t.slot != NOSLOT;
-  const uint32_t my_batches = hi > lo ? (hi - lo + 7) / 8 : 0;
-  const uint32_t nbat = __reduce_max_sync(FULL, my_batches);
-  const float4* Cl = fx.C + lane_col(fx, lig);
-  const float4* Bl = fx.B + lane_col(fx, lig);
-  uint32_t s = t.s, f = t.f;
-  float4 fa = f4zero(), sa = f4zero();
-  uint2 pr = make_uint2(0u, 0u);
-  if (lo + lig < hi) pr = ld_stream_u2(w.csf_pairs + lo + lig, pol_s);
-  uint32_t fi = (hi > lo && f + lig < w.csf_F) ? __ldg(w.csf_fidx + f + lig) : 0u;
-  uint32_t sr = (hi > lo && !chunk && s + lig < w.csf_S) ? __ldg(w.csf_sidx + s + lig) : 0u;
-  bool pending = false;
-  uint32_t base = lo;
-  for (uint32_t it = 0; it < nbat; ++it, base += 8) {
-    const uint32_t n = base < hi ? min(8u, hi - base) : 0u;
-    const bool live = uint32_t(lig) < n;
-    const uint32_t k = pr.x & KMASK;
-    const float v = __uint_as_float(pr.y);
-    const uint32_t eb_all = __ballot_sync(FULL, live && (pr.x & FEND));
-    const uint32_t sb_all = __ballot_sync(FULL, live && !chunk && (pr.x & SEND));
-    const uint32_t ebits = (eb_all >> (8 * g)) & 0xFFu;
-    const uint32_t sbits = (sb_all >> (8 * g)) & 0xFFu;
-    const uint32_t eany = any_group(eb_all);
-    const uint32_t sany = any_group(sb_all);
-    float4 c[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t kj = __shfl_sync(FULL, k, j, 8);
-      if (uint32_t(j) < n) c[j] = ld_row4(rowp(Cl, kj, fx), pol_r);
-    }
-    // fiber rows of the fibers ending in this batch -> slot = end position
-    uint32_t tf = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if ((eany >> j) & 1u) {
-        const uint32_t fj = __shfl_sync(FULL, fi, tf, 8);
-        if ((ebits >> j) & 1u) cp_async16(slots + j * 8, rowp(Bl, fj, fx));
-        tf += (ebits >> j) & 1u;
-      }
-    }
-    // prefetch the next batch's stream words
-    const uint32_t sr_cur = sr;
-    const float vv = v;
-    f += tf;
-    const uint32_t nsl = __popc(sbits);
-    s += nsl;
-    const uint32_t nb = base + 8;
-    if (nb + lig < hi) pr = ld_stream_u2(w.csf_pairs + nb + lig, pol_s);
-    if (tf && nb < hi) fi = (f + lig < w.csf_F) ? __ldg(w.csf_fidx + f + lig) : 0u;
-    if (nsl && nb < hi) sr = (s + lig < w.csf_S) ? __ldg(w.csf_sidx + s + lig) : 0u;
-    cp_async_wait_all();
-    uint32_t ts = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float vj = __shfl_sync(FULL, vv, j, 8);
-      if (uint32_t(j) < n) fa = fma4(vj, c[j], fa);
-      if ((ebits >> j) & 1u) {
-        sa = fmav4(fa, slots[j * 8], sa);
-        fa = f4zero();
-      }
-      if ((sany >> j) & 1u) {
-        const uint32_t row = __shfl_sync(FULL, sr_cur, ts, 8);
-        if ((sbits >> j) & 1u) {
-          if (lane_live(fx, lig)) fx.out[size_t(row) * fx.rs + fx.col4 + lig] = sa;
-          sa = f4zero();
-          ++ts;
-        }
-      }
-    }
-    if (n) pending = !((ebits >> (n - 1)) & 1u);
-  }
-  if (chunk && pending) {  // the chunk ended inside fiber f
-    const uint32_t fj = __ldg(w.csf_fidx + f);
-    sa = fmav4(fa, ld_row4(rowp(Bl, fj, fx), pol_r), sa);
-  }
-  return sa;
-}
-
 // CSF tasks over a "B-position" stream: each fiber's (leaf, value) pairs
 // are followed by one extra position (j | FB, 0) naming the fiber's B row, so
 // B rows are gathered by the same LDG batch as the leaf rows (no shared-memory
@@ -571,7 +483,10 @@ __device__ __forceinline__ void zero_task(const Work& w, const FX& fx, const Tas
 // it.  Chunks of one split slice that land in the same warp are summed with
 // shuffles and handed over with a single vector atomic.
 static constexpr int FAST_BLOCK = 256;
-enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2, KIND_CSF_BPOS = 3, KIND_CSF_BPOS4 = 4, KIND_CSF_UNI = 5 };
+// KIND_CSF is the CSF bucket's task range and counters; its kernels are the
+// light-slice B-position kernel (KIND_CSF_BPOS4) and the heavy-slice
+// padded-layout kernel (KIND_CSF_UNI).
+enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2, KIND_CSF_BPOS4 = 4, KIND_CSF_UNI = 5 };
 
 template <int KIND, class FX>
 __global__ void __launch_bounds__(FAST_BLOCK, KIND == KIND_CSF_UNI ? 3 : (KIND == KIND_CSF_BPOS4 ? 4 : 3))
@@ -584,7 +499,8 @@ __global__ void __launch_bounds__(FAST_BLOCK, KIND == KIND_CSF_UNI ? 3 : (KIND =
   float4* slots = s_slots + (threadIdx.x >> 3) * 64 + lig;
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_r = policy_evict_last();
-  constexpr int K = (KIND == KIND_CSF_BPOS || KIND == KIND_CSF_BPOS4 || KIND == KIND_CSF_UNI) ? KIND_CSF : KIND;
+  static_assert(KIND != KIND_CSF, "CSF tasks run through KIND_CSF_BPOS4 / KIND_CSF_UNI");
+  constexpr int K = (KIND == KIND_CSF_BPOS4 || KIND == KIND_CSF_UNI) ? KIND_CSF : KIND;
   const uint32_t first = K == KIND_CSF ? 0u : (K == KIND_CSL ? w.n0 : w.n1);
   const uint32_t last = K == KIND_CSF ? w.n0 : (K == KIND_CSL ? w.n1 : w.n3);
   // the heavy-slice launch has its own counter pair (words 6, 7) so it can
@@ -598,10 +514,9 @@ __global__ void __launch_bounds__(FAST_BLOCK, KIND == KIND_CSF_UNI ? 3 : (KIND =
     const Task t = w.tasks[base + g];
     if (K == KIND_CSF || K == KIND_CSL) {
       const float4 sa =
-          KIND == KIND_CSF_UNI ? csf_bpos_tasks<true>(w, fx, t, g, lig, pol_s, pol_r)
-          : (KIND == KIND_CSF_BPOS || KIND == KIND_CSF_BPOS4) ? csf_bpos_tasks<false>(w, fx, t, g, lig, pol_s, pol_r)
-          : K == KIND_CSF       ? csf_tasks(w, fx, t, g, lig, pol_s, pol_r, slots)
-                                : csl_tasks(w, fx, t, g, lig, pol_s, pol_r, slots);
+          KIND == KIND_CSF_UNI     ? csf_bpos_tasks<true>(w, fx, t, g, lig, pol_s, pol_r)
+          : KIND == KIND_CSF_BPOS4 ? csf_bpos_tasks<false>(w, fx, t, g, lig, pol_s, pol_r)
+                                   : csl_tasks(w, fx, t, g, lig, pol_s, pol_r, slots);
       const bool mine = t.slot != NOSLOT && t.lo < t.hi;
       const uint32_t slot0 = __shfl_sync(FULL, t.slot, 0);
       const bool same = __all_sync(FULL, mine && t.slot == slot0);
@@ -1124,7 +1039,6 @@ struct hbk_plan {
   cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
   int grid_heavy = 0;
   bool fast = false;
-  int csf_variant = 2;  // 0: smem-slot kernel, 1|2: B-position streams at 3|4 CTAs per SM (HBK_CSF_VARIANT)
   bool bpos = false;
   // R = 32 with B/C extents < 2^27: the Factors3R32 kernels, B-position
   // stream indices pre-scaled to float4 units (bshift 3)
@@ -1665,16 +1579,13 @@ static int fast_occupancy(const hbk_plan* p, int k) {
   int per_sm = 0;
   const void* fn = nullptr;
   if (k == 0)
-    fn = p->bpos ? (p->csf_variant == 2 ? reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF_BPOS4, FX>)
-                                        : reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF_BPOS, FX>))
-                 : reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF, FX>);
+    fn = reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF_BPOS4, FX>);
   else if (k == 1)
     fn = reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSL, FX>);
   else if (k == 2)
     fn = reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_COO, FX>);
   else
-    fn = p->bpos ? reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF_UNI, FX>)
-                 : reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF, FX>);
+    fn = reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF_UNI, FX>);
   HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, p->block, 0));
   return per_sm;
 }
@@ -1697,7 +1608,6 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   const int gpw = p->fast ? 4 : 1;  // task ranges padded so a warp never straddles kinds
   uint32_t task_nnz = TASK_NNZ_CSF;
   if (const char* e = getenv("HBK_TASK_NNZ")) task_nnz = std::max(8, atoi(e));
-  if (const char* e = getenv("HBK_CSF_VARIANT")) p->csf_variant = atoi(e);
   const uint32_t Tcsf = p->fast ? task_nnz : GEN_TASK_NNZ;
   // CSL runs: 256 nonzeros when the CSL slices average >= 48 (delicious-3d
   // mode 2, 56 per slice: -5%), else 128 (flickr / nell-1, 4-36 per slice)
@@ -1720,21 +1630,20 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   // B-position streams (default fast CSF path): every slice with more than
   // Tcsf nonzeros goes to the heavy layout, lighter slices form runs
   // (schedule units run through the same light-slice B-position kernel)
-  p->bpos = p->fast && p->csf_variant >= 1;
-  uint32_t heavy_H = p->bpos ? Tcsf : 4 * Tcsf, heavy_tau = 32, heavy_W = 1024;
-  if (const char* e = getenv("HBK_HEAVY_H")) heavy_H = uint32_t(std::max(0, atoi(e)));
+  p->bpos = p->fast;
+  const uint32_t heavy_H = Tcsf;
+  uint32_t heavy_tau = 32, heavy_W = 1024;
   if (const char* e = getenv("HBK_HEAVY_TAU")) heavy_tau = uint32_t(std::min(65535, std::max(1, atoi(e))));
   if (const char* e = getenv("HBK_HEAVY_W")) heavy_W = uint32_t(std::max(1, atoi(e)));
   heavy_W = std::max(heavy_W, heavy_tau);
-  if (p->bpos) heavy_H = Tcsf;
   // A schedule (mttkrp_scheduled / mttkrp_hbcsf(schedule=...)) fixes the
   // OpCount and which slices are split; on the B-position path its slices run
   // through the same layout as the default plan: single-unit slices whole,
   // multi-unit slices (> block_size nonzeros) as ~1024-nonzero warp tasks of
   // the heavy layout (two 512-nonzero units' worth across four 8-lane groups)
   // instead of one light task per unit (nell-2: 1.00 -> 0.72 ms per mode).
-  const bool units_as_tasks = p->sched && !p->bpos;
-  const bool heavy_on = p->fast && !units_as_tasks && heavy_H > 0 && heavy_H >= Tcsf;
+  const bool units_as_tasks = p->sched && !p->fast;
+  const bool heavy_on = p->fast && !units_as_tasks;
   int64_t heavy_ntasks = 0, heavy_segments = 0;
 
   int64_t n_coo = 0, n_zero = 0;
@@ -1862,18 +1771,6 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       k_bpos_send<<<grid_for(S, 256), 256, 0, st>>>(fpos.as<uint32_t>(), c->ptr[L].as<uint32_t>(),
                                                     S, pp);
       check_launch("k_bpos_send");
-      w.csf_pairs = pp;
-    } else if (p->fast) {
-      p->csf_pairs = dalloc(c->M * sizeof(uint2), st);
-      uint2* pp = p->csf_pairs.as<uint2>();
-      k_pairs<<<grid_for(c->M, 256), 256, 0, st>>>(c->leaf.as<uint32_t>(), c->v32.as<float>(),
-                                                   c->M, pp);
-      check_launch("k_pairs");
-      k_flag_ends<<<grid_for(c->n[L], 256), 256, 0, st>>>(c->ptr[L].as<uint32_t>(), c->n[L], FEND,
-                                                          pp);
-      check_launch("k_flag_ends");
-      k_flag_ends<<<grid_for(S, 256), 256, 0, st>>>(p->csf_send.as<uint32_t>(), S, SEND, pp);
-      check_launch("k_flag_ends");
       w.csf_pairs = pp;
     }
     stream_bytes += p->fast ? 8 * c->M + 4 * c->n[L] + 4 * S : 8 * c->M + 8 * c->n[L] + 8 * S;
@@ -2210,19 +2107,11 @@ static void launch_fast(const hbk_plan* p, const FX& fx, cudaStream_t st, bool s
   if (p->concurrent) HBK_CUDA(cudaEventRecord(p->ev_fork, st));
   if (p->grid_heavy) {
     cudaStream_t s2 = next_stream();
-    if (p->bpos)
-      k_mttkrp3_r32<KIND_CSF_UNI, FX><<<p->grid_heavy, p->block, 0, s2>>>(p->work_heavy, fx);
-    else
-      k_mttkrp3_r32<KIND_CSF, FX><<<p->grid_heavy, p->block, 0, s2>>>(p->work_heavy, fx);
+    k_mttkrp3_r32<KIND_CSF_UNI, FX><<<p->grid_heavy, p->block, 0, s2>>>(p->work_heavy, fx);
   }
   if (p->grids[0]) {
     cudaStream_t s2 = next_stream();
-    if (p->bpos && p->csf_variant == 2)
-      k_mttkrp3_r32<KIND_CSF_BPOS4, FX><<<p->grids[0], p->block, 0, s2>>>(p->work, fx);
-    else if (p->bpos)
-      k_mttkrp3_r32<KIND_CSF_BPOS, FX><<<p->grids[0], p->block, 0, s2>>>(p->work, fx);
-    else
-      k_mttkrp3_r32<KIND_CSF, FX><<<p->grids[0], p->block, 0, s2>>>(p->work, fx);
+    k_mttkrp3_r32<KIND_CSF_BPOS4, FX><<<p->grids[0], p->block, 0, s2>>>(p->work, fx);
   }
   if (p->grids[1]) {
     cudaStream_t s2 = next_stream();

@@ -21,7 +21,8 @@ W, K = 3, 2
 def run(cfg):
     out = ROOT / "gpurun_out" / f"traffic_{cfg}.csv"
     out.parent.mkdir(exist_ok=True)
-    cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+    cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+           "lts__t_sectors.sum,lts__t_sectors_lookup_hit.sum",
            "-k", "regex:k_mttkrp3", "--csv", "--log-file", str(out),
            sys.executable, str(ROOT / "bench.py"), "--config", cfg, "--steps", str(K),
            "--warmup", str(W), "--no-e2e", "--no-cpu-baseline", "--also", "", "--cpd", "none"]
@@ -45,6 +46,7 @@ def run(cfg):
     per_step = sum(lpm)
     assert len(launches) == per_step * (W + K), (len(launches), lpm)
     modes = []
+    sec_all = hit_all = 0.0
     for m, n in enumerate(lpm):
         tot_b, tot_t = 0.0, 0.0
         for s in range(W + K):
@@ -52,11 +54,15 @@ def run(cfg):
             for L in launches[base: base + n]:
                 tot_b += L["dram__bytes_read.sum"] + L["dram__bytes_write.sum"]
                 tot_t += L["gpu__time_duration.sum"]
+                sec_all += L.get("lts__t_sectors.sum", 0.0)
+                hit_all += L.get("lts__t_sectors_lookup_hit.sum", 0.0)
         modes.append((tot_b / (W + K), tot_t / (W + K) / 1e6))
     return {"dram_bytes_per_launch": [b for b, _ in modes],
             "ncu_ms_per_mode": [t for _, t in modes],
             "launches_per_mode": lpm,
-            "note": (f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k regex:k_mttkrp3 on "
+            "l2_hit_rate_pct": 100.0 * hit_all / sec_all if sec_all else None,
+            "note": (f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors(_lookup_hit).sum "
+                     f"-k regex:k_mttkrp3 on "
                      f"bench.py --config {cfg} --steps {K} --warmup {W}: per mode, the sum over that "
                      "mode's launches, averaged over the steps (cold caches per replay)")}
 
