@@ -70,6 +70,7 @@ def parse_args():
                     help="comma list of extra configs (default: flickr-3d,delicious-3d at N=1, none at N>1)")
     ap.add_argument("--cpd", default="nell-1", help="CP-ALS sweep config, or 'none'")
     ap.add_argument("--cpd-iters", type=int, default=5)
+    ap.add_argument("--no-amortize", action="store_true", help="skip the COO amortisation comparison")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     n = max(world, a.gpus)
@@ -710,7 +711,7 @@ def run_ours(args):
     # reference CLI reports it (cli.py:317-327): steps until the format's
     # extra build time is repaid by its faster MTTKRP
     amort = None
-    if env.world == 1 and args.format != "coo":
+    if env.world == 1 and args.format != "coo" and not args.no_amortize:
         s0 = prepare(env, args.config, args, "coo", tensor=st["t"])
         r0 = time_steps(env, s0, args)
         gain_s = (r0["ms_per_step"] - res["ms_per_step"]) * 1e-3

@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 for c in "$@"; do
   for f in hbcsf bcsf csf coo; do
-    python bench.py --config $c --format $f --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --also "" --cpd none 2>/dev/null | tail -1 > gpurun_out/fmt_${c}_${f}.json
+    python bench.py --config $c --format $f --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --also "" --cpd none --no-amortize 2>/dev/null | tail -1 > gpurun_out/fmt_${c}_${f}.json
     python - "$c" "$f" <<'PY'
 import json, sys
 c, f = sys.argv[1], sys.argv[2]

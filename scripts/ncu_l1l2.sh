@@ -13,5 +13,5 @@ M="$M,l1tex__throughput.avg.pct_of_peak_sustained_active,l1tex__data_pipe_lsu_wa
 M="$M,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum,smsp__issue_active.avg.pct_of_peak_sustained_active"
 mkdir -p gpurun_out
 ncu --metrics $M --clock-control none -k regex:k_mttkrp3 -s 3 -c 3 --csv --log-file gpurun_out/${TAG}_l1l2.csv \
-    python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --also "" --cpd none "$@" > gpurun_out/${TAG}_l1l2.log 2>&1
+    python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --also "" --cpd none --no-amortize "$@" > gpurun_out/${TAG}_l1l2.log 2>&1
 echo "ncu rc=$?"

@@ -25,7 +25,7 @@ def run(cfg):
            "lts__t_sectors.sum,lts__t_sectors_lookup_hit.sum",
            "-k", "regex:k_mttkrp3", "--csv", "--log-file", str(out),
            sys.executable, str(ROOT / "bench.py"), "--config", cfg, "--steps", str(K),
-           "--warmup", str(W), "--no-e2e", "--no-cpu-baseline", "--also", "", "--cpd", "none"]
+           "--warmup", str(W), "--no-e2e", "--no-cpu-baseline", "--also", "", "--cpd", "none", "--no-amortize"]
     r = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT)
     line = [l for l in r.stdout.splitlines() if l.startswith("{")]
     if not line:
