@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <random>
+#include <string>
 #include <vector>
 
 #define CK(x)                                                                        \
@@ -65,6 +66,18 @@ __device__ __forceinline__ float4 ld128_na(const float4* p) {
       : "l"(p));
   return v;
 }
+__device__ __forceinline__ float4 ld128_l2h(const float4* p, uint64_t pol) {
+  float4 v;
+  asm("ld.global.nc.L1::evict_last.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float4 ld128_plain(const float4* p) {
+  float4 v;
+  asm("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ uint2 ldstream(const uint2* p) {
   uint2 v;
   asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
@@ -84,6 +97,8 @@ __global__ void k_g8(const float4* __restrict__ F, const uint2* __restrict__ s, 
   }
   const int64_t gid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 3;
   const int64_t ng = (int64_t(gridDim.x) * blockDim.x) >> 3;
+  uint64_t pol = 0;
+  if (SCAN == 3) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   float4 acc = make_float4(0, 0, 0, 0);
   // a group owns contiguous chunks of CH stream positions (the product's
   // ~1024-nonzero tasks), dealt round-robin
@@ -104,6 +119,10 @@ __global__ void k_g8(const float4* __restrict__ F, const uint2* __restrict__ s, 
         r[j] = ld128_ef(F + size_t(k) * 8 + lig);
       else if (SCAN == 2 && (kf >> 31))
         r[j] = ld128_na(F + size_t(k) * 8 + lig);
+      else if (SCAN == 3)
+        r[j] = ld128_l2h(F + size_t(k) * 8 + lig, pol);
+      else if (SCAN == 4)
+        r[j] = ld128_plain(F + size_t(k) * 8 + lig);
       else
         r[j] = ld128(F + size_t(k) * 8 + lig);
     }
@@ -246,6 +265,18 @@ int main(int argc, char** argv) {
     run(nm, [&] { k_g8<false><<<sms * (wps / 8), 256>>>(reinterpret_cast<float4*>(F), ds, n, 0, sink); });
     snprintf(nm, sizeof nm, "g4  %d warps/SM", wps);
     run(nm, [&] { k_g4<false><<<sms * (wps / 8), 256>>>(F, ds, n, 0, sink); });
+  }
+  if (argc > 3 && std::string(argv[3]) == "hint") {  // L2 cache-hint / plain-load variants
+    for (int wps : {24, 32}) {
+      char nm[64];
+      snprintf(nm, sizeof nm, "g8 L1el+L2hint %d w/SM", wps);
+      run(nm, [&] { k_g8<false, 3><<<sms * (wps / 8), 256>>>(reinterpret_cast<float4*>(F), ds, n, 0, sink); });
+      snprintf(nm, sizeof nm, "g8 plain-nc %d w/SM", wps);
+      run(nm, [&] { k_g8<false, 4><<<sms * (wps / 8), 256>>>(reinterpret_cast<float4*>(F), ds, n, 0, sink); });
+      snprintf(nm, sizeof nm, "g8 L1el %d w/SM", wps);
+      run(nm, [&] { k_g8<false, 0><<<sms * (wps / 8), 256>>>(reinterpret_cast<float4*>(F), ds, n, 0, sink); });
+    }
+    return 0;
   }
   if (argc > 3) {  // scan-flagged stream: evict-first / no-allocate for the flagged loads
     for (int wps : {24, 32}) {

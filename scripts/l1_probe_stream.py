@@ -18,6 +18,10 @@ cfg, mode, out = sys.argv[1], int(sys.argv[2]), sys.argv[3]
 # optional: flag (bit 31) the leaf positions of fibers longer than SCAN so the
 # probe can load them with an L1 evict-first / no-allocate hint
 scan = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+# optional: "reorder" — all positions of fibers <= SCAN first (tree order),
+# then the long fibers' positions (a two-phase plan: the short-fiber work runs
+# together, the sweeps after it)
+reorder = len(sys.argv) > 5 and sys.argv[5] == "reorder"
 dims = CONFIGS[cfg]["dims"]
 t = config_tensor(cfg)
 mo = hb.allmode_order(dims, mode)
@@ -45,7 +49,12 @@ if scan:
     long_f = np.repeat(fs > scan, fs)          # per leaf position, in leaf order
     flag = np.zeros(n, bool)
     flag[mask] = long_f
-    pairs[flag, 0] |= np.uint32(1 << 31)
+    flag[bpos] = fs > scan                      # the fiber's B row goes with it
+    if reorder:
+        pairs = np.concatenate([pairs[~flag], pairs[flag]])
+        print(f"reordered: {int((~flag).sum())} short-fiber positions first, {int(flag.sum())} after")
+    else:
+        pairs[flag, 0] |= np.uint32(1 << 31)
     print(f"flagged {flag.mean():.3f} of accesses (fibers > {scan})")
 pairs[:, 1] = vals.view(np.uint32)
 with open(out, "wb") as fp:
