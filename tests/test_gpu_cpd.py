@@ -153,3 +153,35 @@ def test_rank32_fused_path_all_formats(hb):
         fits = np.array([h.fit for h in hist])
         assert len(fits) == len(f64)
         assert np.allclose(fits[1:], f64[1:], atol=1e-5, rtol=0), (fmt, fits - f64)
+
+
+def test_als_update_mode_recovers_rank1_direction():
+    """Reference test_cpd.py:98-110: one update on an exact rank-1 tensor
+    recovers the mode-0 direction (factors[0] is not read)."""
+    import paper_1904_03329_b200 as hb
+
+    rng = np.random.default_rng(98)
+    a, b, c = rng.uniform(0.2, 1, 8), rng.uniform(0.2, 1, 7), rng.uniform(0.2, 1, 6)
+    dense = np.einsum("a,b,c->abc", a, b, c)
+    idx = np.argwhere(dense != 0)
+    t = hb.canonicalize(hb.CooTensor(dense.shape, idx, dense[tuple(idx.T)]))
+    factors = [np.zeros((8, 1)), b[:, None].copy(), c[:, None].copy()]
+    new0, y, ops = hb.als_update_mode(t, factors, 0)
+    corr = float(abs(new0[:, 0] @ a) / (np.linalg.norm(new0[:, 0]) * np.linalg.norm(a)))
+    assert corr > 1 - 1e-10
+    assert y.shape == (8, 1) and ops.total > 0
+    # the same through an HB-CSF representation
+    h = hb.build_hbcsf(t, hb.allmode_order(t.dims, 0))
+    new0h, _, _ = hb.als_update_mode(h, factors, 0)
+    assert np.allclose(new0h, new0, rtol=1e-6)
+
+
+def test_als_update_mode_zero_tensor_gives_zero_factor():
+    """Reference test_cpd.py:113-117."""
+    import paper_1904_03329_b200 as hb
+
+    rng = np.random.default_rng(113)
+    t = hb.CooTensor((4, 4, 4), np.empty((0, 3), dtype=np.int64), np.empty(0))
+    factors = [rng.uniform(size=(4, 2)) for _ in range(3)]
+    new0, _, _ = hb.als_update_mode(hb.canonicalize(t), factors, 0)
+    assert np.array_equal(new0, np.zeros((4, 2)))
