@@ -78,7 +78,7 @@ def parse_args():
         a.config = "nell-2" if n == 1 else "flickr-3d"
     if a.also is None:
         a.also = "flickr-3d,delicious-3d" if n == 1 and a.scale == 1.0 else ""
-    a.also = [c for c in a.also.split(",") if c and c != a.config]
+    a.also = [c for c in a.also.split(",") if c and c != "none" and c != a.config]
     if a.cpd == "none":
         a.cpd = None
     return a

@@ -266,6 +266,16 @@ int hbk_plan_rows(const hbk_plan* p, uint32_t* rows, int64_t* count, void* strea
  * Inf, else 0.  n <= 8. */
 int hbk_nonfinite_f32(const float* const* bufs, const int64_t* counts, int n, int32_t* flags,
                       void* stream);
+/* Host staging of the host-array calling convention (kernels.py:62-88,
+ * the factors' np.asarray + float conversion): narrows n float64 host
+ * arrays srcs[i][0..counts[i]) into page-locked float32 buffers stage[i]
+ * on a pool of host threads and issues the host-to-device copies into
+ * dst[i] (device) on `stream` chunk by chunk as the narrowing proceeds.
+ * Returns once every copy is enqueued (stage[i] must stay untouched until
+ * the stream passes them).  flags[i] (host) = 1 if the fp32 copy of factor
+ * i holds a NaN or Inf (kernels.py:82-86).  n <= 8. */
+int hbk_stage_f64_to_f32(const double* const* srcs, const int64_t* counts, int n,
+                         float* const* stage, float* const* dst, int32_t* flags, void* stream);
 
 /* ------------------------------------------------------- FROSTT text --
  * parse_frostt / load_frostt / write_frostt, coo.py:117-205, on the host

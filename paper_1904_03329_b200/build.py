@@ -9,7 +9,7 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SOURCES = ["csrc/build.cu", "csrc/mttkrp.cu", "csrc/als.cu", "csrc/frostt.cpp"]
+SOURCES = ["csrc/build.cu", "csrc/mttkrp.cu", "csrc/als.cu", "csrc/frostt.cpp", "csrc/stage.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-Wno-deprecated-gpu-targets", f"-I{ROOT / 'include'}"]

@@ -149,6 +149,32 @@ class _HostStage:
             if src.ndim != 2:
                 raise ValueError(f"factor {d} must be a 2-D array")
             srcs[d] = src
+        # float64 -> fp32 (the reference convention): narrowed by libhbk's
+        # host threads and copied chunk by chunk as it goes (hbk_stage_f64_to_f32)
+        nat = [d for d, s in srcs.items() if dt == torch.float32 and s.dtype == np.float64]
+        if nat:
+            with self.lock:
+                stages, devs = {}, {}
+                for d in nat:
+                    rows, width = srcs[d].shape
+                    stages[d] = self._pinned(torch, ("in", d), rows * width, dt)
+                    devs[d] = torch.empty((rows, width), dtype=dt, device="cuda")
+                k = len(nat)
+                flags = (C.c_int32 * k)()
+                N.call("hbk_stage_f64_to_f32",
+                       (C.c_void_p * k)(*[srcs[d].ctypes.data for d in nat]),
+                       (C.c_int64 * k)(*[srcs[d].size for d in nat]), k,
+                       (C.c_void_p * k)(*[stages[d].data_ptr() for d in nat]),
+                       (C.c_void_p * k)(*[devs[d].data_ptr() for d in nat]),
+                       flags, N.stream_ptr())
+                ev = torch.cuda.Event()
+                ev.record(torch.cuda.current_stream())
+                for i, d in enumerate(nat):
+                    self.bufs[("in", d)] = (stages[d], ev)
+                    if flags[i]:
+                        _raise_nonfinite(d, srcs[d])
+                    out[d] = devs[d]
+                    del srcs[d]
         with self.lock:
             stages, jobs = {}, []
             for d, src in srcs.items():
@@ -362,11 +388,17 @@ def _finish(plan: _Plan, factors, mode: int, out=None, precision: str = "fp32"):
     rows, bad = _host_stage().download(torch, y, flags)
     for (d, _, src), b in sorted(zip(checks, bad), key=lambda x: x[0][0]):
         if b:
-            if src is not None and np.isfinite(src).all():
-                raise ValueError(f"factor {d} has entries outside the float32 range of the fp32 "
-                                 "kernel; pass precision='fp64'")
-            raise ValueError(f"factor {d} has non-finite entries")
+            _raise_nonfinite(d, src)
     return rows, plan.opcount
+
+
+def _raise_nonfinite(d: int, src) -> None:
+    """The fp32 copy of factor d holds a NaN/Inf: a non-finite source entry
+    (kernels.py:82-86) or a finite float64 beyond the float32 range."""
+    if src is not None and np.isfinite(src).all():
+        raise ValueError(f"factor {d} has entries outside the float32 range of the fp32 "
+                         "kernel; pass precision='fp64'")
+    raise ValueError(f"factor {d} has non-finite entries")
 
 
 def plan_for(rep, mode: int, rank: int, schedule=None) -> _Plan:
