@@ -347,7 +347,9 @@ __device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const FX& fx, co
 // 8 C rows into registers; v * B[j] o C[k] accumulates into the slice
 // partial (kernels.py:210-214).  Measured: loading both rows into registers
 // (98 registers, 2 CTAs/SM) was 10-14% slower on delicious-3d.
-template <class FX>
+// ACC (blocked CSL layout): slice ends add the partial row into the
+// pre-zeroed output instead of storing it (a slice spans several blocks).
+template <bool ACC, class FX>
 __device__ __forceinline__ float4 csl_tasks(const Work& w, const FX& fx, const Task& t,
                                             int g, int lig, uint64_t pol_s, uint64_t pol_r,
                                             float4* __restrict__ slots) {
@@ -404,7 +406,10 @@ __device__ __forceinline__ float4 csl_tasks(const Work& w, const FX& fx, const T
       if ((sany >> j) & 1u) {
         const uint32_t row = __shfl_sync(FULL, sr_cur, ts, 8);
         if ((sbits >> j) & 1u) {
-          if (lane_live(fx, lig)) fx.out[size_t(row) * fx.rs + fx.col4 + lig] = sa;
+          if (lane_live(fx, lig)) {
+            float4* o = fx.out + size_t(row) * fx.rs + fx.col4 + lig;
+            if (ACC) red_add4(o, sa); else *o = sa;
+          }
           sa = f4zero();
           ++ts;
         }
@@ -486,7 +491,8 @@ static constexpr int FAST_BLOCK = 256;
 // KIND_CSF is the CSF bucket's task range and counters; its kernels are the
 // light-slice B-position kernel (KIND_CSF_BPOS4) and the heavy-slice
 // padded-layout kernel (KIND_CSF_UNI).
-enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2, KIND_CSF_BPOS4 = 4, KIND_CSF_UNI = 5 };
+// KIND_CSL_ACC: the CSL kernel over the blocked (block-major) CSL layout.
+enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2, KIND_CSF_BPOS4 = 4, KIND_CSF_UNI = 5, KIND_CSL_ACC = 6 };
 
 template <int KIND, class FX>
 __global__ void __launch_bounds__(FAST_BLOCK, KIND == KIND_CSF_UNI ? 3 : (KIND == KIND_CSF_BPOS4 ? 4 : 3))
@@ -500,7 +506,9 @@ __global__ void __launch_bounds__(FAST_BLOCK, KIND == KIND_CSF_UNI ? 3 : (KIND =
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_r = policy_evict_last();
   static_assert(KIND != KIND_CSF, "CSF tasks run through KIND_CSF_BPOS4 / KIND_CSF_UNI");
-  constexpr int K = (KIND == KIND_CSF_BPOS4 || KIND == KIND_CSF_UNI) ? KIND_CSF : KIND;
+  constexpr int K = (KIND == KIND_CSF_BPOS4 || KIND == KIND_CSF_UNI) ? KIND_CSF
+                    : KIND == KIND_CSL_ACC                          ? KIND_CSL
+                                                                    : KIND;
   const uint32_t first = K == KIND_CSF ? 0u : (K == KIND_CSL ? w.n0 : w.n1);
   const uint32_t last = K == KIND_CSF ? w.n0 : (K == KIND_CSL ? w.n1 : w.n3);
   // the heavy-slice launch has its own counter pair (words 6, 7) so it can
@@ -516,8 +524,15 @@ __global__ void __launch_bounds__(FAST_BLOCK, KIND == KIND_CSF_UNI ? 3 : (KIND =
       const float4 sa =
           KIND == KIND_CSF_UNI     ? csf_bpos_tasks<true>(w, fx, t, g, lig, pol_s, pol_r)
           : KIND == KIND_CSF_BPOS4 ? csf_bpos_tasks<false>(w, fx, t, g, lig, pol_s, pol_r)
-                                   : csl_tasks(w, fx, t, g, lig, pol_s, pol_r, slots);
+          : KIND == KIND_CSL_ACC   ? csl_tasks<true>(w, fx, t, g, lig, pol_s, pol_r, slots)
+                                   : csl_tasks<false>(w, fx, t, g, lig, pol_s, pol_r, slots);
       const bool mine = t.slot != NOSLOT && t.lo < t.hi;
+      if (KIND == KIND_CSL_ACC) {
+        // chunks of a long virtual slice add their partial rows directly
+        if (mine && lane_live(fx, lig))
+          red_add4(fx.out + size_t(__ldg(w.csl_sidx + t.s)) * fx.rs + fx.col4 + lig, sa);
+        continue;
+      }
       const uint32_t slot0 = __shfl_sync(FULL, t.slot, 0);
       const bool same = __all_sync(FULL, mine && t.slot == slot0);
       const uint32_t row =
@@ -1032,6 +1047,12 @@ struct hbk_plan {
   hbk::Work work_gen{};  // generic kernel (every CSF slice in tree order)
   hbk::Work work_heavy{};
   hbk::Buf heavy_pairs, heavy_fj, heavy_tasks, gen_tasks, probe_sink;
+  // blocked CSL layout (csl_blocked_layout): B rows per block (0 = off), the
+  // block-major stream, and whether the fast CSL kernel accumulates rows
+  int64_t csl_bb = 0;
+  bool csl_acc = false;
+  hbk::Buf vcsl_pairs, vcsl_j, vcsl_sidx;
+  uint32_t vcsl_S = 0;
   // B-position plans launch their bucket kernels on forked streams so each
   // kernel's CTAs fill the tail of the one before (HBK_CONCURRENT=0: serial)
   bool concurrent = false;
@@ -1330,12 +1351,17 @@ __global__ void k_gather_u32(const uint32_t* __restrict__ src, const uint32_t* _
 // ------------------------------------------------ CSL B-row blocking --
 // In a CSL slice the nonzeros are sorted by rest[0] (the B-row index), so the
 // nonzeros whose B rows fall in one block of BB rows are one contiguous
-// segment of the stream.  When the B factor exceeds the L2 budget, the fast
-// path cuts every slice into its per-block segments and orders the tasks by
-// (block, slice): the persistent kernel pulls tasks in that order, so at any
-// time the warps gather B rows from ~one block, which stays L2-resident
-// (on delicious-3d the near-uniform B factor is 2.5x the L2).  Slices cut into
-// several tasks hand over through the split-slice accumulator.
+// segment of the stream.  When the B factor is larger than the L2 can keep
+// beside the hot leaf rows and the plan is CSL-dominated (delicious-3d modes
+// 0 and 2: B = 317 / 68 MB, near-uniform), the fast path lays the CSL stream
+// out block-major: every (block, slice) segment becomes a "virtual slice"
+// ordered by (block, slice), and the tasks are runs of whole virtual slices
+// (or chunks of long ones), so the persistent kernel gathers B rows from about
+// one block at a time, which stays L2-resident.  A slice's segments add their
+// partial rows into the output with red.global.add (the output is zeroed
+// first), so the blocking adds no hand-over between tasks: one 128-B vector
+// atomic per segment (reference semantics unchanged: a row is the sum over its
+// slice's nonzeros, kernels.py:210-214; only fp32 summation order differs).
 __global__ void k_csl_segflags(const uint32_t* __restrict__ j, int64_t M, uint32_t BB,
                                uint32_t* __restrict__ flag) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
@@ -1353,109 +1379,121 @@ __global__ void k_csl_segs(const uint32_t* __restrict__ pos, int64_t M, uint32_t
        i += int64_t(gridDim.x) * blockDim.x)
     if (pos[i + 1] != pos[i]) start[pos[i]] = uint32_t(i);
 }
-// per segment: slice, block, task count; per slice: task count (atomic)
+// per segment: its slice (last slice with sptr[s] <= start), block and length
 __global__ void k_csl_seginfo(const uint32_t* __restrict__ start, int64_t G, uint32_t M,
                               const uint32_t* __restrict__ sptr, int64_t S,
-                              const uint32_t* __restrict__ j, uint32_t BB, uint32_t T,
+                              const uint32_t* __restrict__ j, uint32_t BB,
                               uint32_t* __restrict__ sslice, uint32_t* __restrict__ sblock,
-                              uint32_t* __restrict__ sntask, uint32_t* __restrict__ slice_ntask) {
+                              uint32_t* __restrict__ slen) {
   for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < G;
        g += int64_t(gridDim.x) * blockDim.x) {
     const uint32_t a = start[g], b = (g + 1 < G) ? start[g + 1] : M;
-    int64_t lo = 0, hi = S;  // last slice with sptr[s] <= a
+    int64_t lo = 0, hi = S;
     while (hi - lo > 1) {
       const int64_t mid = (lo + hi) >> 1;
       if (sptr[mid] <= a) lo = mid; else hi = mid;
     }
-    const uint32_t nt = (b - a + T - 1) / T;
     sslice[g] = uint32_t(lo);
     sblock[g] = j[a] / BB;
-    sntask[g] = nt;
-    atomicAdd(slice_ntask + lo, nt);
+    slen[g] = b - a;
   }
 }
-__global__ void k_select_count(const uint32_t* __restrict__ key, const uint32_t* __restrict__ val,
-                               int64_t n, uint32_t want, uint32_t* __restrict__ out) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x)
-    out[i] = key[i] == want ? val[i] : 0u;
-}
-__global__ void k_csl_seg_tasks(const uint32_t* __restrict__ start, int64_t G, uint32_t M,
-                                const uint32_t* __restrict__ sslice, const uint32_t* __restrict__ sblock,
-                                const uint32_t* __restrict__ sntask, const uint32_t* __restrict__ pos_in_block,
-                                uint32_t block, uint32_t base, const uint32_t* __restrict__ slice_ntask,
-                                const uint32_t* __restrict__ slice_slot, uint32_t slot_base,
-                                Task* __restrict__ tasks) {
-  for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < G;
-       g += int64_t(gridDim.x) * blockDim.x) {
-    if (sblock[g] != block) continue;
-    const uint32_t a = start[g], b = (g + 1 < G) ? start[g + 1] : M, m = b - a;
-    const uint32_t nt = sntask[g], s = sslice[g], total = slice_ntask[s];
-    Task* out = tasks + base + pos_in_block[g];
-    for (uint32_t c = 0; c < nt; ++c) {
-      Task t{};
-      t.lo = a + uint32_t((uint64_t(m) * c) / nt);
-      t.hi = a + uint32_t((uint64_t(m) * (c + 1)) / nt);
-      t.s = s;
-      t.f = 0;
-      t.slot = total > 1 ? slot_base + slice_slot[s] : NOSLOT;
-      t.nchunk = total;
-      out[c] = t;
-    }
+// virtual slice r = segment order[r]: its length, output row, and the
+// inverse map segment -> r
+__global__ void k_csl_vslices(const uint32_t* __restrict__ order, int64_t G,
+                              const uint32_t* __restrict__ slen, const uint32_t* __restrict__ sslice,
+                              const uint32_t* __restrict__ slice_idx, uint32_t* __restrict__ vlen,
+                              uint32_t* __restrict__ vsidx, uint32_t* __restrict__ rank_of) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < G;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t g = order[r];
+    vlen[r] = slen[g];
+    vsidx[r] = slice_idx[sslice[g]];
+    rank_of[g] = uint32_t(r);
   }
 }
-__global__ void k_gt1_flags(const uint32_t* __restrict__ n, int64_t S, uint32_t* __restrict__ f) {
-  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < S;
-       s += int64_t(gridDim.x) * blockDim.x)
-    f[s] = n[s] > 1;
+// nonzero i -> its block-major position: (k | SEND at a segment end, v), j
+__global__ void k_csl_vscatter(const uint32_t* __restrict__ pos, const uint32_t* __restrict__ start,
+                               const uint32_t* __restrict__ rank_of, const uint32_t* __restrict__ vstart,
+                               const uint32_t* __restrict__ k, const uint32_t* __restrict__ j,
+                               const float* __restrict__ v, int64_t M, uint2* __restrict__ vpairs,
+                               uint32_t* __restrict__ vj) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t g = pos[i + 1] - 1;
+    const bool last = (i + 1 == M) || (pos[i + 2] != pos[i + 1]);
+    const uint32_t q = vstart[rank_of[g]] + uint32_t(i - start[g]);
+    vpairs[q] = make_uint2(k[i] | (last ? SEND : 0u), __float_as_uint(v[i]));
+    vj[q] = j[i];
+  }
 }
 
-static BucketTasks csl_block_tasks(const hbk_csl* c, uint32_t BB, uint32_t T, uint32_t slot_base,
-                                   int64_t* nblocks_out, cudaStream_t st) {
-  BucketTasks bt;
+__global__ void k_iota_u32(uint32_t* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = uint32_t(i);
+}
+
+struct BlockedCsl {
+  Buf pairs, j, sidx;
+  BucketTasks tasks;
+  int64_t G = 0, nblocks = 0;
+};
+
+static BlockedCsl csl_blocked_layout(const hbk_csl* c, uint32_t BB, uint32_t T, cudaStream_t st) {
+  BlockedCsl out;
   const int64_t M = c->M, S = c->S;
   const uint32_t* j = c->rest[0].as<uint32_t>();
   const uint32_t* sptr = c->slice_ptr.as<uint32_t>();
   const uint32_t nb = uint32_t((c->dims[c->mode_order[1]] + BB - 1) / BB);
-  *nblocks_out = nb;
-  Scratch flag((M + 1) * 4, st);
-  k_csl_segflags<<<grid_for(M, 256), 256, 0, st>>>(j, M, BB, flag.as<uint32_t>());
-  k_csl_slicestarts<<<grid_for(S, 256), 256, 0, st>>>(sptr, S, flag.as<uint32_t>());
+  out.nblocks = nb;
+  Scratch pos((M + 2) * 4, st);
+  k_csl_segflags<<<grid_for(M, 256), 256, 0, st>>>(j, M, BB, pos.as<uint32_t>());
+  k_csl_slicestarts<<<grid_for(S, 256), 256, 0, st>>>(sptr, S, pos.as<uint32_t>());
   check_launch("k_csl_segflags");
-  const uint32_t G = exclusive_scan_total(flag.as<uint32_t>(), M, st);
+  const uint32_t G = exclusive_scan_total(pos.as<uint32_t>(), M, st);
+  out.G = G;
   Scratch start(size_t(G) * 4, st), sslice(size_t(G) * 4, st), sblock(size_t(G) * 4, st),
-      sntask(size_t(G) * 4, st), pos((size_t(G) + 1) * 4, st), slice_nt((S + 1) * 4, st),
-      slice_slot((S + 1) * 4, st);
-  k_csl_segs<<<grid_for(M, 256), 256, 0, st>>>(flag.as<uint32_t>(), M, start.as<uint32_t>());
-  HBK_CUDA(cudaMemsetAsync(slice_nt.p, 0, (S + 1) * 4, st));
+      slen(size_t(G) * 4, st);
+  k_csl_segs<<<grid_for(M, 256), 256, 0, st>>>(pos.as<uint32_t>(), M, start.as<uint32_t>());
   k_csl_seginfo<<<grid_for(G, 256), 256, 0, st>>>(start.as<uint32_t>(), G, uint32_t(M), sptr, S, j,
-                                                  BB, T, sslice.as<uint32_t>(),
-                                                  sblock.as<uint32_t>(), sntask.as<uint32_t>(),
-                                                  slice_nt.as<uint32_t>());
+                                                  BB, sslice.as<uint32_t>(), sblock.as<uint32_t>(),
+                                                  slen.as<uint32_t>());
   check_launch("k_csl_seginfo");
-  k_gt1_flags<<<grid_for(S, 256), 256, 0, st>>>(slice_nt.as<uint32_t>(), S, slice_slot.as<uint32_t>());
-  const uint32_t nslot = exclusive_scan_total(slice_slot.as<uint32_t>(), S, st);
-  HBK_CUDA(cudaMemcpyAsync(pos.p, sntask.p, size_t(G) * 4, cudaMemcpyDeviceToDevice, st));
-  const uint32_t ntask = exclusive_scan_total(pos.as<uint32_t>(), G, st);
-  bt.tasks = Scratch(size_t(std::max<uint32_t>(ntask, 1)) * sizeof(Task), st);
-  uint32_t base = 0;
-  for (uint32_t b = 0; b < nb; ++b) {
-    k_select_count<<<grid_for(G, 256), 256, 0, st>>>(sblock.as<uint32_t>(), sntask.as<uint32_t>(),
-                                                     G, b, pos.as<uint32_t>());
-    const uint32_t nb_tasks = exclusive_scan_total(pos.as<uint32_t>(), G, st);
-    if (nb_tasks) {
-      k_csl_seg_tasks<<<grid_for(G, 256), 256, 0, st>>>(
-          start.as<uint32_t>(), G, uint32_t(M), sslice.as<uint32_t>(), sblock.as<uint32_t>(),
-          sntask.as<uint32_t>(), pos.as<uint32_t>(), b, base, slice_nt.as<uint32_t>(),
-          slice_slot.as<uint32_t>(), slot_base, bt.tasks.as<Task>());
-      check_launch("k_csl_seg_tasks");
-    }
-    base += nb_tasks;
+  // segments are in (slice, block) order; a stable sort by block gives (block, slice)
+  Scratch keys_b(size_t(G) * 4, st), order(size_t(G) * 4, st), iota(size_t(G) * 4, st);
+  k_iota_u32<<<grid_for(G, 256), 256, 0, st>>>(iota.as<uint32_t>(), G);
+  int bits = 1;
+  while ((uint64_t(1) << bits) < nb) ++bits;
+  size_t tmp = 0;
+  HBK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, sblock.as<uint32_t>(), keys_b.as<uint32_t>(),
+                                           iota.as<uint32_t>(), order.as<uint32_t>(), int(G), 0, bits, st));
+  {
+    Scratch t(tmp, st);
+    HBK_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, sblock.as<uint32_t>(), keys_b.as<uint32_t>(),
+                                             iota.as<uint32_t>(), order.as<uint32_t>(), int(G), 0, bits,
+                                             st));
   }
-  HBK_REQUIRE(base == ntask, HBK_ECUDA, "CSL block task accounting mismatch");
-  bt.n = ntask;
-  bt.slots = nslot;
-  return bt;
+  Scratch vstart((size_t(G) + 1) * 4, st), rank_of(size_t(G) * 4, st);
+  out.sidx = dalloc(size_t(std::max<uint32_t>(G, 1)) * 4, st);
+  k_csl_vslices<<<grid_for(G, 256), 256, 0, st>>>(order.as<uint32_t>(), G, slen.as<uint32_t>(),
+                                                  sslice.as<uint32_t>(), c->slice_idx.as<uint32_t>(),
+                                                  vstart.as<uint32_t>(), out.sidx.as<uint32_t>(),
+                                                  rank_of.as<uint32_t>());
+  check_launch("k_csl_vslices");
+  const uint32_t total = exclusive_scan_total(vstart.as<uint32_t>(), G, st);
+  HBK_REQUIRE(total == uint32_t(M), HBK_ECUDA, "blocked CSL layout accounting mismatch");
+  out.pairs = dalloc(size_t(M) * sizeof(uint2), st);
+  out.j = dalloc(size_t(M) * 4, st);
+  k_csl_vscatter<<<grid_for(M, 256), 256, 0, st>>>(pos.as<uint32_t>(), start.as<uint32_t>(),
+                                                   rank_of.as<uint32_t>(), vstart.as<uint32_t>(),
+                                                   c->rest[1].as<uint32_t>(), j, c->v32.as<float>(), M,
+                                                   out.pairs.as<uint2>(), out.j.as<uint32_t>());
+  check_launch("k_csl_vscatter");
+  // tasks: runs of whole virtual slices, long ones chunked (slot fields only
+  // mark chunks: partial rows are added with atomics, no accumulator slots)
+  out.tasks = bucket_tasks(vstart.as<uint32_t>(), nullptr, nullptr, G, uint32_t(M), T, st);
+  return out;
 }
 
 struct HeavyLayout {
@@ -1581,7 +1619,8 @@ static int fast_occupancy(const hbk_plan* p, int k) {
   if (k == 0)
     fn = reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF_BPOS4, FX>);
   else if (k == 1)
-    fn = reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSL, FX>);
+    fn = p->csl_acc ? reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSL_ACC, FX>)
+                    : reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSL, FX>);
   else if (k == 2)
     fn = reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_COO, FX>);
   else
@@ -1784,22 +1823,21 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
                                                            uint32_t(slots));
       check_launch("k_shift_slots");
     }
-    // B-row blocking of the fast CSL tasks (opt-in: HBK_CSL_BLOCK_MB = MB of
-    // B rows per block).  Measured on delicious-3d: 96 MB blocks -7% on mode
-    // 0, smaller blocks up to 3x slower (per-slice segments become tiny tasks
-    // with split hand-overs), so it is off by default.
-    if (p->fast) {
-      double mb = 0.0;
-      if (const char* e = getenv("HBK_CSL_BLOCK_MB")) mb = atof(e);
-      const int64_t BB = std::max<int64_t>(1, int64_t(mb * 1e6 / (R * 4.0)));
-      if (mb > 0 && s->dims[s->mode_order[1]] > BB) {
-        int64_t nb = 0;
-        tcsl_fast = csl_block_tasks(s, uint32_t(BB), Tcsl, uint32_t(slots), &nb, st);
-        csl_blocked = nb > 1;
-        p->info.csl_blocks = nb;
-      }
+    // blocked CSL layout (block size chosen in hbk_plan_create): the fast
+    // kernel runs the block-major virtual slices and accumulates rows, so it
+    // needs no accumulator slots
+    if (p->fast && p->csl_bb > 0) {
+      BlockedCsl bl = csl_blocked_layout(s, uint32_t(p->csl_bb), Tcsl, st);
+      p->vcsl_pairs = bl.pairs;
+      p->vcsl_j = bl.j;
+      p->vcsl_sidx = bl.sidx;
+      p->vcsl_S = uint32_t(bl.G);
+      tcsl_fast = std::move(bl.tasks);
+      csl_blocked = true;
+      p->csl_acc = true;
+      p->info.csl_blocks = bl.nblocks;
     }
-    slots += std::max(tcsl.slots, csl_blocked ? tcsl_fast.slots : int64_t(0));
+    slots += tcsl.slots;
     w.csl_send = s->slice_ptr.as<uint32_t>();
     w.csl_sidx = s->slice_idx.as<uint32_t>();
     w.csl_j = s->rest[0].as<uint32_t>();
@@ -1935,6 +1973,12 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     wg.n2 = keep.n2;
     wg.n3 = keep.n3;
     wg.tasks = keep.tasks;
+  }
+  if (p->csl_acc) {  // the fast kernels read the block-major CSL stream
+    w.csl_pairs = p->vcsl_pairs.as<uint2>();
+    w.csl_j = p->vcsl_j.as<uint32_t>();
+    w.csl_sidx = p->vcsl_sidx.as<uint32_t>();
+    w.csl_S = p->vcsl_S;
   }
 
   // persistent grid: as many CTAs as fit, a multiple of the SM count
@@ -2115,7 +2159,10 @@ static void launch_fast(const hbk_plan* p, const FX& fx, cudaStream_t st, bool s
   }
   if (p->grids[1]) {
     cudaStream_t s2 = next_stream();
-    k_mttkrp3_r32<KIND_CSL, FX><<<p->grids[1], p->block, 0, s2>>>(p->work, fx);
+    if (p->csl_acc)
+      k_mttkrp3_r32<KIND_CSL_ACC, FX><<<p->grids[1], p->block, 0, s2>>>(p->work, fx);
+    else
+      k_mttkrp3_r32<KIND_CSL, FX><<<p->grids[1], p->block, 0, s2>>>(p->work, fx);
   }
   // skip_zero: the rows no bucket owns are left unwritten (COO tasks only)
   Work wc = p->work;
@@ -2219,6 +2266,41 @@ static hbk_csf* merge_csl_as_csf(const hbk_csf* c, const hbk_csl* l, cudaStream_
 }
 }  // namespace hbk
 
+namespace hbk {
+// B rows per block of the blocked CSL layout, 0 = unblocked.  Blocked when the
+// CSL bucket holds at least half of the plan's nonzeros and its B factor's
+// rows (the 32-column slice a pass reads) exceed half the L2: blocks of about
+// 0.18 x L2 (delicious-3d, ms per mode for 8/12/16/20/24/32/40/60/80 MB
+// blocks: mode 0 3.31/3.17/3.07/3.03/3.03/3.05/3.11/3.28/3.48 vs 4.05
+// unblocked, mode 2 3.39/3.19/3.09/3.05/3.00/3.07/3.05/3.31/3.24 vs 3.22).
+// The emulation before it (scripts/remap_block_probe.py) measured the
+// configurations this rule leaves unblocked 2-4% slower blocked.
+// HBK_CSL_BLOCK_MB=x forces x-MB blocks (0 = off), for A/B measurement.
+static int64_t csl_block_rows(const hbk_csl* csl, const hbk_csf* csf, const hbk_coo* coo, int rank,
+                              bool eligible) {
+  if (!csl || csl->M == 0 || !eligible) return 0;
+  const int64_t Brows = csl->dims[csl->mode_order[1]];
+  const double row_bytes = 4.0 * std::min(rank, 32);
+  double mb = -1.0;
+  if (const char* e = getenv("HBK_CSL_BLOCK_MB")) mb = atof(e);
+  if (mb == 0.0) return 0;
+  int64_t BB = 0;
+  if (mb > 0.0) {
+    BB = std::max<int64_t>(1, int64_t(mb * 1e6 / row_bytes));
+  } else {
+    const int64_t total = csl->M + (csf ? csf->M : 0) + (coo ? coo->nnz : 0);
+    int dev = 0, l2 = 0;
+    HBK_CUDA(cudaGetDevice(&dev));
+    HBK_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    const double bbytes = double(Brows) * row_bytes;
+    if (2 * csl->M < total || l2 <= 0 || bbytes <= 0.5 * l2) return 0;
+    const int64_t nb = int64_t(std::ceil(bbytes / (0.18 * l2)));
+    BB = (Brows + nb - 1) / nb;
+  }
+  return BB < Brows ? BB : 0;
+}
+}  // namespace hbk
+
 int hbk_plan_create(hbk_coo* coo, hbk_csl* csl, hbk_csf* csf, hbk_sched* sched, int mode, int rank,
                     void* stream, hbk_plan** out) {
   return guarded([&] {
@@ -2281,8 +2363,9 @@ int hbk_plan_create(hbk_coo* coo, hbk_csl* csl, hbk_csf* csf, hbk_sched* sched, 
       // delicious-3d mode 0, 5.6% faster); lighter CSL slices stay on the CSL
       // kernel, measured 2% faster for them (delicious mode 2, 56 per slice)
       const bool heavy_csl = csl && csl->M > 128 * csl->S;
+      p->csl_bb = csl_block_rows(csl, csf, coo, rank, fast_shape && !sched);
       if (csl && csl->M > 0 && !sched && fast_shape && (!csf || csf->order == 3) &&
-          (e ? atoi(e) != 0 : heavy_csl)) {
+          (e ? atoi(e) != 0 : heavy_csl && p->csl_bb == 0)) {
         hbk_csf* merged = merge_csl_as_csf(csf, csl, st);
         hbk_csf_release(p->csf);
         hbk_csl_release(p->csl);
@@ -2328,6 +2411,9 @@ int hbk_plan_execute_ex(const hbk_plan* p, const float* const* factors, float* o
                       0,
                   HBK_EINVAL, "factor and output buffers must be 16-byte aligned");
       const int R = p->rank;
+      // the blocked CSL layout adds its rows into the output
+      if (p->csl_acc)
+        HBK_CUDA(cudaMemsetAsync(out, 0, size_t(p->dims[p->mode]) * R * sizeof(float), st));
       if (p->r32) {
         launch_fast(p, Factors3R32(fx), st, skip_zero);
       } else {

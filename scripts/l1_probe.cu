@@ -123,6 +123,10 @@ __global__ void k_g8(const float4* __restrict__ F, const uint2* __restrict__ s, 
         r[j] = ld128_l2h(F + size_t(k) * 8 + lig, pol);
       else if (SCAN == 4)
         r[j] = ld128_plain(F + size_t(k) * 8 + lig);
+      else if (SCAN == 5 && int(k) >= H)  // cold rows (frequency rank >= H): no L1 allocation
+        r[j] = ld128_na(F + size_t(k) * 8 + lig);
+      else if (SCAN == 6 && int(k) >= H)  // cold rows: L1 evict-first
+        r[j] = ld128_ef(F + size_t(k) * 8 + lig);
       else
         r[j] = ld128(F + size_t(k) * 8 + lig);
     }
@@ -275,6 +279,20 @@ int main(int argc, char** argv) {
       run(nm, [&] { k_g8<false, 4><<<sms * (wps / 8), 256>>>(reinterpret_cast<float4*>(F), ds, n, 0, sink); });
       snprintf(nm, sizeof nm, "g8 L1el %d w/SM", wps);
       run(nm, [&] { k_g8<false, 0><<<sms * (wps / 8), 256>>>(reinterpret_cast<float4*>(F), ds, n, 0, sink); });
+    }
+    return 0;
+  }
+  if (argc > 3 && std::string(argv[3]) == "hotsplit") {  // L1 allocation by row hotness
+    for (int wps : {24, 32}) {
+      char nm[64];
+      snprintf(nm, sizeof nm, "g8 plain %d w/SM", wps);
+      run(nm, [&] { k_g8<false, 0><<<sms * (wps / 8), 256>>>(reinterpret_cast<float4*>(F), ds, n, 0, sink); });
+      for (int H : {256, 512, 1024, 1536, 2048, 3072, 4096}) {
+        snprintf(nm, sizeof nm, "g8 cold-NA H=%d %d w/SM", H, wps);
+        run(nm, [&] { k_g8<false, 5><<<sms * (wps / 8), 256>>>(reinterpret_cast<float4*>(F), ds, n, H, sink); });
+        snprintf(nm, sizeof nm, "g8 cold-EF H=%d %d w/SM", H, wps);
+        run(nm, [&] { k_g8<false, 6><<<sms * (wps / 8), 256>>>(reinterpret_cast<float4*>(F), ds, n, H, sink); });
+      }
     }
     return 0;
   }

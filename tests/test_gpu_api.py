@@ -345,33 +345,43 @@ def test_nonfinite_scan(n, offset):
 
 
 @pytest.mark.parametrize("block_mb", ["0.002", "0.0005"])
-def test_csl_b_row_blocking_parity(hb, rng, block_mb, monkeypatch):
-    """The fast CSL path cut into per-B-block segments (tasks ordered by
-    block, split slices handed over through the accumulator) gives the
-    oracle's rows.  Tiny blocks force many segments per slice."""
+@pytest.mark.parametrize("rank", [32, 16, 64])
+def test_csl_b_row_blocking_parity(hb, rng, block_mb, rank, monkeypatch):
+    """The blocked CSL layout (block-major virtual slices, rows accumulated
+    with atomics into the zeroed output) gives the oracle's rows, also into a
+    dirty output buffer, for R = 32 and the multi-pass ranks.  Tiny blocks
+    force many segments per slice and chunked long segments."""
+    import torch
+
+    from paper_1904_03329_b200.kernels import mttkrp_device, plan_for
+
     monkeypatch.setenv("HBK_CSL_BLOCK_MB", block_mb)
     monkeypatch.setenv("HBK_CSL_AS_CSF", "0")  # the CSL kernel itself
     dims = (60, 500, 400)
-    # CSL-dominated: distinct (j, k) per slice, so every fiber is a singleton
+    # CSL-dominated: distinct (j, k) per slice, so every fiber is a singleton;
+    # slice 0 is long (chunked virtual slices)
     n = 6000
-    i = rng.integers(0, 60, n)
-    j = rng.integers(0, 500, n)
-    k = rng.integers(0, 400, n)
+    i = np.concatenate([rng.integers(0, 60, n), np.zeros(1500, np.int64)])
+    j = rng.integers(0, 500, n + 1500)
+    k = rng.integers(0, 400, n + 1500)
     idx = np.stack([i, j, k], 1).astype(np.uint32)
-    idx, vals = P.canonical(idx, rng.uniform(0.1, 1.0, n))
+    idx, vals = P.canonical(idx, rng.uniform(0.1, 1.0, n + 1500))
     t = hb.CooTensor(dims, idx, vals)
-    f = [rng.random((d, 32)).astype(np.float32).astype(np.float64) for d in dims]
+    f = [rng.random((d, rank)).astype(np.float32).astype(np.float64) for d in dims]
+    fd = [torch.from_numpy(x).float().cuda() for x in f]
     for mode in range(3):
         mo = hb.allmode_order(dims, mode)
         h = hb.build_hbcsf(t, mo)
-        from paper_1904_03329_b200.kernels import plan_for
-
-        pl = plan_for(h, mode, 32)
-        if h.csl_part.nnz and dims[mo[1]] * 128 > float(block_mb) * 1e6:
+        pl = plan_for(h, mode, rank)
+        if h.csl_part.nnz and dims[mo[1]] * 4 * min(rank, 32) > float(block_mb) * 1e6:
             assert pl.info.csl_blocks > 1
-        y, _ = hb.mttkrp_hbcsf(h, f, mode)
         ref, _ = P.mttkrp_hbcsf(P.hbcsf(idx, vals, dims, mo), f, mode)
+        y, _ = hb.mttkrp_hbcsf(h, f, mode)
         assert P.row_deviation(y, ref) <= 1e-4
+        out = torch.full((dims[mode], rank), 3.0, device="cuda")
+        for _ in range(2):  # repeated executions into the same (dirty) buffer
+            mttkrp_device(h, fd, mode, out=out)
+        assert P.row_deviation(out.double().cpu().numpy(), ref) <= 1e-4
 
 
 def test_execute_captures_into_cuda_graph(hb, rng):
