@@ -1645,21 +1645,16 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
            p->dims[p->mo[1]] < (int64_t(1) << 27);
   p->bshift = p->r32 ? 3u : 0u;
   const int gpw = p->fast ? 4 : 1;  // task ranges padded so a warp never straddles kinds
-  uint32_t task_nnz = TASK_NNZ_CSF;
-  if (const char* e = getenv("HBK_TASK_NNZ")) task_nnz = std::max(8, atoi(e));
-  const uint32_t Tcsf = p->fast ? task_nnz : GEN_TASK_NNZ;
+  const uint32_t Tcsf = p->fast ? TASK_NNZ_CSF : GEN_TASK_NNZ;
   // CSL runs: 256 nonzeros when the CSL slices average >= 48 (delicious-3d
   // mode 2, 56 per slice: -5%), else 128 (flickr / nell-1, 4-36 per slice)
   uint32_t Tcsl = GEN_TASK_NNZ;
   if (p->fast) {
     Tcsl = (p->csl && p->csl->S && p->csl->M >= 48 * p->csl->S) ? 2 * TASK_NNZ_CSL : TASK_NNZ_CSL;
-    if (const char* e = getenv("HBK_TASK_NNZ_CSL")) Tcsl = uint32_t(std::max(8, atoi(e)));
   }
-  uint32_t Tcoo = p->fast ? TASK_NNZ_COO : GEN_TASK_NNZ;
-  if (const char* e = getenv("HBK_TASK_NNZ_COO"))
-    if (p->fast) Tcoo = uint32_t(std::max(8, atoi(e)));
-  uint32_t Tzero = TASK_ROWS_ZERO;
-  if (const char* e = getenv("HBK_TASK_ROWS_ZERO")) Tzero = uint32_t(std::max(8, atoi(e)));
+  // COO / zero-row task sizes: 64-128 and 64-1024 measured within +-2%
+  const uint32_t Tcoo = p->fast ? TASK_NNZ_COO : GEN_TASK_NNZ;
+  const uint32_t Tzero = TASK_ROWS_ZERO;
 
   Work& w = p->work;
   std::memset(&w, 0, sizeof(w));
@@ -1671,10 +1666,9 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   // (schedule units run through the same light-slice B-position kernel)
   p->bpos = p->fast;
   const uint32_t heavy_H = Tcsf;
-  uint32_t heavy_tau = 32, heavy_W = 1024;
-  if (const char* e = getenv("HBK_HEAVY_TAU")) heavy_tau = uint32_t(std::min(65535, std::max(1, atoi(e))));
-  if (const char* e = getenv("HBK_HEAVY_W")) heavy_W = uint32_t(std::max(1, atoi(e)));
-  heavy_W = std::max(heavy_W, heavy_tau);
+  // segment length tau and warp-task size W of the heavy layout (W 1024 vs
+  // 2048: nell-2 -0.9%, others +-0.2%)
+  const uint32_t heavy_tau = 32, heavy_W = 1024;
   // A schedule (mttkrp_scheduled / mttkrp_hbcsf(schedule=...)) fixes the
   // OpCount and which slices are split; on the B-position path its slices run
   // through the same layout as the default plan: single-unit slices whole,
@@ -2012,7 +2006,6 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
       wh.csf_fidx = p->heavy_fj.as<uint32_t>();
       wh.csf_F = uint32_t(heavy_segments);
       per_sm = fast_occupancy_any(p, 3);
-      if (const char* e = getenv("HBK_HEAVY_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
       p->grid_heavy = grid_for_tasks(heavy_ntasks, per_sm, 4);
       wh.total_warps[0] = uint32_t(p->grid_heavy) * (p->block / 32);
       launches += 1;
