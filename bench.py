@@ -12,8 +12,9 @@ tensor, inputs resident in HBM.  Default workload: BASELINE.json configs[1]
 
 N>1: launched by torchrun (one rank per GPU, NCCL) — or, when WORLD_SIZE is
 unset, bench.py launches torchrun itself.  Each mode's output slices are
-sharded across ranks by nonzero count (contiguous row ranges; no collective
-in the timed region); time = max over ranks; value = all ranks' flops / that
+sharded across ranks in contiguous row ranges balanced by cost (nonzeros +
+fibers + a per-row charge, shard.partition_costs; no collective in the timed
+region); time = max over ranks; value = all ranks' flops / that
 time.  ``with_output_allgather`` repeats the steps with the all-gather of
 every mode's output rows.  ``cpd``: the config-5 CP-ALS sweep (nell-1,
 MTTKRP of all modes + row update + factor-row exchange) on the same N ranks.
@@ -364,7 +365,7 @@ def prepare(env, name, args, fmt="hbcsf", tensor=None):
         mo = hb.allmode_order(dims, mode)
         if env.world > 1:
             # this rank's output rows, rebased: its plan writes only them
-            ranges_m = shard.plan_row_ranges(shard.slice_histogram(t, mode).cpu().numpy(), env.world)
+            ranges_m = shard.plan_row_ranges(shard.partition_costs(t, mode).cpu().numpy(), env.world)
             st["all_ranges"].append(ranges_m)
             rr = ranges_m[env.rank]
             part = shard.shard_rows(t, mode, rr[0], rr[1]) if rr[1] > rr[0] else None

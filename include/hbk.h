@@ -323,6 +323,12 @@ int hbk_als_update_rows(const float* Y, const uint32_t* list, int64_t nlist, int
  * Multi-GPU partitioner: slice nnz histogram of `mode`.
  * hist [dev] int64 [dims[mode]] is overwritten.                            */
 int hbk_coo_slice_histogram(const hbk_coo* t, int mode, int64_t* hist, void* stream);
+/* Fibers per slice: the number of distinct (mode, mid_mode) coordinate
+ * pairs of every mode-`mode` slice, i.e. the leaf-parent count of each slice
+ * of the CSF tree ordered (mode, mid_mode, ...) (formats.py:143-162) — the
+ * partitioner's cost model charges a slice its nonzeros plus its fibers (one
+ * gathered factor row each).  hist [dev] int64 [dims[mode]] is overwritten. */
+int hbk_coo_fiber_histogram(const hbk_coo* t, int mode, int mid_mode, int64_t* hist, void* stream);
 /* Keep only entries whose `mode` coordinate lies in [row_begin, row_end)
  * (coordinates and dims unchanged). */
 int hbk_coo_select_rows(const hbk_coo* t, int mode, int64_t row_begin, int64_t row_end,

@@ -140,6 +140,7 @@ _SIGS = {
     "hbk_plan_execute_f64": ([vp, vp, vp, vp], C.c_int),
     "hbk_plan_release": ([vp], None),
     "hbk_coo_slice_histogram": ([vp, C.c_int, vp, vp], C.c_int),
+    "hbk_coo_fiber_histogram": ([vp, C.c_int, C.c_int, vp, vp], C.c_int),
     "hbk_coo_select_rows": ([vp, C.c_int, i64, i64, vp, C.POINTER(vp)], C.c_int),
     "hbk_coo_shard_rows": ([vp, C.c_int, i64, i64, vp, C.POINTER(vp)], C.c_int),
     "hbk_plan_probe": ([vp, vp, vp], C.c_int),

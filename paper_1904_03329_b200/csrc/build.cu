@@ -1612,6 +1612,50 @@ extern "C" int hbk_coo_slice_histogram(const hbk_coo* t, int mode, int64_t* hist
   });
 }
 
+namespace hbk {
+__global__ void k_pair_keys(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, int64_t M,
+                            uint64_t* __restrict__ key) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
+       i += int64_t(gridDim.x) * blockDim.x)
+    key[i] = (uint64_t(a[i]) << 32) | b[i];
+}
+// one count per distinct (slice, mid) pair, into its slice
+__global__ void k_distinct_hist(const uint64_t* __restrict__ key, int64_t M,
+                                unsigned long long* __restrict__ hist) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
+       i += int64_t(gridDim.x) * blockDim.x)
+    if (i == 0 || key[i] != key[i - 1]) atomicAdd(hist + (key[i] >> 32), 1ull);
+}
+}  // namespace hbk
+
+extern "C" int hbk_coo_fiber_histogram(const hbk_coo* t, int mode, int mid_mode, int64_t* hist,
+                                       void* stream) {
+  return guarded([&] {
+    HBK_REQUIRE(mode >= 0 && mode < t->order && mid_mode >= 0 && mid_mode < t->order &&
+                    mid_mode != mode,
+                HBK_EINVAL, "mode out of range");
+    cudaStream_t st = to_stream(stream);
+    HBK_CUDA(cudaMemsetAsync(hist, 0, t->dims[mode] * sizeof(int64_t), st));
+    const int64_t M = t->nnz;
+    if (M == 0) return;
+    Scratch ka(M * 8, st), kb(M * 8, st);
+    k_pair_keys<<<grid_for(M, 256), 256, 0, st>>>(t->cols[mode].as<uint32_t>(),
+                                                  t->cols[mid_mode].as<uint32_t>(), M,
+                                                  ka.as<uint64_t>());
+    check_launch("k_pair_keys");
+    int hi_bits = 1;
+    while ((int64_t(1) << hi_bits) < t->dims[mode]) ++hi_bits;
+    size_t tmp = 0;
+    cub::DoubleBuffer<uint64_t> kbuf(ka.as<uint64_t>(), kb.as<uint64_t>());
+    HBK_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, kbuf, int(M), 0, 32 + hi_bits, st));
+    Scratch t_(tmp, st);
+    HBK_CUDA(cub::DeviceRadixSort::SortKeys(t_.p, tmp, kbuf, int(M), 0, 32 + hi_bits, st));
+    k_distinct_hist<<<grid_for(M, 256), 256, 0, st>>>(kbuf.Current(), M,
+                                                      reinterpret_cast<unsigned long long*>(hist));
+    check_launch("k_distinct_hist");
+  });
+}
+
 static hbk_coo* coo_rows(const hbk_coo* t, int mode, int64_t lo, int64_t hi, bool rebase,
                          cudaStream_t st) {
     HBK_REQUIRE(mode >= 0 && mode < t->order, HBK_EINVAL, "mode out of range");

@@ -4,8 +4,9 @@ One process per GPU (torchrun), ``torch.distributed`` for the plumbing
 (NCCL on the GPUs, gloo for the CPU tests).  The algorithm is the reference's
 ``cp_als`` (cpd.py:198-271) with every mode's rows partitioned:
 
-* mode n's output rows are cut into contiguous ranges balanced by nonzero
-  count (``shard.plan_row_ranges``); rank g owns rows [lo_g, hi_g) of
+* mode n's output rows are cut into contiguous ranges balanced by cost —
+  nonzeros + fibers + a per-row charge (``shard.partition_costs``,
+  ``shard.plan_row_ranges``); rank g owns rows [lo_g, hi_g) of
   factor n and builds the HB-CSF of the entries in that range only
   (``hbk_coo_shard_rows``: rebased, so its MTTKRP writes exactly those rows);
 * the MTTKRP of a mode needs no communication (slices are independent,
@@ -78,8 +79,7 @@ class DeviceShards:
         # needed_by[mode][d]: rows of factor d this rank's shard of `mode` reads
         self.needed_by = [[None] * t.order for _ in range(t.order)]
         for mode in range(t.order):
-            hist = shard.slice_histogram(t, mode).cpu().numpy()
-            ranges = plan_row_ranges(hist, world)
+            ranges = plan_row_ranges(shard.partition_costs(t, mode).cpu().numpy(), world)
             lo, hi = ranges[me]
             self.ranges.append(ranges)
             if hi > lo:

@@ -2,9 +2,15 @@
 
 Output-mode slices are independent (each output row depends only on its
 slice's nonzeros, kernels.py:154-186), so a mode is sharded into contiguous
-row ranges balanced by nonzero count; each rank builds the HB-CSF of its
-shard and produces its rows with no data-path collective.  The exchanges of
-the row-sharded CP-ALS live in distributed.py.
+row ranges; each rank builds the HB-CSF of its shard and produces its rows
+with no data-path collective.  The ranges balance a cost, not the nonzero
+count: a slice costs its gathered factor rows (nonzeros + fibers) plus
+ROW_COST per output row (empty rows included).  Balancing nonzeros alone left
+the rank holding the long tail of light and empty slices 2-3x slower than the
+others at 8 ranks (nell-1 mode 2: 22.1M of 25.5M rows on the last rank); the
+per-rank timings behind ROW_COST are in scripts/shard_scaling.py's log
+(profiles/r2s3/shard_scaling*.log).  The exchanges of the row-sharded CP-ALS
+live in distributed.py.
 
 The range planner is a pure function (unit-tested on CPU).
 """
@@ -15,13 +21,19 @@ import ctypes as C
 import numpy as np
 
 from . import _native as N
-from .coo import CooTensor
+from .coo import CooTensor, allmode_order
+
+# gathered-row equivalents per output row: least-squares fit of per-rank MTTKRP
+# times (configs 2-5, 2/4/8 ranks) to gathered rows and output rows gives
+# 0.0095-0.0117 ms per M gathered rows and 0.024-0.085 ms per M rows
+ROW_COST = 4
 
 
 def plan_row_ranges(slice_nnz, parts: int) -> list[tuple[int, int]]:
     """Split rows [0, len(slice_nnz)) into `parts` contiguous ranges whose
-    nonzero counts are as even as whole slices allow: boundary g is the first
-    row whose prefix count reaches g*M/parts (lower_bound on the prefix sum)."""
+    weights (nonzero counts, or partition_costs) are as even as whole slices
+    allow: boundary g is the first row whose prefix weight reaches
+    g*M/parts (lower_bound on the prefix sum)."""
     counts = np.asarray(slice_nnz, dtype=np.int64)
     rows = len(counts)
     if parts < 1:
@@ -35,6 +47,24 @@ def plan_row_ranges(slice_nnz, parts: int) -> list[tuple[int, int]]:
         cuts.append(min(max(b, cuts[-1]), rows))
     cuts.append(rows)
     return [(cuts[g], cuts[g + 1]) for g in range(parts)]
+
+
+def partition_costs(t: CooTensor, mode: int):
+    """Per-row cost of a mode's slices for plan_row_ranges: nonzeros + fibers
+    of the CSF tree in allmode_order (the factor rows the MTTKRP gathers for
+    the slice) + ROW_COST, on the device (int64 CUDA tensor)."""
+    mid = allmode_order(t.dims, mode)[1]
+    return slice_histogram(t, mode) + fiber_histogram(t, mode, mid) + ROW_COST
+
+
+def fiber_histogram(t: CooTensor, mode: int, mid_mode: int):
+    """Fibers per mode-``mode`` slice of the tree ordered (mode, mid_mode, ...):
+    distinct (mode, mid_mode) coordinate pairs, counted on the device."""
+    torch = N.require_device()
+    hist = torch.empty(t.dims[mode], dtype=torch.int64, device="cuda")
+    N.call("hbk_coo_fiber_histogram", t._dev().ptr, int(mode), int(mid_mode),
+           C.c_void_p(hist.data_ptr()), N.stream_ptr())
+    return hist
 
 
 def slice_histogram(t: CooTensor, mode: int):

@@ -75,7 +75,7 @@ def main():
                 pm = step_ms(st)
                 shard_nnz = [c["coo_nnz"] + c["csl_nnz"] + c["csf_nnz"] if c else 0 for c in st["census"]]
                 ranks.append({"rank": r, "ms": sum(pm), "per_mode_ms": pm, "shard_nnz": shard_nnz,
-                              "rows": st["rows_local"]})
+                              "rows": st["rows_local"], "census": st["census"]})
                 bench.free(st)
             worst = max(x["ms"] for x in ranks)
             eff = res["p1_ms"] / (P * worst)

@@ -598,3 +598,27 @@ def test_host_factor_errors_raised_before_launch(hb, rng):
         hb.mttkrp_hbcsf(h, bad, 0)
     again, _ = hb.mttkrp_hbcsf(h, f, 0)
     assert np.array_equal(ok, again)
+
+
+def test_fiber_histogram_matches_csf(hb, rng):
+    """hbk_coo_fiber_histogram: distinct (slice, mid) pairs per slice equal the
+    per-slice fiber counts of the CSF tree in that order (formats.py:143-162),
+    for every mode and both mid modes; partition_costs = nnz + fibers + ROW_COST."""
+    from paper_1904_03329_b200 import shard
+
+    dims = (70, 50, 90)
+    idx, vals = _powerlaw(rng, dims, 8000)
+    t = hb.CooTensor(dims, idx, vals)
+    for mode in range(3):
+        for mid in (d for d in range(3) if d != mode):
+            leaf = 3 - mode - mid
+            c = hb.build_csf(t, (mode, mid, leaf))
+            want = np.zeros(dims[mode], np.int64)
+            want[c.idxs[0]] = np.diff(c.ptrs[0])
+            got = shard.fiber_histogram(t, mode, mid).cpu().numpy()
+            assert np.array_equal(got, want)
+        nnz = np.bincount(idx[:, mode].astype(np.int64), minlength=dims[mode])
+        mid = hb.allmode_order(dims, mode)[1]
+        fib = shard.fiber_histogram(t, mode, mid).cpu().numpy()
+        cost = shard.partition_costs(t, mode).cpu().numpy()
+        assert np.array_equal(cost, nnz + fib + shard.ROW_COST)
