@@ -227,6 +227,9 @@ typedef struct {
   int64_t hot_rows;        /* reserved (0) */
   int64_t csl_blocks;      /* B-row blocks of the fast CSL task order (0/1 = unblocked) */
   int64_t gather_rows;     /* factor rows one execute gathers (B-position plans) */
+  int64_t leaf_blocks;     /* leaf-row blocks of the leaf-blocked heavy slices (0 = none) */
+  int64_t leaf_blocked_nnz; /* nonzeros in the leaf-blocked heavy slices */
+  int64_t leaf_head_share_ppm; /* share (ppm) of leaf accesses served by the rows a quarter of the L2 holds (leaf-blocking candidates) */
 } hbk_plan_info;
 
 int hbk_plan_create(hbk_coo* coo, hbk_csl* csl, hbk_csf* csf, hbk_sched* sched, int mode,

@@ -95,6 +95,9 @@ class PlanInfo(C.Structure):
         ("hot_rows", i64),
         ("csl_blocks", i64),
         ("gather_rows", i64),
+        ("leaf_blocks", i64),
+        ("leaf_blocked_nnz", i64),
+        ("leaf_head_share_ppm", i64),
     ]
 
 

@@ -21,6 +21,7 @@
 // the last chunk to finish (arrival counter) stores the row — so every output
 // row is written exactly once and no memset of the output is needed.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -267,7 +268,9 @@ __device__ __forceinline__ void flush_split(const Work& w, const FX& fx, bool ac
 // UNIFORM (padded heavy layout): the four groups' streams have identical
 // structure, so B positions are warp-uniform and take a uniform branch
 // instead of predicated FMAs; heavy tasks are slice chunks (no SEND).
-template <bool UNIFORM, class FX>
+// ACC (leaf-blocked view, csf_block_view): slice ends add the partial row
+// into the pre-zeroed output row (a slice is cut into several virtual slices).
+template <bool UNIFORM, bool ACC, class FX>
 __device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const FX& fx, const Task& t,
                                                  int g, int lig, uint64_t pol_s, uint64_t pol_r) {
   const uint32_t lo = t.lo, hi = t.hi;
@@ -330,7 +333,10 @@ __device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const FX& fx, co
       if ((sany >> j) & 1u) {
         const uint32_t row = __shfl_sync(FULL, sr_cur, ts, 8);
         if ((sbits >> j) & 1u) {
-          if (lane_live(fx, lig)) fx.out[size_t(row) * fx.rs + fx.col4 + lig] = sa;
+          if (lane_live(fx, lig)) {
+            float4* o = fx.out + size_t(row) * fx.rs + fx.col4 + lig;
+            if (ACC) red_add4(o, sa); else *o = sa;
+          }
           sa = f4zero();
           ++ts;
         }
@@ -491,11 +497,16 @@ static constexpr int FAST_BLOCK = 256;
 // KIND_CSF is the CSF bucket's task range and counters; its kernels are the
 // light-slice B-position kernel (KIND_CSF_BPOS4) and the heavy-slice
 // padded-layout kernel (KIND_CSF_UNI).
-// KIND_CSL_ACC: the CSL kernel over the blocked (block-major) CSL layout.
-enum { KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2, KIND_CSF_BPOS4 = 4, KIND_CSF_UNI = 5, KIND_CSL_ACC = 6 };
+// KIND_CSL_ACC: the CSL kernel over the blocked (block-major) CSL layout;
+// KIND_CSF_BPOS4_ACC / KIND_CSF_UNI_ACC: the CSF kernels over a leaf-blocked
+// view (rows accumulated).
+enum {
+  KIND_CSF = 0, KIND_CSL = 1, KIND_COO = 2, KIND_CSF_BPOS4 = 4, KIND_CSF_UNI = 5, KIND_CSL_ACC = 6,
+  KIND_CSF_BPOS4_ACC = 7, KIND_CSF_UNI_ACC = 8
+};
 
 template <int KIND, class FX>
-__global__ void __launch_bounds__(FAST_BLOCK, KIND == KIND_CSF_UNI ? 3 : (KIND == KIND_CSF_BPOS4 ? 4 : 3))
+__global__ void __launch_bounds__(FAST_BLOCK, (KIND == KIND_CSF_BPOS4 || KIND == KIND_CSF_BPOS4_ACC) ? 4 : 3)
     k_mttkrp3_r32(const __grid_constant__ Work w, const __grid_constant__ FX fx) {
   // per lane: 8 slots of 16 B (one per batch position) for staged B rows
   __shared__ float4 s_slots[FAST_BLOCK * 8];
@@ -506,14 +517,16 @@ __global__ void __launch_bounds__(FAST_BLOCK, KIND == KIND_CSF_UNI ? 3 : (KIND =
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_r = policy_evict_last();
   static_assert(KIND != KIND_CSF, "CSF tasks run through KIND_CSF_BPOS4 / KIND_CSF_UNI");
-  constexpr int K = (KIND == KIND_CSF_BPOS4 || KIND == KIND_CSF_UNI) ? KIND_CSF
-                    : KIND == KIND_CSL_ACC                          ? KIND_CSL
-                                                                    : KIND;
+  constexpr bool UNI = KIND == KIND_CSF_UNI || KIND == KIND_CSF_UNI_ACC;
+  constexpr bool ACC = KIND == KIND_CSL_ACC || KIND == KIND_CSF_BPOS4_ACC || KIND == KIND_CSF_UNI_ACC;
+  constexpr int K = (KIND == KIND_CSF_BPOS4 || KIND == KIND_CSF_BPOS4_ACC || UNI) ? KIND_CSF
+                    : KIND == KIND_CSL_ACC                                       ? KIND_CSL
+                                                                                 : KIND;
   const uint32_t first = K == KIND_CSF ? 0u : (K == KIND_CSL ? w.n0 : w.n1);
   const uint32_t last = K == KIND_CSF ? w.n0 : (K == KIND_CSL ? w.n1 : w.n3);
   // the heavy-slice launch has its own counter pair (words 6, 7) so it can
   // run concurrently with the light-slice launch
-  uint32_t* ctr = w.ws_ctr + 2 * (KIND == KIND_CSF_UNI ? 3 : K);
+  uint32_t* ctr = w.ws_ctr + 2 * (UNI ? 3 : K);
   for (;;) {
     uint32_t base = 0;
     if (lane == 0) base = atomicAdd(ctr, 4u);
@@ -522,21 +535,26 @@ __global__ void __launch_bounds__(FAST_BLOCK, KIND == KIND_CSF_UNI ? 3 : (KIND =
     const Task t = w.tasks[base + g];
     if (K == KIND_CSF || K == KIND_CSL) {
       const float4 sa =
-          KIND == KIND_CSF_UNI     ? csf_bpos_tasks<true>(w, fx, t, g, lig, pol_s, pol_r)
-          : KIND == KIND_CSF_BPOS4 ? csf_bpos_tasks<false>(w, fx, t, g, lig, pol_s, pol_r)
-          : KIND == KIND_CSL_ACC   ? csl_tasks<true>(w, fx, t, g, lig, pol_s, pol_r, slots)
-                                   : csl_tasks<false>(w, fx, t, g, lig, pol_s, pol_r, slots);
+          UNI                           ? csf_bpos_tasks<true, ACC>(w, fx, t, g, lig, pol_s, pol_r)
+          : K == KIND_CSF               ? csf_bpos_tasks<false, ACC>(w, fx, t, g, lig, pol_s, pol_r)
+                                        : csl_tasks<ACC>(w, fx, t, g, lig, pol_s, pol_r, slots);
       const bool mine = t.slot != NOSLOT && t.lo < t.hi;
-      if (KIND == KIND_CSL_ACC) {
-        // chunks of a long virtual slice add their partial rows directly
-        if (mine && lane_live(fx, lig))
-          red_add4(fx.out + size_t(__ldg(w.csl_sidx + t.s)) * fx.rs + fx.col4 + lig, sa);
-        continue;
-      }
       const uint32_t slot0 = __shfl_sync(FULL, t.slot, 0);
       const bool same = __all_sync(FULL, mine && t.slot == slot0);
       const uint32_t row =
           mine ? (K == KIND_CSF ? __ldg(w.csf_sidx + t.s) : __ldg(w.csl_sidx + t.s)) : 0u;
+      if (ACC) {
+        // chunks of a slice cut into several tasks add their partial rows
+        // directly into the pre-zeroed output (no accumulator hand-over)
+        if (same) {
+          float4 r = add4(sa, shfl_xor4(sa, 8));
+          r = add4(r, shfl_xor4(r, 16));
+          if (g == 0 && lane_live(fx, lig)) red_add4(fx.out + size_t(row) * fx.rs + fx.col4 + lig, r);
+        } else if (mine && lane_live(fx, lig)) {
+          red_add4(fx.out + size_t(row) * fx.rs + fx.col4 + lig, sa);
+        }
+        continue;
+      }
       if (same) {
         float4 r = add4(sa, shfl_xor4(sa, 8));
         r = add4(r, shfl_xor4(r, 16));
@@ -1053,6 +1071,20 @@ struct hbk_plan {
   bool csl_acc = false;
   hbk::Buf vcsl_pairs, vcsl_j, vcsl_sidx;
   uint32_t vcsl_S = 0;
+  // leaf-blocked heavy slices (csf_block_view; chosen in hbk_plan_create):
+  // the fast fp32 path runs sub_blk (the heavy slices, leaf-block-major,
+  // rows accumulated into their pre-zeroed rows) then sub_main (every other
+  // slice, the CSL-as-CSF light slices and the COO bucket); the plan itself
+  // keeps the reference buckets for the generic / fp64 kernel and the OpCount
+  hbk_plan* sub_main = nullptr;
+  hbk_plan* sub_blk = nullptr;
+  hbk::Buf heavy_rows;          // u32 output rows of the heavy slices
+  int64_t n_heavy_rows = 0;
+  int64_t leaf_bb = 0, leaf_min = 0;
+  bool force_generic = false;   // fast structures live in the sub-plans
+  bool acc_csf = false;         // (sub_blk) CSF kernels accumulate rows, no zero-row tasks
+  const hbk::Buf* extra_owned = nullptr;  // (sub_main) rows owned by sub_blk
+  int64_t n_extra_owned = 0;
   // B-position plans launch their bucket kernels on forked streams so each
   // kernel's CTAs fill the tail of the one before (HBK_CONCURRENT=0: serial)
   bool concurrent = false;
@@ -1076,6 +1108,8 @@ struct hbk_plan {
   mutable std::mutex exec_mu;
   cudaEvent_t ev_last = nullptr;
   ~hbk_plan() {
+    delete sub_main;
+    delete sub_blk;
     if (ev_last) cudaEventDestroy(ev_last);
     for (int i = 0; i < 3; ++i) {
       if (side[i]) cudaStreamDestroy(side[i]);
@@ -1617,14 +1651,16 @@ static int fast_occupancy(const hbk_plan* p, int k) {
   int per_sm = 0;
   const void* fn = nullptr;
   if (k == 0)
-    fn = reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF_BPOS4, FX>);
+    fn = p->acc_csf ? reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF_BPOS4_ACC, FX>)
+                    : reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF_BPOS4, FX>);
   else if (k == 1)
     fn = p->csl_acc ? reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSL_ACC, FX>)
                     : reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSL, FX>);
   else if (k == 2)
     fn = reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_COO, FX>);
   else
-    fn = reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF_UNI, FX>);
+    fn = p->acc_csf ? reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF_UNI_ACC, FX>)
+                    : reinterpret_cast<const void*>(k_mttkrp3_r32<KIND_CSF_UNI, FX>);
   HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, p->block, 0));
   return per_sm;
 }
@@ -1639,8 +1675,9 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
   // fast path: order 3, R a multiple of 4 (float4 rows; R > 32 runs in
   // passes of 32 columns); the old-variant streams keep two flag bits in the
   // leaf coordinate, so leaf extents must stay < 2^29
-  p->fast = (N == 3 && R >= 4 && R % 4 == 0 && p->dims[p->mo[2]] < (int64_t(1) << 29) &&
-             p->dims[p->mo[1]] < (int64_t(1) << 29));
+  p->fast = !p->force_generic && (N == 3 && R >= 4 && R % 4 == 0 &&
+                                   p->dims[p->mo[2]] < (int64_t(1) << 29) &&
+                                   p->dims[p->mo[1]] < (int64_t(1) << 29));
   p->r32 = p->fast && R == 32 && p->dims[p->mo[2]] < (int64_t(1) << 27) &&
            p->dims[p->mo[1]] < (int64_t(1) << 27);
   p->bshift = p->r32 ? 3u : 0u;
@@ -1890,6 +1927,12 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
           p->coo->cols[p->mode].as<uint32_t>(), p->coo->nnz, mark.as<uint8_t>());
       check_launch("k_mark_rows");
     }
+    if (p->extra_owned && p->n_extra_owned) {
+      k_mark_rows<<<grid_for(p->n_extra_owned, 256), 256, 0, st>>>(
+          p->extra_owned->as<uint32_t>(), p->n_extra_owned, mark.as<uint8_t>());
+      check_launch("k_mark_rows");
+    }
+    if (p->acc_csf) HBK_CUDA(cudaMemsetAsync(mark.p, 1, rows, st));  // sub_blk writes no zero rows
     Scratch pos((rows + 1) * sizeof(uint32_t), st);
     k_unmarked_flags<<<grid_for(rows, 256), 256, 0, st>>>(mark.as<uint8_t>(), rows,
                                                           pos.as<uint32_t>());
@@ -2125,6 +2168,13 @@ static void launch_generic(const hbk_plan* p, const T* const* factors, T* out, c
 using namespace hbk;
 
 namespace hbk {
+__global__ void k_zero_rows(const uint32_t* __restrict__ rows, int64_t n, uint32_t rs,
+                            float4* __restrict__ out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n * rs;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[size_t(rows[i / rs]) * rs + i % rs] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
 template <class FX>
 static void launch_fast(const hbk_plan* p, const FX& fx, cudaStream_t st, bool skip_zero = false) {
   // kernels in launch order: heavy slices first (the longest), then light
@@ -2144,11 +2194,17 @@ static void launch_fast(const hbk_plan* p, const FX& fx, cudaStream_t st, bool s
   if (p->concurrent) HBK_CUDA(cudaEventRecord(p->ev_fork, st));
   if (p->grid_heavy) {
     cudaStream_t s2 = next_stream();
-    k_mttkrp3_r32<KIND_CSF_UNI, FX><<<p->grid_heavy, p->block, 0, s2>>>(p->work_heavy, fx);
+    if (p->acc_csf)
+      k_mttkrp3_r32<KIND_CSF_UNI_ACC, FX><<<p->grid_heavy, p->block, 0, s2>>>(p->work_heavy, fx);
+    else
+      k_mttkrp3_r32<KIND_CSF_UNI, FX><<<p->grid_heavy, p->block, 0, s2>>>(p->work_heavy, fx);
   }
   if (p->grids[0]) {
     cudaStream_t s2 = next_stream();
-    k_mttkrp3_r32<KIND_CSF_BPOS4, FX><<<p->grids[0], p->block, 0, s2>>>(p->work, fx);
+    if (p->acc_csf)
+      k_mttkrp3_r32<KIND_CSF_BPOS4_ACC, FX><<<p->grids[0], p->block, 0, s2>>>(p->work, fx);
+    else
+      k_mttkrp3_r32<KIND_CSF_BPOS4, FX><<<p->grids[0], p->block, 0, s2>>>(p->work, fx);
   }
   if (p->grids[1]) {
     cudaStream_t s2 = next_stream();
@@ -2257,9 +2313,349 @@ static hbk_csf* merge_csl_as_csf(const hbk_csf* c, const hbk_csl* l, cudaStream_
   check_launch("merge_csl_as_csf");
   return guard.release();
 }
+
+// ------------------------------------------------- leaf-blocked view --
+// csf_block_view(c, sel, want, BB): the order-3 tree of the slices with
+// sel[s] == want, its nonzeros reordered leaf-block-major — (block of BB leaf
+// rows, slice, fiber, leaf) — with every (block, slice) a virtual slice and
+// every (block, fiber) a virtual fiber (BB = 0: no blocking, the selected
+// slices in tree order).  A slice's virtual slices all name its output row,
+// so a plan over the view must accumulate rows (hbk_plan::acc_csf).
+__global__ void k_nz_fiber(const uint32_t* __restrict__ fptr, int64_t F, int64_t M,
+                           uint32_t* __restrict__ nzf) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int64_t lo = 0, hi = F;  // last f with fptr[f] <= i
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (fptr[mid] <= uint32_t(i)) lo = mid; else hi = mid;
+    }
+    nzf[i] = uint32_t(lo);
+  }
+}
+__global__ void k_view_keep(const uint32_t* __restrict__ nzf, const uint32_t* __restrict__ fslice,
+                            const uint8_t* __restrict__ sel, uint8_t want, int64_t M,
+                            uint32_t* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
+       i += int64_t(gridDim.x) * blockDim.x)
+    flag[i] = sel[fslice[nzf[i]]] == want;
+}
+__global__ void k_view_gather(const uint32_t* __restrict__ pos, int64_t M, const uint32_t* __restrict__ leaf,
+                              uint32_t BB, uint32_t* __restrict__ blk, uint32_t* __restrict__ src) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
+       i += int64_t(gridDim.x) * blockDim.x)
+    if (pos[i + 1] != pos[i]) {
+      blk[pos[i]] = BB ? leaf[i] / BB : 0u;
+      src[pos[i]] = uint32_t(i);
+    }
+}
+// per kept element q (after the block sort): source nonzero src[q]; flags of
+// virtual-fiber and virtual-slice starts
+__global__ void k_view_flags(const uint32_t* __restrict__ src, const uint32_t* __restrict__ blk,
+                             const uint32_t* __restrict__ nzf, const uint32_t* __restrict__ fslice,
+                             int64_t K, uint32_t* __restrict__ ffl, uint32_t* __restrict__ sfl) {
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < K;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t f = nzf[src[q]];
+    bool nf = q == 0, ns = q == 0;
+    if (q > 0) {
+      const uint32_t f0 = nzf[src[q - 1]];
+      const bool nb = blk[q] != blk[q - 1];
+      nf = nb || f != f0;
+      ns = nb || fslice[f] != fslice[f0];
+    }
+    ffl[q] = nf;
+    sfl[q] = ns;
+  }
+}
+__global__ void k_view_fill(const uint32_t* __restrict__ src, const uint32_t* __restrict__ nzf,
+                            const uint32_t* __restrict__ fslice, const uint32_t* __restrict__ fpos,
+                            const uint32_t* __restrict__ spos, int64_t K,
+                            const uint32_t* __restrict__ leaf, const float* __restrict__ v32,
+                            const double* __restrict__ v64, const uint32_t* __restrict__ fidx,
+                            const uint32_t* __restrict__ sidx, uint32_t* __restrict__ vleaf,
+                            float* __restrict__ vv32, double* __restrict__ vv64,
+                            uint32_t* __restrict__ vfptr, uint32_t* __restrict__ vfidx,
+                            uint32_t* __restrict__ vsptr, uint32_t* __restrict__ vsidx) {
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < K;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t i = src[q], f = nzf[i];
+    vleaf[q] = leaf[i];
+    vv32[q] = v32[i];
+    if (vv64) vv64[q] = v64[i];
+    if (fpos[q + 1] != fpos[q]) {  // virtual fiber start
+      const uint32_t vf = fpos[q];
+      vfptr[vf] = uint32_t(q);
+      vfidx[vf] = fidx[f];
+      if (spos[q + 1] != spos[q]) {  // virtual slice start (always a fiber start)
+        vsptr[spos[q]] = vf;
+        vsidx[spos[q]] = sidx[fslice[f]];
+      }
+    }
+  }
+}
+
+static hbk_csf* csf_block_view(const hbk_csf* c, const uint8_t* sel, bool want, int64_t BB,
+                               cudaStream_t st) {
+  HBK_REQUIRE(c->order == 3, HBK_EINVAL, "leaf-blocked view needs an order-3 tree");
+  hbk_csf* m = new hbk_csf();
+  std::unique_ptr<hbk_csf, void (*)(hbk_csf*)> guard(m, [](hbk_csf* q) { hbk_csf_release(q); });
+  m->order = 3;
+  std::copy(c->dims, c->dims + 3, m->dims);
+  std::copy(c->mode_order, c->mode_order + 3, m->mode_order);
+  m->split = c->split;
+  const int64_t S = c->n[0], F = c->n[1], M = c->M;
+  Scratch nzf(size_t(std::max<int64_t>(M, 1)) * 4, st), fsl(size_t(std::max<int64_t>(F, 1)) * 4, st);
+  if (M) {
+    k_nz_fiber<<<grid_for(M, 256), 256, 0, st>>>(c->ptr[1].as<uint32_t>(), F, M, nzf.as<uint32_t>());
+    k_fiber_slice<<<grid_for(F, 256), 256, 0, st>>>(c->ptr[0].as<uint32_t>(), S, F, fsl.as<uint32_t>());
+    check_launch("k_nz_fiber");
+  }
+  Scratch pos((M + 1) * 4, st);
+  if (M) {
+    k_view_keep<<<grid_for(M, 256), 256, 0, st>>>(nzf.as<uint32_t>(), fsl.as<uint32_t>(), sel,
+                                                  uint8_t(want), M, pos.as<uint32_t>());
+    check_launch("k_view_keep");
+  }
+  const uint32_t K = M ? exclusive_scan_total(pos.as<uint32_t>(), M, st) : 0u;
+  Scratch blk_a(size_t(std::max<uint32_t>(K, 1)) * 4, st), src_a(size_t(std::max<uint32_t>(K, 1)) * 4, st);
+  Scratch blk_b(size_t(std::max<uint32_t>(K, 1)) * 4, st), src_b(size_t(std::max<uint32_t>(K, 1)) * 4, st);
+  if (K) {
+    k_view_gather<<<grid_for(M, 256), 256, 0, st>>>(pos.as<uint32_t>(), M, c->leaf.as<uint32_t>(),
+                                                    uint32_t(BB), blk_a.as<uint32_t>(), src_a.as<uint32_t>());
+    check_launch("k_view_gather");
+  }
+  const uint32_t* blk = blk_a.as<uint32_t>();
+  const uint32_t* src = src_a.as<uint32_t>();
+  if (K && BB > 0) {
+    const int64_t nb = (c->dims[c->mode_order[2]] + BB - 1) / BB;
+    int bits = 1;
+    while ((int64_t(1) << bits) < nb) ++bits;
+    size_t tmp = 0;
+    HBK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, blk_a.as<uint32_t>(), blk_b.as<uint32_t>(),
+                                             src_a.as<uint32_t>(), src_b.as<uint32_t>(), int(K), 0, bits, st));
+    Scratch t(tmp, st);
+    HBK_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, blk_a.as<uint32_t>(), blk_b.as<uint32_t>(),
+                                             src_a.as<uint32_t>(), src_b.as<uint32_t>(), int(K), 0, bits, st));
+    blk = blk_b.as<uint32_t>();
+    src = src_b.as<uint32_t>();
+  }
+  Scratch fpos((size_t(K) + 1) * 4, st), spos((size_t(K) + 1) * 4, st);
+  if (K) {
+    k_view_flags<<<grid_for(K, 256), 256, 0, st>>>(src, blk, nzf.as<uint32_t>(), fsl.as<uint32_t>(), K,
+                                                   fpos.as<uint32_t>(), spos.as<uint32_t>());
+    check_launch("k_view_flags");
+  }
+  const uint32_t VF = K ? exclusive_scan_total(fpos.as<uint32_t>(), K, st) : 0u;
+  const uint32_t VS = K ? exclusive_scan_total(spos.as<uint32_t>(), K, st) : 0u;
+  m->M = K;
+  m->n[0] = VS;
+  m->n[1] = VF;
+  m->ptr[0] = dalloc(size_t(VS + 1) * 4, st);
+  m->idx[0] = dalloc(size_t(std::max<uint32_t>(VS, 1)) * 4, st);
+  m->ptr[1] = dalloc(size_t(VF + 1) * 4, st);
+  m->idx[1] = dalloc(size_t(std::max<uint32_t>(VF, 1)) * 4, st);
+  m->leaf = dalloc(size_t(std::max<uint32_t>(K, 1)) * 4, st);
+  m->v32 = dalloc(size_t(std::max<uint32_t>(K, 1)) * 4, st);
+  if (c->v64) m->v64 = dalloc(size_t(std::max<uint32_t>(K, 1)) * 8, st);
+  if (K) {
+    k_view_fill<<<grid_for(K, 256), 256, 0, st>>>(
+        src, nzf.as<uint32_t>(), fsl.as<uint32_t>(), fpos.as<uint32_t>(), spos.as<uint32_t>(), K,
+        c->leaf.as<uint32_t>(), c->v32.as<float>(), c->v64 ? c->v64.as<double>() : nullptr,
+        c->idx[1].as<uint32_t>(), c->idx[0].as<uint32_t>(), m->leaf.as<uint32_t>(), m->v32.as<float>(),
+        c->v64 ? m->v64.as<double>() : nullptr, m->ptr[1].as<uint32_t>(), m->idx[1].as<uint32_t>(),
+        m->ptr[0].as<uint32_t>(), m->idx[0].as<uint32_t>());
+    check_launch("k_view_fill");
+  }
+  write_u32(m->ptr[1].as<uint32_t>() + VF, K, st);
+  write_u32(m->ptr[0].as<uint32_t>() + VS, VF, st);
+  return guard.release();
+}
 }  // namespace hbk
 
 namespace hbk {
+__global__ void k_heavy_sel(const uint32_t* __restrict__ ptr0, const uint32_t* __restrict__ ptr1,
+                            int64_t S, uint32_t minnz, uint8_t* __restrict__ sel,
+                            unsigned long long* __restrict__ hnnz, uint32_t* __restrict__ hflag) {
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < S;
+       s += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t m = ptr1[ptr0[s + 1]] - ptr1[ptr0[s]];
+    const bool h = m >= minnz;
+    sel[s] = h;
+    hflag[s] = h;
+    if (h) atomicAdd(hnnz, (unsigned long long)m);
+  }
+}
+__global__ void k_heavy_rows(const uint32_t* __restrict__ pos, const uint32_t* __restrict__ sidx,
+                             int64_t S, uint32_t* __restrict__ rows) {
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < S;
+       s += int64_t(gridDim.x) * blockDim.x)
+    if (pos[s + 1] != pos[s]) rows[pos[s]] = sidx[s];
+}
+
+// Leaf rows per block for leaf-blocking the heavy slices, 0 = off.  On when
+// the leaf factor's rows (the 32-column slice a pass reads) exceed half the
+// L2: the heavy slices' nonzeros are then visited leaf-block by leaf-block so
+// the block's leaf rows are reused out of L2 (LRU replay of the real access
+// streams, scripts/lru_block_sim.py: 63-MB-LRU factor traffic nell-1 mode 0
+// 10.8 -> 8.0 GB, delicious-3d mode 1 24.6 -> 14.2 GB, flickr-3d -26..-38%;
+// measured: delicious-3d mode 1 4.65 -> 3.77 ms, but nell-1 / flickr-3d 2-9%
+// slower — their Zipf leaf heads are L2-resident already, so build_leaf_blocked
+// also requires a flat leaf distribution).  Blocks of 0.18 x L2 (12/16/24/32/48
+// MB measured within 1%).  HBK_LEAF_BLOCK_MB=x forces x-MB blocks (0 = off;
+// forcing also skips the flatness test); HBK_LEAF_MIN sets the heavy-slice
+// threshold (nonzeros), for A/B measurement.
+static int64_t leaf_block_rows(const int64_t* dims, const int* mo, int rank, bool eligible) {
+  if (!eligible) return 0;
+  const int64_t Crows = dims[mo[2]];
+  const double row_bytes = 4.0 * std::min(rank, 32);
+  double mb = -1.0;
+  if (const char* e = getenv("HBK_LEAF_BLOCK_MB")) mb = atof(e);
+  if (mb == 0.0) return 0;
+  int64_t BB = 0;
+  if (mb > 0.0) {
+    BB = std::max<int64_t>(1, int64_t(mb * 1e6 / row_bytes));
+  } else {
+    int dev = 0, l2 = 0;
+    HBK_CUDA(cudaGetDevice(&dev));
+    HBK_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    const double cbytes = double(Crows) * row_bytes;
+    if (l2 <= 0 || cbytes <= 0.5 * l2) return 0;
+    BB = std::max<int64_t>(1, int64_t(0.18 * l2 / row_bytes));
+  }
+  return BB < Crows ? BB : 0;
+}
+
+static hbk_plan* new_plan(hbk_coo* coo, hbk_csl* csl, hbk_csf* csf, hbk_sched* sched, int mode,
+                          int rank, int order, const int64_t* dims, const int* mo) {
+  hbk_plan* p = new hbk_plan();
+  std::unique_ptr<hbk_plan> guard(p);
+  HBK_CUDA(cudaEventCreateWithFlags(&p->ev_last, cudaEventDisableTiming));
+  p->order = order;
+  p->mode = mode;
+  p->rank = rank;
+  std::copy(dims, dims + order, p->dims);
+  std::copy(mo, mo + order, p->mo);
+  p->coo = coo;
+  p->csl = csl;
+  p->csf = csf;
+  p->sched = sched;
+  hbk_coo_retain(coo);
+  hbk_csl_retain(csl);
+  hbk_csf_retain(csf);
+  hbk_sched_retain(sched);
+  return guard.release();
+}
+
+// Split the plan's CSF (+ CSL as singleton-fiber CSF slices) into the heavy
+// slices (>= minnz nonzeros, leaf-blocked, sub_blk) and the rest (sub_main);
+// false (nothing built) when the heavy slices hold under a quarter of the
+// plan's nonzeros.
+__global__ void k_leaf_hist(const uint32_t* __restrict__ leaf, int64_t M, uint32_t* __restrict__ h) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
+       i += int64_t(gridDim.x) * blockDim.x)
+    atomicAdd(h + leaf[i], 1u);
+}
+
+// Share of a tree's leaf accesses that go to its K most used leaf rows.
+static double leaf_head_share(const hbk_csf* c, int64_t K, cudaStream_t st) {
+  const int64_t R = c->dims[c->mode_order[2]];
+  if (c->M == 0 || R == 0) return 1.0;
+  K = std::min(K, R);
+  Scratch h(size_t(R) * 4, st), hs(size_t(R) * 4, st), sum(8, st);
+  HBK_CUDA(cudaMemsetAsync(h.p, 0, size_t(R) * 4, st));
+  k_leaf_hist<<<grid_for(c->M, 256), 256, 0, st>>>(c->leaf.as<uint32_t>(), c->M, h.as<uint32_t>());
+  check_launch("k_leaf_hist");
+  size_t tmp = 0;
+  HBK_CUDA(cub::DeviceRadixSort::SortKeysDescending(nullptr, tmp, h.as<uint32_t>(), hs.as<uint32_t>(),
+                                                    int(R), 0, 32, st));
+  {
+    Scratch t(tmp, st);
+    HBK_CUDA(cub::DeviceRadixSort::SortKeysDescending(t.p, tmp, h.as<uint32_t>(), hs.as<uint32_t>(),
+                                                      int(R), 0, 32, st));
+  }
+  tmp = 0;
+  HBK_CUDA(cub::DeviceReduce::Sum(nullptr, tmp, hs.as<uint32_t>(), sum.as<unsigned long long>(), int(K), st));
+  {
+    Scratch t(tmp, st);
+    HBK_CUDA(cub::DeviceReduce::Sum(t.p, tmp, hs.as<uint32_t>(), sum.as<unsigned long long>(), int(K), st));
+  }
+  unsigned long long top = 0;
+  HBK_CUDA(cudaMemcpyAsync(&top, sum.p, 8, cudaMemcpyDeviceToHost, st));
+  HBK_CUDA(cudaStreamSynchronize(st));
+  return double(top) / double(c->M);
+}
+
+static bool build_leaf_blocked(hbk_plan* p, int64_t BB, uint32_t minnz, cudaStream_t st) {
+  hbk_csf* merged = nullptr;
+  if (p->csl && p->csl->M > 0) {
+    merged = merge_csl_as_csf(p->csf, p->csl, st);
+  } else if (p->csf) {
+    merged = p->csf;
+    hbk_csf_retain(merged);
+  }
+  if (!merged || merged->M == 0) {
+    hbk_csf_release(merged);
+    return false;
+  }
+  std::unique_ptr<hbk_csf, void (*)(hbk_csf*)> gm(merged, [](hbk_csf* q) { hbk_csf_release(q); });
+  // Zipf-headed leaf factors already keep their hot rows in L2: blocking
+  // pays only when the rows a quarter of the L2 could hold serve under half
+  // of the leaf accesses (delicious-3d mode 1, alpha = 0.3: -14%; the
+  // alpha = 1 leaves of nell-1 / flickr-3d measured 2-9% slower blocked)
+  {
+    int dev = 0, l2 = 0;
+    HBK_CUDA(cudaGetDevice(&dev));
+    HBK_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    const int64_t K = std::max<int64_t>(1, int64_t(0.25 * l2 / (4.0 * std::min(p->rank, 32))));
+    const double share = leaf_head_share(merged, K, st);
+    p->info.leaf_head_share_ppm = int64_t(share * 1e6);
+    if (share > 0.5 && !getenv("HBK_LEAF_BLOCK_MB")) return false;
+  }
+  const int64_t S = merged->n[0];
+  Scratch sel(size_t(S), st), cnt(8, st), pos((S + 1) * 4, st);
+  HBK_CUDA(cudaMemsetAsync(cnt.p, 0, 8, st));
+  k_heavy_sel<<<grid_for(S, 256), 256, 0, st>>>(merged->ptr[0].as<uint32_t>(), merged->ptr[1].as<uint32_t>(),
+                                               S, minnz, sel.as<uint8_t>(),
+                                               cnt.as<unsigned long long>(), pos.as<uint32_t>());
+  check_launch("k_heavy_sel");
+  unsigned long long hnnz = 0;
+  HBK_CUDA(cudaMemcpyAsync(&hnnz, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+  HBK_CUDA(cudaStreamSynchronize(st));
+  const int64_t total = merged->M + (p->coo ? p->coo->nnz : 0);
+  if (hnnz == 0 || 4 * int64_t(hnnz) < total) return false;
+  const uint32_t nh = exclusive_scan_total(pos.as<uint32_t>(), S, st);
+  p->heavy_rows = dalloc(size_t(std::max<uint32_t>(nh, 1)) * 4, st);
+  p->n_heavy_rows = nh;
+  k_heavy_rows<<<grid_for(S, 256), 256, 0, st>>>(pos.as<uint32_t>(), merged->idx[0].as<uint32_t>(), S,
+                                                p->heavy_rows.as<uint32_t>());
+  check_launch("k_heavy_rows");
+  hbk_csf* light = csf_block_view(merged, sel.as<uint8_t>(), false, 0, st);
+  std::unique_ptr<hbk_csf, void (*)(hbk_csf*)> gl(light, [](hbk_csf* q) { hbk_csf_release(q); });
+  hbk_csf* blk = csf_block_view(merged, sel.as<uint8_t>(), true, BB, st);
+  std::unique_ptr<hbk_csf, void (*)(hbk_csf*)> gb(blk, [](hbk_csf* q) { hbk_csf_release(q); });
+  std::unique_ptr<hbk_plan> sb(new_plan(nullptr, nullptr, blk, nullptr, p->mode, p->rank, p->order,
+                                        p->dims, p->mo));
+  sb->acc_csf = true;
+  build_plan(sb.get(), st);
+  std::unique_ptr<hbk_plan> sm(new_plan(p->coo, nullptr, light->M ? light : nullptr, nullptr, p->mode,
+                                        p->rank, p->order, p->dims, p->mo));
+  if (!sm->coo && !sm->csf) {  // every slice is heavy: an empty main plan still zero-fills
+    sm->csf = light;
+    hbk_csf_retain(light);
+  }
+  sm->extra_owned = &p->heavy_rows;
+  sm->n_extra_owned = nh;
+  build_plan(sm.get(), st);
+  p->sub_blk = sb.release();
+  p->sub_main = sm.release();
+  p->leaf_bb = BB;
+  p->leaf_min = minnz;
+  p->info.leaf_blocks = (p->dims[p->mo[2]] + BB - 1) / BB;
+  p->info.leaf_blocked_nnz = int64_t(hnnz);
+  return true;
+}
+
 // B rows per block of the blocked CSL layout, 0 = unblocked.  Blocked when the
 // CSL bucket holds at least half of the plan's nonzeros and its B factor's
 // rows (the 32-column slice a pass reads) exceed half the L2: blocks of about
@@ -2357,7 +2753,19 @@ int hbk_plan_create(hbk_coo* coo, hbk_csl* csl, hbk_csf* csf, hbk_sched* sched, 
       // kernel, measured 2% faster for them (delicious mode 2, 56 per slice)
       const bool heavy_csl = csl && csl->M > 128 * csl->S;
       p->csl_bb = csl_block_rows(csl, csf, coo, rank, fast_shape && !sched);
-      if (csl && csl->M > 0 && !sched && fast_shape && (!csf || csf->order == 3) &&
+      // leaf-blocked heavy slices (build_leaf_blocked): the plan keeps the
+      // reference buckets (generic / fp64 kernel), the sub-plans run the fast path
+      const int64_t lbb = leaf_block_rows(dims, mo, rank,
+                                          fast_shape && !sched && order == 3 && p->csl_bb == 0 &&
+                                              (!csf || csf->order == 3));
+      if (lbb > 0) {
+        // heavy-slice threshold: delicious-3d mode 1 at 16/32/64/128/512/2048
+        // nonzeros: 3.84/3.77/3.77/3.81/4.00/4.05 ms (unblocked 4.65)
+        uint32_t minnz = 64;
+        if (const char* e2 = getenv("HBK_LEAF_MIN")) minnz = uint32_t(std::max(1, atoi(e2)));
+        if (build_leaf_blocked(p, lbb, minnz, st)) p->force_generic = true;
+      }
+      if (!p->sub_blk && csl && csl->M > 0 && !sched && fast_shape && (!csf || csf->order == 3) &&
           (e ? atoi(e) != 0 : heavy_csl && p->csl_bb == 0)) {
         hbk_csf* merged = merge_csl_as_csf(csf, csl, st);
         hbk_csf_release(p->csf);
@@ -2367,10 +2775,28 @@ int hbk_plan_create(hbk_coo* coo, hbk_csl* csl, hbk_csf* csf, hbk_sched* sched, 
         csl_slices_merged = csl->S;
       }
     }
+    const hbk_plan_info keep_leaf = p->info;
     build_plan(p, st);
     // OpCount is the reference's (kernels.py:210-214 for the CSL bucket):
     // the CSF count of a singleton-fiber slice adds one per slice
     p->info.op_adds -= csl_slices_merged * rank;
+    if (p->sub_blk) {  // what the fast path launches and gathers
+      const hbk_plan_info& a = p->sub_blk->info;
+      const hbk_plan_info& b = p->sub_main->info;
+      p->info.fast_path = 1;
+      p->info.launches = a.launches + b.launches + 1;  // + the heavy-row zeroing
+      p->info.tasks_csf = a.tasks_csf + b.tasks_csf;
+      p->info.tasks_heavy = a.tasks_heavy + b.tasks_heavy;
+      p->info.tasks_csl = b.tasks_csl;
+      p->info.tasks_coo = b.tasks_coo;
+      p->info.tasks_zero = b.tasks_zero;
+      p->info.split_rows = a.split_rows + b.split_rows;
+      p->info.stream_bytes = a.stream_bytes + b.stream_bytes;
+      p->info.gather_rows = a.gather_rows + b.gather_rows;
+      p->info.leaf_blocks = keep_leaf.leaf_blocks;
+      p->info.leaf_blocked_nnz = keep_leaf.leaf_blocked_nnz;
+    }
+    p->info.leaf_head_share_ppm = keep_leaf.leaf_head_share_ppm;
     *out = guard.release();
   });
 }
@@ -2393,7 +2819,36 @@ int hbk_plan_execute_ex(const hbk_plan* p, const float* const* factors, float* o
       HBK_REQUIRE(d == p->mode || factors[d] != nullptr, HBK_EINVAL, "null factor pointer");
     HBK_REQUIRE(out != nullptr || p->dims[p->mode] == 0, HBK_EINVAL, "null output pointer");
     ExecOrder order(p, st);
-    if (p->fast) {
+    if (p->sub_blk) {
+      // leaf-blocked heavy slices: zero their rows, accumulate them block by
+      // block (sub_blk), then every other slice (sub_main)
+      Factors3 fx;
+      fx.B = reinterpret_cast<const float4*>(factors[p->mo[1]]);
+      fx.C = reinterpret_cast<const float4*>(factors[p->mo[2]]);
+      fx.out = reinterpret_cast<float4*>(out);
+      HBK_REQUIRE((reinterpret_cast<uintptr_t>(fx.B) | reinterpret_cast<uintptr_t>(fx.C) |
+                   reinterpret_cast<uintptr_t>(out)) % 16 == 0,
+                  HBK_EINVAL, "factor and output buffers must be 16-byte aligned");
+      const int R = p->rank;
+      if (p->n_heavy_rows) {
+        const int64_t n4 = p->n_heavy_rows * (R / 4);
+        k_zero_rows<<<grid_for(n4, 256), 256, 0, st>>>(p->heavy_rows.as<uint32_t>(), p->n_heavy_rows,
+                                                       uint32_t(R / 4), fx.out);
+        check_launch("k_zero_rows");
+      }
+      if (p->sub_blk->r32) {
+        launch_fast(p->sub_blk, Factors3R32(fx), st);
+        launch_fast(p->sub_main, Factors3R32(fx), st, skip_zero);
+      } else {
+        fx.rs = uint32_t(R / 4);
+        for (int c0 = 0; c0 < R; c0 += 32) {
+          fx.col4 = uint32_t(c0 / 4);
+          fx.lanes = uint32_t(std::min(8, (R - c0) / 4));
+          launch_fast(p->sub_blk, fx, st);
+          launch_fast(p->sub_main, fx, st, skip_zero);
+        }
+      }
+    } else if (p->fast) {
       Factors3 fx;
       fx.B = reinterpret_cast<const float4*>(factors[p->mo[1]]);
       fx.C = reinterpret_cast<const float4*>(factors[p->mo[2]]);
@@ -2519,9 +2974,25 @@ int hbk_nonfinite_f32(const float* const* bufs, const int64_t* counts, int n, in
   });
 }
 
+namespace hbk {
+static void probe_plan(const hbk_plan* p, const Factors3R32& f32, cudaStream_t st) {
+  float4* sink = p->probe_sink.as<float4>();
+  int dev = 0, sms = 0;
+  HBK_CUDA(cudaGetDevice(&dev));
+  HBK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = sms * 4;
+  if (p->work.n0) k_gather_probe<KIND_CSF><<<grid, FAST_BLOCK, 0, st>>>(p->work, f32, sink);
+  if (p->grid_heavy) k_gather_probe<KIND_CSF><<<grid, FAST_BLOCK, 0, st>>>(p->work_heavy, f32, sink);
+  if (p->work.n1 > p->work.n0) k_gather_probe<KIND_CSL><<<grid, FAST_BLOCK, 0, st>>>(p->work, f32, sink);
+  if (p->work.n2 > p->work.n1) k_gather_probe<KIND_COO><<<grid, FAST_BLOCK, 0, st>>>(p->work, f32, sink);
+  check_launch("k_gather_probe");
+}
+}  // namespace hbk
+
 int hbk_plan_probe(const hbk_plan* p, const float* const* factors, void* stream) {
   return guarded([&] {
-    HBK_REQUIRE(p->bpos && p->r32, HBK_EINVAL,
+    const hbk_plan* a = p->sub_blk ? p->sub_blk : p;
+    HBK_REQUIRE(a->bpos && a->r32 && (!p->sub_main || p->sub_main->r32), HBK_EINVAL,
                 "the gather probe needs a B-position (fast order-3, R=32, extents < 2^27) plan");
     cudaStream_t st = to_stream(stream);
     ExecOrder order(p, st);
@@ -2530,16 +3001,8 @@ int hbk_plan_probe(const hbk_plan* p, const float* const* factors, void* stream)
     fx.C = reinterpret_cast<const float4*>(factors[p->mo[2]]);
     fx.out = nullptr;
     const Factors3R32 f32(fx);
-    float4* sink = p->probe_sink.as<float4>();
-    int dev = 0, sms = 0;
-    HBK_CUDA(cudaGetDevice(&dev));
-    HBK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int grid = sms * 4;
-    if (p->work.n0) k_gather_probe<KIND_CSF><<<grid, FAST_BLOCK, 0, st>>>(p->work, f32, sink);
-    if (p->grid_heavy) k_gather_probe<KIND_CSF><<<grid, FAST_BLOCK, 0, st>>>(p->work_heavy, f32, sink);
-    if (p->work.n1 > p->work.n0) k_gather_probe<KIND_CSL><<<grid, FAST_BLOCK, 0, st>>>(p->work, f32, sink);
-    if (p->work.n2 > p->work.n1) k_gather_probe<KIND_COO><<<grid, FAST_BLOCK, 0, st>>>(p->work, f32, sink);
-    check_launch("k_gather_probe");
+    probe_plan(a, f32, st);
+    if (p->sub_main) probe_plan(p->sub_main, f32, st);
     order.done();
   });
 }

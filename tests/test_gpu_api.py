@@ -622,3 +622,51 @@ def test_fiber_histogram_matches_csf(hb, rng):
         fib = shard.fiber_histogram(t, mode, mid).cpu().numpy()
         cost = shard.partition_costs(t, mode).cpu().numpy()
         assert np.array_equal(cost, nnz + fib + shard.ROW_COST)
+
+
+@pytest.mark.parametrize("block_mb,minnz", [("0.002", "8"), ("0.0005", "64"), ("0.004", "1")])
+@pytest.mark.parametrize("rank", [32, 16, 64])
+def test_leaf_blocked_heavy_slices_parity(hb, rng, block_mb, minnz, rank, monkeypatch):
+    """Leaf-blocked heavy slices (csf_block_view + accumulating sub-plan):
+    the oracle's rows for every mode, R = 32 and multi-pass ranks, into a
+    dirty output buffer; the fp64 (generic) kernel and the OpCount stay the
+    reference's; owned rows unchanged; skip-unowned keeps heavy rows."""
+    import torch
+
+    from paper_1904_03329_b200.kernels import mttkrp_device, plan_for
+
+    monkeypatch.setenv("HBK_LEAF_BLOCK_MB", block_mb)
+    monkeypatch.setenv("HBK_LEAF_MIN", minnz)
+    dims = (80, 60, 500)
+    idx, vals = _powerlaw(rng, dims, 12000)
+    # a few very heavy slices (heavy layout inside the blocked view) and a COO tail
+    extra = np.stack([np.zeros(3000, np.int64), rng.integers(0, 60, 3000), rng.integers(0, 500, 3000)], 1)
+    idx, vals = P.canonical(np.vstack([idx.astype(np.int64), extra]).astype(np.uint32),
+                            np.concatenate([vals, rng.uniform(0.1, 1.0, 3000)]))
+    t = hb.CooTensor(dims, idx, vals)
+    f = [rng.random((d, rank)).astype(np.float32).astype(np.float64) for d in dims]
+    fd = [torch.from_numpy(x).float().cuda() for x in f]
+    for mode in range(3):
+        mo = hb.allmode_order(dims, mode)
+        h = hb.split_fibers(hb.build_hbcsf(t, mo), hb.SplitConfig(fiber_threshold=16))
+        pl = plan_for(h, mode, rank)
+        ref_h = P.split_hbcsf(P.hbcsf(idx, vals, dims, mo), 16)
+        ref, ops = P.mttkrp_hbcsf(ref_h, f, mode)
+        y, oc = hb.mttkrp_hbcsf(h, f, mode)
+        assert P.row_deviation(y, ref) <= 1e-4
+        assert (oc.muls, oc.adds) == tuple(ops)
+        if dims[mo[2]] * 4 * min(rank, 32) > float(block_mb) * 1e6:
+            assert pl.info.leaf_blocks > 1 and pl.info.leaf_blocked_nnz > 0
+        out = torch.full((dims[mode], rank), 3.0, device="cuda")
+        for _ in range(2):
+            mttkrp_device(h, fd, mode, out=out)
+        assert P.row_deviation(out.double().cpu().numpy(), ref) <= 1e-4
+        y64, _ = hb.mttkrp_hbcsf(h, f, mode, precision="fp64")
+        assert P.row_deviation(y64, ref) <= 1e-9
+        owned = pl.owned_rows().cpu().numpy()
+        want = np.nonzero(np.bincount(idx[:, mode].astype(np.int64), minlength=dims[mode]))[0]
+        assert np.array_equal(np.sort(owned), want)
+        out.fill_(7.0)
+        mttkrp_device(h, fd, mode, out=out, skip_unowned=True)
+        got = out.double().cpu().numpy()
+        assert P.row_deviation(got[want], ref[want]) <= 1e-4
