@@ -23,7 +23,7 @@ def run(cfg):
     out.parent.mkdir(exist_ok=True)
     cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
            "lts__t_sectors.sum,lts__t_sectors_lookup_hit.sum",
-           "-k", "regex:k_mttkrp3", "--csv", "--log-file", str(out),
+           "-k", "regex:k_mttkrp3|k_zero_rows", "--csv", "--log-file", str(out),
            sys.executable, str(ROOT / "bench.py"), "--config", cfg, "--steps", str(K),
            "--warmup", str(W), "--no-e2e", "--no-cpu-baseline", "--also", "", "--cpd", "none", "--no-amortize"]
     r = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT)
@@ -62,7 +62,7 @@ def run(cfg):
             "launches_per_mode": lpm,
             "l2_hit_rate_pct": 100.0 * hit_all / sec_all if sec_all else None,
             "note": (f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors(_lookup_hit).sum "
-                     f"-k regex:k_mttkrp3 on "
+                     f"-k regex:k_mttkrp3|k_zero_rows on "
                      f"bench.py --config {cfg} --steps {K} --warmup {W}: per mode, the sum over that "
                      "mode's launches, averaged over the steps (cold caches per replay)")}
 
