@@ -1,5 +1,6 @@
 """Touched-rows exchange volume of row-sharded CP-ALS (SURVEY §8e asks for
-the measured union sizes): for P ranks with nnz-balanced row ranges per mode,
+the measured union sizes): for P ranks with the row ranges cp_als_distributed
+uses (shard.partition_costs: nonzeros + fibers + a per-row charge),
 rank r needs the rows of factor d that its shards of the *other* modes read;
 it owns range_d[r] itself.  Prints, per P, the factor-row ingress per GPU per
 sweep for the touched-rows exchange vs full replication (max and mean over
@@ -30,7 +31,7 @@ def main():
     dims = CONFIGS[cfg]["dims"]
     t = config_tensor(cfg)
     idx = torch.from_numpy(np.ascontiguousarray(t.indices).astype(np.int64)).cuda()
-    hists = [shard.slice_histogram(t, m).cpu().numpy() for m in range(3)]
+    hists = [shard.partition_costs(t, m).cpu().numpy() for m in range(3)]
     out = {"config": cfg, "rank": R, "per_P": {}}
     for P in Ps:
         ranges = [shard.plan_row_ranges(hists[m], P) for m in range(3)]
