@@ -1090,6 +1090,9 @@ struct hbk_plan {
   bool concurrent = false;
   cudaStream_t side[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
+  // leaf-blocked plans: one fork over both sub-plans' kernels (up to 8)
+  cudaStream_t side_all[7] = {};
+  cudaEvent_t ev_join_all[7] = {};
   int grid_heavy = 0;
   bool fast = false;
   bool bpos = false;
@@ -1114,6 +1117,10 @@ struct hbk_plan {
     for (int i = 0; i < 3; ++i) {
       if (side[i]) cudaStreamDestroy(side[i]);
       if (ev_join[i]) cudaEventDestroy(ev_join[i]);
+    }
+    for (int i = 0; i < 7; ++i) {
+      if (side_all[i]) cudaStreamDestroy(side_all[i]);
+      if (ev_join_all[i]) cudaEventDestroy(ev_join_all[i]);
     }
     if (ev_fork) cudaEventDestroy(ev_fork);
     hbk_coo_release(coo);
@@ -2175,39 +2182,26 @@ __global__ void k_zero_rows(const uint32_t* __restrict__ rows, int64_t n, uint32
     out[size_t(rows[i / rs]) * rs + i % rs] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
-template <class FX>
-static void launch_fast(const hbk_plan* p, const FX& fx, cudaStream_t st, bool skip_zero = false) {
-  // kernels in launch order: heavy slices first (the longest), then light
-  // CSF, CSL, COO/zero; with p->concurrent each after the first goes to its
-  // own forked stream
-  int n = 0;
-  auto next_stream = [&]() -> cudaStream_t {
-    if (!p->concurrent || n == 0) {
-      ++n;
-      return st;
-    }
-    cudaStream_t s2 = p->side[n - 1];
-    HBK_CUDA(cudaStreamWaitEvent(s2, p->ev_fork, 0));
-    ++n;
-    return s2;
-  };
-  if (p->concurrent) HBK_CUDA(cudaEventRecord(p->ev_fork, st));
+// A plan's bucket kernels in launch order — heavy slices first (the
+// longest), then light CSF, CSL, COO/zero — each on the stream `next()` hands out.
+template <class FX, class Next>
+static void launch_kernels(const hbk_plan* p, const FX& fx, bool skip_zero, Next&& next) {
   if (p->grid_heavy) {
-    cudaStream_t s2 = next_stream();
+    cudaStream_t s2 = next();
     if (p->acc_csf)
       k_mttkrp3_r32<KIND_CSF_UNI_ACC, FX><<<p->grid_heavy, p->block, 0, s2>>>(p->work_heavy, fx);
     else
       k_mttkrp3_r32<KIND_CSF_UNI, FX><<<p->grid_heavy, p->block, 0, s2>>>(p->work_heavy, fx);
   }
   if (p->grids[0]) {
-    cudaStream_t s2 = next_stream();
+    cudaStream_t s2 = next();
     if (p->acc_csf)
       k_mttkrp3_r32<KIND_CSF_BPOS4_ACC, FX><<<p->grids[0], p->block, 0, s2>>>(p->work, fx);
     else
       k_mttkrp3_r32<KIND_CSF_BPOS4, FX><<<p->grids[0], p->block, 0, s2>>>(p->work, fx);
   }
   if (p->grids[1]) {
-    cudaStream_t s2 = next_stream();
+    cudaStream_t s2 = next();
     if (p->csl_acc)
       k_mttkrp3_r32<KIND_CSL_ACC, FX><<<p->grids[1], p->block, 0, s2>>>(p->work, fx);
     else
@@ -2217,16 +2211,64 @@ static void launch_fast(const hbk_plan* p, const FX& fx, cudaStream_t st, bool s
   Work wc = p->work;
   if (skip_zero) wc.n3 = wc.n2;
   if (p->grids[2] && wc.n3 > wc.n1) {
-    cudaStream_t s2 = next_stream();
+    cudaStream_t s2 = next();
     k_mttkrp3_r32<KIND_COO, FX><<<p->grids[2], p->block, 0, s2>>>(wc, fx);
   }
   check_launch("k_mttkrp3_r32");
-  if (p->concurrent)
-    for (int i = 0; i + 1 < n; ++i) {
-      HBK_CUDA(cudaEventRecord(p->ev_join[i], p->side[i]));
-      HBK_CUDA(cudaStreamWaitEvent(st, p->ev_join[i], 0));
-    }
 }
+
+// Fork / join over `nside` side streams: the first kernel runs on st, each
+// later one on its own side stream forked from st (persistent kernels with
+// full-occupancy grids, so the next one's CTAs fill the SMs the previous
+// one's finishing CTAs free — the launch tails overlap).
+struct Forker {
+  cudaStream_t st;
+  const cudaStream_t* side;
+  const cudaEvent_t* join;
+  cudaEvent_t fork;
+  int nside, n = 0;
+  cudaStream_t operator()() {
+    if (fork == nullptr || n == 0) {
+      ++n;
+      return st;
+    }
+    HBK_REQUIRE(n - 1 < nside, HBK_ECUDA, "not enough side streams");
+    cudaStream_t s2 = side[n - 1];
+    HBK_CUDA(cudaStreamWaitEvent(s2, fork, 0));
+    ++n;
+    return s2;
+  }
+  void begin() {
+    if (fork) HBK_CUDA(cudaEventRecord(fork, st));
+  }
+  void end() {
+    if (fork)
+      for (int i = 0; i + 1 < n; ++i) {
+        HBK_CUDA(cudaEventRecord(join[i], side[i]));
+        HBK_CUDA(cudaStreamWaitEvent(st, join[i], 0));
+      }
+  }
+};
+
+template <class FX>
+static void launch_fast(const hbk_plan* p, const FX& fx, cudaStream_t st, bool skip_zero = false) {
+  Forker f{st, p->side, p->ev_join, p->concurrent ? p->ev_fork : nullptr, 3};
+  f.begin();
+  launch_kernels(p, fx, skip_zero, f);
+  f.end();
+}
+
+// The leaf-blocked pair: the blocked sub-plan's kernels first, the main
+// sub-plan's after them, all under one fork so their tails overlap too.
+template <class FX>
+static void launch_blocked(const hbk_plan* p, const FX& fx, cudaStream_t st, bool skip_zero) {
+  Forker f{st, p->side_all, p->ev_join_all, p->ev_fork, 7};
+  f.begin();
+  launch_kernels(p->sub_blk, fx, false, f);
+  launch_kernels(p->sub_main, fx, skip_zero, f);
+  f.end();
+}
+
 // Orders executions of one plan (see hbk_plan::exec_mu).  Inside a CUDA
 // graph capture the capturing stream already orders the replays, and an
 // event recorded outside the capture may not be waited on, so capture skips it.
@@ -2649,6 +2691,13 @@ static bool build_leaf_blocked(hbk_plan* p, int64_t BB, uint32_t minnz, cudaStre
   build_plan(sm.get(), st);
   p->sub_blk = sb.release();
   p->sub_main = sm.release();
+  if (!getenv("HBK_CONCURRENT") || atoi(getenv("HBK_CONCURRENT")) != 0) {
+    HBK_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+    for (int i = 0; i < 7; ++i) {
+      HBK_CUDA(cudaStreamCreateWithFlags(&p->side_all[i], cudaStreamNonBlocking));
+      HBK_CUDA(cudaEventCreateWithFlags(&p->ev_join_all[i], cudaEventDisableTiming));
+    }
+  }
   p->leaf_bb = BB;
   p->leaf_min = minnz;
   p->info.leaf_blocks = (p->dims[p->mo[2]] + BB - 1) / BB;
@@ -2837,15 +2886,13 @@ int hbk_plan_execute_ex(const hbk_plan* p, const float* const* factors, float* o
         check_launch("k_zero_rows");
       }
       if (p->sub_blk->r32) {
-        launch_fast(p->sub_blk, Factors3R32(fx), st);
-        launch_fast(p->sub_main, Factors3R32(fx), st, skip_zero);
+        launch_blocked(p, Factors3R32(fx), st, skip_zero);
       } else {
         fx.rs = uint32_t(R / 4);
         for (int c0 = 0; c0 < R; c0 += 32) {
           fx.col4 = uint32_t(c0 / 4);
           fx.lanes = uint32_t(std::min(8, (R - c0) / 4));
-          launch_fast(p->sub_blk, fx, st);
-          launch_fast(p->sub_main, fx, st, skip_zero);
+          launch_blocked(p, fx, st, skip_zero);
         }
       }
     } else if (p->fast) {

@@ -36,7 +36,7 @@ for cfg in sys.argv[1:]:
         tot += ms
         print(f"[{tag}] {cfg} mode {mode}: {ms:.3f} ms  leaf_blocks {pl.info.leaf_blocks} "
               f"blocked_nnz {pl.info.leaf_blocked_nnz} head_share {pl.info.leaf_head_share_ppm / 1e6:.3f} "
-              f"csl_blocks {pl.info.csl_blocks}", flush=True)
+              f"csl_blocks {pl.info.csl_blocks} gather_rows {pl.info.gather_rows / 1e6:.1f}M", flush=True)
         del h, pl, y
         torch.cuda.empty_cache()
     print(f"[{tag}] {cfg} step {tot:.3f} ms", flush=True)
