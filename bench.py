@@ -588,7 +588,7 @@ def with_allgather(env, st, args, flops_step):
     output rows on all ranks (all-gather over NCCL) — the standalone MTTKRP
     with and without the output exchange."""
     torch, dist = env.torch, env.dist
-    from paper_1904_03329_b200.distributed import allgather_padded
+    from paper_1904_03329_b200.distributed import allgather_rows
 
     n_modes = len(st["dims"])
     stream = torch.cuda.current_stream()
@@ -597,7 +597,7 @@ def with_allgather(env, st, args, flops_step):
         for m in range(n_modes):
             if st["plans"][m] is not None:
                 st["plans"][m].execute(st["ptrs"][m], st["outs"][m])
-            allgather_padded(torch, dist, st["outs"][m][: st["rows_local"][m]], st["all_ranges"][m])
+            allgather_rows(torch, dist, st["outs"][m][: st["rows_local"][m]], st["all_ranges"][m])
 
     for _ in range(max(1, args.warmup)):
         step_ag()

@@ -44,20 +44,27 @@ def _dist():
     return dist
 
 
-def allgather_padded(torch, dist, local, ranges, group=None):
-    """Replicate a row-sharded (rows, R) matrix: one all_gather_into_tensor of
-    max-shard-sized buffers, then the padding is dropped."""
-    world = len(ranges)
+def allgather_rows(torch, dist, local, ranges, group=None):
+    """Replicate a row-sharded (rows, R) matrix whose ranks own contiguous,
+    unequal row ranges (SURVEY §8e "allgatherv = one broadcast per rank"):
+    rank r's rows are broadcast from r straight into their place in the full
+    matrix, so every rank receives exactly the rows it does not own — no
+    padding to the largest range (the cost-balanced cuts give ranges of very
+    different sizes: 24M of flickr-3d mode 1's 28M rows on one of 8 ranks)."""
+    me = dist.get_rank(group)
     width = local.shape[1]
-    cap = max(1, max(hi - lo for lo, hi in ranges))
-    buf = torch.zeros((cap, width), dtype=local.dtype, device=local.device)
-    buf[: local.shape[0]] = local
-    out = torch.empty((world * cap, width), dtype=local.dtype, device=local.device)
-    if local.device.type == "cuda" and dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(out, buf, group=group)
-    else:
-        dist.all_gather(list(out.chunk(world)), buf, group=group)
-    return torch.cat([out[g * cap: g * cap + (hi - lo)] for g, (lo, hi) in enumerate(ranges)])
+    total = ranges[-1][1] if ranges else 0
+    out = torch.empty((total, width), dtype=local.dtype, device=local.device)
+    lo, hi = ranges[me]
+    out[lo:hi] = local[: hi - lo]
+    works = []
+    for r, (a, b) in enumerate(ranges):
+        if b > a:
+            src = dist.get_global_rank(group, r) if group is not None else r
+            works.append(dist.broadcast(out[a:b], src=src, group=group, async_op=True))
+    for w in works:
+        w.wait()
+    return out
 
 
 class DeviceShards:

@@ -64,13 +64,17 @@ def _run(job, world=2):
 
 # --------------------------------------------------------------- jobs (picklable)
 def _job_allgather(rank, world):
-    from paper_1904_03329_b200.distributed import allgather_padded
+    from paper_1904_03329_b200.distributed import allgather_rows
 
-    ranges = [(0, 5), (5, 6)] if world == 2 else [(0, 6)]
     full = torch.arange(6 * 3, dtype=torch.float64).reshape(6, 3)
-    lo, hi = ranges[rank]
-    got = allgather_padded(torch, dist, full[lo:hi].clone(), ranges)
-    return bool(torch.equal(got, full))
+    ok = True
+    # uneven ranges, and a rank with an empty range
+    for ranges in ([(0, 5), (5, 6)], [(0, 6), (6, 6)], [(0, 0), (0, 6)]):
+        ranges = ranges if world == 2 else [(0, 6)]
+        lo, hi = ranges[rank]
+        got = allgather_rows(torch, dist, full[lo:hi].clone(), ranges)
+        ok = ok and bool(torch.equal(got, full))
+    return ok
 
 
 def _local_mttkrp_factory(idx, vals, dims, ranges, rank):
@@ -157,7 +161,7 @@ def _job_cpd_subgroup(rank, world):
     return res
 
 
-def test_allgather_padded_uneven_world2():
+def test_allgather_rows_uneven_world2():
     assert _run(_job_allgather) == [True, True]
 
 
