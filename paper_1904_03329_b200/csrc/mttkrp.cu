@@ -1557,7 +1557,20 @@ static HeavyLayout heavy_layout(const hbk_csf* c, const uint32_t* loff, const ui
   check_launch("k_heavy_flags");
   const uint32_t nheavy = exclusive_scan_total(hflag.as<uint32_t>(), S, st);  // -> heavy rank
   if (nheavy == 0) return hl;
-  exclusive_scan_total(hoff.as<uint32_t>(), S, st);
+  const uint32_t hnnz = exclusive_scan_total(hoff.as<uint32_t>(), S, st);
+  // warp-task size: W, or smaller when the heavy slices hold too few nonzeros
+  // for ~8 tasks per resident warp (small shards of a multi-GPU partition:
+  // the last wave of ~1024-nonzero tasks left the GPU a third idle at 1/8 of
+  // nell-2)
+  {
+    int dev = 0, sms = 0;
+    HBK_CUDA(cudaGetDevice(&dev));
+    HBK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // (inputs too small to fill the GPU once keep W: one wave either way)
+    const uint64_t want = uint64_t(std::max(sms, 1)) * 24 * 8;
+    const uint64_t wmin = std::max<uint32_t>(4 * tau, 128u);
+    if (hnnz / want >= wmin) W = uint32_t(std::min<uint64_t>(W, hnnz / want));
+  }
   Scratch fslice((F + 1) * 4, st), segoff((F + 1) * 4, st);
   k_fiber_slice<<<grid_for(F, 256), 256, 0, st>>>(fpos, S, F, fslice.as<uint32_t>());
   check_launch("k_fiber_slice");
