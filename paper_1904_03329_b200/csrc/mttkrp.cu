@@ -79,6 +79,11 @@ struct alignas(16) Work {
   const uint32_t* coo_k;
   const float* coo_val;
   const uint4* coo_quads;     // [M] (row, j, k, value bits)
+  // fp64 value streams for the fast kernels' fp64 instantiation, one double
+  // per position of csf_pairs / csl_pairs / coo_quads (0 at B positions)
+  const double* csf_v64;
+  const double* csl_v64;
+  const double* coo_v64;
   // ZERO list
   const uint32_t* zero_rows;
   // split-slice workspace (self-cleaning)
@@ -101,6 +106,9 @@ static constexpr uint32_t FB = 0x80000000u;    // B-row position (B-position str
 static constexpr uint32_t XMASK = 0x3FFFFFFFu;
 
 struct Factors3 {
+  using V = float4;  // 16-byte lane vector and its scalar
+  using S = float;
+  static constexpr bool F64 = false;
   const float4* B;  // factor of mode_order[1] (fiber / rest[0])
   const float4* C;  // factor of mode_order[2] (leaf / rest[1])
   float4* out;
@@ -113,12 +121,39 @@ struct Factors3 {
 // The R = 32 specialisation: one full pass, strides known at compile time
 // (the runtime fields cost registers the B-position kernels do not have).
 struct Factors3R32 {
+  using V = float4;
+  using S = float;
+  static constexpr bool F64 = false;
   const float4* B;
   const float4* C;
   float4* out;
   static constexpr uint32_t rs = 8, col4 = 0, lanes = 8;
   Factors3R32() = default;
   __host__ __device__ explicit Factors3R32(const Factors3& f) : B(f.B), C(f.C), out(f.out) {}
+};
+// fp64 views: a lane holds a double2 (16 bytes, like float4), so a pass of
+// 8 lanes covers 16 columns and the row stride / column offsets stay in
+// 16-byte units.  Factors3D: any even R (runtime stride); Factors3DR32:
+// R = 32 plans, whose B-position streams hold row indices pre-scaled to
+// float4 units (x 8): a double2 row of R = 32 is 16 units, so x 2.
+struct Factors3D {
+  using V = double2;
+  using S = double;
+  static constexpr bool F64 = true;
+  const double2* B;
+  const double2* C;
+  double2* out;
+  uint32_t rs, col4, lanes;
+};
+struct Factors3DR32 {
+  using V = double2;
+  using S = double;
+  static constexpr bool F64 = true;
+  const double2* B;
+  const double2* C;
+  double2* out;
+  uint32_t col4;  // 0 or 8: the two 16-column passes
+  static constexpr uint32_t rs = 16, lanes = 8;
 };
 // A lane's column within the pass; idle lanes of a partial pass mirror the
 // last active one (valid addresses) and never store.
@@ -141,18 +176,26 @@ template <class P>
 __device__ __forceinline__ P* rowp(P* base, uint32_t x, const Factors3R32&) {
   return base + size_t(x) * 8;
 }
-template <class P>
-__device__ __forceinline__ P* rowp(P* base, uint32_t x, const Factors3& fx) {
+template <class P, class FX>
+__device__ __forceinline__ P* rowp(P* base, uint32_t x, const FX& fx) {
   uint64_t r;
   asm("mad.wide.u32 %0, %1, %2, %3;"
       : "=l"(r)
-      : "r"(x), "r"(uint32_t(fx.rs * sizeof(float4))), "l"(base));
+      : "r"(x), "r"(uint32_t(fx.rs * 16u)), "l"(base));
   return reinterpret_cast<P*>(r);
+}
+template <class P>
+__device__ __forceinline__ P* rowp(P* base, uint32_t x, const Factors3DR32&) {
+  return base + size_t(x) * 16;
 }
 template <class P>
 __device__ __forceinline__ P* srowp(P* base, uint32_t x, const Factors3R32&) { return base + x; }
 template <class P>
-__device__ __forceinline__ P* srowp(P* base, uint32_t x, const Factors3& fx) {
+__device__ __forceinline__ P* srowp(P* base, uint32_t x, const Factors3DR32&) {
+  return base + size_t(x) * 2;
+}
+template <class P, class FX>
+__device__ __forceinline__ P* srowp(P* base, uint32_t x, const FX& fx) {
   return rowp(base, x, fx);
 }
 
@@ -192,6 +235,47 @@ __device__ __forceinline__ void st_cg4(float4* p, float4 v) {
                "f"(v.w)
                : "memory");
 }
+// double2 counterparts of the float4 lane-vector operations
+template <class V> __device__ __forceinline__ V vzero();
+template <> __device__ __forceinline__ float4 vzero<float4>() { return f4zero(); }
+template <> __device__ __forceinline__ double2 vzero<double2>() { return make_double2(0.0, 0.0); }
+__device__ __forceinline__ double2 fma4(double a, double2 x, double2 y) {
+  return make_double2(fma(a, x.x, y.x), fma(a, x.y, y.y));
+}
+__device__ __forceinline__ double2 fmav4(double2 a, double2 x, double2 y) {
+  return make_double2(fma(a.x, x.x, y.x), fma(a.y, x.y, y.y));
+}
+__device__ __forceinline__ double2 mul4(double a, double2 x) { return make_double2(a * x.x, a * x.y); }
+__device__ __forceinline__ double2 add4(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 shfl_xor4(double2 v, int m) {
+  return make_double2(__shfl_xor_sync(0xFFFFFFFFu, v.x, m), __shfl_xor_sync(0xFFFFFFFFu, v.y, m));
+}
+__device__ __forceinline__ void red_add4(double2* p, double2 v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v.x) : "memory");
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(reinterpret_cast<double*>(p) + 1), "d"(v.y)
+               : "memory");
+}
+__device__ __forceinline__ double2 ld_cg4(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.cg.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_cg4(double2* p, double2 v) {
+  asm volatile("st.global.cg.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ double2 ld_row4(const double2* p, uint64_t pol) {
+  double2 v;
+  asm("ld.global.nc.L1::evict_last.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+      : "=d"(v.x), "=d"(v.y)
+      : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_stream_f64(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ uint2 ld_stream_u2(const uint2* p, uint64_t pol) {
   uint2 v;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
@@ -222,6 +306,9 @@ __device__ __forceinline__ void cp_async16(float4* smem, const float4* gmem) {
   const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async16(double2* smem, const double2* gmem) {
+  cp_async16(reinterpret_cast<float4*>(smem), reinterpret_cast<const float4*>(gmem));
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
@@ -237,10 +324,10 @@ __device__ __forceinline__ uint32_t any_group(uint32_t ballot) {
 template <class FX>
 __device__ __forceinline__ void flush_split(const Work& w, const FX& fx, bool active,
                                             uint32_t slot, uint32_t nchunk, uint32_t inc,
-                                            uint32_t row, float4 sa, int lane, int lig) {
+                                            uint32_t row, typename FX::V sa, int lane, int lig) {
+  using V = typename FX::V;
   const bool live = lane_live(fx, lig);
-  float4* acc = reinterpret_cast<float4*>(w.ws_acc) + size_t(active ? slot : 0) * fx.rs +
-                fx.col4 + lig;
+  V* acc = reinterpret_cast<V*>(w.ws_acc) + size_t(active ? slot : 0) * fx.rs + fx.col4 + lig;
   if (active && live) red_add4(acc, sa);
   __threadfence();
   __syncwarp();
@@ -250,9 +337,9 @@ __device__ __forceinline__ void flush_split(const Work& w, const FX& fx, bool ac
   if (active && old + inc == nchunk) {
     __threadfence();
     if (live) {
-      const float4 r = ld_cg4(acc);
+      const V r = ld_cg4(acc);
       fx.out[size_t(row) * fx.rs + fx.col4 + lig] = r;
-      st_cg4(acc, f4zero());
+      st_cg4(acc, vzero<V>());
     }
     if (lig == 0) w.ws_cnt[slot] = 0;
   }
@@ -271,19 +358,25 @@ __device__ __forceinline__ void flush_split(const Work& w, const FX& fx, bool ac
 // ACC (leaf-blocked view, csf_block_view): slice ends add the partial row
 // into the pre-zeroed output row (a slice is cut into several virtual slices).
 template <bool UNIFORM, bool ACC, class FX>
-__device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const FX& fx, const Task& t,
-                                                 int g, int lig, uint64_t pol_s, uint64_t pol_r) {
+__device__ __forceinline__ typename FX::V csf_bpos_tasks(const Work& w, const FX& fx, const Task& t,
+                                                        int g, int lig, uint64_t pol_s, uint64_t pol_r) {
+  using V = typename FX::V;
+  using S = typename FX::S;
   const uint32_t lo = t.lo, hi = t.hi;
   const bool chunk = UNIFORM || t.slot != NOSLOT;
   const uint32_t nbat = __reduce_max_sync(FULL, hi > lo ? (hi - lo + 7) / 8 : 0u);
-  const float4* Cl = fx.C + lane_col(fx, lig);
-  const float4* Bl = fx.B + lane_col(fx, lig);
+  const V* Cl = fx.C + lane_col(fx, lig);
+  const V* Bl = fx.B + lane_col(fx, lig);
   const uint2* pairs = w.csf_pairs;
   const uint32_t Sm1 = w.csf_S ? w.csf_S - 1 : 0;
   uint32_t s = t.s;
-  float4 fa = f4zero(), sa = f4zero();
+  V fa = vzero<V>(), sa = vzero<V>();
   uint2 pr = make_uint2(0u, 0u);
-  if (lo + lig < hi) pr = ld_stream_u2(pairs + lo + lig, pol_s);
+  double pv = 0.0;  // fp64 views: the value of this lane's position
+  if (lo + lig < hi) {
+    pr = ld_stream_u2(pairs + lo + lig, pol_s);
+    if constexpr (FX::F64) pv = ld_stream_f64(w.csf_v64 + lo + lig, pol_s);
+  }
   uint32_t sr = chunk ? 0u : __ldg(w.csf_sidx + min(s + lig, Sm1));
   uint32_t base = lo;
   for (uint32_t it = 0; it < nbat; ++it, base += 8) {
@@ -295,18 +388,21 @@ __device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const FX& fx, co
       sbits = (sb_all >> (8 * g)) & 0xFFu;
       sany = any_group(sb_all);
     }
-    float4 r[8];
+    V r[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t xj = __shfl_sync(FULL, pr.x, j, 8);
-      const float4* bp = (UNIFORM ? ((bbits >> j) & 1u) : (xj & FB)) ? Bl : Cl;
+      const V* bp = (UNIFORM ? ((bbits >> j) & 1u) : (xj & FB)) ? Bl : Cl;
       r[j] = ld_row4(srowp(bp, xj & XMASK, fx), pol_r);
     }
-    const float vv = __uint_as_float(pr.y);
+    const S vv = FX::F64 ? S(pv) : S(__uint_as_float(pr.y));
     const uint32_t sr_cur = sr;
     const uint32_t nb = base + 8;
     pr = make_uint2(0u, 0u);
-    if (nb + lig < hi) pr = ld_stream_u2(pairs + nb + lig, pol_s);
+    if (nb + lig < hi) {
+      pr = ld_stream_u2(pairs + nb + lig, pol_s);
+      if constexpr (FX::F64) pv = ld_stream_f64(w.csf_v64 + nb + lig, pol_s);
+    }
     if (!UNIFORM) {
       const uint32_t nsl = __popc(sbits);
       s += nsl;
@@ -315,11 +411,11 @@ __device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const FX& fx, co
     uint32_t ts = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const float vj = __shfl_sync(FULL, vv, j, 8);
+      const S vj = __shfl_sync(FULL, vv, j, 8);
       if (UNIFORM) {
         if ((bbits >> j) & 1u) {
           sa = fmav4(fa, r[j], sa);
-          fa = f4zero();
+          fa = vzero<V>();
         } else {
           fa = fma4(vj, r[j], fa);
         }
@@ -328,16 +424,16 @@ __device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const FX& fx, co
       fa = fma4(vj, r[j], fa);
       if ((bbits >> j) & 1u) {
         sa = fmav4(fa, r[j], sa);
-        fa = f4zero();
+        fa = vzero<V>();
       }
       if ((sany >> j) & 1u) {
         const uint32_t row = __shfl_sync(FULL, sr_cur, ts, 8);
         if ((sbits >> j) & 1u) {
           if (lane_live(fx, lig)) {
-            float4* o = fx.out + size_t(row) * fx.rs + fx.col4 + lig;
+            V* o = fx.out + size_t(row) * fx.rs + fx.col4 + lig;
             if (ACC) red_add4(o, sa); else *o = sa;
           }
-          sa = f4zero();
+          sa = vzero<V>();
           ++ts;
         }
       }
@@ -356,22 +452,26 @@ __device__ __forceinline__ float4 csf_bpos_tasks(const Work& w, const FX& fx, co
 // ACC (blocked CSL layout): slice ends add the partial row into the
 // pre-zeroed output instead of storing it (a slice spans several blocks).
 template <bool ACC, class FX>
-__device__ __forceinline__ float4 csl_tasks(const Work& w, const FX& fx, const Task& t,
-                                            int g, int lig, uint64_t pol_s, uint64_t pol_r,
-                                            float4* __restrict__ slots) {
+__device__ __forceinline__ typename FX::V csl_tasks(const Work& w, const FX& fx, const Task& t,
+                                                   int g, int lig, uint64_t pol_s, uint64_t pol_r,
+                                                   typename FX::V* __restrict__ slots) {
+  using V = typename FX::V;
+  using S = typename FX::S;
   const uint32_t lo = t.lo, hi = t.hi;
   const bool chunk = t.slot != NOSLOT;
   const uint32_t my_batches = hi > lo ? (hi - lo + 7) / 8 : 0;
   const uint32_t nbat = __reduce_max_sync(FULL, my_batches);
-  const float4* Cl = fx.C + lane_col(fx, lig);
-  const float4* Bl = fx.B + lane_col(fx, lig);
+  const V* Cl = fx.C + lane_col(fx, lig);
+  const V* Bl = fx.B + lane_col(fx, lig);
   uint32_t s = t.s;
-  float4 sa = f4zero();
+  V sa = vzero<V>();
   uint2 pr = make_uint2(0u, 0u);
   uint32_t jx = 0;
+  double pv = 0.0;
   if (lo + lig < hi) {
     pr = ld_stream_u2(w.csl_pairs + lo + lig, pol_s);
     jx = ld_stream_u32(w.csl_j + lo + lig, pol_s);
+    if constexpr (FX::F64) pv = ld_stream_f64(w.csl_v64 + lo + lig, pol_s);
   }
   uint32_t sr = (hi > lo && !chunk && s + lig < w.csl_S) ? __ldg(w.csl_sidx + s + lig) : 0u;
   uint32_t base = lo;
@@ -379,11 +479,11 @@ __device__ __forceinline__ float4 csl_tasks(const Work& w, const FX& fx, const T
     const uint32_t n = base < hi ? min(8u, hi - base) : 0u;
     const bool live = uint32_t(lig) < n;
     const uint32_t k = pr.x & KMASK;
-    const float v = __uint_as_float(pr.y);
+    const S v = FX::F64 ? S(pv) : S(__uint_as_float(pr.y));
     const uint32_t sb_all = __ballot_sync(FULL, live && !chunk && (pr.x & SEND));
     const uint32_t sbits = (sb_all >> (8 * g)) & 0xFFu;
     const uint32_t sany = any_group(sb_all);
-    float4 c[8];
+    V c[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t bj = __shfl_sync(FULL, jx, j, 8);
@@ -394,29 +494,30 @@ __device__ __forceinline__ float4 csl_tasks(const Work& w, const FX& fx, const T
       }
     }
     const uint32_t sr_cur = sr;
-    const float vv = v;
+    const S vv = v;
     const uint32_t nsl = __popc(sbits);
     s += nsl;
     const uint32_t nb = base + 8;
     if (nb + lig < hi) {
       pr = ld_stream_u2(w.csl_pairs + nb + lig, pol_s);
       jx = ld_stream_u32(w.csl_j + nb + lig, pol_s);
+      if constexpr (FX::F64) pv = ld_stream_f64(w.csl_v64 + nb + lig, pol_s);
     }
     if (nsl && nb < hi) sr = (s + lig < w.csl_S) ? __ldg(w.csl_sidx + s + lig) : 0u;
     cp_async_wait_all();
     uint32_t ts = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const float vj = __shfl_sync(FULL, vv, j, 8);
+      const S vj = __shfl_sync(FULL, vv, j, 8);
       if (uint32_t(j) < n) sa = fmav4(mul4(vj, slots[j * 8]), c[j], sa);
       if ((sany >> j) & 1u) {
         const uint32_t row = __shfl_sync(FULL, sr_cur, ts, 8);
         if ((sbits >> j) & 1u) {
           if (lane_live(fx, lig)) {
-            float4* o = fx.out + size_t(row) * fx.rs + fx.col4 + lig;
+            V* o = fx.out + size_t(row) * fx.rs + fx.col4 + lig;
             if (ACC) red_add4(o, sa); else *o = sa;
           }
-          sa = f4zero();
+          sa = vzero<V>();
           ++ts;
         }
       }
@@ -429,18 +530,24 @@ __device__ __forceinline__ float4 csl_tasks(const Work& w, const FX& fx, const T
 template <class FX>
 __device__ __forceinline__ void coo_tasks(const Work& w, const FX& fx, const Task& t,
                                           int lig, uint64_t pol_s, uint64_t pol_r,
-                                          float4* __restrict__ slots) {
+                                          typename FX::V* __restrict__ slots) {
+  using V = typename FX::V;
+  using S = typename FX::S;
   const uint32_t lo = t.lo, hi = t.hi;
   const uint32_t my_batches = hi > lo ? (hi - lo + 7) / 8 : 0;
   const uint32_t nbat = __reduce_max_sync(FULL, my_batches);
-  const float4* Cl = fx.C + lane_col(fx, lig);
-  const float4* Bl = fx.B + lane_col(fx, lig);
+  const V* Cl = fx.C + lane_col(fx, lig);
+  const V* Bl = fx.B + lane_col(fx, lig);
   uint4 q = make_uint4(0u, 0u, 0u, 0u);
-  if (lo + lig < hi) q = ld_stream_u4(w.coo_quads + lo + lig, pol_s);
+  double pv = 0.0;
+  if (lo + lig < hi) {
+    q = ld_stream_u4(w.coo_quads + lo + lig, pol_s);
+    if constexpr (FX::F64) pv = ld_stream_f64(w.coo_v64 + lo + lig, pol_s);
+  }
   uint32_t base = lo;
   for (uint32_t it = 0; it < nbat; ++it, base += 8) {
     const uint32_t n = base < hi ? min(8u, hi - base) : 0u;
-    float4 c[8];
+    V c[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t bj = __shfl_sync(FULL, q.y, j, 8);
@@ -451,19 +558,19 @@ __device__ __forceinline__ void coo_tasks(const Work& w, const FX& fx, const Tas
       }
     }
     const uint4 cur = q;
+    const S vcur = FX::F64 ? S(pv) : S(__uint_as_float(q.w));
     const uint32_t nb = base + 8;
-    if (nb + lig < hi) q = ld_stream_u4(w.coo_quads + nb + lig, pol_s);
+    if (nb + lig < hi) {
+      q = ld_stream_u4(w.coo_quads + nb + lig, pol_s);
+      if constexpr (FX::F64) pv = ld_stream_f64(w.coo_v64 + nb + lig, pol_s);
+    }
     cp_async_wait_all();
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t row = __shfl_sync(FULL, cur.x, j, 8);
-      const float vj = __uint_as_float(__shfl_sync(FULL, cur.w, j, 8));
+      const S vj = __shfl_sync(FULL, vcur, j, 8);
       if (uint32_t(j) < n) {
-        float4 r = mul4(vj, slots[j * 8]);
-        r.x *= c[j].x;
-        r.y *= c[j].y;
-        r.z *= c[j].z;
-        r.w *= c[j].w;
+        const V r = fmav4(mul4(vj, slots[j * 8]), c[j], vzero<V>());
         if (lane_live(fx, lig)) fx.out[size_t(row) * fx.rs + fx.col4 + lig] = r;
       }
     }
@@ -483,7 +590,8 @@ __device__ __forceinline__ void zero_task(const Work& w, const FX& fx, const Tas
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t row = __shfl_sync(FULL, rl, j, 8);
-      if (uint32_t(j) < n && lane_live(fx, lig)) fx.out[size_t(row) * fx.rs + fx.col4 + lig] = f4zero();
+      if (uint32_t(j) < n && lane_live(fx, lig))
+        fx.out[size_t(row) * fx.rs + fx.col4 + lig] = vzero<typename FX::V>();
     }
   }
 }
@@ -513,7 +621,8 @@ __global__ void __launch_bounds__(FAST_BLOCK, (KIND == KIND_CSF_BPOS4 || KIND ==
   const int lane = threadIdx.x & 31;
   const int g = lane >> 3;
   const int lig = lane & 7;
-  float4* slots = s_slots + (threadIdx.x >> 3) * 64 + lig;
+  using V = typename FX::V;
+  V* slots = reinterpret_cast<V*>(s_slots) + (threadIdx.x >> 3) * 64 + lig;
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_r = policy_evict_last();
   static_assert(KIND != KIND_CSF, "CSF tasks run through KIND_CSF_BPOS4 / KIND_CSF_UNI");
@@ -534,7 +643,7 @@ __global__ void __launch_bounds__(FAST_BLOCK, (KIND == KIND_CSF_BPOS4 || KIND ==
     if (base >= last) break;
     const Task t = w.tasks[base + g];
     if (K == KIND_CSF || K == KIND_CSL) {
-      const float4 sa =
+      const V sa =
           UNI                           ? csf_bpos_tasks<true, ACC>(w, fx, t, g, lig, pol_s, pol_r)
           : K == KIND_CSF               ? csf_bpos_tasks<false, ACC>(w, fx, t, g, lig, pol_s, pol_r)
                                         : csl_tasks<ACC>(w, fx, t, g, lig, pol_s, pol_r, slots);
@@ -547,7 +656,7 @@ __global__ void __launch_bounds__(FAST_BLOCK, (KIND == KIND_CSF_BPOS4 || KIND ==
         // chunks of a slice cut into several tasks add their partial rows
         // directly into the pre-zeroed output (no accumulator hand-over)
         if (same) {
-          float4 r = add4(sa, shfl_xor4(sa, 8));
+          V r = add4(sa, shfl_xor4(sa, 8));
           r = add4(r, shfl_xor4(r, 16));
           if (g == 0 && lane_live(fx, lig)) red_add4(fx.out + size_t(row) * fx.rs + fx.col4 + lig, r);
         } else if (mine && lane_live(fx, lig)) {
@@ -556,7 +665,7 @@ __global__ void __launch_bounds__(FAST_BLOCK, (KIND == KIND_CSF_BPOS4 || KIND ==
         continue;
       }
       if (same) {
-        float4 r = add4(sa, shfl_xor4(sa, 8));
+        V r = add4(sa, shfl_xor4(sa, 8));
         r = add4(r, shfl_xor4(r, 16));
         flush_split(w, fx, g == 0, t.slot, t.nchunk, 4u, row, r, lane, lig);
       } else if (__any_sync(FULL, mine)) {
@@ -1015,6 +1124,17 @@ __global__ void k_bpos_stream(const uint32_t* __restrict__ lptr, const uint32_t*
     *o = make_uint2((fidx[f] << sh) | FB, 0u);
   }
 }
+// fp64 values of the same stream: each fiber's values, then 0 at its B position
+__global__ void k_bpos_v64(const uint32_t* __restrict__ lptr, const double* __restrict__ val,
+                           int64_t F, double* __restrict__ out) {
+  for (int64_t f = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; f < F;
+       f += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t a = lptr[f], b = lptr[f + 1];
+    double* o = out + a + f;
+    for (uint32_t i = a; i < b; ++i) *o++ = val[i];
+    *o = 0.0;
+  }
+}
 // SEND on the B position of each slice's last fiber
 __global__ void k_bpos_send(const uint32_t* __restrict__ fpos, const uint32_t* __restrict__ lptr,
                             int64_t S, uint2* __restrict__ out) {
@@ -1071,6 +1191,12 @@ struct hbk_plan {
   bool csl_acc = false;
   hbk::Buf vcsl_pairs, vcsl_j, vcsl_sidx;
   uint32_t vcsl_S = 0;
+  // fp64 fast path (built on the first fp64 execution, hbk::ensure_f64):
+  // double value streams beside the kernels' index streams
+  uint32_t heavy_H = 0, heavy_tau = 0, heavy_W = 0, heavy_slot_base = 0;
+  mutable int f64_state = 0;  // 0 unknown, 1 fast path ready, -1 generic kernel
+  mutable hbk::Buf csf_v64s, heavy_v64s;
+  mutable hbk::Work work64{}, work_heavy64{};
   // leaf-blocked heavy slices (csf_block_view; chosen in hbk_plan_create):
   // the fast fp32 path runs sub_blk (the heavy slices, leaf-block-major,
   // rows accumulated into their pre-zeroed rows) then sub_main (every other
@@ -1305,7 +1431,8 @@ __global__ void k_group_fill(const uint32_t* __restrict__ tfirst, const uint32_t
                              const uint32_t* __restrict__ fofs, int64_t NW, uint32_t G,
                              const uint32_t* __restrict__ leaf, const float* __restrict__ val,
                              bool pad, uint32_t sh, uint2* __restrict__ pairs,
-                             uint32_t* __restrict__ fj) {
+                             uint32_t* __restrict__ fj, const double* __restrict__ val64,
+                             double* __restrict__ v64) {
   for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < NW * 4;
        x += int64_t(gridDim.x) * blockDim.x) {
     const int64_t w = x >> 2;
@@ -1326,6 +1453,10 @@ __global__ void k_group_fill(const uint32_t* __restrict__ tfirst, const uint32_t
         for (uint32_t t = 0; t < len; ++t)
           pairs[dst + t] = make_uint2(leaf[off + t] << sh, __float_as_uint(val[off + t]));
         for (uint32_t t = len; t < Lq; ++t) pairs[dst + t] = make_uint2(0u, 0u);
+        if (v64) {
+          for (uint32_t t = 0; t < len; ++t) v64[dst + t] = val64[off + t];
+          for (uint32_t t = len; t <= Lq; ++t) v64[dst + t] = 0.0;
+        }
         dst += Lq;
         pairs[dst++] = make_uint2((j << sh) | FB, 0u);
         fj[fpos++] = j;
@@ -1539,6 +1670,7 @@ static BlockedCsl csl_blocked_layout(const hbk_csl* c, uint32_t BB, uint32_t T, 
 
 struct HeavyLayout {
   Buf pairs, fj, tasks;
+  Buf v64;  // fp64 values of the same stream (heavy_layout(..., val64))
   int64_t ntasks = 0;  // group tasks (4 per warp task)
   int64_t slots = 0;   // heavy slices (one accumulator slot each)
   int64_t segments = 0;
@@ -1547,7 +1679,7 @@ struct HeavyLayout {
 // Builds the heavy-slice layout of a 3rd-order CSF bucket (see above).
 static HeavyLayout heavy_layout(const hbk_csf* c, const uint32_t* loff, const uint32_t* fpos,
                                 uint32_t H, uint32_t tau, uint32_t W, uint32_t slot_base, bool bpos, uint32_t bshift,
-                                cudaStream_t st) {
+                                cudaStream_t st, bool with_v64 = false) {
   HeavyLayout hl;
   const int64_t S = c->n[0], F = c->n[1];
   const uint32_t* lptr = c->ptr[1].as<uint32_t>();
@@ -1634,10 +1766,12 @@ static HeavyLayout heavy_layout(const hbk_csf* c, const uint32_t* loff, const ui
   hl.pairs = dalloc(size_t(std::max<uint32_t>(Mh, 1)) * sizeof(uint2), st);
   hl.fj = dalloc(size_t(std::max<uint32_t>(Fh, 1)) * 4, st);
   hl.tasks = dalloc(size_t(NG) * sizeof(Task), st);
+  if (with_v64) hl.v64 = dalloc(size_t(std::max<uint32_t>(Mh, 1)) * 8, st);
   k_group_fill<<<grid_for(NG, 128), 128, 0, st>>>(
       tfirst.as<uint32_t>(), perm, soff.as<uint32_t>(), slen.as<uint32_t>(), sj.as<uint32_t>(),
       gofs.as<uint32_t>(), fofs.as<uint32_t>(), NW, G, c->leaf.as<uint32_t>(), c->v32.as<float>(),
-      bpos, bshift, hl.pairs.as<uint2>(), hl.fj.as<uint32_t>());
+      bpos, bshift, hl.pairs.as<uint2>(), hl.fj.as<uint32_t>(),
+      with_v64 ? c->v64.as<double>() : nullptr, with_v64 ? hl.v64.as<double>() : nullptr);
   check_launch("k_group_fill");
   k_group_tasks<<<grid_for(NG, 256), 256, 0, st>>>(tslice.as<uint32_t>(), gofs.as<uint32_t>(),
                                                    gnnz.as<uint32_t>(), fofs.as<uint32_t>(),
@@ -1822,6 +1956,10 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
                                   p->bpos ? fpos.as<uint32_t>() : nullptr);
         HeavyLayout hl = heavy_layout(c, p->csf_send.as<uint32_t>(), fpos.as<uint32_t>(), heavy_H,
                                       heavy_tau, heavy_W, uint32_t(tcsf_light.slots), p->bpos, p->bshift, st);
+        p->heavy_H = heavy_H;
+        p->heavy_tau = heavy_tau;
+        p->heavy_W = heavy_W;
+        p->heavy_slot_base = uint32_t(tcsf_light.slots);
         HBK_REQUIRE(tcsf_light.slots + hl.slots == tcsf.slots, HBK_ECUDA,
                     "heavy layout slot accounting mismatch");
         p->heavy_pairs = hl.pairs;
@@ -2198,30 +2336,33 @@ __global__ void k_zero_rows(const uint32_t* __restrict__ rows, int64_t n, uint32
 // A plan's bucket kernels in launch order — heavy slices first (the
 // longest), then light CSF, CSL, COO/zero — each on the stream `next()` hands out.
 template <class FX, class Next>
-static void launch_kernels(const hbk_plan* p, const FX& fx, bool skip_zero, Next&& next) {
+static void launch_kernels(const hbk_plan* p, const FX& fx, bool skip_zero, Next&& next,
+                           const Work* wl = nullptr, const Work* wh = nullptr) {
+  const Work& W = wl ? *wl : p->work;          // light CSF, CSL, COO, zero rows
+  const Work& WH = wh ? *wh : p->work_heavy;   // heavy slices
   if (p->grid_heavy) {
     cudaStream_t s2 = next();
     if (p->acc_csf)
-      k_mttkrp3_r32<KIND_CSF_UNI_ACC, FX><<<p->grid_heavy, p->block, 0, s2>>>(p->work_heavy, fx);
+      k_mttkrp3_r32<KIND_CSF_UNI_ACC, FX><<<p->grid_heavy, p->block, 0, s2>>>(WH, fx);
     else
-      k_mttkrp3_r32<KIND_CSF_UNI, FX><<<p->grid_heavy, p->block, 0, s2>>>(p->work_heavy, fx);
+      k_mttkrp3_r32<KIND_CSF_UNI, FX><<<p->grid_heavy, p->block, 0, s2>>>(WH, fx);
   }
   if (p->grids[0]) {
     cudaStream_t s2 = next();
     if (p->acc_csf)
-      k_mttkrp3_r32<KIND_CSF_BPOS4_ACC, FX><<<p->grids[0], p->block, 0, s2>>>(p->work, fx);
+      k_mttkrp3_r32<KIND_CSF_BPOS4_ACC, FX><<<p->grids[0], p->block, 0, s2>>>(W, fx);
     else
-      k_mttkrp3_r32<KIND_CSF_BPOS4, FX><<<p->grids[0], p->block, 0, s2>>>(p->work, fx);
+      k_mttkrp3_r32<KIND_CSF_BPOS4, FX><<<p->grids[0], p->block, 0, s2>>>(W, fx);
   }
   if (p->grids[1]) {
     cudaStream_t s2 = next();
     if (p->csl_acc)
-      k_mttkrp3_r32<KIND_CSL_ACC, FX><<<p->grids[1], p->block, 0, s2>>>(p->work, fx);
+      k_mttkrp3_r32<KIND_CSL_ACC, FX><<<p->grids[1], p->block, 0, s2>>>(W, fx);
     else
-      k_mttkrp3_r32<KIND_CSL, FX><<<p->grids[1], p->block, 0, s2>>>(p->work, fx);
+      k_mttkrp3_r32<KIND_CSL, FX><<<p->grids[1], p->block, 0, s2>>>(W, fx);
   }
   // skip_zero: the rows no bucket owns are left unwritten (COO tasks only)
-  Work wc = p->work;
+  Work wc = W;
   if (skip_zero) wc.n3 = wc.n2;
   if (p->grids[2] && wc.n3 > wc.n1) {
     cudaStream_t s2 = next();
@@ -2268,6 +2409,62 @@ static void launch_fast(const hbk_plan* p, const FX& fx, cudaStream_t st, bool s
   Forker f{st, p->side, p->ev_join, p->concurrent ? p->ev_fork : nullptr, 3};
   f.begin();
   launch_kernels(p, fx, skip_zero, f);
+  f.end();
+}
+
+// fp64 fast path: the same kernels instantiated on double2 lane vectors (a
+// pass covers 16 columns), over the plan's task lists and index streams plus
+// double value streams built on the first fp64 execution.  Plans whose
+// layouts have no fp64 stream yet (blocked CSL, leaf-blocked sub-plans) and
+// tensors without fp64 values keep the generic kernel.
+static bool ensure_f64(const hbk_plan* p, cudaStream_t st) {
+  if (p->f64_state) return p->f64_state > 0;
+  p->f64_state = -1;
+  if (!p->fast || !p->bpos || p->csl_acc || p->sub_blk || p->acc_csf || p->order != 3) return false;
+  if (const char* e = getenv("HBK_F64_GENERIC"))  // A/B, and the independent fp64 check
+    if (atoi(e) != 0) return false;
+  if ((p->csf && p->csf->M && !p->csf->v64) || (p->csl && p->csl->M && !p->csl->v64) ||
+      (p->coo && p->coo->nnz && !p->coo->v64))
+    return false;
+  Work w = p->work, wh = p->work_heavy;
+  if (p->csf && p->csf->M) {
+    const hbk_csf* c = p->csf;
+    const int64_t S = c->n[0], F = c->n[1];
+    p->csf_v64s = dalloc(size_t(c->M + F) * 8, st);
+    k_bpos_v64<<<grid_for(F, 128), 128, 0, st>>>(c->ptr[1].as<uint32_t>(), c->v64.as<double>(), F,
+                                                 p->csf_v64s.as<double>());
+    check_launch("k_bpos_v64");
+    w.csf_v64 = p->csf_v64s.as<double>();
+    if (p->grid_heavy) {
+      // the heavy layout again (deterministic), emitting its fp64 values
+      Chain2 ch{};
+      ch.nlev = 2;
+      for (int d = 0; d < 2; ++d) ch.ptr[d] = c->ptr[d].as<uint32_t>();
+      Scratch loff((S + 1) * 4, st), fpos((S + 1) * 4, st);
+      k_csf_slice_offsets<<<grid_for(S + 1, 256), 256, 0, st>>>(ch, S, fpos.as<uint32_t>(),
+                                                                loff.as<uint32_t>());
+      check_launch("k_csf_slice_offsets");
+      HeavyLayout hl = heavy_layout(c, loff.as<uint32_t>(), fpos.as<uint32_t>(), p->heavy_H, p->heavy_tau,
+                                    p->heavy_W, p->heavy_slot_base, p->bpos, p->bshift, st, true);
+      HBK_REQUIRE(hl.ntasks == int64_t(p->work_heavy.n0), HBK_ECUDA, "fp64 heavy layout mismatch");
+      p->heavy_v64s = hl.v64;
+      wh.csf_v64 = p->heavy_v64s.as<double>();
+    }
+  }
+  if (p->csl && p->csl->M) w.csl_v64 = p->csl->v64.as<double>();
+  if (p->coo && p->coo->nnz) w.coo_v64 = p->coo->v64.as<double>();
+  p->work64 = w;
+  p->work_heavy64 = wh;
+  HBK_CUDA(cudaStreamSynchronize(st));
+  p->f64_state = 1;
+  return true;
+}
+
+template <class FX>
+static void launch_fast64(const hbk_plan* p, const FX& fx, cudaStream_t st) {
+  Forker f{st, p->side, p->ev_join, p->concurrent ? p->ev_fork : nullptr, 3};
+  f.begin();
+  launch_kernels(p, fx, false, f, &p->work64, &p->work_heavy64);
   f.end();
 }
 
@@ -3076,7 +3273,24 @@ int hbk_plan_execute_f64(const hbk_plan* p, const double* const* factors, double
     HBK_REQUIRE(p->gen_grid > 0, HBK_EINVAL, "plan has no fp64 launch configuration");
     cudaStream_t st = to_stream(stream);
     ExecOrder order(p, st);
-    launch_generic<double>(p, factors, out, st);
+    if (ensure_f64(p, st)) {
+      const int R = p->rank;
+      const double2* B = reinterpret_cast<const double2*>(factors[p->mo[1]]);
+      const double2* Cf = reinterpret_cast<const double2*>(factors[p->mo[2]]);
+      double2* o = reinterpret_cast<double2*>(out);
+      HBK_REQUIRE((reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(Cf) |
+                   reinterpret_cast<uintptr_t>(out)) % 16 == 0,
+                  HBK_EINVAL, "factor and output buffers must be 16-byte aligned");
+      if (p->r32) {
+        for (uint32_t c4 = 0; c4 < 16; c4 += 8) launch_fast64(p, Factors3DR32{B, Cf, o, c4}, st);
+      } else {
+        for (int c0 = 0; c0 < R; c0 += 16)
+          launch_fast64(p, Factors3D{B, Cf, o, uint32_t(R / 2), uint32_t(c0 / 2),
+                                     uint32_t(std::min(8, (R - c0) / 2))}, st);
+      }
+    } else {
+      launch_generic<double>(p, factors, out, st);
+    }
     order.done();
   });
 }

@@ -1,8 +1,9 @@
 """Parity at benchmark scale through size-independent properties (the CPU
 oracle is too slow here): on the Appendix-A generator's tensors, the fast
 fp32 kernels (B-position streams, padded heavy layout, CSL/COO/zero tasks)
-against libhbk's independent generic kernel run in fp64 — different code,
-different layout, different arithmetic — with the reference's row metric;
+against libhbk's independent generic kernel run in fp64 (HBK_F64_GENERIC) —
+different code, different layout, different arithmetic — with the
+reference's row metric; the fp64 fast path against the same generic kernel;
 plus linearity in a factor and bit-repeatability of the fast path."""
 from __future__ import annotations
 
@@ -21,7 +22,7 @@ def _rowdev(y, ref):
 
 @pytest.mark.parametrize("config,scale", [("nell-2", 1.0), ("flickr-3d", 0.5),
                                           ("delicious-3d", 0.5), ("nell-1", 0.5)])
-def test_fast_fp32_matches_generic_fp64_at_scale(config, scale):
+def test_fast_fp32_matches_generic_fp64_at_scale(config, scale, monkeypatch):
     import torch
 
     import paper_1904_03329_b200 as hb
@@ -37,9 +38,17 @@ def test_fast_fp32_matches_generic_fp64_at_scale(config, scale):
     for mode in range(3):
         h = hb.split_fibers(hb.build_hbcsf(t, hb.allmode_order(dims, mode)), hb.SplitConfig())
         y32, _ = mttkrp_device(h, f32, mode)
+        monkeypatch.setenv("HBK_F64_GENERIC", "1")  # the independent generic fp64 kernel
         y64, _ = mttkrp_device(h, f64r, mode)
+        monkeypatch.delenv("HBK_F64_GENERIC")
         assert y32.dtype == torch.float32 and y64.dtype == torch.float64
         assert _rowdev(y32, y64) <= 1e-4, (config, mode)
+        # the fp64 fast path (same streams and tasks as fp32, double2 lanes,
+        # fp64 value streams) against the generic fp64 kernel
+        h2 = hb.split_fibers(hb.build_hbcsf(t, hb.allmode_order(dims, mode)), hb.SplitConfig())
+        y64f, _ = mttkrp_device(h2, f64r, mode)
+        assert _rowdev(y64f, y64) <= 1e-12, (config, mode)
+        del h2
         # linearity in a factor: Y(2C) = 2 Y(C) exactly, except that the
         # chunks of a split slice (thousands for the 3M-nonzero nell-2 slices)
         # meet in red.global.add order, which varies run to run: fp32
