@@ -279,6 +279,10 @@ int hbk_nonfinite_f32(const float* const* bufs, const int64_t* counts, int n, in
  * i holds a NaN or Inf (kernels.py:82-86).  n <= 8. */
 int hbk_stage_f64_to_f32(const double* const* srcs, const int64_t* counts, int n,
                          float* const* stage, float* const* dst, int32_t* flags, void* stream);
+/* The same for the fp64 kernels (precision="fp64"): a page-locked float64
+ * copy (streaming stores) sent chunk by chunk; flags[i] = 1 on a NaN/Inf. */
+int hbk_stage_f64_to_f64(const double* const* srcs, const int64_t* counts, int n,
+                         double* const* stage, double* const* dst, int32_t* flags, void* stream);
 
 /* ------------------------------------------------------- FROSTT text --
  * parse_frostt / load_frostt / write_frostt, coo.py:117-205, on the host

@@ -149,6 +149,7 @@ _SIGS = {
     "hbk_plan_probe": ([vp, vp, vp], C.c_int),
     "hbk_nonfinite_f32": ([vp, vp, C.c_int, vp, vp], C.c_int),
     "hbk_stage_f64_to_f32": ([vp, vp, C.c_int, vp, vp, vp, vp], C.c_int),
+    "hbk_stage_f64_to_f64": ([vp, vp, C.c_int, vp, vp, vp, vp], C.c_int),
     "hbk_plan_rows": ([vp, vp, C.POINTER(C.c_int64), vp], C.c_int),
     "hbk_stream_synchronize": ([vp], C.c_int),
     "hbk_plan_execute_ex": ([vp, vp, vp, C.c_int, vp], C.c_int),

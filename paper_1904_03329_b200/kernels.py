@@ -84,17 +84,18 @@ class _HostStage:
     """Upload/download path of the host-array calling convention (the
     reference's: NumPy float64 factors in, NumPy float64 rows out).
 
-    Each factor is converted to the kernel's dtype *while* being copied into a
-    page-locked staging buffer; the factors of one call (and chunks of large
-    factors) are converted concurrently on a host thread pool (NumPy releases
-    the GIL in these loops), and each factor's host-to-device copy is issued
-    asynchronously as soon as it is staged.  The finiteness check of
-    kernels.py:82-86 runs on the device over the uploaded copies (one
-    hbk_nonfinite_f32 launch after the MTTKRP, flags returned with the rows);
-    only when it fires is the host source examined, to tell a non-finite
-    entry from a finite one beyond the float32 range.  The result comes back
-    through one async device-to-host copy into a pinned buffer, widened to
-    float64 on the host."""
+    NumPy float64 factors go through libhbk's native staging
+    (hbk_stage_f64_to_f32 / _f64): a pool of host threads converts them into
+    page-locked buffers with streaming stores and the host-to-device copies
+    follow chunk by chunk, with the non-finite check of kernels.py:82-86
+    done on the way (raised before any kernel runs).  Page-locked torch
+    tensors of the kernel dtype are copied as they are and checked on the
+    device (one hbk_nonfinite_f32 launch after the MTTKRP, flags returned with
+    the rows); other host arrays (other dtypes) are converted on a Python
+    thread pool and checked the same way.  When a check fires, the host
+    source tells a non-finite entry from a finite one beyond the float32
+    range.  The rows come back widened to float64 on the device, through one
+    async copy into page-locked memory that becomes the returned array."""
 
     CHUNK_BYTES = 1 << 20  # conversion work unit (bytes of the source factor)
 
@@ -149,9 +150,12 @@ class _HostStage:
             if src.ndim != 2:
                 raise ValueError(f"factor {d} must be a 2-D array")
             srcs[d] = src
-        # float64 -> fp32 (the reference convention): narrowed by libhbk's
-        # host threads and copied chunk by chunk as it goes (hbk_stage_f64_to_f32)
-        nat = [d for d, s in srcs.items() if dt == torch.float32 and s.dtype == np.float64]
+        # float64 -> fp32 (the reference convention) or -> fp64 (precision=
+        # "fp64"): narrowed / copied by libhbk's host threads with streaming
+        # stores and sent chunk by chunk as it goes (hbk_stage_f64_to_f32/_f64)
+        nat = [d for d, s in srcs.items()
+               if dt in (torch.float32, torch.float64) and s.dtype == np.float64]
+        fn = "hbk_stage_f64_to_f32" if dt == torch.float32 else "hbk_stage_f64_to_f64"
         if nat:
             with self.lock:
                 stages, devs = {}, {}
@@ -161,7 +165,7 @@ class _HostStage:
                     devs[d] = torch.empty((rows, width), dtype=dt, device="cuda")
                 k = len(nat)
                 flags = (C.c_int32 * k)()
-                N.call("hbk_stage_f64_to_f32",
+                N.call(fn,
                        (C.c_void_p * k)(*[srcs[d].ctypes.data for d in nat]),
                        (C.c_int64 * k)(*[srcs[d].size for d in nat]), k,
                        (C.c_void_p * k)(*[stages[d].data_ptr() for d in nat]),

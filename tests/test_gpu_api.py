@@ -537,7 +537,8 @@ def test_finite_factor_beyond_fp32_range_is_rejected(hb, rng):
 
 @pytest.mark.parametrize("n", [0, 1, 7, 8, 9, 65536 - 3, 65536, 65536 * 3 + 5])
 @pytest.mark.parametrize("offset", [0, 1, 5])
-def test_stage_f64_to_f32(n, offset):
+@pytest.mark.parametrize("dst", ["f32", "f64"])
+def test_stage_f64_to_f32(n, offset, dst):
     """hbk_stage_f64_to_f32 (the host calling convention's float64 -> fp32
     upload): every element round-to-nearest exactly as NumPy's astype, over
     unaligned staging heads, 8-wide bodies, tails and several chunks; the
@@ -551,14 +552,15 @@ def test_stage_f64_to_f32(n, offset):
     rng = np.random.default_rng(n + offset)
     srcs = [rng.standard_normal(n) * 10.0 ** rng.integers(-40, 40, n) if n else np.zeros(0),
             rng.random(777)]
-    stage_base = [torch.empty(len(s) + offset + 8, dtype=torch.float32, pin_memory=True) for s in srcs]
+    tdt, ndt = (torch.float32, np.float32) if dst == "f32" else (torch.float64, np.float64)
+    stage_base = [torch.empty(len(s) + offset + 8, dtype=tdt, pin_memory=True) for s in srcs]
     stages = [b[offset: offset + len(s)] for b, s in zip(stage_base, srcs)]
-    devs = [torch.full((len(s) + 1,), -7.0, device="cuda") for s in srcs]
+    devs = [torch.full((len(s) + 1,), -7.0, dtype=tdt, device="cuda") for s in srcs]
 
     def run(arrs):
         k = len(arrs)
         flags = (C.c_int32 * k)()
-        N.call("hbk_stage_f64_to_f32", (C.c_void_p * k)(*[a.ctypes.data for a in arrs]),
+        N.call(f"hbk_stage_f64_to_{dst}", (C.c_void_p * k)(*[a.ctypes.data for a in arrs]),
                (C.c_int64 * k)(*[a.size for a in arrs]), k,
                (C.c_void_p * k)(*[s.data_ptr() for s in stages]),
                (C.c_void_p * k)(*[d.data_ptr() for d in devs]), flags, N.stream_ptr())
@@ -566,22 +568,23 @@ def test_stage_f64_to_f32(n, offset):
         return list(flags)
 
     with np.errstate(over="ignore"):
-        want = [s.astype(np.float32) for s in srcs]
+        want = [s.astype(ndt) for s in srcs]
     fl = run(srcs)
+    ui = np.uint32 if dst == "f32" else np.uint64
     for s, w, d, f in zip(srcs, want, devs, fl):
         got = d[: len(s)].cpu().numpy()
-        assert np.array_equal(got.view(np.uint32), w.view(np.uint32))
+        assert np.array_equal(got.view(ui), w.view(ui))
         assert d[len(s)].item() == -7.0  # nothing written past the end
         assert f == int(not np.isfinite(w).all())
     if n:
         for pos in sorted({0, n // 2, n - 1}):
-            for bad in (np.nan, np.inf, -np.inf, 1e39):
+            for bad in (np.nan, np.inf, -np.inf) + ((1e39,) if dst == "f32" else ()):
                 s0 = np.clip(srcs[0], -1e30, 1e30)
                 s0[pos] = bad
                 assert run([s0, srcs[1]]) == [1, 0]
         assert run([np.clip(srcs[0], -1e30, 1e30), srcs[1]]) == [0, 0]
     with pytest.raises(ValueError):
-        N.call("hbk_stage_f64_to_f32", None, None, 9, None, None, None, N.stream_ptr())
+        N.call(f"hbk_stage_f64_to_{dst}", None, None, 9, None, None, None, N.stream_ptr())
 
 
 def test_host_factor_errors_raised_before_launch(hb, rng):
