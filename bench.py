@@ -751,6 +751,52 @@ def free(st):
     torch.cuda.empty_cache()
 
 
+def amortization(env, st, res, args):
+    """Preprocessing amortisation against the plain coordinate format, as the
+    reference CLI reports it (cli.py:317-327): steps until the format's extra
+    build time is repaid by its faster MTTKRP."""
+    s0 = prepare(env, args.config, args, "coo", tensor=st["t"])
+    r0 = time_steps(env, s0, args)
+    gain_s = (r0["ms_per_step"] - res["ms_per_step"]) * 1e-3
+    out = {"coo_ms_per_step": r0["ms_per_step"], "coo_preprocessing_s": s0["prep_s"],
+           "preprocessing_s": st["prep_s"],
+           "iterations_to_amortize": (max(0, math.ceil((st["prep_s"] - s0["prep_s"]) / gain_s))
+                                      if gain_s > 0 else None),
+           "note": "per step (all modes); cli.py:317-327 max(0, ceil((prep - prep_coo) / (wall_coo - wall)))"}
+    s0["t"] = None
+    free(s0)
+    return out
+
+
+def measure_also(env, name, args):
+    """A further configuration measured the same way as the headline."""
+    s2 = prepare(env, name, args, args.format)
+    r2 = time_steps(env, s2, args)
+    rf = roofline_of(s2, r2["per_mode_ms"])
+    tr, hit = ncu_traffic(name, args)
+    out = {"config": name, "nnz": s2["nnz"], "value": r2["value"], "unit": "GFLOP/s",
+           "ms_per_step": r2["ms_per_step"], "per_mode_ms": r2["per_mode_ms"],
+           "roofline_frac": rf["frac"], "per_mode_frac": rf["per_mode_frac"],
+           "algorithmic_bytes_per_step": rf["algorithmic_bytes_per_step"],
+           "ncu_dram_bytes_per_launch": tr, "l2_hit_rate_pct": hit,
+           "census": s2["census"] if env.world == 1 else None}
+    free(s2)
+    return out
+
+
+def optional(name, fn, *a, **k):
+    """Run an optional part of the line; a failure is reported in the line
+    (and on stderr) instead of losing the measured step."""
+    try:
+        return fn(*a, **k)
+    except Exception as exc:  # noqa: BLE001 - the line must still be printed
+        import traceback
+
+        traceback.print_exc()
+        print(f"[bench] optional part {name!r} failed: {exc!r}", file=sys.stderr, flush=True)
+        return {"error": f"{type(exc).__name__}: {exc}"}
+
+
 def run_ours(args):
     env = Env()
     torch = env.torch
@@ -765,27 +811,19 @@ def run_ours(args):
                  "traffic_frac": traffic / (mean_ms * 1e-3) / 1e9 / roof["peak"] if traffic else None,
                  "kernel": "k_mttkrp3_r32<kind> (one launch per non-empty bucket kind per mode)",
                  "traffic_unit": "DRAM bytes per MTTKRP launch (ncu dram__bytes_read+write, profiles/)"})
-    roof["gather"] = gather_ceiling(env, st, args, res["per_mode_ms"])
-    with_ag = with_allgather(env, st, args, flops_step) if env.world > 1 else None
-    e2e = None if args.no_e2e else end_to_end(env, st, args, flops_step)
+    roof["gather"] = optional("gather", gather_ceiling, env, st, args, res["per_mode_ms"])
+    with_ag = optional("with_output_allgather", with_allgather, env, st, args, flops_step) if env.world > 1 else None
+    e2e = None if args.no_e2e else optional("e2e", end_to_end, env, st, args, flops_step)
     cpu = parity = None
     if env.rank == 0 and env.world == 1 and not args.no_cpu_baseline:
-        cpu, parity = cpu_leg(env, st, args)
+        both = optional("cpu_baseline", cpu_leg, env, st, args)
+        cpu, parity = both if isinstance(both, tuple) else (both, None)
     # preprocessing amortisation against the plain coordinate format, as the
     # reference CLI reports it (cli.py:317-327): steps until the format's
     # extra build time is repaid by its faster MTTKRP
     amort = None
     if env.world == 1 and args.format != "coo" and not args.no_amortize:
-        s0 = prepare(env, args.config, args, "coo", tensor=st["t"])
-        r0 = time_steps(env, s0, args)
-        gain_s = (r0["ms_per_step"] - res["ms_per_step"]) * 1e-3
-        amort = {"coo_ms_per_step": r0["ms_per_step"], "coo_preprocessing_s": s0["prep_s"],
-                 "preprocessing_s": st["prep_s"],
-                 "iterations_to_amortize": (max(0, math.ceil((st["prep_s"] - s0["prep_s"]) / gain_s))
-                                            if gain_s > 0 else None),
-                 "note": "per step (all modes); cli.py:317-327 max(0, ceil((prep - prep_coo) / (wall_coo - wall)))"}
-        s0["t"] = None
-        free(s0)
+        amort = optional("amortization", amortization, env, st, res, args)
     launches = args.steps * sum(int(pl.info.launches) for pl in st["plans"] if pl is not None)
     census = st["census"]
     header = {k: st[k] for k in ("dims", "nnz", "prep_s", "gen_s")}
@@ -796,19 +834,8 @@ def run_ours(args):
 
     also = []
     for name in args.also:
-        s2 = prepare(env, name, args, args.format)
-        r2 = time_steps(env, s2, args)
-        rf = roofline_of(s2, r2["per_mode_ms"])
-        tr, hit = ncu_traffic(name, args)
-        also.append({"config": name, "nnz": s2["nnz"], "value": r2["value"], "unit": "GFLOP/s",
-                     "ms_per_step": r2["ms_per_step"], "per_mode_ms": r2["per_mode_ms"],
-                     "roofline_frac": rf["frac"], "per_mode_frac": rf["per_mode_frac"],
-                     "algorithmic_bytes_per_step": rf["algorithmic_bytes_per_step"],
-                     "ncu_dram_bytes_per_launch": tr, "l2_hit_rate_pct": hit,
-                     "census": s2["census"] if env.world == 1 else None})
-        free(s2)
-    cpd = measure_cpd(env, args.cpd, args) if args.cpd else None
-
+        also.append(optional(f"also {name}", measure_also, env, name, args))
+    cpd = optional("cpd", measure_cpd, env, args.cpd, args) if args.cpd else None
     if env.rank == 0:
         dims = header["dims"]
         line = {
