@@ -35,6 +35,9 @@
 namespace hbk {
 
 static constexpr uint32_t NOSLOT = 0xFFFFFFFFu;
+// light-task size = heavy-slice threshold (round 2, ms per 3-mode step,
+// 64 / 128 / 256: nell-1 8.47 / 8.29 / 8.31, flickr-3d 6.30 / 6.18 / 6.19,
+// delicious-3d 9.89 / 9.91 / 9.97, nell-2 2.22 all)
 static constexpr uint32_t TASK_NNZ_CSF = 128;
 static constexpr uint32_t TASK_NNZ_CSL = 128;
 static constexpr uint32_t TASK_NNZ_COO = 32;
