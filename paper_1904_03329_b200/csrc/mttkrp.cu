@@ -1198,7 +1198,8 @@ struct hbk_plan {
   // double value streams beside the kernels' index streams
   uint32_t heavy_H = 0, heavy_tau = 0, heavy_W = 0, heavy_slot_base = 0;
   mutable int f64_state = 0;  // 0 unknown, 1 fast path ready, -1 generic kernel
-  mutable hbk::Buf csf_v64s, heavy_v64s;
+  mutable hbk::Buf csf_v64s, heavy_v64s, csl_v64s;
+  uint32_t csl_T = 0;  // the CSL task size the plan was built with (blocked layout rebuild)
   mutable hbk::Work work64{}, work_heavy64{};
   // leaf-blocked heavy slices (csf_block_view; chosen in hbk_plan_create):
   // the fast fp32 path runs sub_blk (the heavy slices, leaf-block-major,
@@ -1592,7 +1593,8 @@ __global__ void k_csl_vscatter(const uint32_t* __restrict__ pos, const uint32_t*
                                const uint32_t* __restrict__ rank_of, const uint32_t* __restrict__ vstart,
                                const uint32_t* __restrict__ k, const uint32_t* __restrict__ j,
                                const float* __restrict__ v, int64_t M, uint2* __restrict__ vpairs,
-                               uint32_t* __restrict__ vj) {
+                               uint32_t* __restrict__ vj, const double* __restrict__ v64,
+                               double* __restrict__ vv64) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < M;
        i += int64_t(gridDim.x) * blockDim.x) {
     const uint32_t g = pos[i + 1] - 1;
@@ -1600,6 +1602,7 @@ __global__ void k_csl_vscatter(const uint32_t* __restrict__ pos, const uint32_t*
     const uint32_t q = vstart[rank_of[g]] + uint32_t(i - start[g]);
     vpairs[q] = make_uint2(k[i] | (last ? SEND : 0u), __float_as_uint(v[i]));
     vj[q] = j[i];
+    if (vv64) vv64[q] = v64[i];
   }
 }
 
@@ -1611,11 +1614,13 @@ __global__ void k_iota_u32(uint32_t* __restrict__ dst, int64_t n) {
 
 struct BlockedCsl {
   Buf pairs, j, sidx;
+  Buf v64;  // fp64 values in the block-major order (csl_blocked_layout(..., true))
   BucketTasks tasks;
   int64_t G = 0, nblocks = 0;
 };
 
-static BlockedCsl csl_blocked_layout(const hbk_csl* c, uint32_t BB, uint32_t T, cudaStream_t st) {
+static BlockedCsl csl_blocked_layout(const hbk_csl* c, uint32_t BB, uint32_t T, cudaStream_t st,
+                                     bool with_v64 = false) {
   BlockedCsl out;
   const int64_t M = c->M, S = c->S;
   const uint32_t* j = c->rest[0].as<uint32_t>();
@@ -1660,10 +1665,13 @@ static BlockedCsl csl_blocked_layout(const hbk_csl* c, uint32_t BB, uint32_t T, 
   HBK_REQUIRE(total == uint32_t(M), HBK_ECUDA, "blocked CSL layout accounting mismatch");
   out.pairs = dalloc(size_t(M) * sizeof(uint2), st);
   out.j = dalloc(size_t(M) * 4, st);
+  if (with_v64) out.v64 = dalloc(size_t(M) * 8, st);
   k_csl_vscatter<<<grid_for(M, 256), 256, 0, st>>>(pos.as<uint32_t>(), start.as<uint32_t>(),
                                                    rank_of.as<uint32_t>(), vstart.as<uint32_t>(),
                                                    c->rest[1].as<uint32_t>(), j, c->v32.as<float>(), M,
-                                                   out.pairs.as<uint2>(), out.j.as<uint32_t>());
+                                                   out.pairs.as<uint2>(), out.j.as<uint32_t>(),
+                                                   with_v64 ? c->v64.as<double>() : nullptr,
+                                                   with_v64 ? out.v64.as<double>() : nullptr);
   check_launch("k_csl_vscatter");
   // tasks: runs of whole virtual slices, long ones chunked (slot fields only
   // mark chunks: partial rows are added with atomics, no accumulator slots)
@@ -2018,6 +2026,7 @@ static void build_plan(hbk_plan* p, cudaStream_t st) {
     // blocked CSL layout (block size chosen in hbk_plan_create): the fast
     // kernel runs the block-major virtual slices and accumulates rows, so it
     // needs no accumulator slots
+    p->csl_T = Tcsl;
     if (p->fast && p->csl_bb > 0) {
       BlockedCsl bl = csl_blocked_layout(s, uint32_t(p->csl_bb), Tcsl, st);
       p->vcsl_pairs = bl.pairs;
@@ -2423,7 +2432,14 @@ static void launch_fast(const hbk_plan* p, const FX& fx, cudaStream_t st, bool s
 static bool ensure_f64(const hbk_plan* p, cudaStream_t st) {
   if (p->f64_state) return p->f64_state > 0;
   p->f64_state = -1;
-  if (!p->fast || !p->bpos || p->csl_acc || p->sub_blk || p->acc_csf || p->order != 3) return false;
+  if (p->sub_blk) {  // leaf-blocked: both sub-plans need their streams
+    if (const char* e = getenv("HBK_F64_GENERIC"))
+      if (atoi(e) != 0) return false;
+    const bool ok = ensure_f64(p->sub_blk, st) && ensure_f64(p->sub_main, st);
+    p->f64_state = ok ? 1 : -1;
+    return ok;
+  }
+  if (!p->fast || !p->bpos || p->order != 3) return false;
   if (const char* e = getenv("HBK_F64_GENERIC"))  // A/B, and the independent fp64 check
     if (atoi(e) != 0) return false;
   if ((p->csf && p->csf->M && !p->csf->v64) || (p->csl && p->csl->M && !p->csl->v64) ||
@@ -2454,7 +2470,16 @@ static bool ensure_f64(const hbk_plan* p, cudaStream_t st) {
       wh.csf_v64 = p->heavy_v64s.as<double>();
     }
   }
-  if (p->csl && p->csl->M) w.csl_v64 = p->csl->v64.as<double>();
+  if (p->csl && p->csl->M) {
+    if (p->csl_acc) {  // the block-major CSL stream again (deterministic), with fp64 values
+      BlockedCsl bl = csl_blocked_layout(p->csl, uint32_t(p->csl_bb), p->csl_T, st, true);
+      HBK_REQUIRE(bl.G == int64_t(p->vcsl_S), HBK_ECUDA, "fp64 blocked CSL layout mismatch");
+      p->csl_v64s = bl.v64;
+      w.csl_v64 = p->csl_v64s.as<double>();
+    } else {
+      w.csl_v64 = p->csl->v64.as<double>();
+    }
+  }
   if (p->coo && p->coo->nnz) w.coo_v64 = p->coo->v64.as<double>();
   p->work64 = w;
   p->work_heavy64 = wh;
@@ -2468,6 +2493,15 @@ static void launch_fast64(const hbk_plan* p, const FX& fx, cudaStream_t st) {
   Forker f{st, p->side, p->ev_join, p->concurrent ? p->ev_fork : nullptr, 3};
   f.begin();
   launch_kernels(p, fx, false, f, &p->work64, &p->work_heavy64);
+  f.end();
+}
+
+template <class FX>
+static void launch_blocked64(const hbk_plan* p, const FX& fx, cudaStream_t st) {
+  Forker f{st, p->side_all, p->ev_join_all, p->ev_fork, 7};
+  f.begin();
+  launch_kernels(p->sub_blk, fx, false, f, &p->sub_blk->work64, &p->sub_blk->work_heavy64);
+  launch_kernels(p->sub_main, fx, false, f, &p->sub_main->work64, &p->sub_main->work_heavy64);
   f.end();
 }
 
@@ -3284,12 +3318,23 @@ int hbk_plan_execute_f64(const hbk_plan* p, const double* const* factors, double
       HBK_REQUIRE((reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(Cf) |
                    reinterpret_cast<uintptr_t>(out)) % 16 == 0,
                   HBK_EINVAL, "factor and output buffers must be 16-byte aligned");
-      if (p->r32) {
-        for (uint32_t c4 = 0; c4 < 16; c4 += 8) launch_fast64(p, Factors3DR32{B, Cf, o, c4}, st);
+      const hbk_plan* q = p->sub_blk ? p->sub_blk : p;  // the kernels' shape (r32)
+      if (p->csl_acc)  // the blocked CSL layout adds its rows
+        HBK_CUDA(cudaMemsetAsync(out, 0, size_t(p->dims[p->mode]) * R * sizeof(double), st));
+      if (p->sub_blk && p->n_heavy_rows) {  // zero the leaf-blocked rows (R doubles = R/2 x 16 B)
+        const int64_t n4 = p->n_heavy_rows * (R / 2);
+        k_zero_rows<<<grid_for(n4, 256), 256, 0, st>>>(p->heavy_rows.as<uint32_t>(), p->n_heavy_rows,
+                                                       uint32_t(R / 2), reinterpret_cast<float4*>(out));
+        check_launch("k_zero_rows");
+      }
+      auto run = [&](const auto& fx) {
+        if (p->sub_blk) launch_blocked64(p, fx, st); else launch_fast64(p, fx, st);
+      };
+      if (q->r32) {
+        for (uint32_t c4 = 0; c4 < 16; c4 += 8) run(Factors3DR32{B, Cf, o, c4});
       } else {
         for (int c0 = 0; c0 < R; c0 += 16)
-          launch_fast64(p, Factors3D{B, Cf, o, uint32_t(R / 2), uint32_t(c0 / 2),
-                                     uint32_t(std::min(8, (R - c0) / 2))}, st);
+          run(Factors3D{B, Cf, o, uint32_t(R / 2), uint32_t(c0 / 2), uint32_t(std::min(8, (R - c0) / 2))});
       }
     } else {
       launch_generic<double>(p, factors, out, st);

@@ -382,6 +382,12 @@ def test_csl_b_row_blocking_parity(hb, rng, block_mb, rank, monkeypatch):
         for _ in range(2):  # repeated executions into the same (dirty) buffer
             mttkrp_device(h, fd, mode, out=out)
         assert P.row_deviation(out.double().cpu().numpy(), ref) <= 1e-4
+        # fp64 through the same blocked layout (block-major fp64 value stream)
+        f64 = [torch.from_numpy(x).cuda() for x in f]
+        out64 = torch.full((dims[mode], rank), 3.0, dtype=torch.float64, device="cuda")
+        for _ in range(2):
+            mttkrp_device(h, f64, mode, out=out64)
+        assert P.row_deviation(out64.cpu().numpy(), ref) <= 1e-12
 
 
 def test_execute_captures_into_cuda_graph(hb, rng):
@@ -665,7 +671,11 @@ def test_leaf_blocked_heavy_slices_parity(hb, rng, block_mb, minnz, rank, monkey
             mttkrp_device(h, fd, mode, out=out)
         assert P.row_deviation(out.double().cpu().numpy(), ref) <= 1e-4
         y64, _ = hb.mttkrp_hbcsf(h, f, mode, precision="fp64")
-        assert P.row_deviation(y64, ref) <= 1e-9
+        assert P.row_deviation(y64, ref) <= 1e-12
+        out64 = torch.full((dims[mode], rank), 3.0, dtype=torch.float64, device="cuda")
+        for _ in range(2):  # the fp64 fast path through the blocked pair, dirty buffer
+            mttkrp_device(h, [x.double() for x in fd], mode, out=out64)
+        assert P.row_deviation(out64.cpu().numpy(), ref) <= 1e-12
         owned = pl.owned_rows().cpu().numpy()
         want = np.nonzero(np.bincount(idx[:, mode].astype(np.int64), minlength=dims[mode]))[0]
         assert np.array_equal(np.sort(owned), want)
