@@ -85,7 +85,7 @@ def test_other_ranks_fast_path_at_scale(R):
         assert _rowdev(y32, y64) <= 1e-4, (R, mode)
 
 
-@pytest.mark.parametrize("config,scale", [("nell-2", 1.0), ("nell-1", 0.5)])
+@pytest.mark.parametrize("config,scale", [("nell-2", 1.0), ("nell-1", 0.5), ("delicious-3d", 0.5)])
 def test_cp_als_fused_matches_fp64_at_scale(config, scale):
     """CP-ALS at benchmark scale: the R = 32 fused fp32 sweep (MTTKRP fast
     path + tensor-core 3xTF32 row update + M^T G_Y M Gram) against the same
