@@ -421,6 +421,300 @@ __global__ void __launch_bounds__(MMA_WARPS * 32, 2)
   }
 }
 
+// ------------------------------------------------ tcgen05 (5th-gen tensor core)
+// The same update on the sm_100 tensor cores.  A CTA of 128 threads streams
+// 128-row tiles of Y through a 3-stage cp.async ring; per tile
+//   1. the tile lands in shared memory as the K-major, 128-byte-swizzled A
+//      operand (row r at 128 r bytes, 16-byte chunk c at (c ^ r%8)), and
+//      thread r splits its row in place into tf32 hi (kept) and lo (to a
+//      second buffer at the same offsets);
+//   2. one thread issues F = Ylo·Mhi + Yhi·Mlo + Yhi·Mhi (tcgen05.mma
+//      kind::tf32, M = 128, N = 32, twelve K = 8 instructions) into a TMEM
+//      accumulator and commits to an mbarrier;
+//   3. thread r reads F row r back (tcgen05.ld 32x32b.x32), stores it, adds
+//      its fit term, and writes Fᵀ split into hi/lo as the K-major operand
+//      of the Gram (four 8-KB K-blocks of 32 tile rows: rows 0-31 = Fhiᵀ,
+//      32-63 = Floᵀ);
+//   4. one thread issues D = [Fhiᵀ; Floᵀ]·Fhi over the tile's rows (sixteen
+//      M = 128 instructions whose rows 64-127 read the neighbouring block and
+//      are ignored — kind::tf32 has no 64-row form we use and no MN-major
+//      operands, scripts/umma_probe.cu), so G = D[0:32] + X + Xᵀ with
+//      X = D[32:64] = FloᵀFhi (3xTF32; FloᵀFlo ~2^-22 dropped).  D accumulates
+//      in TMEM over TC_FLUSH tiles, then warps 0-1 add it into fp64 registers.
+// Y and F cross HBM once each; the MMAs take a few hundred cycles per tile.
+static constexpr int TC_ROWS = 128;
+static constexpr int TC_STAGES = 3;
+static constexpr int TC_FLUSH = 4;  // tiles per fp32 -> fp64 Gram flush (512 rows, as the mma.sync path)
+
+struct AlsTcSmem {
+  alignas(1024) uint32_t ring[TC_STAGES][TC_ROWS * ALS_R];  // Y tiles (swizzled), then their tf32 hi
+  uint32_t fg[4][2 * ALS_R * ALS_R];  // Gram operand blocks (swizzled)
+  uint32_t ylo[TC_ROWS * ALS_R];      // must follow fg: rows 64-127 of the last block's MMA read it
+  uint32_t mhi[ALS_R * ALS_R];        // M^T hi / lo, K-major without swizzle
+  uint32_t mlo[ALS_R * ALS_R];
+  float w[ALS_R];
+  double inner[TC_ROWS / 32];
+  unsigned long long bar_f, bar_g;
+  uint32_t tmem;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// UMMA shared-memory descriptor: start, LBO, SBO (bytes), version 1, layout
+// (0 = no swizzle, 2 = 128-byte swizzle)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(layout) << 61);
+}
+// instruction descriptor kind::tf32: D f32, A/B tf32 K-major, N = 32, M = 128
+static constexpr uint32_t UMMA_ID_TF32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) |
+                                         ((128u >> 4) << 24);
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(UMMA_ID_TF32), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t spin = 0;; ++spin) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (spin > (1u << 24)) __trap();  // a lost commit must not hang the GPU
+  }
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <bool LIST>
+__global__ void __launch_bounds__(TC_ROWS, 2)
+    k_als_update32_tc(const float* __restrict__ Y, int64_t rows, const uint32_t* __restrict__ list,
+                      const float* __restrict__ M, const float* __restrict__ colw,
+                      float* __restrict__ F, double* __restrict__ gram, double* __restrict__ inner) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  AlsTcSmem& S = *reinterpret_cast<AlsTcSmem*>(
+      smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const uint32_t bar_f = smem_u32(&S.bar_f), bar_g = smem_u32(&S.bar_g);
+  // B operand of F: element (j, k) = M[k][j], K-major without swizzle (core
+  // matrices of 8 j x 4 k; LBO 512 B between k-chunks, SBO 128 B between j-groups)
+  for (int i = t; i < ALS_R * ALS_R; i += TC_ROWS) {
+    const int k = i >> 5, j = i & 31;
+    uint32_t hi, lo;
+    split_tf32(M[i], hi, lo);
+    const int o = (j & 7) * 4 + (j >> 3) * 32 + (k & 3) + (k >> 2) * 128;
+    S.mhi[o] = hi;
+    S.mlo[o] = lo;
+  }
+  if (t < ALS_R) S.w[t] = colw ? colw[t] : 1.f;
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_f));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_g));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
+        smem_u32(&S.tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S.tmem, tmem_f = tmem, tmem_g = tmem + 32;
+  const uint32_t lane_base = uint32_t(warp * 32) << 16;
+  const uint32_t a_ylo = smem_u32(S.ylo), a_mhi = smem_u32(S.mhi), a_mlo = smem_u32(S.mlo);
+  const uint32_t a_fg = smem_u32(&S.fg[0][0]);
+
+  const int64_t ntiles = (rows + TC_ROWS - 1) / TC_ROWS;
+  const int64_t G = gridDim.x;
+  // tile -> ring stage: coalesced 16-byte copies (a warp moves four whole
+  // rows per instruction) to their swizzled places; rows past the end zero
+  auto load = [&](int64_t tile, int stage) {
+    uint32_t* dst = S.ring[stage];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = t + TC_ROWS * j, r = i >> 3, c = i & 7;
+      const int64_t gr = tile * TC_ROWS + r;
+      const bool ok = gr < rows;
+      const int64_t rid = ok ? (LIST ? int64_t(__ldg(list + gr)) : gr) : 0;
+      cp16_zfill(reinterpret_cast<float*>(dst + r * 32 + ((c ^ (r & 7)) << 2)), Y + rid * ALS_R + c * 4, ok);
+    }
+  };
+  int64_t tile = blockIdx.x;
+#pragma unroll
+  for (int p = 0; p < TC_STAGES - 1; ++p) {
+    if (tile + p * G < ntiles) load(tile + p * G, p);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  double gacc[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) gacc[c] = 0.0;
+  float in32 = 0.f;
+  double in64 = 0.0;
+  uint32_t ph_f = 0, ph_g = 0;
+  int since = 0, stage = 0;
+  for (; tile < ntiles; tile += G) {
+    const int64_t pre = tile + (TC_STAGES - 1) * G;
+    if (pre < ntiles) load(pre, (stage + TC_STAGES - 1) % TC_STAGES);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(TC_STAGES - 1) : "memory");
+    __syncthreads();
+    // 1. row t: tf32 hi in place, lo alongside (same swizzled offsets)
+    uint32_t* yt = S.ring[stage];
+    float yv[32];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int o = t * 32 + ((c ^ (t & 7)) << 2);
+      const uint4 x = *reinterpret_cast<const uint4*>(yt + o);
+      uint4 h, l;
+      split_tf32(__uint_as_float(x.x), h.x, l.x);
+      split_tf32(__uint_as_float(x.y), h.y, l.y);
+      split_tf32(__uint_as_float(x.z), h.z, l.z);
+      split_tf32(__uint_as_float(x.w), h.w, l.w);
+      *reinterpret_cast<uint4*>(yt + o) = h;
+      *reinterpret_cast<uint4*>(S.ylo + o) = l;
+      yv[4 * c] = __uint_as_float(x.x);
+      yv[4 * c + 1] = __uint_as_float(x.y);
+      yv[4 * c + 2] = __uint_as_float(x.z);
+      yv[4 * c + 3] = __uint_as_float(x.w);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    // 2. F = Y M in 3xTF32
+    if (t == 0) {
+      tc_fence_after();
+      const uint32_t a_yhi = smem_u32(yt);
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const uint64_t ah = umma_desc(a_yhi + s * 32, 16, 1024, 2);
+        const uint64_t al = umma_desc(a_ylo + s * 32, 16, 1024, 2);
+        const uint64_t bh = umma_desc(a_mhi + s * 1024, 512, 128, 0);
+        const uint64_t bl = umma_desc(a_mlo + s * 1024, 512, 128, 0);
+        umma_tf32(tmem_f, al, bh, s > 0);
+        umma_tf32(tmem_f, ah, bl, 1);
+        umma_tf32(tmem_f, ah, bh, 1);
+      }
+      umma_commit(bar_f);
+    }
+    mbar_wait(bar_f, ph_f);
+    ph_f ^= 1;
+    tc_fence_after();
+    // 3. F row t: store, fit term, F^T hi/lo into the Gram operand blocks
+    float f[32];
+    tmem_ld32(tmem_f + lane_base, f);
+    {
+      const int64_t gr = tile * TC_ROWS + t;
+      if (gr < rows) {
+        const int64_t rid = LIST ? int64_t(__ldg(list + gr)) : gr;
+        float4* p = reinterpret_cast<float4*>(F + rid * ALS_R);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          __stcs(p + q, make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]));
+      }
+    }
+    if (inner) {
+#pragma unroll
+      for (int c = 0; c < 32; ++c) in32 = fmaf(S.w[c] * yv[c], f[c], in32);
+    }
+    {
+      // block = warp (tile rows 32w..32w+31 are its K range), row c (hi) / 32 + c (lo),
+      // K position = lane: chunk lane/4 swizzled with c % 8
+      uint32_t* blk = S.fg[warp];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        uint32_t hi, lo;
+        split_tf32(f[c], hi, lo);
+        const int o = (((lane >> 2) ^ (c & 7)) << 2) + (lane & 3);
+        blk[c * 32 + o] = hi;
+        blk[(ALS_R + c) * 32 + o] = lo;
+      }
+    }
+    tc_fence_before();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    // 4. Gram: D (+)= [Fhi^T; Flo^T] Fhi over the tile rows, 8 rows per instruction
+    const bool flush = ++since == TC_FLUSH || tile + G >= ntiles;
+    if (t == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int s = 0; s < TC_ROWS / 8; ++s) {
+        const uint64_t d = umma_desc(a_fg + (s >> 2) * 8192 + (s & 3) * 32, 16, 1024, 2);
+        umma_tf32(tmem_g, d, d, (since > 1 || s > 0) ? 1u : 0u);
+      }
+      if (flush) umma_commit(bar_g);
+    }
+    if (flush) {
+      mbar_wait(bar_g, ph_g);
+      ph_g ^= 1;
+      tc_fence_after();
+      if (warp < 2) {
+        float d[32];
+        tmem_ld32(tmem_g + lane_base, d);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) gacc[c] += double(d[c]);
+      }
+      tc_fence_before();
+      in64 += double(in32);
+      in32 = 0.f;
+      since = 0;
+    }
+    stage = (stage + 1) % TC_STAGES;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  in64 += double(in32);
+  if (inner) {
+    double v = in64;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if (lane == 0) S.inner[warp] = v;
+  }
+  __syncthreads();
+  // G = D0 + X + X^T (D0 rows in warp 0, X rows in warp 1) via the idle ring
+  double* scratch = reinterpret_cast<double*>(&S.ring[0][0]);  // [2][32][32]
+  if (warp < 2) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) scratch[(warp * 32 + lane) * 32 + c] = gacc[c];
+  }
+  __syncthreads();
+  if (int64_t(blockIdx.x) < ntiles)
+    for (int i = t; i < ALS_R * ALS_R; i += TC_ROWS) {
+      const int r = i >> 5, c = i & 31;
+      atomicAdd(gram + i, scratch[i] + scratch[1024 + i] + scratch[1024 + c * 32 + r]);
+    }
+  if (inner && t == 0) atomicAdd(inner, S.inner[0] + S.inner[1] + S.inner[2] + S.inner[3]);
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
+}
+
 // The Gram holds the upper 16x8 tiles, which cover every r <= c; mirror the
 // upper triangle (the diagonal tiles computed both (r, c) and (c, r), which
 // may differ in the last bit) so the result is exactly symmetric.
@@ -430,6 +724,50 @@ __global__ void __launch_bounds__(1024) k_als_mirror(double* __restrict__ gram) 
   G[r][c] = gram[r * ALS_R + c];
   __syncthreads();
   gram[r * ALS_R + c] = r <= c ? G[r][c] : G[c][r];
+}
+
+template <bool LIST>
+static void launch_als_tc(const float* Y, const uint32_t* list, int64_t n, const float* M,
+                          const float* colw, float* F, double* gram, double* inner, cudaStream_t st) {
+  HBK_CUDA(cudaMemsetAsync(gram, 0, sizeof(double) * ALS_R * ALS_R, st));
+  if (inner) HBK_CUDA(cudaMemsetAsync(inner, 0, sizeof(double), st));
+  if (n == 0) return;
+  int dev = 0, sms = 0;
+  HBK_CUDA(cudaGetDevice(&dev));
+  HBK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const size_t bytes = sizeof(AlsTcSmem) + 1024;  // + alignment slack
+  static std::atomic<int> occ[64];
+  int per_sm = dev < 64 ? occ[dev].load(std::memory_order_relaxed) : 0;
+  if (per_sm == 0) {
+    HBK_CUDA(cudaFuncSetAttribute(k_als_update32_tc<LIST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(bytes)));
+    HBK_CUDA(cudaFuncSetAttribute(k_als_update32_tc<LIST>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  int(cudaSharedmemCarveoutMaxShared)));
+    HBK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_update32_tc<LIST>, TC_ROWS,
+                                                           bytes));
+    per_sm = std::max(per_sm, 1);
+    if (dev < 64) occ[dev].store(per_sm, std::memory_order_relaxed);
+  }
+  const int64_t ntiles = (n + TC_ROWS - 1) / TC_ROWS;
+  const int grid = int(std::min<int64_t>(ntiles, int64_t(sms) * per_sm));
+  k_als_update32_tc<LIST><<<grid, TC_ROWS, bytes, st>>>(Y, n, list, M, colw, F, gram, inner);
+  check_launch("k_als_update32_tc");
+  k_als_mirror<<<1, 1024, 0, st>>>(gram);
+  check_launch("k_als_mirror");
+}
+
+// HBK_ALS_KERNEL = mma (default: mma.sync 3xTF32) | tc (tcgen05) | fma (FFMA),
+// read per call so one process can A/B them.  Measured at nell-1 row counts
+// (scripts/als_kernel_bench.py, profiles/r2s7/als_tc.md): mma 0.22 / 0.16 /
+// 1.73 ms, tc 0.43 / 0.32 / 3.58 ms — the tcgen05 kernel is correct (same
+// tests) but latency-bound: one 108-KB CTA of four warps per SM serialises
+// load, split, MMA and epilogue per tile (ncu: 1 warp per scheduler, 19%
+// issue-active), where the mma.sync kernel keeps 16 warps per SM streaming.
+static int als_kernel_choice() {
+  const char* e = getenv("HBK_ALS_KERNEL");
+  if (e && std::string(e) == "fma") return 2;
+  if (e && std::string(e) == "tc") return 0;
+  return 1;
 }
 
 // Tensor-core update over rows 0..n (or list[0..n)): Gram upper tiles and the
@@ -481,11 +819,12 @@ extern "C" int hbk_als_update(const float* Y, int64_t rows, int rank, const floa
     int dev = 0, sms = 0, per_sm = 0;
     HBK_CUDA(cudaGetDevice(&dev));
     HBK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    static const bool use_fma = [] {
-      const char* e = getenv("HBK_ALS_KERNEL");
-      return e && std::string(e) == "fma";
-    }();
-    if (!use_fma) {
+    const int kernel = als_kernel_choice();
+    if (kernel == 0) {
+      launch_als_tc<false>(Y, nullptr, rows, M, colw, F, gram, inner, st);
+      return;
+    }
+    if (kernel == 1) {
       launch_als_mma<false>(Y, nullptr, rows, M, colw, F, gram, inner, st);
       return;
     }
@@ -512,6 +851,9 @@ extern "C" int hbk_als_update_rows(const float* Y, const uint32_t* list, int64_t
     HBK_REQUIRE(nlist == 0 || list, HBK_EINVAL, "null row list");
     HBK_REQUIRE((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(F)) % 16 == 0,
                 HBK_EINVAL, "Y and F must be 16-byte aligned");
-    launch_als_mma<true>(Y, list, nlist, M, colw, F, gram, inner, to_stream(stream));
+    if (als_kernel_choice() == 0)
+      launch_als_tc<true>(Y, list, nlist, M, colw, F, gram, inner, to_stream(stream));
+    else
+      launch_als_mma<true>(Y, list, nlist, M, colw, F, gram, inner, to_stream(stream));
   });
 }

@@ -87,11 +87,15 @@ def test_cp_als_distributed_single_rank_matches_cp_als(hb):
     assert np.allclose([h.fit for h in h1], fits_ref, atol=1e-5, rtol=0)
 
 
+@pytest.mark.parametrize("kernel", ["mma", "tc"])
 @pytest.mark.parametrize("rows", [1, 255, 1000, 70000])
-def test_als_update_kernel_matches_fp64(rows):
+def test_als_update_kernel_matches_fp64(rows, kernel, monkeypatch):
     """hbk_als_update: F = Y M, Gram = F^T F, weighted <Y, F> against an fp64
-    torch restatement (fp32 kernel arithmetic, so 1e-5 relative)."""
+    torch restatement (fp32 kernel arithmetic, so 1e-5 relative) — the
+    default mma.sync kernel and the tcgen05 one (HBK_ALS_KERNEL=tc)."""
     import ctypes as C
+
+    monkeypatch.setenv("HBK_ALS_KERNEL", kernel)
 
     import torch
 
@@ -118,12 +122,15 @@ def test_als_update_kernel_matches_fp64(rows):
                None, C.c_void_p(F.data_ptr()), C.c_void_p(gram.data_ptr()), None, N.stream_ptr())
 
 
+@pytest.mark.parametrize("kernel", ["mma", "tc"])
 @pytest.mark.parametrize("rows", [1, 37, 5000, 70001])
-def test_als_update_rows_matches_full_update(rows):
+def test_als_update_rows_matches_full_update(rows, kernel, monkeypatch):
     """hbk_als_update_rows over the nonzero rows of Y equals hbk_als_update
     over all rows when the other rows are zero (F, Gram, fit term); rows not
     listed keep their previous F contents."""
     import ctypes as C
+
+    monkeypatch.setenv("HBK_ALS_KERNEL", kernel)
 
     import torch
 
