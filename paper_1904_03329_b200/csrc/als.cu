@@ -422,39 +422,42 @@ __global__ void __launch_bounds__(MMA_WARPS * 32, 2)
 }
 
 // ------------------------------------------------ tcgen05 (5th-gen tensor core)
-// The same update on the sm_100 tensor cores.  A CTA of 128 threads streams
-// 128-row tiles of Y through a 3-stage cp.async ring; per tile
-//   1. the tile lands in shared memory as the K-major, 128-byte-swizzled A
-//      operand (row r at 128 r bytes, 16-byte chunk c at (c ^ r%8)), and
-//      thread r splits its row in place into tf32 hi (kept) and lo (to a
-//      second buffer at the same offsets);
-//   2. one thread issues F = Ylo·Mhi + Yhi·Mlo + Yhi·Mhi (tcgen05.mma
-//      kind::tf32, M = 128, N = 32, twelve K = 8 instructions) into a TMEM
-//      accumulator and commits to an mbarrier;
-//   3. thread r reads F row r back (tcgen05.ld 32x32b.x32), stores it, adds
-//      its fit term, and writes Fᵀ split into hi/lo as the K-major operand
-//      of the Gram (four 8-KB K-blocks of 32 tile rows: rows 0-31 = Fhiᵀ,
-//      32-63 = Floᵀ);
-//   4. one thread issues D = [Fhiᵀ; Floᵀ]·Fhi over the tile's rows (sixteen
+// The same update on the sm_100 tensor cores, software-pipelined inside one
+// CTA of 128 threads per SM (thread r = tile row r), 128-row tiles streamed
+// through a 4-stage cp.async ring.  Per tile k:
+//   1. (one tile ahead) tile k+1 lands in shared memory as the K-major,
+//      128-byte-swizzled A operand (row r at 128 r bytes, 16-byte chunk c at
+//      c ^ r%8); thread r splits its row in place into tf32 hi and writes lo
+//      to a second buffer at the same offsets; one thread issues
+//      F(k+1) = Ylo·Mhi + Yhi·Mlo + Yhi·Mhi (tcgen05.mma kind::tf32, M = 128,
+//      N = 32, twelve K = 8 instructions) into the other of two TMEM
+//      accumulators and commits to an mbarrier;
+//   2. thread r reads F(k) row r (tcgen05.ld 32x32b.x32), adds its fit term,
+//      stages the row in the consumed ring slot for a coalesced store, and
+//      writes Fᵀ split into hi/lo as the K-major operand of the Gram (four
+//      8-KB K-blocks of 32 tile rows: rows 0-31 = Fhiᵀ, 32-63 = Floᵀ; double-
+//      buffered against the previous tile's Gram MMAs);
+//   3. one thread issues D (+)= [Fhiᵀ; Floᵀ]·Fhi over the tile's rows (sixteen
 //      M = 128 instructions whose rows 64-127 read the neighbouring block and
-//      are ignored — kind::tf32 has no 64-row form we use and no MN-major
-//      operands, scripts/umma_probe.cu), so G = D[0:32] + X + Xᵀ with
-//      X = D[32:64] = FloᵀFhi (3xTF32; FloᵀFlo ~2^-22 dropped).  D accumulates
-//      in TMEM over TC_FLUSH tiles, then warps 0-1 add it into fp64 registers.
-// Y and F cross HBM once each; the MMAs take a few hundred cycles per tile.
+//      are ignored — kind::tf32 takes no MN-major operands,
+//      scripts/umma_probe.cu), so G = D[0:32] + X + Xᵀ with X = D[32:64] =
+//      FloᵀFhi (3xTF32; FloᵀFlo ~2^-22 dropped).  D accumulates in TMEM over
+//      TC_FLUSH tiles, then warps 0-1 add it into fp64 rows in shared memory.
+// Y and F cross HBM once each.
 static constexpr int TC_ROWS = 128;
-static constexpr int TC_STAGES = 3;
+static constexpr int TC_STAGES = 4;
 static constexpr int TC_FLUSH = 4;  // tiles per fp32 -> fp64 Gram flush (512 rows, as the mma.sync path)
 
 struct AlsTcSmem {
-  alignas(1024) uint32_t ring[TC_STAGES][TC_ROWS * ALS_R];  // Y tiles (swizzled), then their tf32 hi
-  uint32_t fg[4][2 * ALS_R * ALS_R];  // Gram operand blocks (swizzled)
-  uint32_t ylo[TC_ROWS * ALS_R];      // must follow fg: rows 64-127 of the last block's MMA read it
-  uint32_t mhi[ALS_R * ALS_R];        // M^T hi / lo, K-major without swizzle
+  alignas(1024) uint32_t ring[TC_STAGES][TC_ROWS * ALS_R];  // Y (swizzled) -> tf32 hi -> F staging
+  uint32_t fg[2][4][2 * ALS_R * ALS_R];  // Gram operand blocks (swizzled), double-buffered
+  uint32_t lo[2][TC_ROWS * ALS_R];       // must follow fg: the last block's rows 64-127 read it
+  uint32_t mhi[ALS_R * ALS_R];           // M^T hi / lo, K-major without swizzle
   uint32_t mlo[ALS_R * ALS_R];
+  double g[2 * ALS_R][ALS_R];
   float w[ALS_R];
   double inner[TC_ROWS / 32];
-  unsigned long long bar_f, bar_g;
+  unsigned long long bar_f[2], bar_g[2];
   uint32_t tmem;
 };
 
@@ -516,7 +519,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 }
 
 template <bool LIST>
-__global__ void __launch_bounds__(TC_ROWS, 2)
+__global__ void __launch_bounds__(TC_ROWS, 1)
     k_als_update32_tc(const float* __restrict__ Y, int64_t rows, const uint32_t* __restrict__ list,
                       const float* __restrict__ M, const float* __restrict__ colw,
                       float* __restrict__ F, double* __restrict__ gram, double* __restrict__ inner) {
@@ -524,7 +527,6 @@ __global__ void __launch_bounds__(TC_ROWS, 2)
   AlsTcSmem& S = *reinterpret_cast<AlsTcSmem*>(
       smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const uint32_t bar_f = smem_u32(&S.bar_f), bar_g = smem_u32(&S.bar_g);
   // B operand of F: element (j, k) = M[k][j], K-major without swizzle (core
   // matrices of 8 j x 4 k; LBO 512 B between k-chunks, SBO 128 B between j-groups)
   for (int i = t; i < ALS_R * ALS_R; i += TC_ROWS) {
@@ -535,14 +537,17 @@ __global__ void __launch_bounds__(TC_ROWS, 2)
     S.mhi[o] = hi;
     S.mlo[o] = lo;
   }
+  for (int i = t; i < 2 * ALS_R * ALS_R; i += TC_ROWS) (&S.g[0][0])[i] = 0.0;
   if (t < ALS_R) S.w[t] = colw ? colw[t] : 1.f;
   if (t == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_f));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_g));
+    for (int j = 0; j < 2; ++j) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.bar_f[j])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.bar_g[j])));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
         smem_u32(&S.tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -550,48 +555,33 @@ __global__ void __launch_bounds__(TC_ROWS, 2)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = S.tmem, tmem_f = tmem, tmem_g = tmem + 32;
+  const uint32_t tmem = S.tmem, tmem_g = tmem + 64;  // F accumulators at columns 0 / 32
   const uint32_t lane_base = uint32_t(warp * 32) << 16;
-  const uint32_t a_ylo = smem_u32(S.ylo), a_mhi = smem_u32(S.mhi), a_mlo = smem_u32(S.mlo);
-  const uint32_t a_fg = smem_u32(&S.fg[0][0]);
+  const uint32_t a_mhi = smem_u32(S.mhi), a_mlo = smem_u32(S.mlo);
 
   const int64_t ntiles = (rows + TC_ROWS - 1) / TC_ROWS;
-  const int64_t G = gridDim.x;
-  // tile -> ring stage: coalesced 16-byte copies (a warp moves four whole
-  // rows per instruction) to their swizzled places; rows past the end zero
-  auto load = [&](int64_t tile, int stage) {
-    uint32_t* dst = S.ring[stage];
+  const int64_t G = gridDim.x, first = blockIdx.x;
+  const int64_t count = first < ntiles ? (ntiles - 1 - first) / G + 1 : 0;  // this CTA's tiles
+  // k-th tile -> ring slot k % TC_STAGES: coalesced 16-byte copies (a warp
+  // moves four whole rows per instruction) to their swizzled places
+  auto load = [&](int64_t k) {
+    if (k >= count) return;
+    uint32_t* dst = S.ring[k % TC_STAGES];
+    const int64_t r0 = (first + k * G) * TC_ROWS;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int i = t + TC_ROWS * j, r = i >> 3, c = i & 7;
-      const int64_t gr = tile * TC_ROWS + r;
-      const bool ok = gr < rows;
-      const int64_t rid = ok ? (LIST ? int64_t(__ldg(list + gr)) : gr) : 0;
+      const bool ok = r0 + r < rows;
+      const int64_t rid = ok ? (LIST ? int64_t(__ldg(list + r0 + r)) : r0 + r) : 0;
       cp16_zfill(reinterpret_cast<float*>(dst + r * 32 + ((c ^ (r & 7)) << 2)), Y + rid * ALS_R + c * 4, ok);
     }
   };
-  int64_t tile = blockIdx.x;
-#pragma unroll
-  for (int p = 0; p < TC_STAGES - 1; ++p) {
-    if (tile + p * G < ntiles) load(tile + p * G, p);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  double gacc[32];
-#pragma unroll
-  for (int c = 0; c < 32; ++c) gacc[c] = 0.0;
-  float in32 = 0.f;
-  double in64 = 0.0;
-  uint32_t ph_f = 0, ph_g = 0;
-  int since = 0, stage = 0;
-  for (; tile < ntiles; tile += G) {
-    const int64_t pre = tile + (TC_STAGES - 1) * G;
-    if (pre < ntiles) load(pre, (stage + TC_STAGES - 1) % TC_STAGES);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group %0;" ::"n"(TC_STAGES - 1) : "memory");
+  // split tile k (its ring slot has landed) and issue F(k) into accumulator k % 2
+  auto stage_f = [&](int64_t k, float (&yv)[32]) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(TC_STAGES - 2) : "memory");
     __syncthreads();
-    // 1. row t: tf32 hi in place, lo alongside (same swizzled offsets)
-    uint32_t* yt = S.ring[stage];
-    float yv[32];
+    uint32_t* yt = S.ring[k % TC_STAGES];
+    uint32_t* lt = S.lo[k & 1];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int o = t * 32 + ((c ^ (t & 7)) << 2);
@@ -602,7 +592,7 @@ __global__ void __launch_bounds__(TC_ROWS, 2)
       split_tf32(__uint_as_float(x.z), h.z, l.z);
       split_tf32(__uint_as_float(x.w), h.w, l.w);
       *reinterpret_cast<uint4*>(yt + o) = h;
-      *reinterpret_cast<uint4*>(S.ylo + o) = l;
+      *reinterpret_cast<uint4*>(lt + o) = l;
       yv[4 * c] = __uint_as_float(x.x);
       yv[4 * c + 1] = __uint_as_float(x.y);
       yv[4 * c + 2] = __uint_as_float(x.z);
@@ -610,46 +600,59 @@ __global__ void __launch_bounds__(TC_ROWS, 2)
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    // 2. F = Y M in 3xTF32
     if (t == 0) {
       tc_fence_after();
-      const uint32_t a_yhi = smem_u32(yt);
+      const uint32_t ahi = smem_u32(yt), alo = smem_u32(lt), d = tmem + uint32_t(k & 1) * 32;
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
-        const uint64_t ah = umma_desc(a_yhi + s * 32, 16, 1024, 2);
-        const uint64_t al = umma_desc(a_ylo + s * 32, 16, 1024, 2);
+        const uint64_t ah = umma_desc(ahi + s * 32, 16, 1024, 2);
+        const uint64_t al = umma_desc(alo + s * 32, 16, 1024, 2);
         const uint64_t bh = umma_desc(a_mhi + s * 1024, 512, 128, 0);
         const uint64_t bl = umma_desc(a_mlo + s * 1024, 512, 128, 0);
-        umma_tf32(tmem_f, al, bh, s > 0);
-        umma_tf32(tmem_f, ah, bl, 1);
-        umma_tf32(tmem_f, ah, bh, 1);
+        umma_tf32(d, al, bh, s > 0);
+        umma_tf32(d, ah, bl, 1);
+        umma_tf32(d, ah, bh, 1);
       }
-      umma_commit(bar_f);
+      umma_commit(smem_u32(&S.bar_f[k & 1]));
     }
-    mbar_wait(bar_f, ph_f);
-    ph_f ^= 1;
-    tc_fence_after();
-    // 3. F row t: store, fit term, F^T hi/lo into the Gram operand blocks
-    float f[32];
-    tmem_ld32(tmem_f + lane_base, f);
-    {
-      const int64_t gr = tile * TC_ROWS + t;
-      if (gr < rows) {
-        const int64_t rid = LIST ? int64_t(__ldg(list + gr)) : gr;
-        float4* p = reinterpret_cast<float4*>(F + rid * ALS_R);
+  };
+
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          __stcs(p + q, make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]));
-      }
-    }
+  for (int p = 0; p < TC_STAGES - 1; ++p) {
+    load(p);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  float yn[32];
+  if (count > 0) stage_f(0, yn);
+  float in32 = 0.f;
+  double in64 = 0.0;
+  int since = 0;
+  for (int64_t k = 0; k < count; ++k) {
+    float yv[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) yv[c] = yn[c];
+    load(k + TC_STAGES - 1);  // the slot of tile k-1 (its F MMA and F store are done)
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (k + 1 < count) stage_f(k + 1, yn);  // overlaps F(k)'s MMAs
+    // F(k): fit term, staging for the coalesced store, F^T hi/lo for the Gram
+    mbar_wait(smem_u32(&S.bar_f[k & 1]), uint32_t(k >> 1) & 1);
+    tc_fence_after();
+    float f[32];
+    tmem_ld32(tmem + uint32_t(k & 1) * 32 + lane_base, f);
     if (inner) {
 #pragma unroll
       for (int c = 0; c < 32; ++c) in32 = fmaf(S.w[c] * yv[c], f[c], in32);
     }
+    uint32_t* stg = S.ring[k % TC_STAGES];  // F(k) has consumed this slot's hi
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      *reinterpret_cast<float4*>(stg + t * 32 + ((q ^ (t & 7)) << 2)) =
+          make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+    if (k >= 2) mbar_wait(smem_u32(&S.bar_g[k & 1]), uint32_t((k - 2) >> 1) & 1);  // Gram(k-2) read fg[k%2]
     {
       // block = warp (tile rows 32w..32w+31 are its K range), row c (hi) / 32 + c (lo),
       // K position = lane: chunk lane/4 swizzled with c % 8
-      uint32_t* blk = S.fg[warp];
+      uint32_t* blk = S.fg[k & 1][warp];
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
         uint32_t hi, lo;
@@ -662,33 +665,44 @@ __global__ void __launch_bounds__(TC_ROWS, 2)
     tc_fence_before();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    // 4. Gram: D (+)= [Fhi^T; Flo^T] Fhi over the tile rows, 8 rows per instruction
-    const bool flush = ++since == TC_FLUSH || tile + G >= ntiles;
     if (t == 0) {
       tc_fence_after();
+      const uint32_t a_fg = smem_u32(&S.fg[k & 1][0][0]);
 #pragma unroll
       for (int s = 0; s < TC_ROWS / 8; ++s) {
         const uint64_t d = umma_desc(a_fg + (s >> 2) * 8192 + (s & 3) * 32, 16, 1024, 2);
-        umma_tf32(tmem_g, d, d, (since > 1 || s > 0) ? 1u : 0u);
+        umma_tf32(tmem_g, d, d, (since > 0 || s > 0) ? 1u : 0u);
       }
-      if (flush) umma_commit(bar_g);
+      umma_commit(smem_u32(&S.bar_g[k & 1]));
     }
-    if (flush) {
-      mbar_wait(bar_g, ph_g);
-      ph_g ^= 1;
+    // coalesced F store: a warp writes four whole rows per instruction
+    {
+      const int64_t r0 = (first + k * G) * TC_ROWS;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = t + TC_ROWS * j, r = i >> 3, c = i & 7;
+        if (r0 + r < rows) {
+          const int64_t rid = LIST ? int64_t(__ldg(list + r0 + r)) : r0 + r;
+          __stcs(reinterpret_cast<float4*>(F + rid * ALS_R + c * 4),
+                 *reinterpret_cast<const float4*>(stg + r * 32 + ((c ^ (r & 7)) << 2)));
+        }
+      }
+    }
+    if (++since == TC_FLUSH || k + 1 == count) {
+      mbar_wait(smem_u32(&S.bar_g[k & 1]), uint32_t(k >> 1) & 1);
       tc_fence_after();
       if (warp < 2) {
         float d[32];
         tmem_ld32(tmem_g + lane_base, d);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) gacc[c] += double(d[c]);
+        for (int c = 0; c < 32; ++c) S.g[t][c] += double(d[c]);
       }
       tc_fence_before();
       in64 += double(in32);
       in32 = 0.f;
       since = 0;
     }
-    stage = (stage + 1) % TC_STAGES;
+    __syncthreads();  // the staged F rows are read before the slot is refilled
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   in64 += double(in32);
@@ -698,21 +712,15 @@ __global__ void __launch_bounds__(TC_ROWS, 2)
     if (lane == 0) S.inner[warp] = v;
   }
   __syncthreads();
-  // G = D0 + X + X^T (D0 rows in warp 0, X rows in warp 1) via the idle ring
-  double* scratch = reinterpret_cast<double*>(&S.ring[0][0]);  // [2][32][32]
-  if (warp < 2) {
-#pragma unroll
-    for (int c = 0; c < 32; ++c) scratch[(warp * 32 + lane) * 32 + c] = gacc[c];
-  }
-  __syncthreads();
-  if (int64_t(blockIdx.x) < ntiles)
+  // G = D0 + X + X^T (D0 = rows 0-31, X = rows 32-63 of S.g)
+  if (count > 0)
     for (int i = t; i < ALS_R * ALS_R; i += TC_ROWS) {
       const int r = i >> 5, c = i & 31;
-      atomicAdd(gram + i, scratch[i] + scratch[1024 + i] + scratch[1024 + c * 32 + r]);
+      atomicAdd(gram + i, S.g[r][c] + S.g[ALS_R + r][c] + S.g[ALS_R + c][r]);
     }
   if (inner && t == 0) atomicAdd(inner, S.inner[0] + S.inner[1] + S.inner[2] + S.inner[3]);
   tc_fence_after();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
 }
 
 // The Gram holds the upper 16x8 tiles, which cover every r <= c; mirror the
@@ -758,11 +766,10 @@ static void launch_als_tc(const float* Y, const uint32_t* list, int64_t n, const
 
 // HBK_ALS_KERNEL = mma (default: mma.sync 3xTF32) | tc (tcgen05) | fma (FFMA),
 // read per call so one process can A/B them.  Measured at nell-1 row counts
-// (scripts/als_kernel_bench.py, profiles/r2s7/als_tc.md): mma 0.22 / 0.16 /
-// 1.73 ms, tc 0.43 / 0.32 / 3.58 ms — the tcgen05 kernel is correct (same
-// tests) but latency-bound: one 108-KB CTA of four warps per SM serialises
-// load, split, MMA and epilogue per tile (ncu: 1 warp per scheduler, 19%
-// issue-active), where the mma.sync kernel keeps 16 warps per SM streaming.
+// (scripts/als_kernel_bench.py, profiles/r2s7/als_tc.md): mma 0.22 / 0.17 /
+// 1.81 ms, tc 0.45 / 0.34 / 3.81 ms — the tcgen05 kernel is correct (same
+// tests) but issue-bound: one CTA of four warps per SM spends 1,190
+// instructions per warp per tile, most of them transposing F for the Gram.
 static int als_kernel_choice() {
   const char* e = getenv("HBK_ALS_KERNEL");
   if (e && std::string(e) == "fma") return 2;
