@@ -230,10 +230,23 @@ __device__ __forceinline__ uint32_t to_tf32(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return r;
 }
+#ifndef HBK_TF32_SPLIT_CVT
+// x = hi + lo: hi = x rounded to tf32 (round half away, integer add + mask:
+// 2 instructions where cvt.rna.tf32 expands to ~6 with its special-value
+// checks; finite factor values only — |x| near FLT_MAX would round to inf),
+// lo = x - hi exactly (|lo| <= 2^-11 |x|, <= 12 significant bits), passed
+// as-is: the tensor cores read tf32 operands by ignoring the low 13 bits,
+// which drops <= 1 bit of lo (<= 2^-22 |x|), the accuracy of rounding lo too.
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  hi = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
+  lo = __float_as_uint(x - __uint_as_float(hi));
+}
+#else
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
   hi = to_tf32(x);
   lo = to_tf32(x - __uint_as_float(hi));
 }
+#endif
 __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
   asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
@@ -766,8 +779,8 @@ static void launch_als_tc(const float* Y, const uint32_t* list, int64_t n, const
 
 // HBK_ALS_KERNEL = mma (default: mma.sync 3xTF32) | tc (tcgen05) | fma (FFMA),
 // read per call so one process can A/B them.  Measured at nell-1 row counts
-// (scripts/als_kernel_bench.py, profiles/r2s7/als_tc.md): mma 0.22 / 0.17 /
-// 1.81 ms, tc 0.45 / 0.34 / 3.81 ms — the tcgen05 kernel is correct (same
+// (scripts/als_kernel_bench.py, profiles/r2s7/als_tc.md): mma 0.21 / 0.16 /
+// 1.71 ms, tc 0.41 / 0.31 / 3.48 ms — the tcgen05 kernel is correct (same
 // tests) but issue-bound: one CTA of four warps per SM spends 1,190
 // instructions per warp per tile, most of them transposing F for the Gram.
 static int als_kernel_choice() {
