@@ -19,7 +19,9 @@ time.  ``with_output_allgather`` repeats the steps with the all-gather of
 every mode's output rows.  ``cpd``: the config-5 CP-ALS sweep (nell-1,
 MTTKRP of all modes + row update + factor-row exchange) on the same N ranks.
 ``also``: further configurations measured the same way (1 GPU: flickr-3d and
-delicious-3d, the metric's other configurations).
+delicious-3d, the metric's other configurations; N>1: nell-2, the N=1
+headline, so a 1/2/4/8 scaling run has a like-for-like entry at every N
+next to flickr-3d's).
 
 ``--impl reference`` times the reference algorithm on the host CPU: the
 restated reference (oracle/tenkit_port.py) on a stratified whole-slice
@@ -68,7 +70,8 @@ def parse_args():
     ap.add_argument("--cpu-sample-nnz", type=int, default=1_000_000,
                     help="nonzeros per mode in the CPU baseline's stratified slice sample")
     ap.add_argument("--also", default=None,
-                    help="comma list of extra configs (default: flickr-3d,delicious-3d at N=1, none at N>1)")
+                    help="comma list of extra configs (default: flickr-3d,delicious-3d at N=1; "
+                         "nell-2 at N>1, so every N of a scaling run carries the N=1 headline config)")
     ap.add_argument("--cpd", default="nell-1", help="CP-ALS sweep config, or 'none'")
     ap.add_argument("--cpd-iters", type=int, default=5)
     ap.add_argument("--no-amortize", action="store_true", help="skip the COO amortisation comparison")
@@ -78,7 +81,10 @@ def parse_args():
     if a.config is None:
         a.config = "nell-2" if n == 1 else "flickr-3d"
     if a.also is None:
-        a.also = "flickr-3d,delicious-3d" if n == 1 and a.scale == 1.0 else ""
+        if a.scale != 1.0:
+            a.also = ""
+        else:
+            a.also = "flickr-3d,delicious-3d" if n == 1 else "nell-2"
     a.also = [c for c in a.also.split(",") if c and c != "none" and c != a.config]
     if a.cpd == "none":
         a.cpd = None
