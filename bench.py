@@ -742,7 +742,10 @@ def measure_cpd(env, name, args):
     out = {"workload": f"{name}-shaped CP-ALS sweep, R=32 (MTTKRP of all 3 modes + row update + "
                        "factor-row exchange)", "nnz": t.nnz, "ms_per_sweep": sweep * 1e3,
            "value": flops / sweep / 1e9, "unit": "GFLOP/s (MTTKRP-equivalent, 3 modes x 3*nnz*R per sweep)",
-           "sweeps_timed": max(1, len(walls) - 1), "fits": [h.fit for h in hist], "total_s": total,
+           "sweeps_timed": max(1, len(walls) - 1), "fits": [h.fit for h in hist],
+           "fits_note": "fits[0] is the fit of the seeded uniform(0,1) initial guess (cpd.py:236-239 "
+                        "iteration 0), strongly negative because that guess's norm dwarfs the tensor's",
+           "total_s": total,
            "timing": "host wall clock per sweep (median after the first), max over ranks"}
     del t
     torch.cuda.empty_cache()
