@@ -18,4 +18,4 @@ for path in sys.argv[1:]:
     print("==", path)
     for i in sorted(by):
         m = by[i]
-        print(f"{i:3d} {names[i][:40]:40s} {float(m['gpu__time_duration.sum'])/1e3:8.1f}us inst {float(m['smsp__inst_executed.sum'])/1e6:7.1f}M l1pipe {m['l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_active']}% issue {m['smsp__issue_active.avg.pct_of_peak_sustained_active']}% L2hit {m['lts__t_sector_hit_rate.pct']}% dram {float(m['dram__bytes_read.sum'])/1e6:.0f}MB")
+        print(f"{i:3d} {names[i][:40]:40s} {float(m['gpu__time_duration.sum'])/1e3:8.1f}us inst {float(m['smsp__inst_executed.sum'])/1e6:7.1f}M l1pipe {m['l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_active']}% issue {m['smsp__issue_active.avg.pct_of_peak_sustained_active']}% L2hit {m['lts__t_sector_hit_rate.pct']}% dram {float(m['dram__bytes_read.sum'])/1e6:.0f}MB occ {m.get('sm__warps_active.avg.pct_of_peak_sustained_active', '-')}%")
