@@ -575,18 +575,65 @@ def gather_ceiling(env, st, args, per_mode_ms):
         torch.cuda.synchronize()
         probe_ms = [statistics.mean(a.elapsed_time(b) for a, b in pev[m]) if plans[m] is not None
                     else 0.0 for m in range(n_modes)]
-        return {
+        kernel_rps = sum(rows) / (sum(per_mode_ms) * 1e-3)
+        hw = optional("row_ceiling", row_ceiling, env, st, args)
+        out = {
             "rows_per_step": sum(rows),
-            "kernel_rows_per_s": sum(rows) / (sum(per_mode_ms) * 1e-3),
+            "kernel_rows_per_s": kernel_rps,
             "ceiling_rows_per_s": sum(rows) / (sum(probe_ms) * 1e-3),
             "frac": sum(probe_ms) / sum(per_mode_ms),
             "probe_ms_per_mode": probe_ms,
             "note": ("128-byte factor rows delivered to the SMs (leaf rows + fiber rows, 2 per "
                      "CSL/COO nonzero); ceiling = gather-only kernel over the same tasks "
                      "(hbk_plan_probe)"),
+            "hardware": hw,
         }
+        if isinstance(hw, dict) and hw.get("rows_per_s"):
+            hw["frac"] = kernel_rps / hw["rows_per_s"]
+        return out
     except Exception as e:  # calibration is optional; never fail the bench on it
         return {"error": str(e)}
+
+
+def row_ceiling(env, st, args):
+    """Hardware anchor for the row-gather bound (hbk_row_ceiling): random
+    128-byte rows gathered from a zeroed matrix of the plans' factor
+    footprint (rows of the two input factors, rounded up to a power of two)
+    by 8-lane groups, with no index streams or arithmetic, at the kernels'
+    occupancy (3 CTAs/SM) and at full occupancy (8); CUDA events, best of
+    K launches.  Footprint within the L2: the L2 -> SM random-row rate."""
+    torch = env.torch
+    import ctypes as C
+
+    from paper_1904_03329_b200 import _native as N
+
+    dims = st["dims"]
+    foot = max(sum(d for i, d in enumerate(dims) if i != m) for m in range(len(dims)))
+    rows = 1 << max(10, (foot - 1).bit_length())
+    gathers = 1 << 28
+    stream = torch.cuda.current_stream()
+    res = {}
+    for ctas in (3, 8):
+        N.call("hbk_row_ceiling", C.c_int64(rows), ctas, C.c_int64(gathers), N.stream_ptr())
+        torch.cuda.synchronize()
+        best = None
+        for _ in range(max(3, args.steps // 4)):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            N.call("hbk_row_ceiling", C.c_int64(rows), ctas, C.c_int64(gathers), N.stream_ptr())
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b)
+            best = ms if best is None else min(best, ms)
+        groups = ctas * torch.cuda.get_device_properties(0).multi_processor_count * 32
+        per_group = max(8, (gathers // groups + 7) // 8 * 8)
+        res[f"{ctas * 8}_warps_per_sm"] = groups * per_group / (best * 1e-3)
+    rps = max(res.values())
+    return {"rows_per_s": rps, "gbs": rps * 128 / 1e9, "by_occupancy": res,
+            "matrix_rows": rows, "matrix_bytes": rows * 128,
+            "l2_resident": rows * 128 <= torch.cuda.get_device_properties(0).L2_cache_size,
+            "note": "hbk_row_ceiling: random 128-B rows, 8-lane groups, L1-allocating loads, no streams "
+                    "or FMAs; frac = kernel_rows_per_s / rows_per_s"}
 
 
 def with_allgather(env, st, args, flops_step):

@@ -256,6 +256,14 @@ void hbk_plan_release(hbk_plan* p);
  * output).  Its time is the row-gather ceiling of this plan on this GPU;
  * info.gather_rows / time = rows per second.  B-position plans only. */
 int hbk_plan_probe(const hbk_plan* p, const float* const* factors, void* stream);
+/* Hardware roofline anchor: one launch gathering ~`gathers` 128-byte rows at
+ * pseudo-random indices of a zeroed `rows`-row scratch matrix (`rows` a power
+ * of two; the library keeps the scratch), ctas_per_sm x 256-thread CTAs per
+ * SM, 8-lane groups as in the MTTKRP kernels, no index streams or arithmetic.
+ * The caller times it on `stream`; rows per launch = ctas_per_sm x SMs x 32
+ * groups x ceil8(gathers / groups).  Scratch within the L2: the L2 -> SM
+ * random-row rate; beyond it: the HBM random-row rate. */
+int hbk_row_ceiling(int64_t rows, int ctas_per_sm, int64_t gathers, void* stream);
 /* cudaStreamSynchronize on the caller's stream (the host calling convention
  * waits for its result copy without a Python-level stream object).        */
 int hbk_stream_synchronize(void* stream);

@@ -3283,6 +3283,72 @@ static void probe_plan(const hbk_plan* p, const Factors3R32& f32, cudaStream_t s
 }
 }  // namespace hbk
 
+namespace hbk {
+// Hardware row-gather ceiling (roofline anchor for the row-gather-bound
+// configurations): 8-lane groups gather whole 128-B rows at
+// pseudo-random indices (an LCG, two integer instructions per row) of a
+// scratch matrix of `rows` rows (a power of two), 8 rows in flight per
+// group, loads L1-allocating as the kernels' factor-row loads are — the
+// MTTKRP's access shape with no index streams, shuffles or arithmetic.
+// Matrices within the L2 give the L2 -> SM random-row rate, larger ones the
+// HBM random-row rate (scripts/l2_bw_probe.cu sweeps sizes and occupancies).
+__global__ void k_row_ceiling(const float4* __restrict__ a, uint32_t mask, uint32_t per_group,
+                              float* __restrict__ sink) {
+  const uint32_t lig = threadIdx.x & 7;
+  const uint32_t grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  uint32_t x = grp * 0x9E3779B9u + 0x7F4A7C15u;
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  float acc = 0.f;
+  for (uint32_t it = 0; it < per_group; it += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      x = x * 1664525u + 1013904223u;
+      v[u] = __ldg(a + size_t((x >> 8) & mask) * 8 + lig);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+  }
+  if (acc == 1234.5f) *sink = acc;  // keeps the loads; never true for the zeroed matrix
+}
+static std::mutex g_ceiling_mu;
+static void* g_ceiling_buf = nullptr;
+static size_t g_ceiling_bytes = 0;
+}  // namespace hbk
+
+int hbk_row_ceiling(int64_t rows, int ctas_per_sm, int64_t gathers, void* stream) {
+  return guarded([&] {
+    HBK_REQUIRE(rows > 0 && (rows & (rows - 1)) == 0 && rows <= (int64_t(1) << 32), HBK_EINVAL,
+                "rows must be a power of two <= 2^32");
+    HBK_REQUIRE(ctas_per_sm >= 1 && ctas_per_sm <= 8 && gathers > 0, HBK_EINVAL,
+                "ctas_per_sm in 1..8 and gathers > 0");
+    cudaStream_t st = to_stream(stream);
+    std::lock_guard<std::mutex> lk(g_ceiling_mu);
+    const size_t bytes = size_t(rows) * 128 + 16;
+    if (g_ceiling_bytes < bytes) {
+      if (g_ceiling_buf) HBK_CUDA(cudaFree(g_ceiling_buf));
+      g_ceiling_buf = nullptr;
+      g_ceiling_bytes = 0;
+      HBK_CUDA(cudaMalloc(&g_ceiling_buf, bytes));
+      HBK_CUDA(cudaMemsetAsync(g_ceiling_buf, 0, bytes, st));
+      g_ceiling_bytes = bytes;
+    }
+    int dev = 0, sms = 0;
+    HBK_CUDA(cudaGetDevice(&dev));
+    HBK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int grid = sms * ctas_per_sm;
+    const int64_t groups = int64_t(grid) * (FAST_BLOCK / 8);
+    const uint32_t per_group = uint32_t(std::max<int64_t>(8, (gathers / groups + 7) / 8 * 8));
+    // rows 128-byte aligned (as the factor rows are); the sink after them
+    float4* a = static_cast<float4*>(g_ceiling_buf);
+    k_row_ceiling<<<grid, FAST_BLOCK, 0, st>>>(a, uint32_t(rows - 1), per_group,
+                                               reinterpret_cast<float*>(a + size_t(rows) * 8));
+    check_launch("k_row_ceiling");
+  });
+}
+
 int hbk_plan_probe(const hbk_plan* p, const float* const* factors, void* stream) {
   return guarded([&] {
     const hbk_plan* a = p->sub_blk ? p->sub_blk : p;

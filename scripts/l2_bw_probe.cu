@@ -1,0 +1,140 @@
+// L2 -> SM bandwidth ceilings on this B200, for the L2-resident roofline of
+// the MTTKRP kernels: the MTTKRP moves 128-byte factor rows
+// from L2 to the SMs at random row indices, so its ceiling is the rate at
+// which the L2 can deliver such rows, not HBM.
+//
+//   stream: every thread reads consecutive float4s of an L2-resident buffer
+//           (grid-stride, ld.global.cg = L2, not L1), 8 loads in flight
+//   rows:   8-lane groups gather whole 128-B rows at pseudo-random row
+//           indices of an L2-resident matrix, 8 rows in flight per group —
+//           the MTTKRP's access shape without its index streams; -L2 with
+//           ld.global.cg (every row from L2), -L1 with ld.global.nc (L1
+//           allocating, as the kernels load factor rows)
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o l2_bw_probe scripts/l2_bw_probe.cu
+//   ./l2_bw_probe            (one GPU; prints GB/s per variant, best of 7)
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define CK(x)                                                                       \
+  do {                                                                              \
+    cudaError_t e = (x);                                                            \
+    if (e != cudaSuccess) {                                                         \
+      printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+      return 1;                                                                     \
+    }                                                                               \
+  } while (0)
+
+__device__ __forceinline__ float4 ld_cg(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t mix(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
+__global__ void k_stream(const float4* __restrict__ a, size_t n4, int reps, float* sink) {
+  float acc = 0.f;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  const size_t tid = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int r = 0; r < reps; ++r) {
+    for (size_t i = tid; i < n4; i += 8 * stride) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v[u] = i + u * stride < n4 ? ld_cg(a + i + u * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+    }
+  }
+  if (acc == 1234.5f) *sink = acc;
+}
+
+// rows: nrows (a power of two) x 8 float4 (128 B); each 8-lane group gathers
+// `per_group` rows at pseudo-random indices (an LCG: two instructions per row)
+template <bool L1>
+__global__ void k_rows(const float4* __restrict__ a, uint32_t nrows, int per_group, float* sink) {
+  const uint32_t lane = threadIdx.x & 31, lig = lane & 7;
+  const uint32_t grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  uint32_t x = mix(grp + 1u);
+  const uint32_t m = nrows - 1;
+  float acc = 0.f;
+  for (int it = 0; it < per_group; it += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      x = x * 1664525u + 1013904223u;
+      const float4* p = a + size_t((x >> 8) & m) * 8 + lig;
+      v[u] = L1 ? __ldg(p) : ld_cg(p);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+  }
+  if (acc == 1234.5f) *sink = acc;
+}
+
+int main() {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const size_t max_bytes = size_t(64) << 20;
+  float4* buf = nullptr;
+  float* sink = nullptr;
+  CK(cudaMalloc(&buf, max_bytes));
+  CK(cudaMalloc(&sink, 4));
+  CK(cudaMemset(buf, 0, max_bytes));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const size_t sizes[] = {size_t(4) << 20, size_t(16) << 20, size_t(64) << 20};
+  const int ctas_per_sm[] = {2, 4, 8};  // 256-thread CTAs: 16 / 32 / 64 warps per SM
+  for (size_t bytes : sizes) {
+    for (int c : ctas_per_sm) {
+      const int grid = sms * c;
+      // stream: about 4 GB read per launch
+      const size_t n4 = bytes / 16;
+      const int reps = int((size_t(4) << 30) / bytes);
+      float best = 1e30f;
+      for (int t = 0; t < 7; ++t) {
+        CK(cudaEventRecord(e0));
+        k_stream<<<grid, 256>>>(buf, n4, reps, sink);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (t && ms < best) best = ms;
+      }
+      const double read = double(reps) * double(n4) * 16;
+      printf("stream  %3zu MB  %2d warps/SM  %8.1f GB/s\n", bytes >> 20, c * 8, read / best / 1e6);
+      // rows: 128-B rows at random indices, about 4 GB per launch
+      const uint32_t nrows = uint32_t(bytes / 128);
+      const int groups = grid * 256 / 8;
+      const int per_group = int(((size_t(4) << 30) / 128 / groups + 7) / 8 * 8);
+      for (int l1 = 0; l1 < 2; ++l1) {
+        best = 1e30f;
+        for (int t = 0; t < 7; ++t) {
+          CK(cudaEventRecord(e0));
+          if (l1) k_rows<true><<<grid, 256>>>(buf, nrows, per_group, sink);
+          else k_rows<false><<<grid, 256>>>(buf, nrows, per_group, sink);
+          CK(cudaEventRecord(e1));
+          CK(cudaEventSynchronize(e1));
+          float ms;
+          CK(cudaEventElapsedTime(&ms, e0, e1));
+          if (t && ms < best) best = ms;
+        }
+        const double rb = double(groups) * per_group * 128.0;
+        printf("rows%s %3zu MB  %2d warps/SM  %8.1f GB/s  (%.1f G rows/s)\n", l1 ? "-L1" : "-L2",
+               bytes >> 20, c * 8, rb / best / 1e6, rb / 128.0 / best / 1e6);
+      }
+    }
+  }
+  return 0;
+}
