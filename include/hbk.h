@@ -262,7 +262,8 @@ int hbk_plan_probe(const hbk_plan* p, const float* const* factors, void* stream)
  * SM, 8-lane groups as in the MTTKRP kernels, no index streams or arithmetic.
  * The caller times it on `stream`; rows per launch = ctas_per_sm x SMs x 32
  * groups x ceil8(gathers / groups).  Scratch within the L2: the L2 -> SM
- * random-row rate; beyond it: the HBM random-row rate. */
+ * random-row rate; beyond it: the HBM random-row rate.  rows = 0 frees the
+ * scratch (the other arguments are then ignored). */
 int hbk_row_ceiling(int64_t rows, int ctas_per_sm, int64_t gathers, void* stream);
 /* cudaStreamSynchronize on the caller's stream (the host calling convention
  * waits for its result copy without a Python-level stream object).        */

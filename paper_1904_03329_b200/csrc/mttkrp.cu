@@ -3320,6 +3320,13 @@ static size_t g_ceiling_bytes = 0;
 
 int hbk_row_ceiling(int64_t rows, int ctas_per_sm, int64_t gathers, void* stream) {
   return guarded([&] {
+    if (rows == 0) {  // release the scratch matrix
+      std::lock_guard<std::mutex> lk(g_ceiling_mu);
+      if (g_ceiling_buf) HBK_CUDA(cudaFree(g_ceiling_buf));
+      g_ceiling_buf = nullptr;
+      g_ceiling_bytes = 0;
+      return;
+    }
     HBK_REQUIRE(rows > 0 && (rows & (rows - 1)) == 0 && rows <= (int64_t(1) << 32), HBK_EINVAL,
                 "rows must be a power of two <= 2^32");
     HBK_REQUIRE(ctas_per_sm >= 1 && ctas_per_sm <= 8 && gathers > 0, HBK_EINVAL,

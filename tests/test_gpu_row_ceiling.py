@@ -32,3 +32,6 @@ def test_row_ceiling_launch_and_guards():
     groups = 3 * torch.cuda.get_device_properties(0).multi_processor_count * 32
     rows = groups * max(8, ((1 << 22) // groups + 7) // 8 * 8)
     assert rows / (ms * 1e-3) > 1e9  # well above a billion rows/s on any B200
+    N.call("hbk_row_ceiling", C.c_int64(0), 1, C.c_int64(1), N.stream_ptr())  # frees the scratch
+    N.call("hbk_row_ceiling", C.c_int64(1 << 10), 1, C.c_int64(1 << 16), N.stream_ptr())  # re-allocates
+    torch.cuda.synchronize()
