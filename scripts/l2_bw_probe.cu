@@ -82,6 +82,98 @@ __global__ void k_rows(const float4* __restrict__ a, uint32_t nrows, int per_gro
   if (acc == 1234.5f) *sink = acc;
 }
 
+// rows with the MTTKRP's per-row overheads: each lane of a group holds one
+// position's (index, value); per batch of 8 the group broadcasts them with
+// 16 SHFL (as the kernels do), gathers the 8 rows, and (FMA) accumulates
+// value * row with 4 FFMA per row per lane
+template <bool FMA>
+__global__ void k_rows_shfl(const float4* __restrict__ a, uint32_t nrows, int per_group, float* sink) {
+  const uint32_t lane = threadIdx.x & 31, lig = lane & 7;
+  const uint32_t gid = (blockIdx.x * blockDim.x + threadIdx.x);
+  uint32_t x = mix(gid + 1u);
+  const uint32_t m = nrows - 1;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float accs = 0.f;
+  for (int it = 0; it < per_group; it += 8) {
+    x = x * 1664525u + 1013904223u;
+    const uint32_t mine = (x >> 8) & m;
+    const float val = __uint_as_float(0x3f800000u | (x & 0x7fffu));
+    float4 v[8];
+    float w[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t r = __shfl_sync(0xffffffffu, mine, u, 8);
+      v[u] = __ldg(a + size_t(r) * 8 + lig);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) w[u] = __shfl_sync(0xffffffffu, val, u, 8);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (FMA) {
+        acc.x = fmaf(w[u], v[u].x, acc.x); acc.y = fmaf(w[u], v[u].y, acc.y);
+        acc.z = fmaf(w[u], v[u].z, acc.z); acc.w = fmaf(w[u], v[u].w, acc.w);
+      } else {
+        accs += v[u].x + v[u].y + v[u].z + v[u].w + w[u];
+      }
+    }
+  }
+  if (acc.x + acc.y + acc.z + acc.w + accs == 1234.5f) *sink = acc.x;
+}
+
+// rows with a Zipf(1) row distribution (P(r) ~ 1/(r+1), r = 2^(u log2 N) - 1),
+// optionally scattered over the matrix by an odd multiplier (SCRAMBLE): the
+// skew of the FROSTT-shaped tensors' leaf modes, for L2-slice hot spots
+template <bool SCRAMBLE>
+__global__ void k_rows_zipf(const float4* __restrict__ a, uint32_t nrows, int per_group, float* sink) {
+  const uint32_t lig = threadIdx.x & 7;
+  const uint32_t grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  uint32_t x = mix(grp + 1u);
+  const uint32_t m = nrows - 1;
+  const float l2n = log2f(float(nrows));
+  float acc = 0.f;
+  for (int it = 0; it < per_group; it += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      x = x * 1664525u + 1013904223u;
+      uint32_t r = uint32_t(exp2f(float(x >> 8) * (1.0f / 16777216.0f) * l2n)) - 1u;
+      if (SCRAMBLE) r *= 2654435761u;
+      v[u] = __ldg(a + size_t(r & m) * 8 + lig);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+  }
+  if (acc == 1234.5f) *sink = acc;
+}
+
+// Zipf rows with the H hottest rows replicated REP times after the matrix:
+// a group reads replica (group id mod REP) of a hot row, spreading the hot
+// rows' requests over REP times more L2 lines / slices
+template <int REP>
+__global__ void k_rows_zipf_rep(const float4* __restrict__ a, uint32_t nrows, uint32_t H, int per_group,
+                                float* sink) {
+  const uint32_t lig = threadIdx.x & 7;
+  const uint32_t grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  uint32_t x = mix(grp + 1u);
+  const uint32_t m = nrows - 1;
+  const float l2n = log2f(float(nrows));
+  const uint32_t rep = grp % REP;
+  float acc = 0.f;
+  for (int it = 0; it < per_group; it += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      x = x * 1664525u + 1013904223u;
+      const uint32_t r = (uint32_t(exp2f(float(x >> 8) * (1.0f / 16777216.0f) * l2n)) - 1u) & m;
+      const size_t row = r < H ? size_t(nrows) + size_t(r) * REP + rep : size_t(r);
+      v[u] = __ldg(a + row * 8 + lig);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+  }
+  if (acc == 1234.5f) *sink = acc;
+}
+
 int main() {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -94,8 +186,8 @@ int main() {
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  const size_t sizes[] = {size_t(4) << 20, size_t(16) << 20, size_t(64) << 20};
-  const int ctas_per_sm[] = {2, 4, 8};  // 256-thread CTAs: 16 / 32 / 64 warps per SM
+  const size_t sizes[] = {size_t(8) << 20};
+  const int ctas_per_sm[] = {3, 8};  // 256-thread CTAs: 16 / 24 / 32 / 64 warps per SM
   for (size_t bytes : sizes) {
     for (int c : ctas_per_sm) {
       const int grid = sms * c;
@@ -132,6 +224,58 @@ int main() {
         }
         const double rb = double(groups) * per_group * 128.0;
         printf("rows%s %3zu MB  %2d warps/SM  %8.1f GB/s  (%.1f G rows/s)\n", l1 ? "-L1" : "-L2",
+               bytes >> 20, c * 8, rb / best / 1e6, rb / 128.0 / best / 1e6);
+      }
+      for (int sc = 0; sc < 2; ++sc) {
+        best = 1e30f;
+        for (int t = 0; t < 7; ++t) {
+          CK(cudaEventRecord(e0));
+          if (sc) k_rows_zipf<true><<<grid, 256>>>(buf, nrows, per_group, sink);
+          else k_rows_zipf<false><<<grid, 256>>>(buf, nrows, per_group, sink);
+          CK(cudaEventRecord(e1));
+          CK(cudaEventSynchronize(e1));
+          float ms;
+          CK(cudaEventElapsedTime(&ms, e0, e1));
+          if (t && ms < best) best = ms;
+        }
+        const double rb = double(groups) * per_group * 128.0;
+        printf("rows-zipf%s %3zu MB  %2d warps/SM  %8.1f GB/s  (%.1f G rows/s)\n", sc ? "-scrambled" : "",
+               bytes >> 20, c * 8, rb / best / 1e6, rb / 128.0 / best / 1e6);
+      }
+      for (int cfg = 0; cfg < 6; ++cfg) {
+        const int rep = (cfg % 3 == 0) ? 2 : (cfg % 3 == 1 ? 4 : 8);
+        const uint32_t H = cfg < 3 ? 256u : 2048u;
+        if (size_t(nrows + H * rep) * 128 > max_bytes) continue;
+        best = 1e30f;
+        for (int t = 0; t < 7; ++t) {
+          CK(cudaEventRecord(e0));
+          if (rep == 2) k_rows_zipf_rep<2><<<grid, 256>>>(buf, nrows, H, per_group, sink);
+          else if (rep == 4) k_rows_zipf_rep<4><<<grid, 256>>>(buf, nrows, H, per_group, sink);
+          else k_rows_zipf_rep<8><<<grid, 256>>>(buf, nrows, H, per_group, sink);
+          CK(cudaEventRecord(e1));
+          CK(cudaEventSynchronize(e1));
+          float ms;
+          CK(cudaEventElapsedTime(&ms, e0, e1));
+          if (t && ms < best) best = ms;
+        }
+        const double rb = double(groups) * per_group * 128.0;
+        printf("rows-zipf-rep%d-H%u %3zu MB  %2d warps/SM  %8.1f GB/s  (%.1f G rows/s)\n", rep, H,
+               bytes >> 20, c * 8, rb / best / 1e6, rb / 128.0 / best / 1e6);
+      }
+      for (int fma = 0; fma < 2; ++fma) {
+        best = 1e30f;
+        for (int t = 0; t < 7; ++t) {
+          CK(cudaEventRecord(e0));
+          if (fma) k_rows_shfl<true><<<grid, 256>>>(buf, nrows, per_group, sink);
+          else k_rows_shfl<false><<<grid, 256>>>(buf, nrows, per_group, sink);
+          CK(cudaEventRecord(e1));
+          CK(cudaEventSynchronize(e1));
+          float ms;
+          CK(cudaEventElapsedTime(&ms, e0, e1));
+          if (t && ms < best) best = ms;
+        }
+        const double rb = double(groups) * per_group * 128.0;
+        printf("rows-L1-shfl%s %3zu MB  %2d warps/SM  %8.1f GB/s  (%.1f G rows/s)\n", fma ? "-fma" : "",
                bytes >> 20, c * 8, rb / best / 1e6, rb / 128.0 / best / 1e6);
       }
     }
