@@ -600,7 +600,8 @@ def row_ceiling(env, st, args):
     128-byte rows gathered from a zeroed matrix of the plans' factor
     footprint (rows of the two input factors, rounded up to a power of two)
     by 8-lane groups, with no index streams or arithmetic, at the kernels'
-    occupancy (3 CTAs/SM) and at full occupancy (8); CUDA events, best of
+    occupancy (4 CTAs/SM: the heavy-slice kernel's 64 registers) and at full
+    occupancy (8); CUDA events, best of
     K launches.  Footprint within the L2: the L2 -> SM random-row rate."""
     torch = env.torch
     import ctypes as C
@@ -613,7 +614,7 @@ def row_ceiling(env, st, args):
     gathers = 1 << 28
     stream = torch.cuda.current_stream()
     res = {}
-    for ctas in (3, 8):
+    for ctas in (4, 8):
         N.call("hbk_row_ceiling", C.c_int64(rows), ctas, C.c_int64(gathers), N.stream_ptr())
         torch.cuda.synchronize()
         best = None
