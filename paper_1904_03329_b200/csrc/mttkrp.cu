@@ -3316,13 +3316,20 @@ __global__ void k_row_ceiling(const float4* __restrict__ a, uint32_t mask, uint3
 static std::mutex g_ceiling_mu;
 static void* g_ceiling_buf = nullptr;
 static size_t g_ceiling_bytes = 0;
+static int g_ceiling_dev = -1;  // the device the scratch lives on
 }  // namespace hbk
 
 int hbk_row_ceiling(int64_t rows, int ctas_per_sm, int64_t gathers, void* stream) {
   return guarded([&] {
-    if (rows == 0) {  // release the scratch matrix
+    if (rows == 0) {  // release the scratch matrix (on its device)
       std::lock_guard<std::mutex> lk(g_ceiling_mu);
-      if (g_ceiling_buf) HBK_CUDA(cudaFree(g_ceiling_buf));
+      if (g_ceiling_buf) {
+        int prev = 0;
+        HBK_CUDA(cudaGetDevice(&prev));
+        HBK_CUDA(cudaSetDevice(g_ceiling_dev));
+        HBK_CUDA(cudaFree(g_ceiling_buf));
+        HBK_CUDA(cudaSetDevice(prev));
+      }
       g_ceiling_buf = nullptr;
       g_ceiling_bytes = 0;
       return;
@@ -3334,6 +3341,16 @@ int hbk_row_ceiling(int64_t rows, int ctas_per_sm, int64_t gathers, void* stream
     cudaStream_t st = to_stream(stream);
     std::lock_guard<std::mutex> lk(g_ceiling_mu);
     const size_t bytes = size_t(rows) * 128 + 16;
+    int cur = 0;
+    HBK_CUDA(cudaGetDevice(&cur));
+    if (g_ceiling_buf && g_ceiling_dev != cur) {  // scratch of another device: free it there
+      int prev = cur;
+      HBK_CUDA(cudaSetDevice(g_ceiling_dev));
+      HBK_CUDA(cudaFree(g_ceiling_buf));
+      HBK_CUDA(cudaSetDevice(prev));
+      g_ceiling_buf = nullptr;
+      g_ceiling_bytes = 0;
+    }
     if (g_ceiling_bytes < bytes) {
       if (g_ceiling_buf) HBK_CUDA(cudaFree(g_ceiling_buf));
       g_ceiling_buf = nullptr;
@@ -3341,6 +3358,7 @@ int hbk_row_ceiling(int64_t rows, int ctas_per_sm, int64_t gathers, void* stream
       HBK_CUDA(cudaMalloc(&g_ceiling_buf, bytes));
       HBK_CUDA(cudaMemsetAsync(g_ceiling_buf, 0, bytes, st));
       g_ceiling_bytes = bytes;
+      g_ceiling_dev = cur;
     }
     int dev = 0, sms = 0;
     HBK_CUDA(cudaGetDevice(&dev));
