@@ -12,6 +12,8 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
+import time
 
 from . import _native as N
 from .coo import CooTensor, canonicalize, unique_coordinates
@@ -56,7 +58,6 @@ def powerlaw_tensor(dims, nnz: int, alpha, seed: int, scale: float = 1.0) -> Coo
     gen.manual_seed(int(seed))
     have = torch.empty((0, len(dims)), dtype=torch.int32, device="cuda")
     need = nnz
-    import os, time
     verbose = bool(os.environ.get("HBK_GEN_VERBOSE"))
     for it in range(64):
         tic = time.perf_counter()
