@@ -13,7 +13,9 @@
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o l2_bw_probe scripts/l2_bw_probe.cu
 //   ./l2_bw_probe            (one GPU; prints GB/s per variant, best of 7)
+#include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -149,7 +151,7 @@ __global__ void k_rows_zipf(const float4* __restrict__ a, uint32_t nrows, int pe
 // Zipf rows with the H hottest rows replicated REP times after the matrix:
 // a group reads replica (group id mod REP) of a hot row, spreading the hot
 // rows' requests over REP times more L2 lines / slices
-template <int REP>
+template <int REP, bool PER_SM>
 __global__ void k_rows_zipf_rep(const float4* __restrict__ a, uint32_t nrows, uint32_t H, int per_group,
                                 float* sink) {
   const uint32_t lig = threadIdx.x & 7;
@@ -157,7 +159,9 @@ __global__ void k_rows_zipf_rep(const float4* __restrict__ a, uint32_t nrows, ui
   uint32_t x = mix(grp + 1u);
   const uint32_t m = nrows - 1;
   const float l2n = log2f(float(nrows));
-  const uint32_t rep = grp % REP;
+  uint32_t smid;
+  asm("mov.u32 %0, %%smid;" : "=r"(smid));
+  const uint32_t rep = PER_SM ? smid % REP : grp % REP;
   float acc = 0.f;
   for (int it = 0; it < per_group; it += 8) {
     float4 v[8];
@@ -170,6 +174,35 @@ __global__ void k_rows_zipf_rep(const float4* __restrict__ a, uint32_t nrows, ui
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+  }
+  if (acc == 1234.5f) *sink = acc;
+}
+
+// rows named by an index STREAM, as the MTTKRP reads them: each group walks
+// its own contiguous span of a u32 index array (HBM, L1 no-allocate), one
+// coalesced load per lane per batch of 8, 8 SHFL to broadcast, 8 row gathers
+// (L1-allocating).  Index arrays: uniform or Zipf(1), generated on the host.
+__global__ void k_rows_stream(const float4* __restrict__ a, const uint32_t* __restrict__ idx,
+                              int per_group, float* sink) {
+  const uint32_t lig = threadIdx.x & 7;
+  const uint32_t grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const uint32_t* my = idx + size_t(grp) * per_group;
+  float acc = 0.f;
+  uint32_t cur;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(cur) : "l"(my + lig));
+  for (int it = 0; it < per_group; it += 8) {
+    uint32_t nxt = 0;
+    if (it + 8 < per_group)
+      asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(nxt) : "l"(my + it + 8 + lig));
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t r = __shfl_sync(0xffffffffu, cur, u, 8);
+      v[u] = __ldg(a + size_t(r) * 8 + lig);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+    cur = nxt;
   }
   if (acc == 1234.5f) *sink = acc;
 }
@@ -187,7 +220,30 @@ int main() {
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   const size_t sizes[] = {size_t(8) << 20};
-  const int ctas_per_sm[] = {3, 8};  // 256-thread CTAs: 16 / 24 / 32 / 64 warps per SM
+  // index streams for k_rows_stream: 2^26 indices, uniform and Zipf(1) over
+  // the 8-MB matrix's 65,536 rows (host-generated, fixed seed)
+  const size_t nidx = size_t(1) << 26;
+  const uint32_t srows = uint32_t((size_t(8) << 20) / 128);
+  uint32_t* h_idx = (uint32_t*)malloc(nidx * 4);
+  uint32_t* d_uni = nullptr;
+  uint32_t* d_zipf = nullptr;
+  CK(cudaMalloc(&d_uni, nidx * 4));
+  CK(cudaMalloc(&d_zipf, nidx * 4));
+  {
+    uint64_t st = 88172645463325252ull;
+    auto nextu = [&]() { st ^= st << 13; st ^= st >> 7; st ^= st << 17; return st; };
+    for (size_t i = 0; i < nidx; ++i) h_idx[i] = uint32_t(nextu() % srows);
+    CK(cudaMemcpy(d_uni, h_idx, nidx * 4, cudaMemcpyHostToDevice));
+    const double ln = log(double(srows) + 1.0);
+    for (size_t i = 0; i < nidx; ++i) {
+      const double u = double(nextu() >> 11) * (1.0 / 9007199254740992.0);
+      uint32_t r = uint32_t(floor(exp(u * ln))) - 1u;
+      if (r >= srows) r = srows - 1;
+      h_idx[i] = uint32_t((uint64_t(r) * 2654435761ull) % srows);  // scattered hot rows
+    }
+    CK(cudaMemcpy(d_zipf, h_idx, nidx * 4, cudaMemcpyHostToDevice));
+  }
+  const int ctas_per_sm[] = {4, 8};  // 256-thread CTAs: 16 / 24 / 32 / 64 warps per SM
   for (size_t bytes : sizes) {
     for (int c : ctas_per_sm) {
       const int grid = sms * c;
@@ -242,16 +298,23 @@ int main() {
         printf("rows-zipf%s %3zu MB  %2d warps/SM  %8.1f GB/s  (%.1f G rows/s)\n", sc ? "-scrambled" : "",
                bytes >> 20, c * 8, rb / best / 1e6, rb / 128.0 / best / 1e6);
       }
-      for (int cfg = 0; cfg < 6; ++cfg) {
+      for (int cfg = 0; cfg < 12; ++cfg) {
         const int rep = (cfg % 3 == 0) ? 2 : (cfg % 3 == 1 ? 4 : 8);
-        const uint32_t H = cfg < 3 ? 256u : 2048u;
+        const uint32_t H = (cfg / 3) % 2 == 0 ? 256u : 2048u;
+        const bool per_sm = cfg >= 6;
         if (size_t(nrows + H * rep) * 128 > max_bytes) continue;
         best = 1e30f;
         for (int t = 0; t < 7; ++t) {
           CK(cudaEventRecord(e0));
-          if (rep == 2) k_rows_zipf_rep<2><<<grid, 256>>>(buf, nrows, H, per_group, sink);
-          else if (rep == 4) k_rows_zipf_rep<4><<<grid, 256>>>(buf, nrows, H, per_group, sink);
-          else k_rows_zipf_rep<8><<<grid, 256>>>(buf, nrows, H, per_group, sink);
+          if (per_sm) {
+            if (rep == 2) k_rows_zipf_rep<2, true><<<grid, 256>>>(buf, nrows, H, per_group, sink);
+            else if (rep == 4) k_rows_zipf_rep<4, true><<<grid, 256>>>(buf, nrows, H, per_group, sink);
+            else k_rows_zipf_rep<8, true><<<grid, 256>>>(buf, nrows, H, per_group, sink);
+          } else {
+            if (rep == 2) k_rows_zipf_rep<2, false><<<grid, 256>>>(buf, nrows, H, per_group, sink);
+            else if (rep == 4) k_rows_zipf_rep<4, false><<<grid, 256>>>(buf, nrows, H, per_group, sink);
+            else k_rows_zipf_rep<8, false><<<grid, 256>>>(buf, nrows, H, per_group, sink);
+          }
           CK(cudaEventRecord(e1));
           CK(cudaEventSynchronize(e1));
           float ms;
@@ -259,8 +322,27 @@ int main() {
           if (t && ms < best) best = ms;
         }
         const double rb = double(groups) * per_group * 128.0;
-        printf("rows-zipf-rep%d-H%u %3zu MB  %2d warps/SM  %8.1f GB/s  (%.1f G rows/s)\n", rep, H,
+        printf("rows-zipf-rep%d%s-H%u %3zu MB  %2d warps/SM  %8.1f GB/s  (%.1f G rows/s)\n", rep,
+               per_sm ? "-persm" : "", H,
                bytes >> 20, c * 8, rb / best / 1e6, rb / 128.0 / best / 1e6);
+      }
+      if (bytes == (size_t(8) << 20)) {
+        const int per_group_s = int(nidx / groups) / 8 * 8;
+        for (int z = 0; z < 2; ++z) {
+          best = 1e30f;
+          for (int t = 0; t < 7; ++t) {
+            CK(cudaEventRecord(e0));
+            k_rows_stream<<<grid, 256>>>(buf, z ? d_zipf : d_uni, per_group_s, sink);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            if (t && ms < best) best = ms;
+          }
+          const double rb = double(groups) * per_group_s * 128.0;
+          printf("rows-stream-%s %3zu MB  %2d warps/SM  %8.1f GB/s  (%.1f G rows/s)\n", z ? "zipf" : "uniform",
+                 bytes >> 20, c * 8, rb / best / 1e6, rb / 128.0 / best / 1e6);
+        }
       }
       for (int fma = 0; fma < 2; ++fma) {
         best = 1e30f;
