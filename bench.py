@@ -626,14 +626,14 @@ def row_ceiling(env, st, args):
             torch.cuda.synchronize()
             ms = a.elapsed_time(b)
             best = ms if best is None else min(best, ms)
-        groups = ctas * torch.cuda.get_device_properties(0).multi_processor_count * 32
+        groups = ctas * torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count * 32
         per_group = max(8, (gathers // groups + 7) // 8 * 8)
         res[f"{ctas * 8}_warps_per_sm"] = groups * per_group / (best * 1e-3)
     N.call("hbk_row_ceiling", C.c_int64(0), 1, C.c_int64(1), N.stream_ptr())  # free the scratch
     rps = max(res.values())
     return {"rows_per_s": rps, "gbs": rps * 128 / 1e9, "by_occupancy": res,
             "matrix_rows": rows, "matrix_bytes": rows * 128,
-            "l2_resident": rows * 128 <= torch.cuda.get_device_properties(0).L2_cache_size,
+            "l2_resident": rows * 128 <= torch.cuda.get_device_properties(torch.cuda.current_device()).L2_cache_size,
             "note": "hbk_row_ceiling: random 128-B rows, 8-lane groups, L1-allocating loads, no streams "
                     "or FMAs; frac = kernel_rows_per_s / rows_per_s"}
 

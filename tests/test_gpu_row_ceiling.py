@@ -29,7 +29,7 @@ def test_row_ceiling_launch_and_guards():
     torch.cuda.synchronize()
     ms = a.elapsed_time(b)
     assert 0 < ms < 1000
-    groups = 3 * torch.cuda.get_device_properties(0).multi_processor_count * 32
+    groups = 3 * torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count * 32
     rows = groups * max(8, ((1 << 22) // groups + 7) // 8 * 8)
     assert rows / (ms * 1e-3) > 1e9  # well above a billion rows/s on any B200
     N.call("hbk_row_ceiling", C.c_int64(0), 1, C.c_int64(1), N.stream_ptr())  # frees the scratch
