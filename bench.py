@@ -590,6 +590,9 @@ def gather_ceiling(env, st, args, per_mode_ms):
         }
         if isinstance(hw, dict) and hw.get("rows_per_s"):
             hw["frac"] = kernel_rps / hw["rows_per_s"]
+            pat = hw.get("pattern")
+            if isinstance(pat, dict) and pat.get("rows_per_s"):
+                pat["frac"] = kernel_rps / pat["rows_per_s"]
         return out
     except Exception as e:  # calibration is optional; never fail the bench on it
         return {"error": str(e)}
@@ -602,7 +605,9 @@ def row_ceiling(env, st, args):
     by 8-lane groups, with no index streams or arithmetic, at the kernels'
     occupancy (4 CTAs/SM: the heavy-slice kernel's 64 registers) and at full
     occupancy (8); CUDA events, best of
-    K launches.  Footprint within the L2: the L2 -> SM random-row rate."""
+    K launches.  Footprint within the L2: the L2 -> SM random-row rate.
+    ``pattern``: the same matrix through an index stream with the tensor's
+    skew (hbk_row_ceiling_stream) — the kernels' access structure."""
     torch = env.torch
     import ctypes as C
 
@@ -629,9 +634,51 @@ def row_ceiling(env, st, args):
         groups = ctas * torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count * 32
         per_group = max(8, (gathers // groups + 7) // 8 * 8)
         res[f"{ctas * 8}_warps_per_sm"] = groups * per_group / (best * 1e-3)
+    # the kernels' own access structure: rows named by an index stream (one
+    # coalesced load per lane per 8 positions + SHFL), with the leaf mode's
+    # power-law skew (Appendix A generator's inverse CDF, hot rows scattered)
+    pattern = None
+    try:
+        import paper_1904_03329_b200 as hb
+        from paper_1904_03329_b200.generate import CONFIGS
+
+        cfg = CONFIGS.get(args.config, {})
+        alpha = cfg.get("alpha") or (0.0,) * len(dims)
+        a = float(alpha[hb.allmode_order(dims, 0)[-1]])
+        n = 1 << 26
+        g = torch.Generator(device="cuda")
+        g.manual_seed(1904)
+        u = torch.rand(n, generator=g, device="cuda", dtype=torch.float64)
+        top = float(rows + 1)
+        x = torch.exp(u * math.log(top)) if a == 1.0 else ((top ** (1.0 - a) - 1.0) * u + 1.0) ** (1.0 / (1.0 - a))
+        r = (torch.floor(x).to(torch.int64) - 1).clamp_(0, rows - 1)
+        idx = ((r * 2654435761) % rows).to(torch.int32)
+        del u, x, r
+        ctas = 4
+        N.call("hbk_row_ceiling_stream", C.c_void_p(idx.data_ptr()), C.c_int64(n), C.c_int64(rows), ctas,
+               N.stream_ptr())
+        torch.cuda.synchronize()
+        best = None
+        for _ in range(max(3, args.steps // 4)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            N.call("hbk_row_ceiling_stream", C.c_void_p(idx.data_ptr()), C.c_int64(n), C.c_int64(rows), ctas,
+                   N.stream_ptr())
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        groups = ctas * torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count * 32
+        per_group = n // groups // 8 * 8
+        pattern = {"rows_per_s": groups * per_group / (best * 1e-3), "alpha": a, "warps_per_sm": ctas * 8,
+                   "note": "hbk_row_ceiling_stream: the same matrix gathered through a u32 index stream read as "
+                           "the kernels read theirs, rows drawn with the leaf mode's power-law skew"}
+        del idx
+    except Exception as exc:  # noqa: BLE001 - optional detail of an optional part
+        pattern = {"error": f"{type(exc).__name__}: {exc}"}
     N.call("hbk_row_ceiling", C.c_int64(0), 1, C.c_int64(1), N.stream_ptr())  # free the scratch
     rps = max(res.values())
-    return {"rows_per_s": rps, "gbs": rps * 128 / 1e9, "by_occupancy": res,
+    return {"rows_per_s": rps, "gbs": rps * 128 / 1e9, "by_occupancy": res, "pattern": pattern,
             "matrix_rows": rows, "matrix_bytes": rows * 128,
             "l2_resident": rows * 128 <= torch.cuda.get_device_properties(torch.cuda.current_device()).L2_cache_size,
             "note": "hbk_row_ceiling: random 128-B rows, 8-lane groups, L1-allocating loads, no streams "

@@ -265,6 +265,13 @@ int hbk_plan_probe(const hbk_plan* p, const float* const* factors, void* stream)
  * random-row rate; beyond it: the HBM random-row rate.  rows = 0 frees the
  * scratch (the other arguments are then ignored). */
 int hbk_row_ceiling(int64_t rows, int ctas_per_sm, int64_t gathers, void* stream);
+/* The same matrix (hbk_row_ceiling with the same rows must have run first),
+ * gathered through an index stream read like the MTTKRP kernels read theirs:
+ * each 8-lane group walks a contiguous span of idx[n] (device u32, taken
+ * modulo rows), one coalesced load per lane per 8 positions, SHFL
+ * broadcasts, L1-allocating row loads.  Rows per launch = groups x
+ * floor8(n / groups).  The caller picks the row distribution. */
+int hbk_row_ceiling_stream(const uint32_t* idx, int64_t n, int64_t rows, int ctas_per_sm, void* stream);
 /* cudaStreamSynchronize on the caller's stream (the host calling convention
  * waits for its result copy without a Python-level stream object).        */
 int hbk_stream_synchronize(void* stream);

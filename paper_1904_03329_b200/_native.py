@@ -148,6 +148,7 @@ _SIGS = {
     "hbk_coo_shard_rows": ([vp, C.c_int, i64, i64, vp, C.POINTER(vp)], C.c_int),
     "hbk_plan_probe": ([vp, vp, vp], C.c_int),
     "hbk_row_ceiling": ([i64, C.c_int, i64, vp], C.c_int),
+    "hbk_row_ceiling_stream": ([vp, i64, i64, C.c_int, vp], C.c_int),
     "hbk_nonfinite_f32": ([vp, vp, C.c_int, vp, vp], C.c_int),
     "hbk_stage_f64_to_f32": ([vp, vp, C.c_int, vp, vp, vp, vp], C.c_int),
     "hbk_stage_f64_to_f64": ([vp, vp, C.c_int, vp, vp, vp, vp], C.c_int),

@@ -3319,6 +3319,37 @@ static size_t g_ceiling_bytes = 0;
 static int g_ceiling_dev = -1;  // the device the scratch lives on
 }  // namespace hbk
 
+namespace hbk {
+// The same gather driven by an index STREAM read the way the MTTKRP kernels
+// read theirs: each 8-lane group walks its own contiguous span of idx (HBM,
+// L1 no-allocate), one coalesced load per lane per batch of 8 positions
+// (the next batch's loaded one batch ahead), 8 SHFL broadcasts, 8
+// L1-allocating row loads — the kernels' access structure without their
+// arithmetic, for a caller-chosen row distribution (e.g. the tensor's skew).
+__global__ void k_row_ceiling_stream(const float4* __restrict__ a, const uint32_t* __restrict__ idx,
+                                     uint32_t mask, uint32_t per_group, float* __restrict__ sink) {
+  const uint32_t lig = threadIdx.x & 7;
+  const uint32_t grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const uint32_t* my = idx + size_t(grp) * per_group;
+  const uint64_t pol = policy_evict_first();
+  float acc = 0.f;
+  uint32_t cur = ld_stream_u32(my + lig, pol);
+  for (uint32_t it = 0; it < per_group; it += 8) {
+    const uint32_t nxt = it + 8 < per_group ? ld_stream_u32(my + it + 8 + lig, pol) : 0u;
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t r = __shfl_sync(FULL, cur, u, 8) & mask;
+      v[u] = __ldg(a + size_t(r) * 8 + lig);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+    cur = nxt;
+  }
+  if (acc == 1234.5f) *sink = acc;
+}
+}  // namespace hbk
+
 int hbk_row_ceiling(int64_t rows, int ctas_per_sm, int64_t gathers, void* stream) {
   return guarded([&] {
     if (rows == 0) {  // release the scratch matrix (on its device)
@@ -3371,6 +3402,30 @@ int hbk_row_ceiling(int64_t rows, int ctas_per_sm, int64_t gathers, void* stream
     k_row_ceiling<<<grid, FAST_BLOCK, 0, st>>>(a, uint32_t(rows - 1), per_group,
                                                reinterpret_cast<float*>(a + size_t(rows) * 8));
     check_launch("k_row_ceiling");
+  });
+}
+
+int hbk_row_ceiling_stream(const uint32_t* idx, int64_t n, int64_t rows, int ctas_per_sm, void* stream) {
+  return guarded([&] {
+    HBK_REQUIRE(rows > 0 && (rows & (rows - 1)) == 0 && rows <= (int64_t(1) << 32), HBK_EINVAL,
+                "rows must be a power of two <= 2^32");
+    HBK_REQUIRE(ctas_per_sm >= 1 && ctas_per_sm <= 8 && idx != nullptr && n > 0, HBK_EINVAL,
+                "ctas_per_sm in 1..8 and a non-empty index stream");
+    int dev = 0, sms = 0;
+    HBK_CUDA(cudaGetDevice(&dev));
+    HBK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int grid = sms * ctas_per_sm;
+    const int64_t groups = int64_t(grid) * (FAST_BLOCK / 8);
+    const int64_t per_group = n / groups / 8 * 8;
+    HBK_REQUIRE(per_group >= 8, HBK_EINVAL, "index stream too short for this grid (need 8 per group)");
+    cudaStream_t st = to_stream(stream);
+    std::lock_guard<std::mutex> lk(g_ceiling_mu);
+    HBK_REQUIRE(g_ceiling_buf && g_ceiling_dev == dev && g_ceiling_bytes >= size_t(rows) * 128 + 16,
+                HBK_EINVAL, "call hbk_row_ceiling with the same rows first (it owns the matrix)");
+    float4* a = static_cast<float4*>(g_ceiling_buf);
+    k_row_ceiling_stream<<<grid, FAST_BLOCK, 0, st>>>(a, idx, uint32_t(rows - 1), uint32_t(per_group),
+                                                      reinterpret_cast<float*>(a + size_t(rows) * 8));
+    check_launch("k_row_ceiling_stream");
   });
 }
 

@@ -35,3 +35,26 @@ def test_row_ceiling_launch_and_guards():
     N.call("hbk_row_ceiling", C.c_int64(0), 1, C.c_int64(1), N.stream_ptr())  # frees the scratch
     N.call("hbk_row_ceiling", C.c_int64(1 << 10), 1, C.c_int64(1 << 16), N.stream_ptr())  # re-allocates
     torch.cuda.synchronize()
+
+
+def test_row_ceiling_stream_needs_the_matrix_and_runs():
+    import torch
+
+    from paper_1904_03329_b200 import _native as N
+
+    N.require_device()
+    rows = 1 << 12
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    n = 4 * sms * 32 * 64
+    idx = torch.randint(0, rows, (n,), device="cuda", dtype=torch.int32)
+    N.call("hbk_row_ceiling", C.c_int64(0), 1, C.c_int64(1), N.stream_ptr())  # no matrix now
+    with pytest.raises(ValueError):
+        N.call("hbk_row_ceiling_stream", C.c_void_p(idx.data_ptr()), C.c_int64(n), C.c_int64(rows), 4,
+               N.stream_ptr())
+    N.call("hbk_row_ceiling", C.c_int64(rows), 4, C.c_int64(1 << 16), N.stream_ptr())
+    with pytest.raises(ValueError):  # too short for the grid
+        N.call("hbk_row_ceiling_stream", C.c_void_p(idx.data_ptr()), C.c_int64(64), C.c_int64(rows), 4,
+               N.stream_ptr())
+    N.call("hbk_row_ceiling_stream", C.c_void_p(idx.data_ptr()), C.c_int64(n), C.c_int64(rows), 4,
+           N.stream_ptr())
+    torch.cuda.synchronize()
