@@ -207,7 +207,65 @@ __global__ void k_rows_stream(const float4* __restrict__ a, const uint32_t* __re
   if (acc == 1234.5f) *sink = acc;
 }
 
-int main() {
+// uniform random rows over any row count (multiply-shift range reduction)
+__global__ void k_rows_any(const float4* __restrict__ a, uint32_t nrows, int per_group, float* sink) {
+  const uint32_t lig = threadIdx.x & 7;
+  const uint32_t grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  uint32_t x = mix(grp + 1u);
+  float acc = 0.f;
+  for (int it = 0; it < per_group; it += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      x = x * 1664525u + 1013904223u;
+      const uint32_t r = uint32_t((uint64_t(x) * nrows) >> 32);
+      v[u] = __ldg(a + size_t(r) * 8 + lig);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+  }
+  if (acc == 1234.5f) *sink = acc;
+}
+
+static int size_sweep() {
+  // uniform random rows over matrices of growing footprint: where the rate
+  // falls from the L2 rate to the HBM rate is the L2 capacity the gather sees
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const size_t maxb = size_t(512) << 20;
+  float4* buf = nullptr;
+  float* sink = nullptr;
+  CK(cudaMalloc(&buf, maxb));
+  CK(cudaMalloc(&sink, 4));
+  CK(cudaMemset(buf, 0, maxb));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const int grid = sms * 4;
+  const int groups = grid * 256 / 8;
+  const int per_group = int(((size_t(4) << 30) / 128 / groups + 7) / 8 * 8);
+  for (int mb = 16; mb <= 512; mb += (mb < 160 ? 16 : 64)) {
+    // nrows must be a power of two for the LCG mask: use the largest power
+    // of two <= mb, and scale rows onto [0, rows_mb) by a multiply-shift
+    const uint32_t rows = uint32_t((size_t(mb) << 20) / 128);
+    float best = 1e30f;
+    for (int t = 0; t < 5; ++t) {
+      CK(cudaEventRecord(e0));
+      k_rows_any<<<grid, 256>>>(buf, rows, per_group, sink);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (t && ms < best) best = ms;
+    }
+    const double rb = double(groups) * per_group * 128.0;
+    printf("sweep %4d MB  %8.1f GB/s  (%.1f G rows/s)\n", mb, rb / best / 1e6, rb / 128.0 / best / 1e6);
+  }
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1 && argv[1][0] == 's') return size_sweep();
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const size_t max_bytes = size_t(64) << 20;
