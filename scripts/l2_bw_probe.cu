@@ -182,6 +182,7 @@ __global__ void k_rows_zipf_rep(const float4* __restrict__ a, uint32_t nrows, ui
 // its own contiguous span of a u32 index array (HBM, L1 no-allocate), one
 // coalesced load per lane per batch of 8, 8 SHFL to broadcast, 8 row gathers
 // (L1-allocating).  Index arrays: uniform or Zipf(1), generated on the host.
+template <bool CG>
 __global__ void k_rows_stream(const float4* __restrict__ a, const uint32_t* __restrict__ idx,
                               int per_group, float* sink) {
   const uint32_t lig = threadIdx.x & 7;
@@ -198,7 +199,7 @@ __global__ void k_rows_stream(const float4* __restrict__ a, const uint32_t* __re
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const uint32_t r = __shfl_sync(0xffffffffu, cur, u, 8);
-      v[u] = __ldg(a + size_t(r) * 8 + lig);
+      v[u] = CG ? ld_cg(a + size_t(r) * 8 + lig) : __ldg(a + size_t(r) * 8 + lig);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
@@ -386,11 +387,13 @@ int main(int argc, char** argv) {
       }
       if (bytes == (size_t(8) << 20)) {
         const int per_group_s = int(nidx / groups) / 8 * 8;
-        for (int z = 0; z < 2; ++z) {
+        for (int zc = 0; zc < 4; ++zc) {
+          const int z = zc & 1, cg = zc >> 1;
           best = 1e30f;
           for (int t = 0; t < 7; ++t) {
             CK(cudaEventRecord(e0));
-            k_rows_stream<<<grid, 256>>>(buf, z ? d_zipf : d_uni, per_group_s, sink);
+            if (cg) k_rows_stream<true><<<grid, 256>>>(buf, z ? d_zipf : d_uni, per_group_s, sink);
+            else k_rows_stream<false><<<grid, 256>>>(buf, z ? d_zipf : d_uni, per_group_s, sink);
             CK(cudaEventRecord(e1));
             CK(cudaEventSynchronize(e1));
             float ms;
@@ -398,7 +401,8 @@ int main(int argc, char** argv) {
             if (t && ms < best) best = ms;
           }
           const double rb = double(groups) * per_group_s * 128.0;
-          printf("rows-stream-%s %3zu MB  %2d warps/SM  %8.1f GB/s  (%.1f G rows/s)\n", z ? "zipf" : "uniform",
+          printf("rows-stream-%s%s %3zu MB  %2d warps/SM  %8.1f GB/s  (%.1f G rows/s)\n", z ? "zipf" : "uniform",
+                 cg ? "-cg" : "",
                  bytes >> 20, c * 8, rb / best / 1e6, rb / 128.0 / best / 1e6);
         }
       }
